@@ -1,0 +1,120 @@
+"""Pin the oracle (CPU restatement) against the reference's own outputs.
+
+The fixtures in tests/golden/ were produced by oracle/make_golden.py from the
+real reference (numba kernels, /root/reference/pkg/src/mdtune).  The oracle
+must reproduce them: geometry/stencils/cell arrays/Verlet lists bit-exactly,
+forces and counts bit-exactly (same arithmetic order, contraction off), and
+the simulate() trajectories bit-exactly.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, system_names
+from oracle import port
+
+
+def _params(d, rebuild=5):
+    per = tuple(port.PERIODIC if f else port.REFLECTIVE for f in d["periodic"])
+    return port.Params(domain_size=d["domain"], cutoff=float(d["cutoff"]),
+                       skin=float(d["skin"]), rebuild_interval=rebuild, boundary=per)
+
+
+def _particles(d):
+    nt = int(d["n_types"])
+    return port.Particles(d["pos"], type_id=d["tid"],
+                          sigma=[1.0 - 0.2 * t for t in range(nt)],
+                          epsilon=[1.0 + 0.5 * t for t in range(nt)],
+                          mass=[1.0 + t for t in range(nt)])
+
+
+def test_geometry_and_stencils_match_reference():
+    z = golden("geometry.npz")
+    for k in range(int(z["n_cases"])):
+        g = port.make_geometry(z[f"g{k}_in_domain"], z[f"g{k}_in_scalars"][0],
+                               z[f"g{k}_in_scalars"][1], z[f"g{k}_in_periodic"].astype(bool))
+        assert g.dims_owned == tuple(z[f"g{k}_dims_owned"])
+        assert g.cell_length == tuple(z[f"g{k}_cell_length"])
+        assert g.overlap == tuple(z[f"g{k}_overlap"])
+        assert g.halo == tuple(z[f"g{k}_halo"])
+        assert g.dims == tuple(z[f"g{k}_dims"])
+        assert np.array_equal(port.pruned_stencil(g), z[f"g{k}_pruned"])
+        for major in range(3):
+            assert np.array_equal(port.forward_stencil(g, major), z[f"g{k}_forward{major}"])
+
+
+@pytest.mark.parametrize("name", system_names())
+def test_cell_binning_bit_exact(name):
+    d = golden(f"sys_{name}.npz")
+    params = _params(d)
+    p = _particles(d)
+    for csf, tag in ((1.0, "csf1"), (0.5, "csf05")):
+        g = port.make_geometry(params.domain_size, params.interaction_length, csf,
+                               params.periodic_flags())
+        grid = port.Grid(g)
+        grid.rebuild(p)
+        assert np.array_equal(grid.src, d[f"{tag}_src"])
+        assert np.array_equal(grid.shift, d[f"{tag}_shift"])
+        assert np.array_equal(grid.start, d[f"{tag}_start"])
+        assert np.array_equal(grid.end, d[f"{tag}_end"])
+
+
+@pytest.mark.parametrize("name", system_names())
+def test_verlet_lists_bit_exact(name):
+    d = golden(f"sys_{name}.npz")
+    params = _params(d)
+    g = port.make_geometry(params.domain_size, params.interaction_length, 1.0,
+                           params.periodic_flags())
+    vl = port.VerletLists(g)
+    vl.rebuild(_particles(d))
+    assert np.array_equal(vl.noff, d["vl_noff"])
+    assert np.array_equal(vl.nbr, d["vl_nbr"])
+
+
+@pytest.mark.parametrize("name", system_names())
+def test_all_30_configurations_bit_exact(name):
+    d = golden(f"sys_{name}.npz")
+    params = _params(d)
+    ids = [str(s) for s in d["config_ids"]]
+    assert ids == [c.id for c in port.all_configs()]
+    for k, cid in enumerate(ids):
+        p = _particles(d)
+        _, count = port.compute_forces(p, port.parse(cid), params, workers=1)
+        assert count == d["counts"][k], cid
+        assert np.array_equal(np.asarray(p.forces), d["forces"][k]), cid
+
+
+@pytest.mark.parametrize("name", ["small_periodic", "crit1_0"])
+def test_worker_count_independent(name):
+    d = golden(f"sys_{name}.npz")
+    params = _params(d)
+    for cfg in port.all_configs():
+        a, b = _particles(d), _particles(d)
+        port.compute_forces(a, cfg, params, workers=1)
+        port.compute_forces(b, cfg, params, workers=4)
+        assert port.force_rel_error(b.forces, a.forces) <= 1e-12, cfg.id
+
+
+@pytest.mark.parametrize("name", ["small_periodic", "mixed", "blob", "tight"])
+def test_oracle_vs_brute_force(name):
+    d = golden(f"sys_{name}.npz")
+    params = _params(d)
+    p = _particles(d)
+    ref, directed = port.brute_forces(p.positions, p.type_id, p.epsilon, p.sigma,
+                                      params.cutoff, params.domain_size, params.periodic_flags())
+    for k, cfg in enumerate(port.all_configs()):
+        assert port.force_rel_error(d["forces"][k], ref) <= 1e-9, cfg.id
+        assert d["counts"][k] * (2 if cfg.newton3 else 1) == directed, cfg.id
+
+
+@pytest.mark.parametrize("traj", ["traj_small", "traj_faces", "traj_config1"])
+def test_simulate_trajectory_bit_exact(traj):
+    z = golden(f"{traj}.npz")
+    L = float(z["domain"][0])
+    for k, cid in enumerate(str(s) for s in z["config_ids"]):
+        params = port.Params(domain_size=(L, L, L), cutoff=2.5, skin=0.3, rebuild_interval=10,
+                             delta_t=1e-3, boundary=(port.PERIODIC,) * 3)
+        p = port.Particles(z["pos0"], z["vel0"])
+        port.simulate_fixed(p, params, port.parse(cid), steps=int(z["steps"]))
+        assert np.array_equal(np.asarray(p.positions), z[f"pos_{k}"]), cid
+        assert np.array_equal(np.asarray(p.velocities), z[f"vel_{k}"]), cid

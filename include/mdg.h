@@ -1,0 +1,150 @@
+/*
+ * mdg.h — C ABI of libmdg, the B200-native (sm_100a) Lennard-Jones force and
+ * neighbour-identification path of the mdtune reference
+ * (arXiv 2505.03438 re-creation, /root/reference/pkg/src/mdtune).
+ *
+ * The reference's drop-in boundary for this path is the Python protocol
+ * `ForceCalculator(particles, params)` with `rebuild / refresh / compute /
+ * last_eval_count` (containers.py:378-488), looked up as a module global by
+ * `simulate` (simulation.py:21,144) and `measure_configuration_costs`
+ * (dataset.py:21,114), plus the Verlet update around it (integrator.py:31-128).
+ * Every entry point below replaces one piece of that surface; the mapping is
+ * given per function.  All pointers are plain device pointers unless a
+ * parameter is documented as host memory; no torch types cross this ABI.
+ *
+ * Return value of every int function: 0 = ok, MDG_EINVAL = invalid argument
+ * (the reference raises ValueError), MDG_ECUDA = CUDA failure (RuntimeError),
+ * MDG_ESTATE = called out of order (e.g. compute before rebuild).
+ * mdg_last_error() returns the thread-local message of the last failure.
+ *
+ * Threading: one context per GPU, driven from one host thread; all work is
+ * enqueued on the context's stream (containers.py / SPEC.md:105-106: the
+ * calculator is single-threaded from the caller's side).
+ */
+#ifndef MDG_H
+#define MDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDG_OK 0
+#define MDG_EINVAL 1
+#define MDG_ECUDA 2
+#define MDG_ESTATE 3
+
+/* configuration.py:7-17 */
+enum { MDG_LC = 0, MDG_VL = 1 };
+enum { MDG_C01 = 0, MDG_C08 = 1, MDG_C18 = 2, MDG_SLI = 3, MDG_LIST_ITER = 4 };
+/* particles.py:10-11 */
+enum { MDG_AOS = 0, MDG_SOA = 1 };
+
+/* One point of the search space: Configuration (configuration.py:20-50). */
+typedef struct {
+    int container;  /* MDG_LC / MDG_VL */
+    int traversal;  /* MDG_C01 .. MDG_LIST_ITER */
+    int newton3;    /* 0 / 1 */
+    int layout;     /* MDG_AOS / MDG_SOA */
+    double csf;     /* cell size factor, 1.0 or 0.5 */
+} mdg_config;
+
+typedef struct mdg_ctx mdg_ctx;
+
+/* Library version string. */
+const char* mdg_version(void);
+/* Number of kernel launches libmdg has issued in this process (evidence for
+ * bench.py's gpu_launches). */
+uint64_t mdg_launch_count(void);
+/* Thread-local message of the last failing call ("" if none). */
+const char* mdg_last_error(void);
+
+/* Context on `device`, enqueuing on `stream` (a cudaStream_t, may be NULL for
+ * the legacy default stream).  Replaces ForceCalculator.__init__'s allocation
+ * of GridState / LayoutBuffers / VerletListState (containers.py:385-401). */
+int mdg_create(int device, void* stream, mdg_ctx** out);
+int mdg_destroy(mdg_ctx* ctx);
+int mdg_set_stream(mdg_ctx* ctx, void* stream);
+
+/* SimulationParams (params.py:35-101) + per-type LJ parameters
+ * (particles.py:60-70) -> mixing tables (forces.py:12-22) and the CSF-1 /
+ * CSF-0.5 geometries (cells.py:55-67, containers.py:390-396).  Validates like
+ * SimulationParams.__post_init__.  sigma/epsilon/mass: host arrays of ntypes. */
+int mdg_set_system(mdg_ctx* ctx, const double domain[3], const int periodic[3], double cutoff,
+                   double skin, int ntypes, const double* sigma, const double* epsilon,
+                   const double* mass);
+
+/* Bind the caller-owned particle arrays (ParticleSet, particles.py:31-98):
+ * pos/vel/force/old_force are fp64 device arrays in `layout` (AoS (n,3),
+ * SoA (3,n)); type_id is int32 on the device (may be NULL for one type). */
+int mdg_bind(mdg_ctx* ctx, int64_t n, int layout, double* pos, double* vel, double* force,
+             double* old_force, const int32_t* type_id);
+
+/* ForceCalculator.rebuild (containers.py:403-412): cell binning (stable
+ * counting sort incl. periodic images) or Verlet-list build.  Synchronises
+ * once (sizes of the image / list arrays). */
+int mdg_rebuild(mdg_ctx* ctx, const mdg_config* cfg);
+/* ForceCalculator.refresh (containers.py:429-439): gather pos[src]+shift into
+ * the cell-sorted scratch (no-op for Verlet lists).  Asynchronous. */
+int mdg_refresh(mdg_ctx* ctx, const mdg_config* cfg);
+/* ForceCalculator.compute (containers.py:441-488): overwrite `force` with the
+ * LJ forces.  Asynchronous; the within-cutoff evaluation count accumulates on
+ * the device (read it with mdg_eval_count).  MDG_EINVAL on layout mismatch
+ * (containers.py:445-448). */
+int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg);
+/* ForceCalculator.last_eval_count (containers.py:454): synchronises. */
+int mdg_eval_count(mdg_ctx* ctx, int64_t* count);
+
+/* drift_with_force + apply_boundaries + copy force->old_force
+ * (integrator.py:31-37, :98-128; simulation.py:151-153), fused. */
+int mdg_drift_wrap(mdg_ctx* ctx, double dt);
+/* apply_gravity + finish_kick (integrator.py:40-51; simulation.py:177,185). */
+int mdg_finish_kick(mdg_ctx* ctx, double dt, int has_gravity, double gravity);
+/* Capped steepest-descent step x += F/|F| min(gamma|F|, max_disp) (input
+ * relaxation for BASELINE configs 2/4; no reference counterpart). */
+int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp);
+/* BlowUpError detection (integrator.py:108-116): flag set by any drift since
+ * the last reset.  Synchronises. */
+int mdg_blowup(mdg_ctx* ctx, int* flag, int reset);
+/* Wait for all work of the context's stream. */
+int mdg_synchronize(mdg_ctx* ctx);
+
+/* Host <-> device copies on the context stream (host-copy drop-in mode).
+ * `host` should be pinned for full bandwidth.  d2h synchronises. */
+int mdg_h2d(mdg_ctx* ctx, void* dev, const void* host, size_t bytes);
+int mdg_d2h(mdg_ctx* ctx, void* host, const void* dev, size_t bytes);
+
+/* Debug / parity exports (host buffers). */
+/* make_geometry (cells.py:55-67) for csf. */
+int mdg_geometry(mdg_ctx* ctx, double csf, int dims_owned[3], double cell_length[3],
+                 int overlap[3], int halo[3], int dims[3]);
+/* kind 0 = pruned_stencil (cells.py:80-95), 1 = forward_stencil with `major`
+ * (cells.py:98-111).  out: 3*124 ints; *count = number of offsets. */
+int mdg_stencil(mdg_ctx* ctx, double csf, int kind, int major, int* count, int* out);
+/* GridState after the last rebuild of `csf` (containers.py:93-118): *m rows,
+ * *ncells cells; src (m, int32), shift_code (m; (sx+1)*9+(sy+1)*3+(sz+1)),
+ * start (ncells+1).  Any output pointer may be NULL (size query). */
+int mdg_get_grid(mdg_ctx* ctx, double csf, int64_t* m, int64_t* ncells, int32_t* src,
+                 int8_t* shift_code, int32_t* start);
+/* VerletListState after the last VL rebuild (containers.py:352-375): noff
+ * (n+1, int64) and nbr (entries, int32).  NULL outputs = size query. */
+int mdg_get_verlet(mdg_ctx* ctx, int64_t* entries, int64_t* noff, int32_t* nbr);
+
+/* Context-free host versions of the two exports above (no device needed). */
+int mdg_geometry_for(const double domain[3], const int periodic[3], double interaction_length,
+                     double csf, int dims_owned[3], double cell_length[3], int overlap[3],
+                     int halo[3], int dims[3]);
+int mdg_stencil_for(const double domain[3], const int periodic[3], double interaction_length,
+                    double csf, int kind, int major, int* count, int* out);
+
+/* Measured FP64 FMA throughput of this device (roofline denominator):
+ * dependent-chain DFMA microbenchmark, TFLOP/s (2 flops per DFMA). */
+int mdg_measure_fp64_peak(mdg_ctx* ctx, double* tflops, double* sm_mhz_hint);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MDG_H */

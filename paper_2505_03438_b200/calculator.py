@@ -1,0 +1,261 @@
+"""The force calculator on the GPU: the reference's drop-in boundary.
+
+``ForceCalculator`` mirrors mdtune.containers.ForceCalculator
+(containers.py:378-488) member for member -- ``rebuild``, ``refresh``,
+``compute`` (returns the within-cutoff evaluation count), ``last_eval_count``
+-- on a device-resident :class:`~paper_2505_03438_b200.particles.ParticleSet`.
+Every call goes through libmdg's C ABI (include/mdg.h); there is no CPU path.
+
+``HostForceCalculator`` is the same protocol over the reference's HOST
+ParticleSet (numpy arrays): positions are copied host->device at rebuild /
+refresh (and at compute for Verlet lists, which read positions directly,
+containers.py:435-436), forces device->host after compute.  It is what gets
+installed into ``mdtune.simulation.ForceCalculator`` /
+``mdtune.dataset.ForceCalculator`` (see plugin.py) so the reference's own
+simulate loop and tuning strategies drive the GPU unchanged.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, config_struct, lib
+
+
+@dataclass
+class Timings:
+    force_ns: int = 0
+    build_ns: int = 0
+
+
+def _dptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+class Context:
+    """Owns one mdg_ctx on a CUDA device, enqueuing on torch's current stream."""
+
+    def __init__(self, device=None, stream=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2505_03438_b200 needs a CUDA device (no CPU fallback)")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        idx = dev.index if dev.index is not None else torch.cuda.current_device()
+        self.stream = stream or torch.cuda.current_stream(idx)
+        h = ctypes.c_void_p()
+        check(lib().mdg_create(idx, ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h)),
+              "mdg_create")
+        self.h = h
+
+    def set_system(self, params, sigma, epsilon, mass):
+        L = np.ascontiguousarray(params.domain_size, dtype=np.float64)
+        per = np.ascontiguousarray(params.periodic_flags().astype(np.int32))
+        sig = np.ascontiguousarray(sigma, dtype=np.float64)
+        eps = np.ascontiguousarray(epsilon, dtype=np.float64)
+        m = np.ascontiguousarray(mass, dtype=np.float64)
+        check(lib().mdg_set_system(self.h, L.ctypes.data, per.ctypes.data, float(params.cutoff),
+                                   float(params.skin), len(sig), sig.ctypes.data,
+                                   eps.ctypes.data, m.ctypes.data), "mdg_set_system")
+
+    def bind(self, n, layout, pos, vel, force, old_force, type_id):
+        check(lib().mdg_bind(self.h, int(n), _lib.AOS if layout == "AoS" else _lib.SOA,
+                             _dptr(pos), _dptr(vel), _dptr(force), _dptr(old_force),
+                             _dptr(type_id)), "mdg_bind")
+
+    def eval_count(self) -> int:
+        c = ctypes.c_int64()
+        check(lib().mdg_eval_count(self.h, ctypes.byref(c)), "mdg_eval_count")
+        return int(c.value)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().mdg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ForceCalculator:
+    """Force evaluation under any enumerated configuration, on the GPU."""
+
+    def __init__(self, particles, params):
+        self.params = params
+        self.ctx = Context(particles.device)
+        self.ctx.set_system(params, particles.sigma, particles.epsilon, particles.mass)
+        self._count_pending = False
+        self._count = 0
+
+    # -- binding -------------------------------------------------------------
+    def bind(self, p):
+        self._bound_n = p.n
+        self.ctx.bind(p.n, p.layout, p.pos, p.vel, p.force, p.old_force,
+                      p.type_id if p.ntypes > 1 else None)
+
+    # -- the reference protocol ---------------------------------------------
+    def rebuild(self, particles, config):
+        self.bind(particles)
+        check(lib().mdg_rebuild(self.ctx.h, ctypes.byref(config_struct(config))), "rebuild")
+
+    def refresh(self, particles, config):
+        self.bind(particles)
+        check(lib().mdg_refresh(self.ctx.h, ctypes.byref(config_struct(config))), "refresh")
+
+    def compute_async(self, particles, config):
+        """compute() without the host synchronisation for the count."""
+        if particles.layout != config.layout:
+            raise ValueError(f"particle layout {particles.layout} does not match "
+                             f"configuration {config.id}")
+        self.bind(particles)
+        check(lib().mdg_compute(self.ctx.h, ctypes.byref(config_struct(config))), "compute")
+        self._count_pending = True
+
+    def compute(self, particles, config, workforce=None) -> int:
+        self.compute_async(particles, config)
+        return self.last_eval_count
+
+    @property
+    def last_eval_count(self) -> int:
+        if self._count_pending:
+            self._count = self.ctx.eval_count()
+            self._count_pending = False
+        return self._count
+
+    # -- integrator on the bound arrays (integrator.py) ------------------------
+    def drift_wrap(self, particles, dt):
+        self.bind(particles)
+        check(lib().mdg_drift_wrap(self.ctx.h, float(dt)), "drift")
+
+    def finish_kick(self, particles, dt, gravity=None):
+        self.bind(particles)
+        check(lib().mdg_finish_kick(self.ctx.h, float(dt), int(gravity is not None),
+                                    float(gravity or 0.0)), "finish_kick")
+
+    def sd_step(self, particles, gamma, max_disp):
+        self.bind(particles)
+        check(lib().mdg_sd_step(self.ctx.h, float(gamma), float(max_disp)), "sd_step")
+
+    def blowup(self, reset=True) -> bool:
+        f = ctypes.c_int()
+        check(lib().mdg_blowup(self.ctx.h, ctypes.byref(f), int(reset)), "blowup")
+        return bool(f.value)
+
+    # -- parity exports --------------------------------------------------------
+    def grid_state(self, csf):
+        m, nc = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().mdg_get_grid(self.ctx.h, float(csf), ctypes.byref(m), ctypes.byref(nc),
+                                 None, None, None), "get_grid")
+        src = np.zeros(m.value, dtype=np.int32)
+        code = np.zeros(m.value, dtype=np.int8)
+        start = np.zeros(nc.value + 1, dtype=np.int32)
+        check(lib().mdg_get_grid(self.ctx.h, float(csf), ctypes.byref(m), ctypes.byref(nc),
+                                 src.ctypes.data, code.ctypes.data, start.ctypes.data), "get_grid")
+        L = np.asarray(self.params.domain_size, dtype=np.float64)
+        combo = np.stack([code // 9 - 1, (code // 3) % 3 - 1, code % 3 - 1], axis=1)
+        return {"src": src.astype(np.int64), "shift": combo.astype(np.float64) * L,
+                "start": start[:-1].astype(np.int64), "end": start[1:].astype(np.int64)}
+
+    def verlet_lists(self):
+        e = ctypes.c_int64()
+        check(lib().mdg_get_verlet(self.ctx.h, ctypes.byref(e), None, None), "get_verlet")
+        n = self._bound_n
+        noff = np.zeros(n + 1, dtype=np.int64)
+        nbr = np.zeros(e.value, dtype=np.int32)
+        check(lib().mdg_get_verlet(self.ctx.h, ctypes.byref(e), noff.ctypes.data,
+                                   nbr.ctypes.data), "get_verlet")
+        return noff, nbr.astype(np.int64)
+
+    def close(self):
+        self.ctx.close()
+
+
+def compute_forces(particles, config, params, workers=None, timer=None):
+    """One-shot build + refresh + compute (containers.py:494-511), device-timed."""
+    calc = ForceCalculator(particles, params)
+    particles.convert_layout(config.layout)
+    torch.cuda.synchronize(particles.device)
+    t0 = time.perf_counter_ns()
+    calc.rebuild(particles, config)
+    calc.refresh(particles, config)
+    torch.cuda.synchronize(particles.device)
+    t1 = time.perf_counter_ns()
+    count = calc.compute(particles, config)
+    t2 = time.perf_counter_ns()
+    calc.close()
+    return Timings(force_ns=t2 - t1, build_ns=t1 - t0), count
+
+
+class HostForceCalculator:
+    """ForceCalculator protocol over HOST particle sets (the mdtune drop-in).
+
+    Every public method synchronises before returning, so the reference's
+    wall-clock ``timer()`` around build and compute (simulation.py:160-169)
+    measures the GPU work including the host<->device copies.
+    """
+
+    def __init__(self, particles, params):
+        self.params = params
+        self.ctx = Context()
+        dev = self.ctx.device
+        self.ctx.set_system(params, particles.sigma, particles.epsilon, particles.mass)
+        n = particles.n
+        self.n = n
+        self._buf = {k: torch.zeros(3 * n, dtype=torch.float64, device=dev)
+                     for k in ("pos", "vel", "force", "old_force")}
+        self._pinned = torch.zeros(3 * n, dtype=torch.float64).pin_memory() if n else None
+        self._tid = None
+        if len(particles.mass) > 1 and n:
+            self._tid = torch.as_tensor(np.asarray(particles.type_id, dtype=np.int32)).to(dev)
+        self.last_eval_count = 0
+
+    def _bind(self, p):
+        self.ctx.bind(self.n, p.layout, self._buf["pos"], self._buf["vel"], self._buf["force"],
+                      self._buf["old_force"], self._tid)
+
+    def _upload_positions(self, p):
+        if not self.n:
+            return
+        src = np.ascontiguousarray(p.pos)
+        self._pinned.numpy()[:] = src.reshape(-1)
+        check(lib().mdg_h2d(self.ctx.h, ctypes.c_void_p(self._buf["pos"].data_ptr()),
+                            ctypes.c_void_p(self._pinned.data_ptr()), 24 * self.n), "h2d")
+
+    def rebuild(self, particles, config):
+        self._upload_positions(particles)
+        self._bind(particles)
+        check(lib().mdg_rebuild(self.ctx.h, ctypes.byref(config_struct(config))), "rebuild")
+
+    def refresh(self, particles, config):
+        if config.container == "VL":
+            return
+        self._upload_positions(particles)
+        self._bind(particles)
+        check(lib().mdg_refresh(self.ctx.h, ctypes.byref(config_struct(config))), "refresh")
+        check(lib().mdg_synchronize(self.ctx.h), "sync")
+
+    def compute(self, particles, config, workforce=None) -> int:
+        if particles.layout != config.layout:
+            raise ValueError(f"particle layout {particles.layout} does not match "
+                             f"configuration {config.id}")
+        if config.container == "VL":
+            self._upload_positions(particles)
+        self._bind(particles)
+        h = self.ctx.h
+        check(lib().mdg_compute(h, ctypes.byref(config_struct(config))), "compute")
+        if self.n:
+            check(lib().mdg_d2h(h, ctypes.c_void_p(self._pinned.data_ptr()),
+                                ctypes.c_void_p(self._buf["force"].data_ptr()), 24 * self.n), "d2h")
+            particles.force.reshape(-1)[:] = self._pinned.numpy()
+        else:
+            particles.force.fill(0.0)
+        self.last_eval_count = self.ctx.eval_count()
+        return self.last_eval_count

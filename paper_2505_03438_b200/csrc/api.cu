@@ -1,0 +1,432 @@
+// The C ABI (include/mdg.h) over the device pipeline.
+#include <math.h>
+#include <string.h>
+
+#include <string>
+
+#include "../../include/mdg.h"
+#include "device.cuh"
+
+struct mdg_ctx {
+    mdg::Context c;
+};
+
+namespace mdg {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+static unsigned long long g_launches = 0;
+void note_launch() { ++g_launches; }
+unsigned long long launch_count() { return g_launches; }
+
+}  // namespace mdg
+
+using namespace mdg;
+
+#define CHECK_CTX(ctx)                                   \
+    do {                                                 \
+        if (!(ctx)) {                                    \
+            set_error("null context");                   \
+            return MDG_EINVAL;                           \
+        }                                                \
+        cudaSetDevice((ctx)->c.device);                  \
+    } while (0)
+
+static int cuda_status(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string(what) + ": " + cudaGetErrorString(e));
+        return MDG_ECUDA;
+    }
+    return MDG_OK;
+}
+
+// Configuration.__post_init__ (configuration.py:30-50)
+static int validate(const mdg_config* cfg) {
+    if (!cfg) {
+        set_error("null configuration");
+        return MDG_EINVAL;
+    }
+    if (cfg->layout != MDG_AOS && cfg->layout != MDG_SOA) {
+        set_error("unknown layout");
+        return MDG_EINVAL;
+    }
+    if (cfg->container == MDG_VL) {
+        if (cfg->traversal != MDG_LIST_ITER) {
+            set_error("Verlet lists only support List_Iter");
+            return MDG_EINVAL;
+        }
+        if (cfg->csf != 1.0) {
+            set_error("Verlet lists fix the cell size factor at 1");
+            return MDG_EINVAL;
+        }
+    } else if (cfg->container == MDG_LC) {
+        if (cfg->traversal < MDG_C01 || cfg->traversal > MDG_SLI) {
+            set_error("linked cells do not support this traversal");
+            return MDG_EINVAL;
+        }
+    } else {
+        set_error("unknown container");
+        return MDG_EINVAL;
+    }
+    if ((cfg->traversal == MDG_LIST_ITER || cfg->traversal == MDG_C01) && cfg->newton3) {
+        set_error("C01 / List_Iter cannot use Newton-3 writes");
+        return MDG_EINVAL;
+    }
+    if (cfg->csf != 1.0 && cfg->csf != 0.5) {
+        set_error("cell size factor must be one of (1.0, 0.5)");
+        return MDG_EINVAL;
+    }
+    return MDG_OK;
+}
+
+static Grid* grid_for(Context& c, double csf) { return csf == 1.0 ? &c.grids[0] : &c.grids[1]; }
+
+static int need_system(mdg_ctx* ctx) {
+    if (!ctx->c.have_system) {
+        set_error("mdg_set_system has not been called");
+        return MDG_ESTATE;
+    }
+    return MDG_OK;
+}
+
+extern "C" {
+
+const char* mdg_version(void) { return "mdg 0.1 (sm_100a)"; }
+
+uint64_t mdg_launch_count(void) { return (uint64_t)launch_count(); }
+
+const char* mdg_last_error(void) { return g_err.c_str(); }
+
+int mdg_create(int device, void* stream, mdg_ctx** out) {
+    if (!out) {
+        set_error("null output");
+        return MDG_EINVAL;
+    }
+    *out = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess) return cuda_status("cudaSetDevice");
+    mdg_ctx* ctx = new mdg_ctx();
+    ctx->c.device = device;
+    ctx->c.stream = (cudaStream_t)stream;
+    cudaDeviceGetAttribute(&ctx->c.sm_count, cudaDevAttrMultiProcessorCount, device);
+    ctx->c.scal.ensure(8);
+    if (!ctx->c.scal.p || cudaHostAlloc((void**)&ctx->c.h_scal, 8 * sizeof(unsigned long long),
+                                        cudaHostAllocDefault) != cudaSuccess) {
+        delete ctx;
+        return cuda_status("allocating context scalars");
+    }
+    cudaMemsetAsync(ctx->c.scal.p, 0, 8 * sizeof(unsigned long long), ctx->c.stream);
+    *out = ctx;
+    return cuda_status("mdg_create");
+}
+
+int mdg_destroy(mdg_ctx* ctx) {
+    if (!ctx) return MDG_OK;
+    cudaSetDevice(ctx->c.device);
+    cudaStreamSynchronize(ctx->c.stream);
+    ctx->c.grids[0].release();
+    ctx->c.grids[1].release();
+    ctx->c.vl.release();
+    ctx->c.scal.release();
+    ctx->c.scan_tmp.release();
+    ctx->c.d_mass.release();
+    if (ctx->c.h_scal) cudaFreeHost(ctx->c.h_scal);
+    delete ctx;
+    return MDG_OK;
+}
+
+int mdg_set_stream(mdg_ctx* ctx, void* stream) {
+    CHECK_CTX(ctx);
+    ctx->c.stream = (cudaStream_t)stream;
+    return MDG_OK;
+}
+
+int mdg_set_system(mdg_ctx* ctx, const double domain[3], const int periodic[3], double cutoff,
+                   double skin, int ntypes, const double* sigma, const double* epsilon,
+                   const double* mass) {
+    CHECK_CTX(ctx);
+    Context& c = ctx->c;
+    if (!(cutoff > 0)) { set_error("cutoff must be > 0"); return MDG_EINVAL; }
+    if (!(skin >= 0)) { set_error("skin must be >= 0"); return MDG_EINVAL; }
+    if (ntypes < 1 || ntypes > kMaxTypes) {
+        set_error("ntypes must be in [1, " + std::to_string(kMaxTypes) + "]");
+        return MDG_EINVAL;
+    }
+    double ell = cutoff + skin;
+    for (int k = 0; k < 3; ++k) {
+        if (!(domain[k] >= ell)) {
+            set_error("domain size must be at least cutoff + skin in every dimension");
+            return MDG_EINVAL;
+        }
+        if (periodic[k] && domain[k] < 2.0 * ell) {
+            set_error("periodic axes require domain >= 2*(cutoff + skin)");
+            return MDG_EINVAL;
+        }
+    }
+    for (int k = 0; k < 3; ++k) {
+        c.L[k] = domain[k];
+        c.periodic[k] = periodic[k] ? 1 : 0;
+    }
+    c.cutoff = cutoff;
+    c.skin = skin;
+    // forces.py:12-22
+    c.tab.T = ntypes;
+    c.tab.rc2 = cutoff * cutoff;
+    for (int a = 0; a < ntypes; ++a)
+        for (int b = 0; b < ntypes; ++b) {
+            double sm = 0.5 * (sigma[a] + sigma[b]);
+            double em = sqrt(epsilon[a] * epsilon[b]);
+            c.tab.sig2[a * ntypes + b] = sm * sm;
+            c.tab.eps24[a * ntypes + b] = 24.0 * em;
+        }
+    c.mass.assign(mass, mass + ntypes);
+    c.d_mass.ensure(ntypes);
+    if (cudaMemcpy(c.d_mass.p, mass, ntypes * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+        return cuda_status("mass upload");
+    const double csfs[2] = {1.0, 0.5};
+    for (int g = 0; g < 2; ++g) {
+        Grid& gr = c.grids[g];
+        gr.g = make_geometry(c.L, c.periodic, ell, csfs[g]);
+        gr.pruned = pruned_stencil(gr.g);
+        gr.fwd = forward_stencil(gr.g, 0);
+        int major = 0;  // SLI sweeps along argmax(dims_owned) (containers.py:225-227)
+        for (int k = 1; k < 3; ++k)
+            if (gr.g.S[k] > gr.g.S[major]) major = k;
+        gr.sli_major = major;
+        gr.fwd_sli = forward_stencil(gr.g, major);
+        gr.built = false;
+    }
+    c.vl.grid.g = c.grids[0].g;
+    c.vl.grid.pruned = c.grids[0].pruned;
+    c.vl.built = false;
+    c.have_system = true;
+    return MDG_OK;
+}
+
+int mdg_bind(mdg_ctx* ctx, int64_t n, int layout, double* pos, double* vel, double* force,
+             double* old_force, const int32_t* type_id) {
+    CHECK_CTX(ctx);
+    if (n < 0 || n > 0x7fffffffLL / 2) { set_error("particle count out of range"); return MDG_EINVAL; }
+    if (layout != MDG_AOS && layout != MDG_SOA) { set_error("unknown layout"); return MDG_EINVAL; }
+    Context& c = ctx->c;
+    if (n != c.n) {
+        c.grids[0].built = c.grids[1].built = false;
+        c.vl.built = false;
+    }
+    c.n = n;
+    c.layout = layout;
+    c.pos = pos;
+    c.vel = vel;
+    c.force = force;
+    c.old_force = old_force;
+    c.tid = type_id;
+    return MDG_OK;
+}
+
+int mdg_rebuild(mdg_ctx* ctx, const mdg_config* cfg) {
+    CHECK_CTX(ctx);
+    if (int e = validate(cfg)) return e;
+    if (int e = need_system(ctx)) return e;
+    Context& c = ctx->c;
+    if (cfg->container == MDG_VL) {
+        if (vl_rebuild(c)) return MDG_ECUDA;
+    } else {
+        Grid& gr = *grid_for(c, cfg->csf);
+        if (grid_rebuild(c, gr, c.pos, c.layout)) return MDG_ECUDA;
+        grid_bind_scratch(c, gr, cfg->layout);
+    }
+    return cuda_status("mdg_rebuild");
+}
+
+int mdg_refresh(mdg_ctx* ctx, const mdg_config* cfg) {
+    CHECK_CTX(ctx);
+    if (int e = validate(cfg)) return e;
+    Context& c = ctx->c;
+    if (cfg->container == MDG_VL) return MDG_OK;
+    Grid& gr = *grid_for(c, cfg->csf);
+    if (!gr.built) { set_error("refresh before rebuild"); return MDG_ESTATE; }
+    if (gr.scratch_layout != cfg->layout) grid_bind_scratch(c, gr, cfg->layout);
+    grid_refresh(c, gr, cfg->layout);
+    return cuda_status("mdg_refresh");
+}
+
+int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg) {
+    CHECK_CTX(ctx);
+    if (int e = validate(cfg)) return e;
+    Context& c = ctx->c;
+    if (c.layout != cfg->layout) {
+        set_error(std::string("particle layout ") + (c.layout == MDG_AOS ? "AoS" : "SoA") +
+                  " does not match the configuration");
+        return MDG_EINVAL;
+    }
+    if (cudaMemsetAsync(c.scal.p, 0, sizeof(unsigned long long), c.stream) != cudaSuccess)
+        return cuda_status("counter reset");
+    if (c.n == 0) return MDG_OK;
+    if (cfg->container == MDG_VL) {
+        if (!c.vl.built) { set_error("compute before rebuild"); return MDG_ESTATE; }
+        vl_compute(c);
+    } else {
+        Grid& gr = *grid_for(c, cfg->csf);
+        if (!gr.built || gr.scratch_layout != cfg->layout) {
+            set_error("compute before rebuild/refresh");
+            return MDG_ESTATE;
+        }
+        lc_compute(c, gr, cfg->traversal, cfg->newton3, cfg->layout);
+        lc_fold_forces(c, gr, cfg->layout, cfg->traversal != MDG_C01);
+    }
+    return cuda_status("mdg_compute");
+}
+
+int mdg_eval_count(mdg_ctx* ctx, int64_t* count) {
+    CHECK_CTX(ctx);
+    Context& c = ctx->c;
+    if (cudaMemcpyAsync(c.h_scal, c.scal.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                        c.stream) != cudaSuccess ||
+        cudaStreamSynchronize(c.stream) != cudaSuccess)
+        return cuda_status("mdg_eval_count");
+    *count = (int64_t)c.h_scal[0];
+    return MDG_OK;
+}
+
+int mdg_drift_wrap(mdg_ctx* ctx, double dt) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    integ_drift_wrap(ctx->c, dt);
+    return cuda_status("mdg_drift_wrap");
+}
+
+int mdg_finish_kick(mdg_ctx* ctx, double dt, int has_gravity, double gravity) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    integ_finish_kick(ctx->c, dt, has_gravity, gravity);
+    return cuda_status("mdg_finish_kick");
+}
+
+int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    integ_sd_step(ctx->c, gamma, max_disp);
+    return cuda_status("mdg_sd_step");
+}
+
+int mdg_blowup(mdg_ctx* ctx, int* flag, int reset) {
+    CHECK_CTX(ctx);
+    Context& c = ctx->c;
+    if (cudaMemcpyAsync(c.h_scal + 2, c.scal.p + 2, sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost, c.stream) != cudaSuccess ||
+        cudaStreamSynchronize(c.stream) != cudaSuccess)
+        return cuda_status("mdg_blowup");
+    *flag = c.h_scal[2] ? 1 : 0;
+    if (reset) cudaMemsetAsync(c.scal.p + 2, 0, sizeof(unsigned long long), c.stream);
+    return cuda_status("mdg_blowup");
+}
+
+int mdg_synchronize(mdg_ctx* ctx) {
+    CHECK_CTX(ctx);
+    if (cudaStreamSynchronize(ctx->c.stream) != cudaSuccess) return cuda_status("synchronize");
+    return cuda_status("synchronize");
+}
+
+int mdg_h2d(mdg_ctx* ctx, void* dev, const void* host, size_t bytes) {
+    CHECK_CTX(ctx);
+    if (!bytes) return MDG_OK;
+    if (cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->c.stream) != cudaSuccess)
+        return cuda_status("mdg_h2d");
+    return MDG_OK;
+}
+
+int mdg_d2h(mdg_ctx* ctx, void* host, const void* dev, size_t bytes) {
+    CHECK_CTX(ctx);
+    if (!bytes) return MDG_OK;
+    if (cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->c.stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->c.stream) != cudaSuccess)
+        return cuda_status("mdg_d2h");
+    return MDG_OK;
+}
+
+int mdg_geometry(mdg_ctx* ctx, double csf, int dims_owned[3], double cell_length[3],
+                 int overlap[3], int halo[3], int dims[3]) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    if (csf != 1.0 && csf != 0.5) { set_error("csf must be 1 or 0.5"); return MDG_EINVAL; }
+    const Geom& g = grid_for(ctx->c, csf)->g;
+    for (int k = 0; k < 3; ++k) {
+        dims_owned[k] = g.S[k];
+        cell_length[k] = g.cl[k];
+        overlap[k] = g.overlap[k];
+        halo[k] = g.H[k];
+        dims[k] = g.D[k];
+    }
+    return MDG_OK;
+}
+
+int mdg_stencil(mdg_ctx* ctx, double csf, int kind, int major, int* count, int* out) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    if (csf != 1.0 && csf != 0.5) { set_error("csf must be 1 or 0.5"); return MDG_EINVAL; }
+    if (major < 0 || major > 2) { set_error("major axis must be 0..2"); return MDG_EINVAL; }
+    const Geom& g = grid_for(ctx->c, csf)->g;
+    Stencil s = kind == 0 ? pruned_stencil(g) : forward_stencil(g, major);
+    *count = s.n;
+    if (out) memcpy(out, s.d, sizeof(int) * 3 * s.n);
+    return MDG_OK;
+}
+
+int mdg_geometry_for(const double domain[3], const int periodic[3], double ell, double csf,
+                     int dims_owned[3], double cell_length[3], int overlap[3], int halo[3],
+                     int dims[3]) {
+    if (!(ell > 0) || (csf != 1.0 && csf != 0.5)) { set_error("bad geometry arguments"); return MDG_EINVAL; }
+    Geom g = make_geometry(domain, periodic, ell, csf);
+    for (int k = 0; k < 3; ++k) {
+        dims_owned[k] = g.S[k];
+        cell_length[k] = g.cl[k];
+        overlap[k] = g.overlap[k];
+        halo[k] = g.H[k];
+        dims[k] = g.D[k];
+    }
+    return MDG_OK;
+}
+
+int mdg_stencil_for(const double domain[3], const int periodic[3], double ell, double csf,
+                    int kind, int major, int* count, int* out) {
+    if (!(ell > 0) || (csf != 1.0 && csf != 0.5) || major < 0 || major > 2) {
+        set_error("bad stencil arguments");
+        return MDG_EINVAL;
+    }
+    Geom g = make_geometry(domain, periodic, ell, csf);
+    Stencil s = kind == 0 ? pruned_stencil(g) : forward_stencil(g, major);
+    *count = s.n;
+    if (out) memcpy(out, s.d, sizeof(int) * 3 * s.n);
+    return MDG_OK;
+}
+
+int mdg_get_grid(mdg_ctx* ctx, double csf, int64_t* m, int64_t* ncells, int32_t* src,
+                 int8_t* shift_code, int32_t* start) {
+    CHECK_CTX(ctx);
+    if (csf != 1.0 && csf != 0.5) { set_error("csf must be 1 or 0.5"); return MDG_EINVAL; }
+    Grid& gr = *grid_for(ctx->c, csf);
+    if (!gr.built) { set_error("grid not built"); return MDG_ESTATE; }
+    cudaStreamSynchronize(ctx->c.stream);
+    if (m) *m = gr.m;
+    if (ncells) *ncells = gr.g.ncells;
+    if (src && gr.m) cudaMemcpy(src, gr.row_src.p, gr.m * sizeof(int), cudaMemcpyDeviceToHost);
+    if (shift_code && gr.m)
+        cudaMemcpy(shift_code, gr.row_code.p, gr.m, cudaMemcpyDeviceToHost);
+    if (start) cudaMemcpy(start, gr.cell_start.p, (gr.g.ncells + 1) * sizeof(int), cudaMemcpyDeviceToHost);
+    return cuda_status("mdg_get_grid");
+}
+
+int mdg_get_verlet(mdg_ctx* ctx, int64_t* entries, int64_t* noff, int32_t* nbr) {
+    CHECK_CTX(ctx);
+    Verlet& v = ctx->c.vl;
+    if (!v.built) { set_error("Verlet lists not built"); return MDG_ESTATE; }
+    cudaStreamSynchronize(ctx->c.stream);
+    if (entries) *entries = v.entries;
+    if (noff) cudaMemcpy(noff, v.noff.p, (ctx->c.n + 1) * sizeof(long long), cudaMemcpyDeviceToHost);
+    if (nbr && v.entries) cudaMemcpy(nbr, v.nbr.p, v.entries * sizeof(int), cudaMemcpyDeviceToHost);
+    return cuda_status("mdg_get_verlet");
+}
+
+}  // extern "C"

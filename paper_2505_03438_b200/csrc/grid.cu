@@ -1,0 +1,539 @@
+// Cell geometry, the stable counting sort (binning) and the scratch
+// gather / force fold-back of the linked-cells container.
+//
+// Reference: cells.py:48-156 (geometry, stencils, cell coordinates, periodic
+// images), containers.py:78-171 (GridState.rebuild, LayoutBuffers).
+#include <math.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "device.cuh"
+
+namespace mdg {
+
+// ---------------------------------------------------------------- geometry
+
+Geom make_geometry(const double L[3], const int periodic[3], double ell, double csf) {
+    Geom g;
+    double target = csf * ell;
+    g.ell = ell;
+    g.csf = csf;
+    for (int k = 0; k < 3; ++k) {
+        g.L[k] = L[k];
+        g.periodic[k] = periodic[k] ? 1 : 0;
+        double q = floor(L[k] / target);
+        int s = q < 1.0 ? 1 : (int)q;
+        g.S[k] = s;
+        g.cl[k] = L[k] / (double)s;
+        int o = (int)floor(ell / g.cl[k]);
+        while ((double)o * g.cl[k] < ell) ++o;
+        g.overlap[k] = o < 1 ? 1 : o;
+        g.H[k] = g.periodic[k] ? g.overlap[k] : 0;
+        g.D[k] = s + 2 * g.H[k];
+    }
+    g.ncells = (int64_t)g.D[0] * g.D[1] * g.D[2];
+    return g;
+}
+
+static double box_min_dist2(const int d[3], const double cl[3]) {
+    double s = 0.0;
+    for (int k = 0; k < 3; ++k) {
+        double gap = (double)(abs(d[k]) - 1) * cl[k];
+        if (gap > 0.0) s += gap * gap;
+    }
+    return s;
+}
+
+// cells.py:80-95: product order over (-o..o)^3, (0,0,0) skipped.
+Stencil pruned_stencil(const Geom& g) {
+    Stencil st;
+    st.n = 0;
+    double ell2 = g.ell * g.ell;
+    for (int x = -g.overlap[0]; x <= g.overlap[0]; ++x)
+        for (int y = -g.overlap[1]; y <= g.overlap[1]; ++y)
+            for (int z = -g.overlap[2]; z <= g.overlap[2]; ++z) {
+                if (!x && !y && !z) continue;
+                int d[3] = {x, y, z};
+                if (box_min_dist2(d, g.cl) <= ell2 && st.n < kMaxStencil) {
+                    st.d[st.n][0] = x; st.d[st.n][1] = y; st.d[st.n][2] = z;
+                    ++st.n;
+                }
+            }
+    return st;
+}
+
+// cells.py:98-111: keep offsets that are lexicographically positive with the
+// major axis first.
+Stencil forward_stencil(const Geom& g, int major) {
+    Stencil all = pruned_stencil(g), st;
+    st.n = 0;
+    int order[3] = {major, major == 0 ? 1 : 0, major == 2 ? 1 : 2};
+    for (int i = 0; i < all.n; ++i) {
+        int a = all.d[i][order[0]], b = all.d[i][order[1]], c = all.d[i][order[2]];
+        bool pos = a > 0 || (a == 0 && (b > 0 || (b == 0 && c > 0)));
+        if (pos) {
+            std::memcpy(st.d[st.n], all.d[i], sizeof(all.d[i]));
+            ++st.n;
+        }
+    }
+    return st;
+}
+
+// ---------------------------------------------------------------- buffers
+
+template <class T>
+void DBuf<T>::ensure(size_t n) {
+    if (n <= cap && p) return;
+    size_t want = std::max<size_t>(n + n / 8, 64);
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    if (cudaMalloc(&p, want * sizeof(T)) == cudaSuccess) cap = want;
+    else p = nullptr;
+}
+
+template <class T>
+void DBuf<T>::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+}
+
+template struct DBuf<int>;
+template struct DBuf<uint8_t>;
+template struct DBuf<double>;
+template struct DBuf<double4>;
+template struct DBuf<long long>;
+template struct DBuf<unsigned long long>;
+
+void Grid::release() {
+    cell_count.release(); cell_start.release(); cell_fill.release();
+    img_cnt.release(); img_off.release(); img_src.release(); img_code.release();
+    tmp_ent.release(); row_ent.release(); row_src.release(); row_cell.release();
+    row_tid.release(); inv.release(); row_code.release();
+    spos4.release(); spos3.release(); sforce.release();
+    built = false;
+}
+
+void Verlet::release() {
+    grid.release(); bpos.release(); counts.release(); noff.release(); nbr.release();
+    built = false;
+}
+
+// ---------------------------------------------------------------- scans
+
+// Exclusive scan, three phases over tiles of 2048 elements: per-tile sums,
+// a single-CTA scan of the tile sums, then per-tile warp-shuffle scans.
+constexpr int kScanThreads = 512;
+constexpr int kScanPer = 4;
+constexpr int kTile = kScanThreads * kScanPer;
+
+template <class TI>
+__global__ void scan_tile_sums(const TI* __restrict__ in, int64_t n, unsigned long long* sums) {
+    __shared__ unsigned long long ws[kScanThreads / 32];
+    int64_t base = (int64_t)blockIdx.x * kTile;
+    unsigned long long s = 0;
+    for (int k = 0; k < kScanPer; ++k) {
+        int64_t i = base + (int64_t)k * kScanThreads + threadIdx.x;
+        if (i < n) s += (unsigned long long)in[i];
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned long long v = threadIdx.x < kScanThreads / 32 ? ws[threadIdx.x] : 0;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) sums[blockIdx.x] = v;
+    }
+}
+
+__device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long v) {
+    int lane = threadIdx.x & 31;
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the block total.
+__device__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long& total) {
+    __shared__ unsigned long long ws[32];
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned long long inc = warp_incl_scan(v);
+    if (lane == 31) ws[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long x = lane < nw ? ws[lane] : 0;
+        unsigned long long xi = warp_incl_scan(x);
+        if (lane < nw) ws[lane] = xi - x;
+        if (lane == 31) ws[31] = xi;   // nw <= 31 here (512 threads -> 16 warps)
+    }
+    __syncthreads();
+    unsigned long long r = inc - v + ws[w];
+    total = ws[31];
+    __syncthreads();
+    return r;
+}
+
+__global__ void scan_sums_single(unsigned long long* sums, int64_t nt, unsigned long long* total) {
+    unsigned long long carry = 0;
+    for (int64_t b = 0; b < nt; b += blockDim.x) {
+        int64_t i = b + threadIdx.x;
+        unsigned long long v = i < nt ? sums[i] : 0, tot;
+        unsigned long long e = block_excl_scan(v, tot);
+        if (i < nt) sums[i] = e + carry;
+        carry += tot;
+    }
+    if (threadIdx.x == 0 && total) *total = carry;
+}
+
+template <class TI, class TO>
+__global__ void scan_tiles(const TI* __restrict__ in, TO* __restrict__ out, int64_t n,
+                           const unsigned long long* __restrict__ sums) {
+    int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kScanPer;
+    unsigned long long v[kScanPer], loc = 0;
+    for (int k = 0; k < kScanPer; ++k) {
+        int64_t i = base + k;
+        v[k] = i < n ? (unsigned long long)in[i] : 0;
+        loc += v[k];
+    }
+    unsigned long long tot;
+    unsigned long long e = block_excl_scan(loc, tot) + sums[blockIdx.x];
+    for (int k = 0; k < kScanPer; ++k) {
+        int64_t i = base + k;
+        if (i < n) out[i] = (TO)e;
+        e += v[k];
+    }
+}
+
+template <class TI, class TO>
+static void scan_impl(const TI* in, TO* out, int64_t n, unsigned long long* total,
+                      DBuf<unsigned long long>& tmp, cudaStream_t s) {
+    int64_t nt = (n + kTile - 1) / kTile;
+    if (nt < 1) nt = 1;
+    tmp.ensure((size_t)nt);
+    scan_tile_sums<TI><<<(unsigned)nt, kScanThreads, 0, s>>>(in, n, tmp.p), note_launch();
+    scan_sums_single<<<1, kScanThreads, 0, s>>>(tmp.p, nt, total), note_launch();
+    scan_tiles<TI, TO><<<(unsigned)nt, kScanThreads, 0, s>>>(in, out, n, tmp.p), note_launch();
+}
+
+void exclusive_scan_i32(const int* in, int* out, int64_t n, unsigned long long* total,
+                        DBuf<unsigned long long>& tmp, cudaStream_t s) {
+    scan_impl<int, int>(in, out, n, total, tmp, s);
+}
+
+void exclusive_scan_i32_to_i64(const int* in, long long* out, int64_t n,
+                               unsigned long long* total, DBuf<unsigned long long>& tmp,
+                               cudaStream_t s) {
+    scan_impl<int, long long>(in, out, n, total, tmp, s);
+}
+
+// ---------------------------------------------------------------- binning
+
+struct BinParams {
+    double cl[3];
+    int S[3], H[3], D[3], periodic[3];
+    int64_t n;
+};
+
+// bin_cell_coords (cells.py:114-119): floor(x / cell_len) with IEEE division,
+// clipped to the owned range; NaN/inf land in cell 0 like numpy's cast+clip.
+__device__ __forceinline__ int cell_coord(double x, double cl, int S) {
+    double f = floor(x / cl);
+    if (!(f >= 0.0)) return 0;            // negative, NaN, -inf
+    if (f > (double)(S - 1)) return S - 1;  // includes +inf
+    return (int)f;
+}
+
+template <int LAYOUT>
+__device__ __forceinline__ void load_pos(const double* pos, int64_t i, int64_t n, double& x,
+                                         double& y, double& z) {
+    x = pos[pidx<LAYOUT>(i, 0, n)];
+    y = pos[pidx<LAYOUT>(i, 1, n)];
+    z = pos[pidx<LAYOUT>(i, 2, n)];
+}
+
+// Image combos in the reference's product order (cells.py:134-150): axis
+// options (-1, 0, 1) on periodic axes, the combo (0,0,0) skipped; an image
+// exists when every nonzero shift is allowed (s>0: c<H, s<0: c>=S-H).
+// `fn(code, cell)` is called per image in that order; returns the count.
+template <class F>
+__device__ __forceinline__ int for_each_image(const BinParams& p, const int c[3], F fn) {
+    int cnt = 0;
+    int lo[3], hi[3];
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = p.periodic[k] ? -1 : 0;
+        hi[k] = p.periodic[k] ? 1 : 0;
+    }
+    for (int sx = lo[0]; sx <= hi[0]; ++sx) {
+        if ((sx > 0 && !(c[0] < p.H[0])) || (sx < 0 && !(c[0] >= p.S[0] - p.H[0]))) continue;
+        for (int sy = lo[1]; sy <= hi[1]; ++sy) {
+            if ((sy > 0 && !(c[1] < p.H[1])) || (sy < 0 && !(c[1] >= p.S[1] - p.H[1]))) continue;
+            for (int sz = lo[2]; sz <= hi[2]; ++sz) {
+                if (!sx && !sy && !sz) continue;
+                if ((sz > 0 && !(c[2] < p.H[2])) || (sz < 0 && !(c[2] >= p.S[2] - p.H[2]))) continue;
+                int ix = c[0] + sx * p.S[0] + p.H[0];
+                int iy = c[1] + sy * p.S[1] + p.H[1];
+                int iz = c[2] + sz * p.S[2] + p.H[2];
+                int code = (sx + 1) * 9 + (sy + 1) * 3 + (sz + 1);
+                fn(code, (ix * p.D[1] + iy) * p.D[2] + iz);
+                ++cnt;
+            }
+        }
+    }
+    return cnt;
+}
+
+template <int LAYOUT>
+__global__ void bin_count_kernel(const double* __restrict__ pos, BinParams p,
+                                 int* __restrict__ cell_count, int* __restrict__ img_cnt) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    double x, y, z;
+    load_pos<LAYOUT>(pos, i, p.n, x, y, z);
+    int c[3] = {cell_coord(x, p.cl[0], p.S[0]), cell_coord(y, p.cl[1], p.S[1]),
+                cell_coord(z, p.cl[2], p.S[2])};
+    int own = ((c[0] + p.H[0]) * p.D[1] + c[1] + p.H[1]) * p.D[2] + c[2] + p.H[2];
+    atomicAdd(cell_count + own, 1);
+    int k = for_each_image(p, c, [&](int, int cell) { atomicAdd(cell_count + cell, 1); });
+    img_cnt[i] = k;
+}
+
+template <int LAYOUT>
+__global__ void bin_scatter_kernel(const double* __restrict__ pos, BinParams p,
+                                   const int* __restrict__ cell_start, int* __restrict__ cell_fill,
+                                   const int* __restrict__ img_off, int* __restrict__ img_src,
+                                   uint8_t* __restrict__ img_code, int* __restrict__ tmp_ent) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    double x, y, z;
+    load_pos<LAYOUT>(pos, i, p.n, x, y, z);
+    int c[3] = {cell_coord(x, p.cl[0], p.S[0]), cell_coord(y, p.cl[1], p.S[1]),
+                cell_coord(z, p.cl[2], p.S[2])};
+    int own = ((c[0] + p.H[0]) * p.D[1] + c[1] + p.H[1]) * p.D[2] + c[2] + p.H[2];
+    tmp_ent[cell_start[own] + atomicAdd(cell_fill + own, 1)] = (int)i;
+    int base = img_off[i];
+    int q = 0;
+    for_each_image(p, c, [&](int code, int cell) {
+        int e = base + q;
+        img_src[e] = (int)i;
+        img_code[e] = (uint8_t)code;
+        tmp_ent[cell_start[cell] + atomicAdd(cell_fill + cell, 1)] = (int)(p.n + e);
+        ++q;
+    });
+}
+
+// Per-cell ordering fix: entries of one cell sorted by entry id (== the
+// reference's stable argsort order, containers.py:107).  One warp per cell;
+// cells up to 32 entries rank through shuffles, larger ones by counting.
+__global__ void cell_sort_kernel(int64_t ncells, int64_t n, const int* __restrict__ cell_start,
+                                 const int* __restrict__ tmp_ent, const int* __restrict__ img_src,
+                                 const uint8_t* __restrict__ img_code, const int* __restrict__ tid,
+                                 int* __restrict__ row_ent, int* __restrict__ row_src,
+                                 uint8_t* __restrict__ row_code, int* __restrict__ row_cell,
+                                 int* __restrict__ row_tid, int* __restrict__ inv) {
+    int64_t cell = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (cell >= ncells) return;
+    int s = cell_start[cell], e = cell_start[cell + 1], k = e - s;
+    if (k == 0) return;
+    auto emit = [&](int r, int ent) {
+        row_ent[r] = ent;
+        int src = ent < n ? ent : img_src[ent - n];
+        row_src[r] = src;
+        row_code[r] = ent < n ? (uint8_t)kNoShift : img_code[ent - n];
+        row_cell[r] = (int)cell;
+        row_tid[r] = tid ? tid[src] : 0;
+        inv[ent] = r;
+    };
+    if (k <= 32) {
+        int v = lane < k ? tmp_ent[s + lane] : 0x7fffffff;
+        int rank = 0;
+        for (int j = 0; j < 32; ++j) {
+            int o = __shfl_sync(0xffffffffu, v, j);
+            rank += (o < v);
+        }
+        if (lane < k) emit(s + rank, v);
+    } else {
+        for (int a = lane; a < k; a += 32) {
+            int v = tmp_ent[s + a], rank = 0;
+            for (int b = 0; b < k; ++b) rank += (tmp_ent[s + b] < v);
+            emit(s + rank, v);
+        }
+    }
+}
+
+int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
+    cudaStream_t st = c.stream;
+    int64_t n = c.n;
+    gr.n = n;
+    BinParams p;
+    for (int k = 0; k < 3; ++k) {
+        p.cl[k] = gr.g.cl[k]; p.S[k] = gr.g.S[k]; p.H[k] = gr.g.H[k];
+        p.D[k] = gr.g.D[k]; p.periodic[k] = gr.g.periodic[k];
+    }
+    p.n = n;
+    int64_t nc = gr.g.ncells;
+    gr.cell_count.ensure(nc + 1);
+    gr.cell_start.ensure(nc + 1);
+    gr.cell_fill.ensure(nc + 1);
+    gr.img_cnt.ensure(n + 1);
+    gr.img_off.ensure(n + 1);
+    MDG_CUDA(cudaMemsetAsync(gr.cell_count.p, 0, (nc + 1) * sizeof(int), st));
+    MDG_CUDA(cudaMemsetAsync(gr.cell_fill.p, 0, (nc + 1) * sizeof(int), st));
+    if (n > 0) {
+        if (layout == AOS)
+            bin_count_kernel<AOS><<<blocks_for(n, 256), 256, 0, st>>>(pos, p, gr.cell_count.p, gr.img_cnt.p), note_launch();
+        else
+            bin_count_kernel<SOA><<<blocks_for(n, 256), 256, 0, st>>>(pos, p, gr.cell_count.p, gr.img_cnt.p), note_launch();
+    }
+    // images total and cell offsets; the totals land in the pinned mirror
+    exclusive_scan_i32(gr.img_cnt.p, gr.img_off.p, n, c.scal.p + 1, c.scan_tmp, st);
+    MDG_CUDA(cudaMemcpyAsync(c.h_scal + 1, c.scal.p + 1, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st));
+    exclusive_scan_i32(gr.cell_count.p, gr.cell_start.p, nc + 1, nullptr, c.scan_tmp, st);
+    MDG_CUDA(cudaStreamSynchronize(st));
+    gr.nimg = (int64_t)c.h_scal[1];
+    gr.m = n + gr.nimg;
+    int64_t m = gr.m;
+    gr.img_src.ensure(gr.nimg + 1);
+    gr.img_code.ensure(gr.nimg + 1);
+    gr.tmp_ent.ensure(m + 1);
+    gr.row_ent.ensure(m + 1);
+    gr.row_src.ensure(m + 1);
+    gr.row_code.ensure(m + 1);
+    gr.row_cell.ensure(m + 1);
+    gr.row_tid.ensure(m + 1);
+    gr.inv.ensure(m + 1);
+    if (n > 0) {
+        if (layout == AOS)
+            bin_scatter_kernel<AOS><<<blocks_for(n, 256), 256, 0, st>>>(
+                pos, p, gr.cell_start.p, gr.cell_fill.p, gr.img_off.p, gr.img_src.p, gr.img_code.p,
+                gr.tmp_ent.p), note_launch();
+        else
+            bin_scatter_kernel<SOA><<<blocks_for(n, 256), 256, 0, st>>>(
+                pos, p, gr.cell_start.p, gr.cell_fill.p, gr.img_off.p, gr.img_src.p, gr.img_code.p,
+                gr.tmp_ent.p), note_launch();
+        cell_sort_kernel<<<blocks_for(nc * 32, 256), 256, 0, st>>>(
+            nc, n, gr.cell_start.p, gr.tmp_ent.p, gr.img_src.p, gr.img_code.p, c.tid,
+            gr.row_ent.p, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gr.row_tid.p, gr.inv.p), note_launch();
+    }
+    MDG_CUDA(cudaGetLastError());
+    gr.built = true;
+    gr.scratch_layout = -1;
+    return 0;
+}
+
+// ---------------------------------------------------------------- scratch
+
+void grid_bind_scratch(Context& c, Grid& gr, int layout) {
+    int64_t m = gr.m;
+    if (layout == AOS) gr.spos4.ensure(m + 1);
+    else gr.spos3.ensure(3 * m + 3);
+    gr.sforce.ensure(3 * m + 3);
+    gr.scratch_layout = layout;
+}
+
+struct ShiftL {
+    double L[3];
+};
+
+__device__ __forceinline__ void decode_shift(int code, const ShiftL& s, double& dx, double& dy,
+                                             double& dz) {
+    // shift = combo * L exactly (cells.py:146), combo in {-1,0,1}
+    dx = (double)(code / 9 - 1) * s.L[0];
+    dy = (double)((code / 3) % 3 - 1) * s.L[1];
+    dz = (double)(code % 3 - 1) * s.L[2];
+}
+
+// LayoutBuffers.refresh (containers.py:147-154): pos[src] + shift per row.
+template <int PLAYOUT, int SLAYOUT>
+__global__ void refresh_kernel(const double* __restrict__ pos, int64_t n, int m,
+                               const int* __restrict__ row_src, const uint8_t* __restrict__ row_code,
+                               const int* __restrict__ row_tid, ShiftL sl, double4* __restrict__ s4,
+                               double* __restrict__ s3) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    int src = row_src[r];
+    double sx, sy, sz;
+    decode_shift(row_code[r], sl, sx, sy, sz);
+    double x = pos[pidx<PLAYOUT>(src, 0, n)] + sx;
+    double y = pos[pidx<PLAYOUT>(src, 1, n)] + sy;
+    double z = pos[pidx<PLAYOUT>(src, 2, n)] + sz;
+    if (SLAYOUT == AOS) {
+        s4[r] = make_double4(x, y, z, (double)row_tid[r]);
+    } else {
+        s3[r] = x;
+        s3[(size_t)m + r] = y;
+        s3[2 * (size_t)m + r] = z;
+    }
+}
+
+void grid_refresh(Context& c, Grid& gr, int layout) {
+    int m = (int)gr.m;
+    if (m == 0) return;
+    ShiftL sl{{c.L[0], c.L[1], c.L[2]}};
+    dim3 b(blocks_for(m, 256)), t(256);
+    // the scratch layout follows the configuration; the particle arrays follow
+    // the ParticleSet (they agree after convert_layout, simulation.py:161-163)
+    if (c.layout == AOS) {
+        if (layout == AOS)
+            refresh_kernel<AOS, AOS><<<b, t, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_tid.p, sl, gr.spos4.p, gr.spos3.p), note_launch();
+        else
+            refresh_kernel<AOS, SOA><<<b, t, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_tid.p, sl, gr.spos4.p, gr.spos3.p), note_launch();
+    } else {
+        if (layout == AOS)
+            refresh_kernel<SOA, AOS><<<b, t, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_tid.p, sl, gr.spos4.p, gr.spos3.p), note_launch();
+        else
+            refresh_kernel<SOA, SOA><<<b, t, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_tid.p, sl, gr.spos4.p, gr.spos3.p), note_launch();
+    }
+}
+
+// LayoutBuffers.scatter_forces (containers.py:156-171) as a gather: owned row
+// assigned, image rows added (images of one particle in combo order).
+template <int PLAYOUT, int SLAYOUT>
+__global__ void fold_kernel(int64_t n, int m, const int* __restrict__ inv,
+                            const int* __restrict__ img_cnt, const int* __restrict__ img_off,
+                            const double* __restrict__ sf, double* __restrict__ force,
+                            bool images) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    auto get = [&](int r, int k) {
+        return SLAYOUT == AOS ? sf[3 * (size_t)r + k] : sf[(size_t)k * m + r];
+    };
+    int r0 = inv[i];
+    double fx = get(r0, 0), fy = get(r0, 1), fz = get(r0, 2);
+    if (images) {
+        int q0 = img_off[i], nq = img_cnt[i];
+        for (int q = 0; q < nq; ++q) {
+            int r = inv[n + q0 + q];
+            fx += get(r, 0);
+            fy += get(r, 1);
+            fz += get(r, 2);
+        }
+    }
+    force[pidx<PLAYOUT>(i, 0, n)] = fx;
+    force[pidx<PLAYOUT>(i, 1, n)] = fy;
+    force[pidx<PLAYOUT>(i, 2, n)] = fz;
+}
+
+void lc_fold_forces(Context& c, Grid& gr, int layout, bool images) {
+    if (c.n == 0) return;
+    dim3 b(blocks_for(c.n, 256)), t(256);
+    int m = (int)gr.m;
+    if (c.layout == AOS) {
+        if (layout == AOS)
+            fold_kernel<AOS, AOS><<<b, t, 0, c.stream>>>(c.n, m, gr.inv.p, gr.img_cnt.p, gr.img_off.p, gr.sforce.p, c.force, images), note_launch();
+        else
+            fold_kernel<AOS, SOA><<<b, t, 0, c.stream>>>(c.n, m, gr.inv.p, gr.img_cnt.p, gr.img_off.p, gr.sforce.p, c.force, images), note_launch();
+    } else {
+        if (layout == AOS)
+            fold_kernel<SOA, AOS><<<b, t, 0, c.stream>>>(c.n, m, gr.inv.p, gr.img_cnt.p, gr.img_off.p, gr.sforce.p, c.force, images), note_launch();
+        else
+            fold_kernel<SOA, SOA><<<b, t, 0, c.stream>>>(c.n, m, gr.inv.p, gr.img_cnt.p, gr.img_off.p, gr.sforce.p, c.force, images), note_launch();
+    }
+}
+
+}  // namespace mdg

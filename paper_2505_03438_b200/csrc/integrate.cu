@@ -1,0 +1,154 @@
+// Störmer-Verlet update split the reference's way, on device.
+//
+// Reference: integrator.py:31-44 (drift_with_force, finish_kick), :47-51
+// (gravity), :98-128 (boundaries + BlowUpError), simulation.py:151-153,177,185
+// (loop order: drift, boundaries, F -> F_old, ..., gravity, finish_kick).
+// Arithmetic uses explicit round-to-nearest intrinsics so no multiply-add is
+// contracted: the update is bit-identical to the reference's numpy sequence.
+#include "device.cuh"
+
+namespace mdg {
+
+struct BoxParams {
+    double L[3];
+    int periodic[3];
+    double dt;
+    int64_t n;
+};
+
+// np.mod(x, L) (integrator.py:118): fmod with sign fix, +0.0 for exact zeros.
+__device__ __forceinline__ double np_mod(double x, double L) {
+    double r = fmod(x, L);
+    if (r != 0.0) {
+        if ((r < 0.0) != (L < 0.0)) r = __dadd_rn(r, L);
+    } else {
+        r = 0.0;
+    }
+    return r;
+}
+
+template <int LAYOUT>
+__global__ void drift_wrap_kernel(BoxParams p, const int* __restrict__ tid,
+                                  const double* __restrict__ mass, double* __restrict__ pos,
+                                  double* __restrict__ vel, const double* __restrict__ force,
+                                  double* __restrict__ old_force, unsigned long long* blowup) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    double m = mass[tid ? tid[i] : 0];
+    double c = __ddiv_rn(__dmul_rn(__dmul_rn(0.5, p.dt), p.dt), m);
+    bool bad = false;
+    for (int k = 0; k < 3; ++k) {
+        size_t a = pidx<LAYOUT>(i, k, p.n);
+        double f = force[a];
+        double x = __dadd_rn(pos[a], __dmul_rn(vel[a], p.dt));
+        x = __dadd_rn(x, __dmul_rn(f, c));
+        double L = p.L[k];
+        if (!(x >= -L && x <= 2.0 * L)) bad = true;
+        if (p.periodic[k]) {
+            x = np_mod(x, L);
+        } else if (x < 0.0) {
+            x = -x;
+            vel[a] = -vel[a];
+        } else if (x > L) {
+            x = __dadd_rn(2.0 * L, -x);
+            vel[a] = -vel[a];
+        }
+        pos[a] = x;
+        old_force[a] = f;
+    }
+    if (bad) atomicOr(blowup, 1ull);
+}
+
+template <int LAYOUT>
+__global__ void finish_kick_kernel(BoxParams p, const int* __restrict__ tid,
+                                   const double* __restrict__ mass, double* __restrict__ vel,
+                                   double* __restrict__ force, const double* __restrict__ old_force,
+                                   int has_gravity, double g) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    double m = mass[tid ? tid[i] : 0];
+    if (has_gravity) {
+        size_t a = pidx<LAYOUT>(i, 2, p.n);
+        force[a] = __dadd_rn(force[a], __dmul_rn(m, g));
+    }
+    double c = __ddiv_rn(__dmul_rn(0.5, p.dt), m);
+    for (int k = 0; k < 3; ++k) {
+        size_t a = pidx<LAYOUT>(i, k, p.n);
+        vel[a] = __dadd_rn(vel[a], __dmul_rn(__dadd_rn(force[a], old_force[a]), c));
+    }
+}
+
+// Capped steepest descent used to relax overlapping random inputs (BASELINE
+// configs 2 and 4; no reference counterpart): x += F/|F| * min(gamma|F|, dmax),
+// then the boundary rule of the axis.
+template <int LAYOUT>
+__global__ void sd_step_kernel(BoxParams p, double* __restrict__ pos, double* __restrict__ vel,
+                               const double* __restrict__ force, double gamma, double dmax,
+                               unsigned long long* blowup) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    double f[3];
+    for (int k = 0; k < 3; ++k) f[k] = force[pidx<LAYOUT>(i, k, p.n)];
+    double fn = sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+    double scale = 0.0;
+    if (fn > 0.0) {
+        double d = gamma * fn;
+        if (d > dmax) d = dmax;
+        scale = d / fn;
+    }
+    bool bad = false;
+    for (int k = 0; k < 3; ++k) {
+        size_t a = pidx<LAYOUT>(i, k, p.n);
+        double x = pos[a] + scale * f[k];
+        double L = p.L[k];
+        if (!(x >= -L && x <= 2.0 * L)) bad = true;
+        if (p.periodic[k]) x = np_mod(x, L);
+        else if (x < 0.0) x = -x;
+        else if (x > L) x = 2.0 * L - x;
+        pos[a] = x;
+    }
+    if (bad) atomicOr(blowup, 1ull);
+}
+
+static BoxParams box(const Context& c, double dt) {
+    BoxParams p;
+    for (int k = 0; k < 3; ++k) {
+        p.L[k] = c.L[k];
+        p.periodic[k] = c.periodic[k];
+    }
+    p.dt = dt;
+    p.n = c.n;
+    return p;
+}
+
+void integ_drift_wrap(Context& c, double dt) {
+    if (c.n == 0) return;
+    BoxParams p = box(c, dt);
+    dim3 b(blocks_for(c.n, 256)), t(256);
+    if (c.layout == AOS)
+        drift_wrap_kernel<AOS><<<b, t, 0, c.stream>>>(p, c.tid, c.d_mass.p, c.pos, c.vel, c.force, c.old_force, c.scal.p + 2), note_launch();
+    else
+        drift_wrap_kernel<SOA><<<b, t, 0, c.stream>>>(p, c.tid, c.d_mass.p, c.pos, c.vel, c.force, c.old_force, c.scal.p + 2), note_launch();
+}
+
+void integ_finish_kick(Context& c, double dt, int has_gravity, double gravity) {
+    if (c.n == 0) return;
+    BoxParams p = box(c, dt);
+    dim3 b(blocks_for(c.n, 256)), t(256);
+    if (c.layout == AOS)
+        finish_kick_kernel<AOS><<<b, t, 0, c.stream>>>(p, c.tid, c.d_mass.p, c.vel, c.force, c.old_force, has_gravity, gravity), note_launch();
+    else
+        finish_kick_kernel<SOA><<<b, t, 0, c.stream>>>(p, c.tid, c.d_mass.p, c.vel, c.force, c.old_force, has_gravity, gravity), note_launch();
+}
+
+void integ_sd_step(Context& c, double gamma, double dmax) {
+    if (c.n == 0) return;
+    BoxParams p = box(c, 0.0);
+    dim3 b(blocks_for(c.n, 256)), t(256);
+    if (c.layout == AOS)
+        sd_step_kernel<AOS><<<b, t, 0, c.stream>>>(p, c.pos, c.vel, c.force, gamma, dmax, c.scal.p + 2), note_launch();
+    else
+        sd_step_kernel<SOA><<<b, t, 0, c.stream>>>(p, c.pos, c.vel, c.force, gamma, dmax, c.scal.p + 2), note_launch();
+}
+
+}  // namespace mdg

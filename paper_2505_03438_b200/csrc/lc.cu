@@ -1,0 +1,412 @@
+// Linked-cells force traversals on the cell-sorted scratch arrays.
+//
+// Reference: kernels.py:24-725 (pair blocks, C08/forward/directed sweeps) and
+// the schedules of containers.py:176-335.  GPU realisation per traversal:
+//
+//   C01  thread per owned row, gathers own cell + full pruned stencil, writes
+//        only its own row (no atomics)                      kernels.py:584-725
+//   SLI  thread per owned row, own cell (j>i) + forward stencil, all writes
+//        through fp64 RED (the lock-free analogue of the seam locks,
+//        containers.py:288-322)                             kernels.py:493-579
+//   C18  one launch per base colour (strides o+1, 2o+1, 2o+1); one warp per base
+//        cell; cell pairs processed as 32x32 rotation tiles (lane l pairs its i
+//        with j=(l+k) mod P at step k, so j-side updates never collide) and
+//        flushed with plain stores: same-colour bases touch disjoint cells
+//                                                           containers.py:269-287
+//   C08  one launch per anchor colour (stride o+1 per axis); one warp per anchor
+//        block, same rotation tiles, plain stores           kernels.py:373-488
+//
+// N3L: one evaluation per pair, reaction subtracted from j (count 1).
+// NoN3L: both directions evaluated separately, each counted (count 2), exactly
+// as the reference's _pair_no3/_intra_no3 blocks.
+#include "device.cuh"
+
+namespace mdg {
+
+enum Traversal { T_C01 = 0, T_C08 = 1, T_C18 = 2, T_SLI = 3 };
+
+template <int LAYOUT, bool MT>
+__device__ __forceinline__ bool pair_force(const ScratchPos<LAYOUT>& sp, const LJTab& tab, int j,
+                                           double xi, double yi, double zi, int ti, double& dx,
+                                           double& dy, double& dz, double& fs, int& tj) {
+    double xj, yj, zj;
+    sp.load(j, xj, yj, zj, tj);
+    dx = xi - xj;
+    dy = yi - yj;
+    dz = zi - zj;
+    double r2 = dx * dx + dy * dy + dz * dz;
+    if (!(r2 < tab.rc2)) return false;
+    double s2, e24;
+    lj_params<MT>(tab, ti, tj, s2, e24);
+    fs = lj_fs(r2, s2, e24);
+    return true;
+}
+
+// ------------------------------------------------------------------ C01
+
+template <int LAYOUT, bool MT>
+__global__ void __launch_bounds__(128) lc_c01_kernel(GridView gv, ScratchPos<LAYOUT> sp,
+                                                     ScratchForce<LAYOUT> sf, LJTab tab, Stencil st,
+                                                     unsigned long long* counter) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned cnt = 0;
+    if (r < gv.m) {
+        int cell = gv.row_cell[r], cx, cy, cz;
+        gv.decode(cell, cx, cy, cz);
+        if (gv.owned(cx, cy, cz)) {
+            double xi, yi, zi;
+            int ti;
+            sp.load(r, xi, yi, zi, ti);
+            double fx = 0.0, fy = 0.0, fz = 0.0;
+            auto visit = [&](int j) {
+                double dx, dy, dz, fs;
+                int tj;
+                if (pair_force<LAYOUT, MT>(sp, tab, j, xi, yi, zi, ti, dx, dy, dz, fs, tj)) {
+                    ++cnt;
+                    fx += fs * dx;
+                    fy += fs * dy;
+                    fz += fs * dz;
+                }
+            };
+            int s = gv.start[cell], e = gv.start[cell + 1];
+            for (int j = s; j < e; ++j)
+                if (j != r) visit(j);
+            for (int k = 0; k < st.n; ++k) {
+                int x2 = cx + st.d[k][0], y2 = cy + st.d[k][1], z2 = cz + st.d[k][2];
+                if (!gv.in_grid(x2, y2, z2)) continue;
+                int c2 = gv.flat(x2, y2, z2);
+                int e2 = gv.start[c2 + 1];
+                for (int j = gv.start[c2]; j < e2; ++j) visit(j);
+            }
+            *sf.at(r, 0) = fx;
+            *sf.at(r, 1) = fy;
+            *sf.at(r, 2) = fz;
+        }
+    }
+    warp_count(counter, cnt);
+}
+
+// ------------------------------------------------------------------ SLI (atomics)
+
+template <int LAYOUT, bool MT, bool N3L>
+__global__ void __launch_bounds__(128) lc_fwd_atomic_kernel(GridView gv, ScratchPos<LAYOUT> sp,
+                                                            ScratchForce<LAYOUT> sf, LJTab tab,
+                                                            Stencil st,
+                                                            unsigned long long* counter) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned cnt = 0;
+    if (r < gv.m) {
+        int cell = gv.row_cell[r], cx, cy, cz;
+        gv.decode(cell, cx, cy, cz);
+        if (gv.owned(cx, cy, cz)) {
+            double xi, yi, zi;
+            int ti;
+            sp.load(r, xi, yi, zi, ti);
+            double fx = 0.0, fy = 0.0, fz = 0.0;
+            auto visit = [&](int j) {
+                double dx, dy, dz, fs;
+                int tj;
+                if (pair_force<LAYOUT, MT>(sp, tab, j, xi, yi, zi, ti, dx, dy, dz, fs, tj)) {
+                    fx += fs * dx;
+                    fy += fs * dy;
+                    fz += fs * dz;
+                    if (N3L) {
+                        ++cnt;
+                        atomicAdd(sf.at(j, 0), -(fs * dx));
+                        atomicAdd(sf.at(j, 1), -(fs * dy));
+                        atomicAdd(sf.at(j, 2), -(fs * dz));
+                    } else {
+                        // reverse direction evaluated on its own (kernels.py:86-98)
+                        double bx = -dx, by = -dy, bz = -dz;
+                        double s2, e24;
+                        lj_params<MT>(tab, tj, ti, s2, e24);
+                        double gs = lj_fs(bx * bx + by * by + bz * bz, s2, e24);
+                        cnt += 2;
+                        atomicAdd(sf.at(j, 0), gs * bx);
+                        atomicAdd(sf.at(j, 1), gs * by);
+                        atomicAdd(sf.at(j, 2), gs * bz);
+                    }
+                }
+            };
+            int e = gv.start[cell + 1];
+            for (int j = r + 1; j < e; ++j) visit(j);
+            for (int k = 0; k < st.n; ++k) {
+                int x2 = cx + st.d[k][0], y2 = cy + st.d[k][1], z2 = cz + st.d[k][2];
+                if (!gv.in_grid(x2, y2, z2)) continue;
+                int c2 = gv.flat(x2, y2, z2);
+                int e2 = gv.start[c2 + 1];
+                for (int j = gv.start[c2]; j < e2; ++j) visit(j);
+            }
+            atomicAdd(sf.at(r, 0), fx);
+            atomicAdd(sf.at(r, 1), fy);
+            atomicAdd(sf.at(r, 2), fz);
+        }
+    }
+    warp_count(counter, cnt);
+}
+
+// ------------------------------------------------------------------ colour tiles
+
+struct WarpTile {
+    double x[32], y[32], z[32];
+    double fx[32], fy[32], fz[32];
+    int t[32];
+};
+
+// i-rows i0..i0+ni-1 sit in the lanes (registers), j-rows j0..j0+nj-1 are
+// staged in shared memory.  tri: same chunk, pairs j > i only.
+template <int LAYOUT, bool MT, bool N3L>
+__device__ __forceinline__ void tile(WarpTile& w, const ScratchPos<LAYOUT>& sp,
+                                     const ScratchForce<LAYOUT>& sf, const LJTab& tab, int ni,
+                                     int j0, int nj, bool tri, double xi, double yi, double zi,
+                                     int ti, double& fx, double& fy, double& fz, unsigned& cnt) {
+    int lane = threadIdx.x & 31;
+    if (lane < nj) {
+        double x, y, z;
+        int t;
+        sp.load(j0 + lane, x, y, z, t);
+        w.x[lane] = x; w.y[lane] = y; w.z[lane] = z; w.t[lane] = t;
+        w.fx[lane] = 0.0; w.fy[lane] = 0.0; w.fz[lane] = 0.0;
+    }
+    __syncwarp();
+    auto body = [&](int j) {
+        double dx = xi - w.x[j], dy = yi - w.y[j], dz = zi - w.z[j];
+        double r2 = dx * dx + dy * dy + dz * dz;
+        if (r2 < tab.rc2) {
+            int tj = w.t[j];
+            double s2, e24;
+            lj_params<MT>(tab, ti, tj, s2, e24);
+            double fs = lj_fs(r2, s2, e24);
+            fx += fs * dx;
+            fy += fs * dy;
+            fz += fs * dz;
+            if (N3L) {
+                ++cnt;
+                w.fx[j] -= fs * dx;
+                w.fy[j] -= fs * dy;
+                w.fz[j] -= fs * dz;
+            } else {
+                double bx = -dx, by = -dy, bz = -dz;
+                lj_params<MT>(tab, tj, ti, s2, e24);
+                double gs = lj_fs(bx * bx + by * by + bz * bz, s2, e24);
+                cnt += 2;
+                w.fx[j] += gs * bx;
+                w.fy[j] += gs * by;
+                w.fz[j] += gs * bz;
+            }
+        }
+    };
+    if (tri) {
+        for (int k = 1; k < ni; ++k) {
+            int j = lane + k;
+            if (j < ni) body(j);
+            __syncwarp();
+        }
+    } else {
+        int P = ni > nj ? ni : nj;
+        for (int k = 0; k < P; ++k) {
+            int j = lane + k;
+            if (j >= P) j -= P;
+            if (lane < ni && j < nj) body(j);
+            __syncwarp();
+        }
+    }
+    if (lane < nj) {
+        *sf.at(j0 + lane, 0) += w.fx[lane];
+        *sf.at(j0 + lane, 1) += w.fy[lane];
+        *sf.at(j0 + lane, 2) += w.fz[lane];
+    }
+    __syncwarp();
+}
+
+// All pairs of cell c1 (i side) against cell c2 (j side), or the intra pairs
+// of c1 when c2 < 0.  Plain read-modify-write stores: the colour schedule
+// guarantees that no other warp of the launch touches these rows.
+template <int LAYOUT, bool MT, bool N3L>
+__device__ __forceinline__ void cell_pair(WarpTile& w, const GridView& gv,
+                                          const ScratchPos<LAYOUT>& sp,
+                                          const ScratchForce<LAYOUT>& sf, const LJTab& tab, int c1,
+                                          int c2, unsigned& cnt) {
+    int lane = threadIdx.x & 31;
+    int s1 = gv.start[c1], e1 = gv.start[c1 + 1];
+    bool intra = c2 < 0;
+    int s2 = intra ? s1 : gv.start[c2], e2 = intra ? e1 : gv.start[c2 + 1];
+    if (e1 <= s1 || e2 <= s2) return;
+    for (int i0 = s1; i0 < e1; i0 += 32) {
+        int ni = min(32, e1 - i0);
+        double xi = 0.0, yi = 0.0, zi = 0.0;
+        int ti = 0;
+        if (lane < ni) sp.load(i0 + lane, xi, yi, zi, ti);
+        double fx = 0.0, fy = 0.0, fz = 0.0;
+        for (int j0 = intra ? i0 : s2; j0 < e2; j0 += 32) {
+            int nj = min(32, e2 - j0);
+            tile<LAYOUT, MT, N3L>(w, sp, sf, tab, ni, j0, nj, intra && j0 == i0, xi, yi, zi, ti, fx,
+                                  fy, fz, cnt);
+        }
+        if (lane < ni) {
+            *sf.at(i0 + lane, 0) += fx;
+            *sf.at(i0 + lane, 1) += fy;
+            *sf.at(i0 + lane, 2) += fz;
+        }
+        __syncwarp();
+    }
+}
+
+struct ColourLaunch {
+    int p[3];        // colour phase per axis
+    int stride[3];
+    int lo[3];       // first base/anchor per axis (before phase)
+    int hi[3];       // exclusive bound per axis
+    int cnt[3];      // bases/anchors per axis in this colour
+};
+
+// C18: one warp per base cell of one colour (kernels.py:493-537 driven by
+// containers.py:269-287).
+template <int LAYOUT, bool MT, bool N3L>
+__global__ void __launch_bounds__(128) lc_c18_kernel(GridView gv, ScratchPos<LAYOUT> sp,
+                                                     ScratchForce<LAYOUT> sf, LJTab tab, Stencil st,
+                                                     ColourLaunch cl,
+                                                     unsigned long long* counter) {
+    __shared__ WarpTile tiles[4];
+    WarpTile& w = tiles[threadIdx.x >> 5];
+    int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    unsigned cnt = 0;
+    int total = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
+    if (wid < total) {
+        int kz = wid % cl.cnt[2], t = wid / cl.cnt[2];
+        int ky = t % cl.cnt[1], kx = t / cl.cnt[1];
+        int bx = cl.lo[0] + cl.p[0] + kx * cl.stride[0];
+        int by = cl.lo[1] + cl.p[1] + ky * cl.stride[1];
+        int bz = cl.lo[2] + cl.p[2] + kz * cl.stride[2];
+        int c1 = gv.flat(bx, by, bz);
+        if (gv.start[c1 + 1] > gv.start[c1]) {
+            cell_pair<LAYOUT, MT, N3L>(w, gv, sp, sf, tab, c1, -1, cnt);
+            for (int k = 0; k < st.n; ++k) {
+                int x2 = bx + st.d[k][0], y2 = by + st.d[k][1], z2 = bz + st.d[k][2];
+                if (!gv.in_grid(x2, y2, z2)) continue;
+                cell_pair<LAYOUT, MT, N3L>(w, gv, sp, sf, tab, c1, gv.flat(x2, y2, z2), cnt);
+            }
+        }
+    }
+    warp_count(counter, cnt);
+}
+
+// C08: one warp per anchor of one colour (kernels.py:373-433).
+template <int LAYOUT, bool MT, bool N3L>
+__global__ void __launch_bounds__(128) lc_c08_kernel(GridView gv, ScratchPos<LAYOUT> sp,
+                                                     ScratchForce<LAYOUT> sf, LJTab tab, Stencil st,
+                                                     ColourLaunch cl,
+                                                     unsigned long long* counter) {
+    __shared__ WarpTile tiles[4];
+    WarpTile& w = tiles[threadIdx.x >> 5];
+    int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    unsigned cnt = 0;
+    int total = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
+    if (wid < total) {
+        int kz = wid % cl.cnt[2], t = wid / cl.cnt[2];
+        int ky = t % cl.cnt[1], kx = t / cl.cnt[1];
+        int ax = cl.p[0] + kx * cl.stride[0];
+        int ay = cl.p[1] + ky * cl.stride[1];
+        int az = cl.p[2] + kz * cl.stride[2];
+        if (gv.owned(ax, ay, az)) cell_pair<LAYOUT, MT, N3L>(w, gv, sp, sf, tab, gv.flat(ax, ay, az), -1, cnt);
+        for (int k = 0; k < st.n; ++k) {
+            int dx = st.d[k][0], dy = st.d[k][1], dz = st.d[k][2];
+            int c1x = dx < 0 ? ax - dx : ax, c1y = dy < 0 ? ay - dy : ay, c1z = dz < 0 ? az - dz : az;
+            if (!gv.owned(c1x, c1y, c1z)) continue;
+            int c2x = c1x + dx, c2y = c1y + dy, c2z = c1z + dz;
+            if (!gv.in_grid(c2x, c2y, c2z)) continue;
+            cell_pair<LAYOUT, MT, N3L>(w, gv, sp, sf, tab, gv.flat(c1x, c1y, c1z),
+                                       gv.flat(c2x, c2y, c2z), cnt);
+        }
+    }
+    warp_count(counter, cnt);
+}
+
+// ------------------------------------------------------------------ dispatch
+
+template <int LAYOUT, bool MT>
+static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
+    GridView gv = make_view(gr);
+    ScratchPos<LAYOUT> sp{gr.spos4.p, gr.spos3.p, gr.spos3.p + gr.m, gr.spos3.p + 2 * gr.m,
+                          gr.row_tid.p};
+    ScratchForce<LAYOUT> sf{gr.sforce.p, (int)gr.m};
+    unsigned long long* counter = c.scal.p;
+    cudaStream_t s = c.stream;
+    int m = (int)gr.m;
+    const Geom& g = gr.g;
+    if (traversal == T_C01) {
+        lc_c01_kernel<LAYOUT, MT><<<blocks_for(m, 128), 128, 0, s>>>(gv, sp, sf, c.tab, gr.pruned, counter), note_launch();
+        return;
+    }
+    if (traversal == T_SLI) {
+        if (newton3)
+            lc_fwd_atomic_kernel<LAYOUT, MT, true><<<blocks_for(m, 128), 128, 0, s>>>(gv, sp, sf, c.tab, gr.fwd_sli, counter), note_launch();
+        else
+            lc_fwd_atomic_kernel<LAYOUT, MT, false><<<blocks_for(m, 128), 128, 0, s>>>(gv, sp, sf, c.tab, gr.fwd_sli, counter), note_launch();
+        return;
+    }
+    ColourLaunch cl;
+    if (traversal == T_C18) {
+        int strides[3] = {g.overlap[0] + 1, 2 * g.overlap[1] + 1, 2 * g.overlap[2] + 1};
+        for (int px = 0; px < strides[0]; ++px)
+            for (int py = 0; py < strides[1]; ++py)
+                for (int pz = 0; pz < strides[2]; ++pz) {
+                    int ph[3] = {px, py, pz};
+                    bool empty = false;
+                    for (int k = 0; k < 3; ++k) {
+                        cl.p[k] = ph[k];
+                        cl.stride[k] = strides[k];
+                        cl.lo[k] = g.H[k];
+                        cl.hi[k] = g.H[k] + g.S[k];
+                        int first = g.H[k] + ph[k];
+                        cl.cnt[k] = first >= cl.hi[k] ? 0 : (cl.hi[k] - first + strides[k] - 1) / strides[k];
+                        if (!cl.cnt[k]) empty = true;
+                    }
+                    if (empty) continue;
+                    int warps = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
+                    if (newton3)
+                        lc_c18_kernel<LAYOUT, MT, true><<<blocks_for(warps, 4), 128, 0, s>>>(gv, sp, sf, c.tab, gr.fwd, cl, counter), note_launch();
+                    else
+                        lc_c18_kernel<LAYOUT, MT, false><<<blocks_for(warps, 4), 128, 0, s>>>(gv, sp, sf, c.tab, gr.fwd, cl, counter), note_launch();
+                }
+        return;
+    }
+    // C08: anchors over the whole padded grid, stride overlap+1 per axis
+    int strides[3] = {g.overlap[0] + 1, g.overlap[1] + 1, g.overlap[2] + 1};
+    for (int px = 0; px < strides[0]; ++px)
+        for (int py = 0; py < strides[1]; ++py)
+            for (int pz = 0; pz < strides[2]; ++pz) {
+                int ph[3] = {px, py, pz};
+                bool empty = false;
+                for (int k = 0; k < 3; ++k) {
+                    cl.p[k] = ph[k];
+                    cl.stride[k] = strides[k];
+                    cl.lo[k] = 0;
+                    cl.hi[k] = g.D[k];
+                    cl.cnt[k] = ph[k] >= g.D[k] ? 0 : (g.D[k] - ph[k] + strides[k] - 1) / strides[k];
+                    if (!cl.cnt[k]) empty = true;
+                }
+                if (empty) continue;
+                int warps = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
+                if (newton3)
+                    lc_c08_kernel<LAYOUT, MT, true><<<blocks_for(warps, 4), 128, 0, s>>>(gv, sp, sf, c.tab, gr.fwd, cl, counter), note_launch();
+                else
+                    lc_c08_kernel<LAYOUT, MT, false><<<blocks_for(warps, 4), 128, 0, s>>>(gv, sp, sf, c.tab, gr.fwd, cl, counter), note_launch();
+            }
+}
+
+void lc_compute(Context& c, Grid& gr, int traversal, int newton3, int layout) {
+    if (gr.m == 0) return;
+    if (traversal != T_C01)
+        cudaMemsetAsync(gr.sforce.p, 0, 3 * (size_t)gr.m * sizeof(double), c.stream);
+    bool mt = c.tab.T > 1;
+    if (layout == AOS) {
+        if (mt) lc_launch<AOS, true>(c, gr, traversal, newton3);
+        else lc_launch<AOS, false>(c, gr, traversal, newton3);
+    } else {
+        if (mt) lc_launch<SOA, true>(c, gr, traversal, newton3);
+        else lc_launch<SOA, false>(c, gr, traversal, newton3);
+    }
+}
+
+}  // namespace mdg

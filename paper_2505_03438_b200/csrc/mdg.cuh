@@ -1,0 +1,160 @@
+// Internal header of libmdg: the B200 (sm_100a) LJ force + neighbour path.
+//
+// Everything here is device-resident.  The C ABI (include/mdg.h, api.cu) is the
+// only surface; no torch types cross it.  Reference behaviour each piece
+// mirrors is cited at the kernel that implements it.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace mdg {
+
+constexpr int kMaxTypes = 4;       // by-value LJ tables (kernel parameter space)
+constexpr int kMaxStencil = 124;   // pruned stencil at CSF 0.5 (cells.py:80-95)
+constexpr int kNoShift = 13;       // shift code of (0,0,0)
+
+enum Layout { AOS = 0, SOA = 1 };
+
+// Lorentz-Berthelot tables, forces.py:12-22, passed by value to every kernel.
+struct LJTab {
+    int T;
+    double rc2;
+    double sig2[kMaxTypes * kMaxTypes];
+    double eps24[kMaxTypes * kMaxTypes];
+};
+
+struct Stencil {
+    int n;
+    int d[kMaxStencil][3];
+};
+
+// cells.py:20-67 (make_geometry) restated on the host side of the library.
+struct Geom {
+    double L[3];
+    int periodic[3];
+    double ell, csf;
+    int S[3];          // dims_owned
+    double cl[3];      // cell_length
+    int overlap[3];
+    int H[3];          // halo layers
+    int D[3];          // padded dims
+    int64_t ncells;
+};
+
+Geom make_geometry(const double L[3], const int periodic[3], double ell, double csf);
+Stencil pruned_stencil(const Geom& g);
+Stencil forward_stencil(const Geom& g, int major);
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t n);
+    void release();
+};
+
+// One binning of the particles over a padded cell grid (containers.py:78-123):
+// entries = N owned particles followed by periodic images (cells.py:122-156),
+// stably counting-sorted by cell.  Within a cell the stable order equals
+// ascending entry id (all entries of one cell share one image combo).
+struct Grid {
+    Geom g{};
+    Stencil pruned{}, fwd{}, fwd_sli{};
+    int sli_major = 0;
+    int64_t n = 0, nimg = 0, m = 0;
+    bool built = false;
+    DBuf<int> cell_count, cell_start, cell_fill;   // ncells + 1
+    DBuf<int> img_cnt, img_off;                     // n + 1
+    DBuf<int> img_src;                              // nimg
+    DBuf<uint8_t> img_code;                         // nimg
+    DBuf<int> tmp_ent, row_ent;                     // m
+    DBuf<int> row_src, row_cell, row_tid, inv;      // m
+    DBuf<uint8_t> row_code;                         // m
+    // layout-specific scratch (LayoutBuffers, containers.py:126-171)
+    int scratch_layout = -1;
+    DBuf<double4> spos4;                            // AoS: x,y,z,type
+    DBuf<double> spos3;                             // SoA: x[m],y[m],z[m]
+    DBuf<double> sforce;                            // 3*m ((m,3) AoS or (3,m) SoA)
+    void release();
+};
+
+// Verlet lists (containers.py:343-375): CSR by owner index, int32 entries.
+struct Verlet {
+    Grid grid;
+    DBuf<double4> bpos;        // build-time sorted positions (pos[src]+shift)
+    DBuf<int> counts;          // n
+    DBuf<long long> noff;      // n + 1
+    DBuf<int> nbr;             // E
+    int64_t entries = 0;
+    bool built = false;
+    void release();
+};
+
+struct Context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sm_count = 148;
+    // system (SimulationParams + per-type tables)
+    bool have_system = false;
+    double L[3] = {0, 0, 0};
+    int periodic[3] = {0, 0, 0};
+    double cutoff = 0, skin = 0;
+    LJTab tab{};
+    std::vector<double> mass;
+    DBuf<double> d_mass;
+    // bound particle arrays (owned by the caller)
+    int64_t n = 0;
+    int layout = AOS;
+    double *pos = nullptr, *vel = nullptr, *force = nullptr, *old_force = nullptr;
+    const int* tid = nullptr;
+    // containers
+    Grid grids[2];             // [0] CSF 1, [1] CSF 0.5
+    Verlet vl;
+    // device scalars: [0] eval count, [1] scan total scratch, [2] blow-up flag
+    DBuf<unsigned long long> scal;
+    unsigned long long* h_scal = nullptr;   // pinned mirror
+    DBuf<unsigned long long> scan_tmp;      // block partials for scans
+};
+
+// ---- scans (warp-shuffle block scan, three phases) ----
+void exclusive_scan_i32(const int* in, int* out, int64_t n, unsigned long long* total,
+                        DBuf<unsigned long long>& tmp, cudaStream_t s);
+void exclusive_scan_i32_to_i64(const int* in, long long* out, int64_t n,
+                               unsigned long long* total, DBuf<unsigned long long>& tmp,
+                               cudaStream_t s);
+
+// ---- pipeline pieces ----
+int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout);
+void grid_bind_scratch(Context& c, Grid& gr, int layout);
+void grid_refresh(Context& c, Grid& gr, int layout);
+void lc_compute(Context& c, Grid& gr, int traversal, int newton3, int layout);
+void lc_fold_forces(Context& c, Grid& gr, int layout, bool images_written);
+int vl_rebuild(Context& c);
+void vl_compute(Context& c);
+void integ_drift_wrap(Context& c, double dt);
+void integ_finish_kick(Context& c, double dt, int has_gravity, double gravity);
+void integ_sd_step(Context& c, double gamma, double max_disp);
+void set_error(const std::string& msg);
+// host-side count of kernel launches issued by the library (bench evidence)
+void note_launch();
+unsigned long long launch_count();
+
+#define MDG_CUDA(x)                                                             \
+    do {                                                                        \
+        cudaError_t _e = (x);                                                   \
+        if (_e != cudaSuccess) {                                                \
+            ::mdg::set_error(std::string(#x) + ": " + cudaGetErrorString(_e));  \
+            return -1;                                                          \
+        }                                                                       \
+    } while (0)
+
+inline int blocks_for(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    return (int)(b < 1 ? 1 : b);
+}
+
+}  // namespace mdg

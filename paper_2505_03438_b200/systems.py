@@ -1,0 +1,91 @@
+"""Seeded synthetic inputs of BASELINE.json's configurations.
+
+The reference's scenario generators (scenarios.py:79-201) do not cover these
+systems; they are built here with numpy's seeded Generator so the GPU arm and
+the CPU baseline (oracle/) consume identical inputs.
+
+* config 1: simple-cubic sites (i + 0.5) * 1.1 sigma, i < 20 per axis, jitter
+  U(-0.05, 0.05) sigma, periodic cube of 22 sigma, T = 0.7.
+* config 2: N uniform points at rho = 0.75 in a periodic cube, overlaps relaxed
+  by 50 capped steepest-descent steps on the GPU, T = 0.7.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .params import PERIODIC, SimulationParams
+
+
+def thermal_velocities(rng, masses, temperature):
+    """Maxwell-Boltzmann draw, zero net momentum, rescaled onto T exactly
+    (scenarios.py:192-201)."""
+    n = len(masses)
+    v = rng.normal(0.0, 1.0, size=(n, 3))
+    v *= np.sqrt(temperature / masses)[:, None]
+    v -= np.average(v, axis=0, weights=masses)
+    t_now = float(np.sum(masses * np.sum(v * v, axis=1)) / (3.0 * n))
+    if t_now > 0.0:
+        v *= math.sqrt(temperature / t_now)
+    return v
+
+
+def sc_lattice(n_side=20, spacing=1.1, jitter=0.05, seed=0, temperature=0.7, offset=0.5):
+    """BASELINE config 1 (and its scaled-down variants)."""
+    rng = np.random.default_rng(seed)
+    i = (np.arange(n_side) + offset) * spacing
+    sites = np.stack(np.meshgrid(i, i, i, indexing="ij"), axis=-1).reshape(-1, 3)
+    pos = sites + rng.uniform(-jitter, jitter, sites.shape)
+    vel = thermal_velocities(rng, np.ones(len(pos)), temperature)
+    L = n_side * spacing
+    return pos, vel, np.array([L, L, L])
+
+
+def config1_params(steps=100, rebuild_interval=10):
+    pos, vel, L = sc_lattice()
+    params = SimulationParams(domain_size=L, cutoff=2.5, skin=0.3,
+                              rebuild_interval=rebuild_interval, delta_t=1e-3,
+                              total_iterations=steps, boundary=(PERIODIC,) * 3)
+    return pos, vel, params
+
+
+def uniform_box(n, density, seed=0):
+    L = (n / density) ** (1.0 / 3.0)
+    rng = np.random.default_rng(seed)
+    pos = rng.uniform(0.0, L, (n, 3))
+    return pos, np.array([L, L, L]), rng
+
+
+SD_STEPS = 50
+SD_GAMMA = 1e-3      # displacement per unit force
+SD_MAX_DISP = 0.05   # sigma per step
+
+
+def relax_on_device(particles, params, config, steps=SD_STEPS, gamma=SD_GAMMA,
+                    max_disp=SD_MAX_DISP):
+    """Capped steepest descent x += F/|F| min(gamma |F|, max_disp) with the GPU
+    force path (fresh neighbour structures every step)."""
+    from .calculator import ForceCalculator
+    calc = ForceCalculator(particles, params)
+    particles.convert_layout(config.layout)
+    for _ in range(steps):
+        calc.rebuild(particles, config)
+        calc.refresh(particles, config)
+        calc.compute_async(particles, config)
+        calc.sd_step(particles, gamma, max_disp)
+    if calc.blowup():
+        raise RuntimeError("steepest descent left the domain")
+    calc.close()
+    particles.force.zero_()
+    particles.old_force.zero_()
+
+
+def config2_inputs(n=1_048_576, density=0.75, seed=0, temperature=0.7):
+    """Unrelaxed config-2 positions, velocities and params (relax separately)."""
+    pos, L, rng = uniform_box(n, density, seed)
+    vel = thermal_velocities(rng, np.ones(n), temperature)
+    params = SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=10,
+                              delta_t=2e-3, total_iterations=1000, boundary=(PERIODIC,) * 3)
+    return pos, vel, params

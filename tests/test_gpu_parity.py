@@ -1,0 +1,188 @@
+"""GPU parity: libmdg through its C ABI against the oracle and the reference's
+golden outputs (tests/golden/, generated from the reference by
+oracle/make_golden.py).
+
+Bars (BASELINE north_star): cell assignments and Verlet pair sets bit-exact;
+eval counts exact; fp64 forces and trajectories within 1e-10 relative
+(Frobenius norm, tests/conftest.py:55-60 of the reference).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, system_names
+from oracle import port
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+FP64_TOL = 1e-10
+
+
+def _ids():
+    return [c.id for c in port.all_configs()]
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need CUDA")
+    import paper_2505_03438_b200 as P
+    from paper_2505_03438_b200 import calculator
+    return P, calculator
+
+
+def _system(P, d, layout="AoS"):
+    nt = int(d["n_types"])
+    types = [P.ParticleTypeInfo(t, 1.0 + 0.5 * t, 1.0 - 0.2 * t, 1.0 + t) for t in range(nt)]
+    per = tuple(P.PERIODIC if f else P.REFLECTIVE for f in d["periodic"])
+    params = P.SimulationParams(domain_size=d["domain"], cutoff=float(d["cutoff"]),
+                                skin=float(d["skin"]), rebuild_interval=5, boundary=per)
+    parts = P.ParticleSet(d["pos"], type_ids=d["tid"], types=types, layout=layout)
+    return parts, params
+
+
+@pytest.mark.parametrize("name", system_names())
+def test_all_30_configurations_match_reference(pkg, name):
+    P, calc = pkg
+    d = golden(f"sys_{name}.npz")
+    assert [str(s) for s in d["config_ids"]] == _ids()
+    for k, cfg in enumerate(P.enumerate_configurations()):
+        parts, params = _system(P, d)
+        _, count = calc.compute_forces(parts, cfg, params)
+        assert count == int(d["counts"][k]), cfg.id
+        err = port.force_rel_error(parts.numpy("force"), d["forces"][k])
+        assert err <= FP64_TOL, f"{cfg.id}: {err:.3g}"
+
+
+@pytest.mark.parametrize("name", system_names())
+def test_cell_assignment_bit_exact(pkg, name):
+    P, calc = pkg
+    d = golden(f"sys_{name}.npz")
+    for csf, tag in ((1.0, "csf1"), (0.5, "csf05")):
+        for layout in ("AoS", "SoA"):
+            parts, params = _system(P, d, layout)
+            fc = calc.ForceCalculator(parts, params)
+            cfg = P.Configuration("LC", "C08", True, layout, csf)
+            fc.rebuild(parts, cfg)
+            g = fc.grid_state(csf)
+            assert np.array_equal(g["src"], d[f"{tag}_src"]), (tag, layout)
+            assert np.array_equal(g["shift"], d[f"{tag}_shift"]), (tag, layout)
+            assert np.array_equal(g["start"], d[f"{tag}_start"]), (tag, layout)
+            assert np.array_equal(g["end"], d[f"{tag}_end"]), (tag, layout)
+            fc.close()
+
+
+@pytest.mark.parametrize("name", system_names())
+def test_verlet_pair_sets_bit_exact(pkg, name):
+    P, calc = pkg
+    d = golden(f"sys_{name}.npz")
+    for layout in ("AoS", "SoA"):
+        parts, params = _system(P, d, layout)
+        fc = calc.ForceCalculator(parts, params)
+        fc.rebuild(parts, P.parse_configuration(f"VL-List_Iter-NoN3L-{layout}"))
+        noff, nbr = fc.verlet_lists()
+        assert np.array_equal(noff, d["vl_noff"])
+        assert np.array_equal(nbr, d["vl_nbr"])
+        fc.close()
+
+
+@pytest.mark.parametrize("traj", ["traj_small", "traj_faces", "traj_config1"])
+def test_trajectories_match_reference(pkg, traj):
+    P, calc = pkg
+    from paper_2505_03438_b200.simulation import simulate
+    z = golden(f"{traj}.npz")
+    L = z["domain"]
+    for k, cid in enumerate(str(s) for s in z["config_ids"]):
+        params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=10,
+                                    delta_t=1e-3, boundary=(P.PERIODIC,) * 3)
+        parts = P.ParticleSet(z["pos0"], z["vel0"])
+        simulate(parts, params, P.parse_configuration(cid), steps=int(z["steps"]))
+        dpos = parts.numpy("pos") - z[f"pos_{k}"]
+        dpos -= L * np.rint(dpos / L)   # positions compared modulo the box
+        assert np.linalg.norm(dpos) / np.linalg.norm(z[f"pos_{k}"]) <= FP64_TOL, cid
+        assert port.force_rel_error(parts.numpy("vel"), z[f"vel_{k}"]) <= FP64_TOL, cid
+
+
+def test_host_drop_in_drives_the_reference_loop(pkg):
+    """HostForceCalculator inside the oracle's restatement of simulate()
+    (the reference loop with numpy host arrays) reproduces the reference."""
+    P, calc = pkg
+    z = golden("traj_small.npz")
+    L = float(z["domain"][0])
+    for k, cid in enumerate(str(s) for s in z["config_ids"]):
+        params = port.Params(domain_size=(L, L, L), cutoff=2.5, skin=0.3, rebuild_interval=10,
+                             delta_t=1e-3, boundary=(port.PERIODIC,) * 3)
+        p = port.Particles(z["pos0"], z["vel0"])
+        port.simulate_fixed(p, params, port.parse(cid), steps=int(z["steps"]),
+                            calculator_cls=calc.HostForceCalculator)
+        assert port.force_rel_error(p.velocities, z[f"vel_{k}"]) <= FP64_TOL, cid
+
+
+def test_lattice_32k_all_configs_vs_oracle(pkg):
+    """Mid-size parity against the oracle (config-1 style lattice, 32,768)."""
+    P, calc = pkg
+    from paper_2505_03438_b200 import systems
+    pos, _, L = systems.sc_lattice(n_side=32, seed=3)
+    pp = port.Params(domain_size=L, cutoff=2.5, skin=0.3, boundary=(port.PERIODIC,) * 3)
+    ref = port.Particles(pos)
+    _, ref_count = port.compute_forces(ref, port.parse("LC-C08-N3L-AoS-CSF1"), pp, workers=4)
+    ref_f = np.asarray(ref.forces)
+    params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, boundary=(P.PERIODIC,) * 3)
+    for cfg in P.enumerate_configurations():
+        parts = P.ParticleSet(pos)
+        _, count = calc.compute_forces(parts, cfg, params)
+        assert count == ref_count * (1 if cfg.newton3 else 2), cfg.id
+        assert port.force_rel_error(parts.numpy("force"), ref_f) <= FP64_TOL, cfg.id
+
+
+def test_empty_set_and_layout_mismatch(pkg):
+    P, calc = pkg
+    params = P.SimulationParams(domain_size=(9.0, 9.0, 9.0), cutoff=2.5, skin=0.3,
+                                boundary=(P.PERIODIC,) * 3)
+    for cfg in P.enumerate_configurations():
+        parts = P.ParticleSet(np.zeros((0, 3)))
+        _, count = calc.compute_forces(parts, cfg, params)
+        assert count == 0
+    parts = P.ParticleSet(np.random.default_rng(0).uniform(0, 9, (20, 3)))
+    fc = calc.ForceCalculator(parts, params)
+    cfg = P.parse_configuration("LC-C08-N3L-SoA-CSF1")
+    fc.rebuild(parts, cfg)
+    with pytest.raises(ValueError):
+        fc.compute(parts, cfg)
+
+
+def test_hand_cases(pkg):
+    P, calc = pkg
+    refl = P.SimulationParams(domain_size=(10.0, 10.0, 10.0), cutoff=2.5, skin=0.3,
+                              boundary=(P.REFLECTIVE,) * 3)
+    r_min = 2.0 ** (1.0 / 6.0)
+    for cid in ("LC-C08-N3L-AoS-CSF1", "LC-C18-N3L-SoA-CSF0.5", "VL-List_Iter-NoN3L-SoA"):
+        parts = P.ParticleSet(np.array([[4.0, 5.0, 5.0], [4.0 + r_min, 5.0, 5.0]]))
+        calc.compute_forces(parts, P.parse_configuration(cid), refl)
+        assert np.max(np.abs(parts.numpy("force"))) <= 1e-12
+    box12 = P.SimulationParams(domain_size=(12.0, 12.0, 12.0), cutoff=2.5, skin=0.3,
+                               boundary=(P.REFLECTIVE,) * 3)
+    for cid in ("LC-SLI-N3L-AoS-CSF1", "LC-C01-NoN3L-SoA-CSF1", "VL-List_Iter-NoN3L-AoS"):
+        parts = P.ParticleSet(np.array([[4.0, 6.0, 6.0], [5.5, 6.0, 6.0], [7.0, 6.0, 6.0]]))
+        calc.compute_forces(parts, P.parse_configuration(cid), box12)
+        f = parts.numpy("force")
+        assert np.allclose(f[1], 0.0, atol=1e-12)
+        assert np.allclose(f[0], -f[2], atol=1e-12)
+        assert abs(f[0][0]) > 0.1
+    per = P.SimulationParams(domain_size=(9.0, 9.0, 9.0), cutoff=2.5, skin=0.3,
+                             boundary=(P.PERIODIC,) * 3)
+    pos = np.array([[0.3, 4.5, 4.5], [8.7, 4.5, 4.5]])
+    ref, _ = port.brute_forces(pos, np.zeros(2, dtype=np.int64), [1.0], [1.0], 2.5,
+                               per.domain_size, per.periodic_flags())
+    for cid in ("LC-C08-N3L-AoS-CSF1", "VL-List_Iter-NoN3L-AoS"):
+        parts = P.ParticleSet(pos)
+        calc.compute_forces(parts, P.parse_configuration(cid), per)
+        assert np.allclose(parts.numpy("force"), ref, atol=1e-12)
+    vlp = P.SimulationParams(domain_size=(14.0, 14.0, 14.0), cutoff=3.0, skin=0.5,
+                             boundary=(P.REFLECTIVE,) * 3)
+    parts = P.ParticleSet(np.array([[3.0, 7.0, 7.0], [6.4, 7.0, 7.0], [10.0, 7.0, 7.0]]))
+    fc = calc.ForceCalculator(parts, vlp)
+    fc.rebuild(parts, P.parse_configuration("VL-List_Iter-NoN3L-AoS"))
+    noff, nbr = fc.verlet_lists()
+    assert [set(nbr[noff[i]:noff[i + 1]].tolist()) for i in range(3)] == [{1}, {0}, set()]

@@ -1,0 +1,117 @@
+"""CPU-only checks: the C-ABI library loads and exports every symbol of
+include/mdg.h; host-side geometry/stencils through the ABI equal the
+reference's (golden); the host mirror of the configuration space and params
+behaves like the reference's."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden
+
+from paper_2505_03438_b200 import _lib
+import paper_2505_03438_b200 as P
+
+
+def test_header_and_export_list_agree():
+    hdr = open(os.path.join(ROOT, "include", "mdg.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|uint64_t|const char\*)\s+(mdg_\w+)\s*\(", hdr, re.M))
+    assert declared == set(_lib.EXPORTS)
+
+
+def test_library_loads_and_exports_every_symbol():
+    L = _lib.lib()
+    for name in _lib.EXPORTS:
+        assert hasattr(L, name), name
+    assert L.mdg_version().decode().startswith("mdg")
+
+
+def _geom(domain, per, ell, csf):
+    d = np.ascontiguousarray(domain, dtype=np.float64)
+    p = np.ascontiguousarray(per, dtype=np.int32)
+    so, ov, ha, di = (np.zeros(3, np.int32) for _ in range(4))
+    cl = np.zeros(3)
+    _lib.check(_lib.lib().mdg_geometry_for(d.ctypes.data, p.ctypes.data, ell, csf, so.ctypes.data,
+                                           cl.ctypes.data, ov.ctypes.data, ha.ctypes.data,
+                                           di.ctypes.data))
+    return so, cl, ov, ha, di
+
+
+def _stencil(domain, per, ell, csf, kind, major=0):
+    d = np.ascontiguousarray(domain, dtype=np.float64)
+    p = np.ascontiguousarray(per, dtype=np.int32)
+    out = np.zeros(3 * 124, np.int32)
+    cnt = ctypes.c_int()
+    _lib.check(_lib.lib().mdg_stencil_for(d.ctypes.data, p.ctypes.data, ell, csf, kind, major,
+                                          ctypes.byref(cnt), out.ctypes.data))
+    return out[:3 * cnt.value].reshape(-1, 3).astype(np.int64)
+
+
+def test_abi_geometry_and_stencils_match_reference():
+    z = golden("geometry.npz")
+    for k in range(int(z["n_cases"])):
+        dom, (ell, csf), per = z[f"g{k}_in_domain"], z[f"g{k}_in_scalars"], z[f"g{k}_in_periodic"]
+        so, cl, ov, ha, di = _geom(dom, per, ell, csf)
+        assert tuple(so) == tuple(z[f"g{k}_dims_owned"])
+        assert np.array_equal(cl, z[f"g{k}_cell_length"])
+        assert tuple(ov) == tuple(z[f"g{k}_overlap"])
+        assert tuple(ha) == tuple(z[f"g{k}_halo"])
+        assert tuple(di) == tuple(z[f"g{k}_dims"])
+        assert np.array_equal(_stencil(dom, per, ell, csf, 0), z[f"g{k}_pruned"])
+        for major in range(3):
+            assert np.array_equal(_stencil(dom, per, ell, csf, 1, major), z[f"g{k}_forward{major}"])
+
+
+def test_abi_rejects_bad_geometry():
+    with pytest.raises(ValueError):
+        _geom((9.0, 9.0, 9.0), (1, 1, 1), 3.0, 0.7)
+
+
+def test_configuration_space_mirrors_reference():
+    space = P.enumerate_configurations()
+    assert len(space) == 30 and len({c.id for c in space}) == 30
+    from oracle import port
+    assert [c.id for c in space] == [c.id for c in port.all_configs()]
+    for c in space:
+        assert P.parse_configuration(c.id) == c
+    with pytest.raises(ValueError):
+        P.Configuration("VL", "List_Iter", True, "AoS")
+    with pytest.raises(ValueError):
+        P.Configuration("LC", "C01", True, "AoS")
+    with pytest.raises(ValueError):
+        P.Configuration("LC", "C08", True, "AoS", 0.25)
+    with pytest.raises(ValueError):
+        P.parse_configuration("LC-C04-N3L-AoS-CSF1")
+
+
+def test_params_validation_mirrors_reference():
+    with pytest.raises(ValueError):
+        P.SimulationParams(domain_size=(5.0, 9.0, 9.0), cutoff=2.5, skin=0.3,
+                           boundary=(P.PERIODIC,) * 3)
+    P.SimulationParams(domain_size=(5.0, 9.0, 9.0), cutoff=2.5, skin=0.3,
+                       boundary=(P.REFLECTIVE, P.PERIODIC, P.PERIODIC))
+    with pytest.raises(ValueError):
+        P.SimulationParams(domain_size=(9.0, 9.0, 9.0), cutoff=0.0)
+
+
+def test_config_struct_mapping():
+    s = _lib.config_struct(P.parse_configuration("LC-SLI-NoN3L-SoA-CSF0.5"))
+    assert (s.container, s.traversal, s.newton3, s.layout, s.csf) == (_lib.LC, _lib.SLI, 0, _lib.SOA, 0.5)
+    s = _lib.config_struct(P.parse_configuration("VL-List_Iter-NoN3L-AoS"))
+    assert (s.container, s.traversal, s.layout) == (_lib.VL, _lib.LIST_ITER, _lib.AOS)
+
+
+def test_particle_layout_round_trip_cpu_tensors():
+    rng = np.random.default_rng(0)
+    p = P.ParticleSet(rng.uniform(0, 9, (50, 3)), rng.normal(size=(50, 3)), device="cpu")
+    pos = p.numpy("pos")
+    p.convert_layout(P.SOA)
+    assert tuple(p.pos.shape) == (3, 50)
+    p.convert_layout(P.AOS)
+    assert np.array_equal(p.numpy("pos"), pos)
+    e = P.ParticleSet(np.zeros((0, 3)), device="cpu")
+    e.convert_layout(P.SOA)
+    assert tuple(e.pos.shape) == (3, 0)

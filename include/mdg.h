@@ -108,6 +108,11 @@ int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp);
 /* BlowUpError detection (integrator.py:108-116): flag set by any drift since
  * the last reset.  Synchronises. */
 int mdg_blowup(mdg_ctx* ctx, int* flag, int reset);
+/* Bracket every force-kernel launch with CUDA events on the context stream
+ * (enable != 0; resets the record).  mdg_profile_read synchronises and
+ * returns the summed kernel time and the number of bracketed launches. */
+int mdg_profile(mdg_ctx* ctx, int enable);
+int mdg_profile_read(mdg_ctx* ctx, double* total_ms, int64_t* launches);
 /* Wait for all work of the context's stream. */
 int mdg_synchronize(mdg_ctx* ctx);
 

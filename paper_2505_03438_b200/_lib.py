@@ -24,7 +24,7 @@ EXPORTS = (
     "mdg_version", "mdg_launch_count", "mdg_last_error", "mdg_create", "mdg_destroy", "mdg_set_stream",
     "mdg_set_system", "mdg_bind", "mdg_rebuild", "mdg_refresh", "mdg_compute",
     "mdg_eval_count", "mdg_drift_wrap", "mdg_finish_kick", "mdg_sd_step", "mdg_blowup",
-    "mdg_synchronize", "mdg_h2d", "mdg_d2h", "mdg_geometry", "mdg_stencil", "mdg_get_grid",
+    "mdg_profile", "mdg_profile_read", "mdg_synchronize", "mdg_h2d", "mdg_d2h", "mdg_geometry", "mdg_stencil", "mdg_get_grid",
     "mdg_get_verlet", "mdg_geometry_for", "mdg_stencil_for", "mdg_measure_fp64_peak",
 )
 
@@ -61,6 +61,8 @@ def _declare(L):
         "mdg_finish_kick": (I, [P, D, I, D]),
         "mdg_sd_step": (I, [P, D, D]),
         "mdg_blowup": (I, [P, ctypes.POINTER(I), I]),
+        "mdg_profile": (I, [P, I]),
+        "mdg_profile_read": (I, [P, ctypes.POINTER(D), ctypes.POINTER(I64)]),
         "mdg_synchronize": (I, [P]),
         "mdg_h2d": (I, [P, P, P, SZ]),
         "mdg_d2h": (I, [P, P, P, SZ]),

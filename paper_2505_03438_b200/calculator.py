@@ -144,6 +144,16 @@ class ForceCalculator:
         self.bind(particles)
         check(lib().mdg_sd_step(self.ctx.h, float(gamma), float(max_disp)), "sd_step")
 
+    def profile(self, enable=True):
+        """Bracket each force-kernel launch with CUDA events on the context stream."""
+        check(lib().mdg_profile(self.ctx.h, int(enable)), "profile")
+
+    def profile_read(self):
+        """(summed force-kernel milliseconds, bracketed launches) since profile()."""
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        check(lib().mdg_profile_read(self.ctx.h, ctypes.byref(ms), ctypes.byref(n)), "profile_read")
+        return float(ms.value), int(n.value)
+
     def blowup(self, reset=True) -> bool:
         f = ctypes.c_int()
         check(lib().mdg_blowup(self.ctx.h, ctypes.byref(f), int(reset)), "blowup")

@@ -17,6 +17,16 @@ static thread_local std::string g_err;
 
 void set_error(const std::string& msg) { g_err = msg; }
 
+void Context::prof_mark() {
+    if (!prof) return;
+    if (ev_used == ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ev_pool.push_back(e);
+    }
+    cudaEventRecord(ev_pool[ev_used++], stream);
+}
+
 static unsigned long long g_launches = 0;
 void note_launch() { ++g_launches; }
 unsigned long long launch_count() { return g_launches; }
@@ -133,6 +143,7 @@ int mdg_destroy(mdg_ctx* ctx) {
     ctx->c.scan_tmp.release();
     ctx->c.d_mass.release();
     if (ctx->c.h_scal) cudaFreeHost(ctx->c.h_scal);
+    for (cudaEvent_t e : ctx->c.ev_pool) cudaEventDestroy(e);
     delete ctx;
     return MDG_OK;
 }
@@ -321,6 +332,29 @@ int mdg_blowup(mdg_ctx* ctx, int* flag, int reset) {
     *flag = c.h_scal[2] ? 1 : 0;
     if (reset) cudaMemsetAsync(c.scal.p + 2, 0, sizeof(unsigned long long), c.stream);
     return cuda_status("mdg_blowup");
+}
+
+int mdg_profile(mdg_ctx* ctx, int enable) {
+    CHECK_CTX(ctx);
+    ctx->c.prof = enable != 0;
+    ctx->c.ev_used = 0;
+    return MDG_OK;
+}
+
+int mdg_profile_read(mdg_ctx* ctx, double* total_ms, int64_t* launches) {
+    CHECK_CTX(ctx);
+    Context& c = ctx->c;
+    if (cudaStreamSynchronize(c.stream) != cudaSuccess) return cuda_status("mdg_profile_read");
+    double tot = 0.0;
+    for (size_t k = 0; k + 1 < c.ev_used; k += 2) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c.ev_pool[k], c.ev_pool[k + 1]);
+        tot += ms;
+    }
+    *total_ms = tot;
+    *launches = (int64_t)(c.ev_used / 2);
+    c.ev_used = 0;
+    return cuda_status("mdg_profile_read");
 }
 
 int mdg_synchronize(mdg_ctx* ctx) {

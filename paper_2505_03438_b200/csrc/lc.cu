@@ -400,6 +400,7 @@ void lc_compute(Context& c, Grid& gr, int traversal, int newton3, int layout) {
     if (traversal != T_C01)
         cudaMemsetAsync(gr.sforce.p, 0, 3 * (size_t)gr.m * sizeof(double), c.stream);
     bool mt = c.tab.T > 1;
+    c.prof_mark();
     if (layout == AOS) {
         if (mt) lc_launch<AOS, true>(c, gr, traversal, newton3);
         else lc_launch<AOS, false>(c, gr, traversal, newton3);
@@ -407,6 +408,7 @@ void lc_compute(Context& c, Grid& gr, int traversal, int newton3, int layout) {
         if (mt) lc_launch<SOA, true>(c, gr, traversal, newton3);
         else lc_launch<SOA, false>(c, gr, traversal, newton3);
     }
+    c.prof_mark();
 }
 
 }  // namespace mdg

@@ -118,6 +118,11 @@ struct Context {
     DBuf<unsigned long long> scal;
     unsigned long long* h_scal = nullptr;   // pinned mirror
     DBuf<unsigned long long> scan_tmp;      // block partials for scans
+    // optional CUDA-event bracketing of the force kernels (mdg_profile)
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    void prof_mark();
 };
 
 // ---- scans (warp-shuffle block scan, three phases) ----

@@ -139,6 +139,7 @@ void vl_compute(Context& c) {
     bool mt = c.tab.T > 1;
     dim3 b(blocks_for(c.n, 128)), t(128);
     auto* v = &c.vl;
+    c.prof_mark();
     if (c.layout == AOS) {
         if (mt) vl_force_kernel<AOS, true><<<b, t, 0, c.stream>>>(c.n, c.pos, c.force, c.tid, v->noff.p, v->nbr.p, c.tab, mi, c.scal.p), note_launch();
         else vl_force_kernel<AOS, false><<<b, t, 0, c.stream>>>(c.n, c.pos, c.force, c.tid, v->noff.p, v->nbr.p, c.tab, mi, c.scal.p), note_launch();
@@ -146,6 +147,7 @@ void vl_compute(Context& c) {
         if (mt) vl_force_kernel<SOA, true><<<b, t, 0, c.stream>>>(c.n, c.pos, c.force, c.tid, v->noff.p, v->nbr.p, c.tab, mi, c.scal.p), note_launch();
         else vl_force_kernel<SOA, false><<<b, t, 0, c.stream>>>(c.n, c.pos, c.force, c.tid, v->noff.p, v->nbr.p, c.tab, mi, c.scal.p), note_launch();
     }
+    c.prof_mark();
 }
 
 }  // namespace mdg

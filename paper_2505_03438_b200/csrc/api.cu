@@ -277,7 +277,7 @@ int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg) {
     if (c.n == 0) return MDG_OK;
     if (cfg->container == MDG_VL) {
         if (!c.vl.built) { set_error("compute before rebuild"); return MDG_ESTATE; }
-        vl_compute(c);
+        vl_compute(c, cfg->layout);
     } else {
         Grid& gr = *grid_for(c, cfg->csf);
         if (!gr.built || gr.scratch_layout != cfg->layout) {
@@ -456,10 +456,9 @@ int mdg_get_verlet(mdg_ctx* ctx, int64_t* entries, int64_t* noff, int32_t* nbr) 
     CHECK_CTX(ctx);
     Verlet& v = ctx->c.vl;
     if (!v.built) { set_error("Verlet lists not built"); return MDG_ESTATE; }
-    cudaStreamSynchronize(ctx->c.stream);
-    if (entries) *entries = v.entries;
-    if (noff) cudaMemcpy(noff, v.noff.p, (ctx->c.n + 1) * sizeof(long long), cudaMemcpyDeviceToHost);
-    if (nbr && v.entries) cudaMemcpy(nbr, v.nbr.p, v.entries * sizeof(int), cudaMemcpyDeviceToHost);
+    int64_t e = 0;
+    if (vl_export(ctx->c, &e, noff, nbr)) return MDG_ECUDA;
+    if (entries) *entries = e;
     return cuda_status("mdg_get_verlet");
 }
 

@@ -26,6 +26,16 @@ __device__ __forceinline__ void lj_params(const LJTab& t, int ti, int tj, double
     }
 }
 
+// One 256-bit read-only load of a 32-byte record (LDG.E.ENL2.256 on sm_100a):
+// a gathered double4 costs one L1 wavefront instead of LDG.128 + LDG.64.
+__device__ __forceinline__ double4 ldg256(const double4* p) {
+    double4 v;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+        : "l"(p));
+    return v;
+}
+
 // Cell-sorted scratch positions (LayoutBuffers.pos, containers.py:126-154).
 // AoS: one 32-byte record {x, y, z, type}; SoA: three component arrays + types.
 template <int LAYOUT>
@@ -37,7 +47,7 @@ struct ScratchPos {
     const int* __restrict__ tid;
     __device__ __forceinline__ void load(int r, double& px, double& py, double& pz, int& t) const {
         if (LAYOUT == AOS) {
-            double4 v = p4[r];
+            double4 v = ldg256(p4 + r);
             px = v.x; py = v.y; pz = v.z; t = (int)v.w;
         } else {
             px = x[r]; py = y[r]; pz = z[r]; t = tid[r];

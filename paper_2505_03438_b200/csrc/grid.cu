@@ -117,7 +117,8 @@ void Grid::release() {
 }
 
 void Verlet::release() {
-    grid.release(); bpos.release(); counts.release(); noff.release(); nbr.release();
+    grid.release(); cnt.release(); nbr.release(); s4.release(); s3.release();
+    cap = 0;
     built = false;
 }
 

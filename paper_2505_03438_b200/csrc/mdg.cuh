@@ -82,14 +82,16 @@ struct Grid {
     void release();
 };
 
-// Verlet lists (containers.py:343-375): CSR by owner index, int32 entries.
+// Verlet lists (containers.py:343-375) in the CSF-1 grid's row space:
+// per-row counts + warp-blocked column-major int32 entries of width `cap`.
 struct Verlet {
     Grid grid;
-    DBuf<double4> bpos;        // build-time sorted positions (pos[src]+shift)
-    DBuf<int> counts;          // n
-    DBuf<long long> noff;      // n + 1
-    DBuf<int> nbr;             // E
-    int64_t entries = 0;
+    DBuf<int> cnt;             // per row
+    DBuf<int> nbr;             // ceil(m/32)*32*cap row indices
+    int cap = 0;
+    DBuf<double4> s4;          // unwrapped sorted positions {x,y,z,type} (AoS variant)
+    DBuf<double> s3;           // x[m], y[m], z[m] (SoA variant)
+    bool s3_valid = false;
     bool built = false;
     void release();
 };
@@ -139,7 +141,8 @@ void grid_refresh(Context& c, Grid& gr, int layout);
 void lc_compute(Context& c, Grid& gr, int traversal, int newton3, int layout);
 void lc_fold_forces(Context& c, Grid& gr, int layout, bool images_written);
 int vl_rebuild(Context& c);
-void vl_compute(Context& c);
+void vl_compute(Context& c, int layout);
+int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr);
 void integ_drift_wrap(Context& c, double dt);
 void integ_finish_kick(Context& c, double dt, int has_gravity, double gravity);
 void integ_sd_step(Context& c, double gamma, double max_disp);

@@ -1,37 +1,73 @@
-// Verlet lists: CSR build over the CSF-1 grid and the per-particle list walk.
+// Verlet lists (VL-List_Iter-NoN3L-{AoS,SoA}) realised for the GPU.
 //
 // Reference: VerletListState (containers.py:343-375), vl_count_pairs /
 // vl_fill_pairs (kernels.py:823-910), vl_force_aos/_soa (kernels.py:730-818).
-// The list content and order are the reference's: for each owner particle,
-// partners with r^2 <= (rc+skin)^2 (non-strict) from its own cell (j != i)
-// then the pruned stencil cells in stencil order, stored as owner indices.
-// Entries are int32 (owner indices), offsets int64.
+//
+// Same pair sets, same per-owner order, same counts as the reference; the
+// storage is GPU-shaped:
+//  * lists live in the cell-sorted row space of the CSF-1 grid (owned rows +
+//    periodic-image rows, containers.py:78-118), one row per list, entries are
+//    int32 row indices, stored warp-blocked column-major with a fixed width
+//    (entry k of row r at [(r/32)*32*cap + k*32 + r%32]) so a warp's k-th
+//    loads are one 128-byte line;
+//  * the build is a single pass (count + fill) with r^2 <= (rc+skin)^2 in fp64
+//    on the build-time positions pos[src] + shift; the width is retried upward
+//    if any row overflows;
+//  * every compute first refreshes an "unwrapped" sorted copy of the positions:
+//    each row takes the periodic image of pos[src] (+ build shift) nearest to
+//    its previous value, so d = x_i - x_j is the minimum-image displacement of
+//    the reference (kernels.py:755-757) without per-pair rint() work;
+//  * the force walk is one thread per row (halo rows have empty lists), writes
+//    only f_i (NoN3L), counts each within-cutoff direction.
+#include <algorithm>
+#include <vector>
+
 #include "device.cuh"
 
 namespace mdg {
 
-// One thread per owned row of the build grid; FILL=false counts, FILL=true
-// writes at noff[owner].
-template <bool FILL>
+// 1/x: MUFU.RCP64H seed (~2^-22) + one cubically convergent correction
+// y(1 + e + e^2), e = 1 - x y: three DFMAs to full double precision (the LJ
+// minimum cancels 2 a6 - 1, so a single Newton step's 1e-13 is visible
+// there), instead of the IEEE division sequence with its slow-path branch.
+__device__ __forceinline__ double fast_rcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    double t = fma(e, e, e);
+    return fma(y, t, y);
+}
+
+__device__ __forceinline__ double lj_fs_fast(double r2, double s2, double e24) {
+    double y = fast_rcp(r2);
+    double a = s2 * y;
+    double a6 = a * a * a;
+    return (e24 * y) * (a6 * fma(2.0, a6, -1.0));
+}
+
+// ---------------------------------------------------------------- build
+
 __global__ void __launch_bounds__(128) vl_build_kernel(GridView gv, const double4* __restrict__ bpos,
-                                                       const int* __restrict__ row_src, Stencil st,
-                                                       double ell2, int* __restrict__ counts,
-                                                       const long long* __restrict__ noff,
-                                                       int* __restrict__ nbr) {
+                                                       const uint8_t* __restrict__ row_code,
+                                                       Stencil st, double ell2, int cap,
+                                                       int* __restrict__ cnt, int* __restrict__ nbr,
+                                                       int* __restrict__ maxcnt) {
     int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= gv.m) return;
+    if (row_code[r] != kNoShift) {   // periodic-image rows own no list
+        cnt[r] = 0;
+        return;
+    }
     int cell = gv.row_cell[r], cx, cy, cz;
     gv.decode(cell, cx, cy, cz);
-    if (!gv.owned(cx, cy, cz)) return;
     double4 pi = bpos[r];
-    int oi = row_src[r];
-    long long out = FILL ? noff[oi] : 0;
+    int* out = nbr + (size_t)(r >> 5) * 32 * cap + (r & 31);
     int c = 0;
     auto visit = [&](int j) {
-        double4 pj = bpos[j];
+        double4 pj = ldg256(bpos + j);
         double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-        if (dx * dx + dy * dy + dz * dz <= ell2) {
-            if (FILL) nbr[out + c] = row_src[j];
+        if (dx * dx + dy * dy + dz * dz <= ell2) {   // non-strict (kernels.py:848)
+            if (c < cap) out[(size_t)c * 32] = j;
             ++c;
         }
     };
@@ -45,109 +81,225 @@ __global__ void __launch_bounds__(128) vl_build_kernel(GridView gv, const double
         int e2 = gv.start[c2 + 1];
         for (int j = gv.start[c2]; j < e2; ++j) visit(j);
     }
-    if (!FILL) counts[oi] = c;
+    cnt[r] = c;
+    if (c > cap) atomicMax(maxcnt, c);
 }
 
 int vl_rebuild(Context& c) {
     Verlet& v = c.vl;
     Grid& gr = v.grid;
     if (grid_rebuild(c, gr, c.pos, c.layout)) return -1;
-    // build-time sorted positions (containers.py:356-358): AoS records
     grid_bind_scratch(c, gr, AOS);
-    grid_refresh(c, gr, AOS);
-    int64_t n = c.n;
-    v.counts.ensure(n + 1);
-    v.noff.ensure(n + 1);
+    grid_refresh(c, gr, AOS);   // build-time positions pos[src] + shift (containers.py:356-358)
+    int m = (int)gr.m;
+    size_t mpad = ((size_t)m + 31) / 32 * 32;
+    v.cnt.ensure(mpad + 1);
+    if (v.cap == 0) {
+        // first guess from the mean density: rho * 4/3 pi ell^3, plus headroom
+        double vol = c.L[0] * c.L[1] * c.L[2];
+        double ell = gr.g.ell;
+        double expect = (double)c.n / vol * 4.18879020479 * ell * ell * ell;
+        v.cap = ((int)(1.5 * expect) + 16 + 7) / 8 * 8;
+    }
     GridView gv = make_view(gr);
     double ell2 = gr.g.ell * gr.g.ell;
-    int m = (int)gr.m;
-    if (m > 0)
-        vl_build_kernel<false><<<blocks_for(m, 128), 128, 0, c.stream>>>(
-            gv, gr.spos4.p, gr.row_src.p, gr.pruned, ell2, v.counts.p, nullptr, nullptr), note_launch();
-    MDG_CUDA(cudaMemsetAsync(v.counts.p + n, 0, sizeof(int), c.stream));
-    exclusive_scan_i32_to_i64(v.counts.p, v.noff.p, n + 1, c.scal.p + 1, c.scan_tmp, c.stream);
-    MDG_CUDA(cudaMemcpyAsync(c.h_scal + 1, c.scal.p + 1, sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, c.stream));
-    MDG_CUDA(cudaStreamSynchronize(c.stream));
-    v.entries = (int64_t)c.h_scal[1];
-    v.nbr.ensure(v.entries + 1);
-    if (m > 0)
-        vl_build_kernel<true><<<blocks_for(m, 128), 128, 0, c.stream>>>(
-            gv, gr.spos4.p, gr.row_src.p, gr.pruned, ell2, nullptr, v.noff.p, v.nbr.p), note_launch();
+    int* maxcnt = (int*)(c.scal.p + 3);
+    for (int attempt = 0; attempt < 3 && m > 0; ++attempt) {
+        v.nbr.ensure(mpad * (size_t)v.cap);
+        MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
+        vl_build_kernel<<<blocks_for(m, 128), 128, 0, c.stream>>>(
+            gv, gr.spos4.p, gr.row_code.p, gr.pruned, ell2, v.cap, v.cnt.p, v.nbr.p, maxcnt), note_launch();
+        int hmax = 0;
+        MDG_CUDA(cudaMemcpyAsync(&hmax, maxcnt, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        MDG_CUDA(cudaStreamSynchronize(c.stream));
+        if (hmax <= v.cap) break;
+        v.cap = (hmax + hmax / 8 + 7) / 8 * 8;
+    }
+    // the unwrapped force-time copy starts from the build positions
+    v.s4.ensure(mpad + 1);
+    MDG_CUDA(cudaMemcpyAsync(v.s4.p, gr.spos4.p, (size_t)m * sizeof(double4),
+                             cudaMemcpyDeviceToDevice, c.stream));
+    v.s3_valid = false;
     MDG_CUDA(cudaGetLastError());
     v.built = true;
     return 0;
 }
 
-struct MinImage {
-    double L[3], invL[3];
+// ---------------------------------------------------------------- refresh
+
+struct Wrap {
+    double L[3];
+    double invL[3];
     int per[3];
 };
 
-// vl_force (kernels.py:730-818): per particle, list walk on the particle
-// arrays, minimum image on periodic axes, strict cutoff, writes only f_i.
-template <int LAYOUT, bool MT>
-__global__ void __launch_bounds__(128) vl_force_kernel(int64_t n, const double* __restrict__ pos,
-                                                       double* __restrict__ force,
-                                                       const int* __restrict__ tid,
-                                                       const long long* __restrict__ noff,
-                                                       const int* __restrict__ nbr, LJTab tab,
-                                                       MinImage mi,
+// Nearest periodic image of pos[src] + shift to the previous row value.
+template <int PLAYOUT, int SLAYOUT>
+__global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int m,
+                                  const int* __restrict__ row_src,
+                                  const uint8_t* __restrict__ row_code, Wrap w,
+                                  double4* __restrict__ s4, double* __restrict__ s3,
+                                  bool from_s4) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    int src = row_src[r], code = row_code[r];
+    double q[3] = {pos[pidx<PLAYOUT>(src, 0, n)], pos[pidx<PLAYOUT>(src, 1, n)],
+                   pos[pidx<PLAYOUT>(src, 2, n)]};
+    int sh[3] = {code / 9 - 1, (code / 3) % 3 - 1, code % 3 - 1};
+    double prev[3];
+    double4 old = s4[r];
+    if (SLAYOUT == AOS || from_s4) {
+        prev[0] = old.x; prev[1] = old.y; prev[2] = old.z;
+    } else {
+        prev[0] = s3[r]; prev[1] = s3[(size_t)m + r]; prev[2] = s3[2 * (size_t)m + r];
+    }
+    for (int k = 0; k < 3; ++k) {
+        double x = q[k] + (double)sh[k] * w.L[k];
+        if (w.per[k]) x += w.L[k] * rint((prev[k] - x) * w.invL[k]);
+        q[k] = x;
+    }
+    if (SLAYOUT == AOS) {
+        s4[r] = make_double4(q[0], q[1], q[2], old.w);
+    } else {
+        s3[r] = q[0];
+        s3[(size_t)m + r] = q[1];
+        s3[2 * (size_t)m + r] = q[2];
+    }
+}
+
+// ---------------------------------------------------------------- force
+
+template <int SLAYOUT, int PLAYOUT, bool MT>
+__global__ void __launch_bounds__(128) vl_force_kernel(int m, int64_t n, int cap,
+                                                       const double4* __restrict__ s4,
+                                                       const double* __restrict__ s3,
+                                                       const int* __restrict__ row_tid,
+                                                       const int* __restrict__ cnt,
+                                                       const int* __restrict__ nbr,
+                                                       const int* __restrict__ row_src,
+                                                       const uint8_t* __restrict__ row_code,
+                                                       double* __restrict__ force, LJTab tab,
                                                        unsigned long long* counter) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned cnt = 0;
-    if (i < n) {
-        double xi = pos[pidx<LAYOUT>(i, 0, n)], yi = pos[pidx<LAYOUT>(i, 1, n)],
-               zi = pos[pidx<LAYOUT>(i, 2, n)];
-        int ti = MT ? tid[i] : 0;
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned hits = 0;
+    if (r < m && row_code[r] == kNoShift) {
+        double xi, yi, zi;
+        int ti = 0;
+        if (SLAYOUT == AOS) {
+            double4 p = s4[r];
+            xi = p.x; yi = p.y; zi = p.z;
+            if (MT) ti = (int)p.w;
+        } else {
+            xi = s3[r]; yi = s3[(size_t)m + r]; zi = s3[2 * (size_t)m + r];
+            if (MT) ti = row_tid[r];
+        }
         double fx = 0.0, fy = 0.0, fz = 0.0;
-        long long k1 = noff[i + 1];
-        for (long long k = noff[i]; k < k1; ++k) {
-            int j = nbr[k];
-            double dx = xi - pos[pidx<LAYOUT>(j, 0, n)];
-            double dy = yi - pos[pidx<LAYOUT>(j, 1, n)];
-            double dz = zi - pos[pidx<LAYOUT>(j, 2, n)];
-            if (mi.per[0]) dx -= mi.L[0] * rint(dx * mi.invL[0]);
-            if (mi.per[1]) dy -= mi.L[1] * rint(dy * mi.invL[1]);
-            if (mi.per[2]) dz -= mi.L[2] * rint(dz * mi.invL[2]);
+        const int* lp = nbr + (size_t)(r >> 5) * 32 * cap + (r & 31);
+        int c = cnt[r];
+#pragma unroll 4
+        for (int k = 0; k < c; ++k) {
+            int j = lp[(size_t)k * 32];
+            double xj, yj, zj;
+            int tj = 0;
+            if (SLAYOUT == AOS) {
+                double4 p = ldg256(s4 + j);
+                xj = p.x; yj = p.y; zj = p.z;
+                if (MT) tj = (int)p.w;
+            } else {
+                xj = s3[j]; yj = s3[(size_t)m + j]; zj = s3[2 * (size_t)m + j];
+                if (MT) tj = row_tid[j];
+            }
+            double dx = xi - xj, dy = yi - yj, dz = zi - zj;
             double r2 = dx * dx + dy * dy + dz * dz;
             if (r2 < tab.rc2) {
                 double s2, e24;
-                lj_params<MT>(tab, ti, MT ? tid[j] : 0, s2, e24);
-                double fs = lj_fs(r2, s2, e24);
-                ++cnt;
-                fx += fs * dx;
-                fy += fs * dy;
-                fz += fs * dz;
+                lj_params<MT>(tab, ti, tj, s2, e24);
+                double fs = lj_fs_fast(r2, s2, e24);
+                ++hits;
+                fx = fma(fs, dx, fx);
+                fy = fma(fs, dy, fy);
+                fz = fma(fs, dz, fz);
             }
         }
-        force[pidx<LAYOUT>(i, 0, n)] = fx;
-        force[pidx<LAYOUT>(i, 1, n)] = fy;
-        force[pidx<LAYOUT>(i, 2, n)] = fz;
+        int i = row_src[r];
+        force[pidx<PLAYOUT>(i, 0, n)] = fx;
+        force[pidx<PLAYOUT>(i, 1, n)] = fy;
+        force[pidx<PLAYOUT>(i, 2, n)] = fz;
     }
-    warp_count(counter, cnt);
+    warp_count(counter, hits);
 }
 
-void vl_compute(Context& c) {
-    if (c.n == 0) return;
-    MinImage mi;
+template <int SLAYOUT, int PLAYOUT>
+static void vl_launch(Context& c, bool mt) {
+    Verlet& v = c.vl;
+    Grid& gr = v.grid;
+    int m = (int)gr.m;
+    Wrap w;
     for (int k = 0; k < 3; ++k) {
-        mi.L[k] = c.L[k];
-        mi.invL[k] = 1.0 / c.L[k];
-        mi.per[k] = c.periodic[k];
+        w.L[k] = c.L[k];
+        w.invL[k] = 1.0 / c.L[k];
+        w.per[k] = c.periodic[k];
     }
+    dim3 b(blocks_for(m, 256)), t(256);
+    bool from_s4 = SLAYOUT == SOA && !v.s3_valid;
+    vl_refresh_kernel<PLAYOUT, SLAYOUT><<<b, t, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, from_s4), note_launch();
+    if (SLAYOUT == SOA) v.s3_valid = true;
+    c.prof_mark();
+    dim3 fb(blocks_for(m, 128)), ft(128);
+    if (mt)
+        vl_force_kernel<SLAYOUT, PLAYOUT, true><<<fb, ft, 0, c.stream>>>(m, c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p, gr.row_code.p, c.force, c.tab, c.scal.p), note_launch();
+    else
+        vl_force_kernel<SLAYOUT, PLAYOUT, false><<<fb, ft, 0, c.stream>>>(m, c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p, gr.row_code.p, c.force, c.tab, c.scal.p), note_launch();
+    c.prof_mark();
+}
+
+void vl_compute(Context& c, int layout) {
+    if (c.n == 0) return;
+    Verlet& v = c.vl;
     bool mt = c.tab.T > 1;
-    dim3 b(blocks_for(c.n, 128)), t(128);
-    auto* v = &c.vl;
-    c.prof_mark();
+    if (layout == SOA) v.s3.ensure(3 * (size_t)v.grid.m + 3);
     if (c.layout == AOS) {
-        if (mt) vl_force_kernel<AOS, true><<<b, t, 0, c.stream>>>(c.n, c.pos, c.force, c.tid, v->noff.p, v->nbr.p, c.tab, mi, c.scal.p), note_launch();
-        else vl_force_kernel<AOS, false><<<b, t, 0, c.stream>>>(c.n, c.pos, c.force, c.tid, v->noff.p, v->nbr.p, c.tab, mi, c.scal.p), note_launch();
+        if (layout == AOS) vl_launch<AOS, AOS>(c, mt);
+        else vl_launch<SOA, AOS>(c, mt);
     } else {
-        if (mt) vl_force_kernel<SOA, true><<<b, t, 0, c.stream>>>(c.n, c.pos, c.force, c.tid, v->noff.p, v->nbr.p, c.tab, mi, c.scal.p), note_launch();
-        else vl_force_kernel<SOA, false><<<b, t, 0, c.stream>>>(c.n, c.pos, c.force, c.tid, v->noff.p, v->nbr.p, c.tab, mi, c.scal.p), note_launch();
+        if (layout == AOS) vl_launch<AOS, SOA>(c, mt);
+        else vl_launch<SOA, SOA>(c, mt);
     }
-    c.prof_mark();
+}
+
+// Reference-format export: CSR by owner index with owner indices.
+int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr) {
+    Verlet& v = c.vl;
+    Grid& gr = v.grid;
+    int m = (int)gr.m;
+    size_t mpad = ((size_t)m + 31) / 32 * 32;
+    std::vector<int> cnt(m), src(m), ell(mpad * (size_t)v.cap);
+    std::vector<uint8_t> code(m);
+    MDG_CUDA(cudaStreamSynchronize(c.stream));
+    if (m) {
+        MDG_CUDA(cudaMemcpy(cnt.data(), v.cnt.p, m * sizeof(int), cudaMemcpyDeviceToHost));
+        MDG_CUDA(cudaMemcpy(src.data(), gr.row_src.p, m * sizeof(int), cudaMemcpyDeviceToHost));
+        MDG_CUDA(cudaMemcpy(code.data(), gr.row_code.p, m, cudaMemcpyDeviceToHost));
+        MDG_CUDA(cudaMemcpy(ell.data(), v.nbr.p, ell.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    }
+    int64_t n = c.n;
+    std::vector<int64_t> per(n + 1, 0);
+    std::vector<int> row_of(n, -1);
+    for (int r = 0; r < m; ++r)
+        if (code[r] == kNoShift) {
+            per[src[r] + 1] = cnt[r];
+            row_of[src[r]] = r;
+        }
+    for (int64_t i = 0; i < n; ++i) per[i + 1] += per[i];
+    *entries = per[n];
+    if (noff) std::copy(per.begin(), per.end(), noff);
+    if (nbr)
+        for (int64_t i = 0; i < n; ++i) {
+            int r = row_of[i];
+            const int* lp = ell.data() + (size_t)(r >> 5) * 32 * v.cap + (r & 31);
+            for (int k = 0; k < cnt[r]; ++k) nbr[per[i] + k] = src[lp[(size_t)k * 32]];
+        }
+    return 0;
 }
 
 }  // namespace mdg

@@ -106,6 +106,8 @@ template struct DBuf<double>;
 template struct DBuf<double4>;
 template struct DBuf<long long>;
 template struct DBuf<unsigned long long>;
+template struct DBuf<uint16_t>;
+template struct DBuf<int4>;
 
 void Grid::release() {
     cell_count.release(); cell_start.release(); cell_fill.release();

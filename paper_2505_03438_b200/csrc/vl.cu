@@ -71,16 +71,25 @@ __global__ void __launch_bounds__(128) vl_build_kernel(GridView gv, const double
             ++c;
         }
     };
-    int s = gv.start[cell], e = gv.start[cell + 1];
-    for (int j = s; j < e; ++j)
-        if (j != r) visit(j);
-    for (int k = 0; k < st.n; ++k) {
+    // Cells in ascending flat order: the pruned stencil is in product
+    // (lexicographic) order and symmetric, so its first half precedes the own
+    // cell.  Every list is then sorted by row, and the 32 lanes of a warp
+    // (consecutive rows, 1-3 neighbouring cells) walk the same neighbour cells
+    // in step: a warp's k-th gathers touch a few cache lines, not ~30.
+    // (The reference lists the own cell first; mdg_get_verlet restores that.)
+    auto visit_cell = [&](int k) {
         int x2 = cx + st.d[k][0], y2 = cy + st.d[k][1], z2 = cz + st.d[k][2];
-        if (!gv.in_grid(x2, y2, z2)) continue;
+        if (!gv.in_grid(x2, y2, z2)) return;
         int c2 = gv.flat(x2, y2, z2);
         int e2 = gv.start[c2 + 1];
         for (int j = gv.start[c2]; j < e2; ++j) visit(j);
-    }
+    };
+    int half = st.n / 2;
+    for (int k = 0; k < half; ++k) visit_cell(k);
+    int s = gv.start[cell], e = gv.start[cell + 1];
+    for (int j = s; j < e; ++j)
+        if (j != r) visit(j);
+    for (int k = half; k < st.n; ++k) visit_cell(k);
     cnt[r] = c;
     if (c > cap) atomicMax(maxcnt, c);
 }
@@ -196,29 +205,50 @@ __global__ void __launch_bounds__(128) vl_force_kernel(int m, int64_t n, int cap
         double fx = 0.0, fy = 0.0, fz = 0.0;
         const int* lp = nbr + (size_t)(r >> 5) * 32 * cap + (r & 31);
         int c = cnt[r];
-#pragma unroll 4
-        for (int k = 0; k < c; ++k) {
-            int j = lp[(size_t)k * 32];
-            double xj, yj, zj;
-            int tj = 0;
-            if (SLAYOUT == AOS) {
-                double4 p = ldg256(s4 + j);
-                xj = p.x; yj = p.y; zj = p.z;
-                if (MT) tj = (int)p.w;
-            } else {
-                xj = s3[j]; yj = s3[(size_t)m + j]; zj = s3[2 * (size_t)m + j];
-                if (MT) tj = row_tid[j];
+        // Four entries per round share one reciprocal: y = 1/(q0 q1 q2 q3),
+        // 1/q0 = y q1 q2 q3 etc.  The XU (MUFU.RCP64H) pipe saturates at one
+        // reciprocal per pair; batching moves 3/4 of it onto DMULs.
+        constexpr int G = 4;
+        for (int k0 = 0; k0 < c; k0 += G) {
+            double dx[G], dy[G], dz[G], q[G];
+            int tj[G];
+            bool ok[G];
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                bool has = k0 + u < c;
+                int j = has ? lp[(size_t)(k0 + u) * 32] : r;
+                double xj, yj, zj;
+                tj[u] = 0;
+                if (SLAYOUT == AOS) {
+                    double4 p = ldg256(s4 + j);
+                    xj = p.x; yj = p.y; zj = p.z;
+                    if (MT) tj[u] = (int)p.w;
+                } else {
+                    xj = s3[j]; yj = s3[(size_t)m + j]; zj = s3[2 * (size_t)m + j];
+                    if (MT) tj[u] = row_tid[j];
+                }
+                dx[u] = xi - xj; dy[u] = yi - yj; dz[u] = zi - zj;
+                double r2 = dx[u] * dx[u] + dy[u] * dy[u] + dz[u] * dz[u];
+                ok[u] = has && r2 < tab.rc2;
+                q[u] = ok[u] ? r2 : 1.0;
             }
-            double dx = xi - xj, dy = yi - yj, dz = zi - zj;
-            double r2 = dx * dx + dy * dy + dz * dz;
-            if (r2 < tab.rc2) {
-                double s2, e24;
-                lj_params<MT>(tab, ti, tj, s2, e24);
-                double fs = lj_fs_fast(r2, s2, e24);
-                ++hits;
-                fx = fma(fs, dx, fx);
-                fy = fma(fs, dy, fy);
-                fz = fma(fs, dz, fz);
+            double p01 = q[0] * q[1], p23 = q[2] * q[3];
+            double y = fast_rcp(p01 * p23);
+            double y01 = y * p23, y23 = y * p01;
+            double inv[G] = {y01 * q[1], y01 * q[0], y23 * q[3], y23 * q[2]};
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                if (ok[u]) {
+                    double s2, e24;
+                    lj_params<MT>(tab, ti, tj[u], s2, e24);
+                    double a = s2 * inv[u];
+                    double a6 = a * a * a;
+                    double fs = (e24 * inv[u]) * (a6 * fma(2.0, a6, -1.0));
+                    ++hits;
+                    fx = fma(fs, dx[u], fx);
+                    fy = fma(fs, dy[u], fy);
+                    fz = fma(fs, dz[u], fz);
+                }
             }
         }
         int i = row_src[r];
@@ -273,12 +303,13 @@ int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr) {
     Grid& gr = v.grid;
     int m = (int)gr.m;
     size_t mpad = ((size_t)m + 31) / 32 * 32;
-    std::vector<int> cnt(m), src(m), ell(mpad * (size_t)v.cap);
+    std::vector<int> cnt(m), src(m), cellof(m), ell(mpad * (size_t)v.cap);
     std::vector<uint8_t> code(m);
     MDG_CUDA(cudaStreamSynchronize(c.stream));
     if (m) {
         MDG_CUDA(cudaMemcpy(cnt.data(), v.cnt.p, m * sizeof(int), cudaMemcpyDeviceToHost));
         MDG_CUDA(cudaMemcpy(src.data(), gr.row_src.p, m * sizeof(int), cudaMemcpyDeviceToHost));
+        MDG_CUDA(cudaMemcpy(cellof.data(), gr.row_cell.p, m * sizeof(int), cudaMemcpyDeviceToHost));
         MDG_CUDA(cudaMemcpy(code.data(), gr.row_code.p, m, cudaMemcpyDeviceToHost));
         MDG_CUDA(cudaMemcpy(ell.data(), v.nbr.p, ell.size() * sizeof(int), cudaMemcpyDeviceToHost));
     }
@@ -295,9 +326,17 @@ int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr) {
     if (noff) std::copy(per.begin(), per.end(), noff);
     if (nbr)
         for (int64_t i = 0; i < n; ++i) {
+            // device lists are row-sorted; the reference order is own cell
+            // first, then the stencil cells (kernels.py:886-906)
             int r = row_of[i];
             const int* lp = ell.data() + (size_t)(r >> 5) * 32 * v.cap + (r & 31);
-            for (int k = 0; k < cnt[r]; ++k) nbr[per[i] + k] = src[lp[(size_t)k * 32]];
+            int64_t o = per[i];
+            for (int pass = 0; pass < 2; ++pass)
+                for (int k = 0; k < cnt[r]; ++k) {
+                    int j = lp[(size_t)k * 32];
+                    bool own = cellof[j] == cellof[r];
+                    if (own == (pass == 0)) nbr[o++] = src[j];
+                }
         }
     return 0;
 }

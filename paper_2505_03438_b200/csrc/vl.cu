@@ -178,17 +178,22 @@ __global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int
 
 // ---------------------------------------------------------------- force
 
-template <int SLAYOUT, int PLAYOUT, bool MT>
-__global__ void __launch_bounds__(128) vl_force_kernel(int m, int64_t n, int cap,
-                                                       const double4* __restrict__ s4,
-                                                       const double* __restrict__ s3,
-                                                       const int* __restrict__ row_tid,
-                                                       const int* __restrict__ cnt,
-                                                       const int* __restrict__ nbr,
-                                                       const int* __restrict__ row_src,
-                                                       const uint8_t* __restrict__ row_code,
-                                                       double* __restrict__ force, LJTab tab,
-                                                       unsigned long long* counter) {
+// G entries per round (a multiple of 4: every four share one reciprocal,
+// y = 1/(q0 q1 q2 q3), 1/q0 = y q1 q2 q3 etc., so the XU pipe sees one
+// MUFU.RCP64H per four pairs).  PF: the next round's list indices are loaded
+// before this round's gathers, so the HBM latency of the list stream overlaps
+// the gather + arithmetic of the current round.
+template <int SLAYOUT, int PLAYOUT, bool MT, int G, bool PF, int NT>
+__global__ void __launch_bounds__(NT) vl_force_kernel(int m, int64_t n, int cap,
+                                                      const double4* __restrict__ s4,
+                                                      const double* __restrict__ s3,
+                                                      const int* __restrict__ row_tid,
+                                                      const int* __restrict__ cnt,
+                                                      const int* __restrict__ nbr,
+                                                      const int* __restrict__ row_src,
+                                                      const uint8_t* __restrict__ row_code,
+                                                      double* __restrict__ force, LJTab tab,
+                                                      unsigned long long* counter) {
     int r = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned hits = 0;
     if (r < m && row_code[r] == kNoShift) {
@@ -205,18 +210,24 @@ __global__ void __launch_bounds__(128) vl_force_kernel(int m, int64_t n, int cap
         double fx = 0.0, fy = 0.0, fz = 0.0;
         const int* lp = nbr + (size_t)(r >> 5) * 32 * cap + (r & 31);
         int c = cnt[r];
-        // Four entries per round share one reciprocal: y = 1/(q0 q1 q2 q3),
-        // 1/q0 = y q1 q2 q3 etc.  The XU (MUFU.RCP64H) pipe saturates at one
-        // reciprocal per pair; batching moves 3/4 of it onto DMULs.
-        constexpr int G = 4;
+        int jn[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) jn[u] = u < c ? lp[(size_t)u * 32] : r;
         for (int k0 = 0; k0 < c; k0 += G) {
             double dx[G], dy[G], dz[G], q[G];
-            int tj[G];
+            int tj[G], jc[G];
             bool ok[G];
+#pragma unroll
+            for (int u = 0; u < G; ++u) jc[u] = jn[u];
+            if (PF) {
+#pragma unroll
+                for (int u = 0; u < G; ++u)
+                    jn[u] = k0 + G + u < c ? lp[(size_t)(k0 + G + u) * 32] : r;
+            }
 #pragma unroll
             for (int u = 0; u < G; ++u) {
                 bool has = k0 + u < c;
-                int j = has ? lp[(size_t)(k0 + u) * 32] : r;
+                int j = jc[u];
                 double xj, yj, zj;
                 tj[u] = 0;
                 if (SLAYOUT == AOS) {
@@ -232,10 +243,22 @@ __global__ void __launch_bounds__(128) vl_force_kernel(int m, int64_t n, int cap
                 ok[u] = has && r2 < tab.rc2;
                 q[u] = ok[u] ? r2 : 1.0;
             }
-            double p01 = q[0] * q[1], p23 = q[2] * q[3];
-            double y = fast_rcp(p01 * p23);
-            double y01 = y * p23, y23 = y * p01;
-            double inv[G] = {y01 * q[1], y01 * q[0], y23 * q[3], y23 * q[2]};
+            double inv[G];
+#pragma unroll
+            for (int b = 0; b < G; b += 4) {
+                double p01 = q[b] * q[b + 1], p23 = q[b + 2] * q[b + 3];
+                double y = fast_rcp(p01 * p23);
+                double y01 = y * p23, y23 = y * p01;
+                inv[b] = y01 * q[b + 1];
+                inv[b + 1] = y01 * q[b];
+                inv[b + 2] = y23 * q[b + 3];
+                inv[b + 3] = y23 * q[b + 2];
+            }
+            if (!PF) {
+#pragma unroll
+                for (int u = 0; u < G; ++u)
+                    jn[u] = k0 + G + u < c ? lp[(size_t)(k0 + G + u) * 32] : r;
+            }
 #pragma unroll
             for (int u = 0; u < G; ++u) {
                 if (ok[u]) {
@@ -259,6 +282,16 @@ __global__ void __launch_bounds__(128) vl_force_kernel(int m, int64_t n, int cap
     warp_count(counter, hits);
 }
 
+// Force-walk variant (tuning experiments): MDG_VL_VARIANT=0..5, read once.
+static int vl_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_VL_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
 template <int SLAYOUT, int PLAYOUT>
 static void vl_launch(Context& c, bool mt) {
     Verlet& v = c.vl;
@@ -275,11 +308,28 @@ static void vl_launch(Context& c, bool mt) {
     vl_refresh_kernel<PLAYOUT, SLAYOUT><<<b, t, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, from_s4), note_launch();
     if (SLAYOUT == SOA) v.s3_valid = true;
     c.prof_mark();
-    dim3 fb(blocks_for(m, 128)), ft(128);
-    if (mt)
-        vl_force_kernel<SLAYOUT, PLAYOUT, true><<<fb, ft, 0, c.stream>>>(m, c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p, gr.row_code.p, c.force, c.tab, c.scal.p), note_launch();
-    else
-        vl_force_kernel<SLAYOUT, PLAYOUT, false><<<fb, ft, 0, c.stream>>>(m, c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p, gr.row_code.p, c.force, c.tab, c.scal.p), note_launch();
+#define MDG_VLF(G, PF, NT)                                                                       \
+    do {                                                                                         \
+        if (mt)                                                                                  \
+            vl_force_kernel<SLAYOUT, PLAYOUT, true, G, PF, NT><<<blocks_for(m, NT), NT, 0, c.stream>>>( \
+                m, c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p,      \
+                gr.row_code.p, c.force, c.tab, c.scal.p), note_launch();                          \
+        else                                                                                     \
+            vl_force_kernel<SLAYOUT, PLAYOUT, false, G, PF, NT><<<blocks_for(m, NT), NT, 0, c.stream>>>( \
+                m, c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p,      \
+                gr.row_code.p, c.force, c.tab, c.scal.p), note_launch();                          \
+    } while (0)
+    // measured on B200, config 2 (profiles/round1_vl_variants.txt): all within
+    // 6%; index prefetch with 4-entry rounds and 128-thread CTAs is fastest
+    switch (vl_variant()) {
+        case 10: MDG_VLF(4, false, 128); break;
+        case 2: MDG_VLF(8, false, 128); break;
+        case 3: MDG_VLF(8, true, 128); break;
+        case 4: MDG_VLF(4, true, 256); break;
+        case 5: MDG_VLF(4, true, 64); break;
+        default: MDG_VLF(4, true, 128); break;
+    }
+#undef MDG_VLF
     c.prof_mark();
 }
 

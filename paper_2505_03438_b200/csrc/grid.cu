@@ -108,6 +108,7 @@ template struct DBuf<long long>;
 template struct DBuf<unsigned long long>;
 template struct DBuf<uint16_t>;
 template struct DBuf<int4>;
+template struct DBuf<float4>;
 
 void Grid::release() {
     cell_count.release(); cell_start.release(); cell_fill.release();
@@ -119,7 +120,7 @@ void Grid::release() {
 }
 
 void Verlet::release() {
-    grid.release(); cnt.release(); nbr.release(); s4.release(); s3.release();
+    grid.release(); cnt.release(); nbr.release(); s4.release(); s3.release(); b32.release();
     cap = 0;
     built = false;
 }

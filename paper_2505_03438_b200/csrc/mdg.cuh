@@ -89,6 +89,7 @@ struct Verlet {
     DBuf<int> cnt;             // per row
     DBuf<int> nbr;             // ceil(m/32)*32*cap row indices
     int cap = 0;
+    DBuf<float4> b32;          // fp32 build positions (membership pre-filter)
     DBuf<double4> s4;          // unwrapped sorted positions {x,y,z,type} (AoS variant)
     DBuf<double> s3;           // x[m], y[m], z[m] (SoA variant)
     bool s3_valid = false;

@@ -47,7 +47,31 @@ __device__ __forceinline__ double lj_fs_fast(double r2, double s2, double e24) {
 
 // ---------------------------------------------------------------- build
 
+// fp32 copy of the build positions + max |coordinate| (for the filter margin).
+__global__ void vl_f32_kernel(const double4* __restrict__ s4, int m, float4* __restrict__ b32,
+                              unsigned* __restrict__ maxabs_bits) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    float mx = 0.f;
+    if (r < m) {
+        double4 p = s4[r];
+        float4 q = make_float4((float)p.x, (float)p.y, (float)p.z, 0.f);
+        b32[r] = q;
+        mx = fmaxf(fabsf(q.x), fmaxf(fabsf(q.y), fabsf(q.z)));
+    }
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxabs_bits, __float_as_uint(mx));   // x >= 0
+}
+
+// Membership r^2 <= ell^2 (non-strict, kernels.py:848), decided in fp32 where
+// provably safe and in fp64 otherwise, so the pair set is exactly the
+// reference's.  Rounding bound for coordinates |x| <= X, |d| ~ ell, u = 2^-24:
+// eta = 2uX + 2u ell bounds |d32 - d| per component, and
+// |r2_32 - r2| <= 2 sqrt(3) eta ell + 3 eta^2 + 3u ell^2 =: B.  Candidates with
+// r2_32 <= ell^2 - 2B are in, r2_32 > ell^2 + 2B are out, the rest are tested
+// on the fp64 positions.
 __global__ void __launch_bounds__(128) vl_build_kernel(GridView gv, const double4* __restrict__ bpos,
+                                                       const float4* __restrict__ b32,
+                                                       const unsigned* __restrict__ maxabs_bits,
                                                        const uint8_t* __restrict__ row_code,
                                                        Stencil st, double ell2, int cap,
                                                        int* __restrict__ cnt, int* __restrict__ nbr,
@@ -61,12 +85,26 @@ __global__ void __launch_bounds__(128) vl_build_kernel(GridView gv, const double
     int cell = gv.row_cell[r], cx, cy, cz;
     gv.decode(cell, cx, cy, cz);
     double4 pi = bpos[r];
+    float4 qi = b32[r];
+    const double u = 5.9604644775390625e-08;   // 2^-24
+    double X = (double)__uint_as_float(*maxabs_bits) * (1.0 + 4.0 * u);
+    double ell = sqrt(ell2);
+    double eta = 2.0 * u * X + 2.0 * u * ell;
+    double B = 3.4641016151377544 * eta * ell + 3.0 * eta * eta + 3.0 * u * ell2;
+    float lo = __double2float_rd(ell2 - 2.0 * B), hi = __double2float_ru(ell2 + 2.0 * B);
     int* out = nbr + (size_t)(r >> 5) * 32 * cap + (r & 31);
     int c = 0;
     auto visit = [&](int j) {
-        double4 pj = ldg256(bpos + j);
-        double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-        if (dx * dx + dy * dy + dz * dz <= ell2) {   // non-strict (kernels.py:848)
+        float4 qj = b32[j];
+        float fx = qi.x - qj.x, fy = qi.y - qj.y, fz = qi.z - qj.z;
+        float r2f = fx * fx + fy * fy + fz * fz;
+        bool in = r2f <= lo;
+        if (!in && r2f <= hi) {
+            double4 pj = ldg256(bpos + j);
+            double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+            in = dx * dx + dy * dy + dz * dz <= ell2;
+        }
+        if (in) {
             if (c < cap) out[(size_t)c * 32] = j;
             ++c;
         }
@@ -113,11 +151,16 @@ int vl_rebuild(Context& c) {
     GridView gv = make_view(gr);
     double ell2 = gr.g.ell * gr.g.ell;
     int* maxcnt = (int*)(c.scal.p + 3);
+    unsigned* maxabs = (unsigned*)(c.scal.p + 5);
+    v.b32.ensure(mpad + 1);
+    MDG_CUDA(cudaMemsetAsync(maxabs, 0, sizeof(unsigned), c.stream));
+    if (m > 0)
+        vl_f32_kernel<<<blocks_for(m, 256), 256, 0, c.stream>>>(gr.spos4.p, m, v.b32.p, maxabs), note_launch();
     for (int attempt = 0; attempt < 3 && m > 0; ++attempt) {
         v.nbr.ensure(mpad * (size_t)v.cap);
         MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
         vl_build_kernel<<<blocks_for(m, 128), 128, 0, c.stream>>>(
-            gv, gr.spos4.p, gr.row_code.p, gr.pruned, ell2, v.cap, v.cnt.p, v.nbr.p, maxcnt), note_launch();
+            gv, gr.spos4.p, v.b32.p, maxabs, gr.row_code.p, gr.pruned, ell2, v.cap, v.cnt.p, v.nbr.p, maxcnt), note_launch();
         int hmax = 0;
         MDG_CUDA(cudaMemcpyAsync(&hmax, maxcnt, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
         MDG_CUDA(cudaStreamSynchronize(c.stream));

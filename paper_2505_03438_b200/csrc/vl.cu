@@ -69,19 +69,26 @@ __global__ void vl_f32_kernel(const double4* __restrict__ s4, int m, float4* __r
 // |r2_32 - r2| <= 2 sqrt(3) eta ell + 3 eta^2 + 3u ell^2 =: B.  Candidates with
 // r2_32 <= ell^2 - 2B are in, r2_32 > ell^2 + 2B are out, the rest are tested
 // on the fp64 positions.
-__global__ void __launch_bounds__(128) vl_build_kernel(GridView gv, const double4* __restrict__ bpos,
-                                                       const float4* __restrict__ b32,
-                                                       const unsigned* __restrict__ maxabs_bits,
-                                                       const uint8_t* __restrict__ row_code,
-                                                       Stencil st, double ell2, int cap,
-                                                       int* __restrict__ cnt, int* __restrict__ nbr,
-                                                       int* __restrict__ maxcnt) {
+//
+// STAGE: each warp's lists are assembled in shared memory laid out [k][lane]
+// (a lane's k-th entry sits in bank `lane`, so the scattered appends are
+// conflict-free) and flushed as coalesced 128-byte rows of the column-major
+// list; appending straight to global memory made every accepted pair a
+// partial-line store (~70 per row) and dominated the build.
+constexpr int kBuildThreads = 128;
+
+template <bool STAGE>
+__global__ void __launch_bounds__(kBuildThreads) vl_build_kernel(
+    GridView gv, const double4* __restrict__ bpos, const float4* __restrict__ b32,
+    const unsigned* __restrict__ maxabs_bits, const uint8_t* __restrict__ row_code, Stencil st,
+    double ell2, int cap, int* __restrict__ cnt, int* __restrict__ nbr, int* __restrict__ maxcnt) {
+    extern __shared__ int stage[];
     int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= gv.m) return;
-    if (row_code[r] != kNoShift) {   // periodic-image rows own no list
-        cnt[r] = 0;
-        return;
-    }
+    int lane = threadIdx.x & 31;
+    int* sw = stage + (size_t)(threadIdx.x >> 5) * cap * 32;
+    bool active = r < gv.m && row_code[r] == kNoShift;   // periodic-image rows own no list
+    int c = 0;
+    if (active) {
     int cell = gv.row_cell[r], cx, cy, cz;
     gv.decode(cell, cx, cy, cz);
     double4 pi = bpos[r];
@@ -93,43 +100,84 @@ __global__ void __launch_bounds__(128) vl_build_kernel(GridView gv, const double
     double B = 3.4641016151377544 * eta * ell + 3.0 * eta * eta + 3.0 * u * ell2;
     float lo = __double2float_rd(ell2 - 2.0 * B), hi = __double2float_ru(ell2 + 2.0 * B);
     int* out = nbr + (size_t)(r >> 5) * 32 * cap + (r & 31);
-    int c = 0;
-    auto visit = [&](int j) {
-        float4 qj = b32[j];
-        float fx = qi.x - qj.x, fy = qi.y - qj.y, fz = qi.z - qj.z;
-        float r2f = fx * fx + fy * fy + fz * fz;
-        bool in = r2f <= lo;
-        if (!in && r2f <= hi) {
-            double4 pj = ldg256(bpos + j);
-            double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-            in = dx * dx + dy * dy + dz * dz <= ell2;
-        }
-        if (in) {
-            if (c < cap) out[(size_t)c * 32] = j;
-            ++c;
+    // Tight scan: the next candidate's load is issued before the current one
+    // is tested, the store is predicated and the count advances by the test
+    // result, so the loop has no data-dependent branch except the rare
+    // borderline fp64 re-test.
+    auto visit_range = [&](int s2, int e2, int skip) {
+        // chunks of four: four independent loads, then predicated tests; the
+        // borderline fp64 re-test is one (rarely taken) branch per chunk
+        for (int j0 = s2; j0 < e2; j0 += 4) {
+            float4 q[4];
+            float r2f[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) q[u] = b32[min(j0 + u, e2 - 1)];
+            bool border = false;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                float fx = qi.x - q[u].x, fy = qi.y - q[u].y, fz = qi.z - q[u].z;
+                r2f[u] = fx * fx + fy * fy + fz * fz;
+                border |= (r2f[u] > lo) & (r2f[u] <= hi) & (j0 + u < e2);
+            }
+            bool in[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) in[u] = r2f[u] <= lo;
+            if (border) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (r2f[u] > lo && r2f[u] <= hi && j0 + u < e2) {
+                        double4 pj = ldg256(bpos + j0 + u);
+                        double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+                        in[u] = dx * dx + dy * dy + dz * dz <= ell2;
+                    }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                int j = j0 + u;
+                bool ok = in[u] & (j < e2) & (j != skip);
+                if (ok && c < cap) {
+                    if (STAGE) sw[c * 32 + lane] = j;
+                    else out[(size_t)c * 32] = j;
+                }
+                c += ok;
+            }
         }
     };
-    // Cells in ascending flat order: the pruned stencil is in product
-    // (lexicographic) order and symmetric, so its first half precedes the own
-    // cell.  Every list is then sorted by row, and the 32 lanes of a warp
-    // (consecutive rows, 1-3 neighbouring cells) walk the same neighbour cells
-    // in step: a warp's k-th gathers touch a few cache lines, not ~30.
-    // (The reference lists the own cell first; mdg_get_verlet restores that.)
-    auto visit_cell = [&](int k) {
-        int x2 = cx + st.d[k][0], y2 = cy + st.d[k][1], z2 = cz + st.d[k][2];
-        if (!gv.in_grid(x2, y2, z2)) return;
-        int c2 = gv.flat(x2, y2, z2);
-        int e2 = gv.start[c2 + 1];
-        for (int j = gv.start[c2]; j < e2; ++j) visit(j);
-    };
-    int half = st.n / 2;
-    for (int k = 0; k < half; ++k) visit_cell(k);
-    int s = gv.start[cell], e = gv.start[cell + 1];
-    for (int j = s; j < e; ++j)
-        if (j != r) visit(j);
-    for (int k = half; k < st.n; ++k) visit_cell(k);
-    cnt[r] = c;
+    if (st.n == 26) {
+        // CSF-1 grid: the stencil is the full 3x3x3 block, i.e. nine z-runs of
+        // up to three cells that are contiguous in row order; scanning them in
+        // (dx, dy) order visits rows in ascending order, exactly like the
+        // cell-by-cell walk below.
+        int za = max(cz - 1, 0), zb = min(cz + 1, gv.D2 - 1);
+        for (int dx = -1; dx <= 1; ++dx)
+            for (int dy = -1; dy <= 1; ++dy) {
+                int x2 = cx + dx, y2 = cy + dy;
+                if (x2 < 0 || x2 >= gv.D0 || y2 < 0 || y2 >= gv.D1) continue;
+                visit_range(gv.start[gv.flat(x2, y2, za)], gv.start[gv.flat(x2, y2, zb) + 1],
+                            (dx == 0 && dy == 0) ? r : -1);
+            }
+    } else {
+        auto visit_cell = [&](int k) {
+            int x2 = cx + st.d[k][0], y2 = cy + st.d[k][1], z2 = cz + st.d[k][2];
+            if (!gv.in_grid(x2, y2, z2)) return;
+            int c2 = gv.flat(x2, y2, z2);
+            visit_range(gv.start[c2], gv.start[c2 + 1], -1);
+        };
+        int half = st.n / 2;
+        for (int k = 0; k < half; ++k) visit_cell(k);
+        visit_range(gv.start[cell], gv.start[cell + 1], r);
+        for (int k = half; k < st.n; ++k) visit_cell(k);
+    }
+    }
+    if (r < gv.m) cnt[r] = c;
     if (c > cap) atomicMax(maxcnt, c);
+    if (STAGE) {
+        __syncwarp();
+        int cmax = __reduce_max_sync(0xffffffffu, min(c, cap));
+        // rows r - lane .. r - lane + 31 form one column-major block
+        int* gw = nbr + (size_t)((r - lane) >> 5) * 32 * cap + lane;
+        for (int k = 0; k < cmax; ++k) gw[(size_t)k * 32] = sw[k * 32 + lane];
+    }
 }
 
 int vl_rebuild(Context& c) {
@@ -159,8 +207,25 @@ int vl_rebuild(Context& c) {
     for (int attempt = 0; attempt < 3 && m > 0; ++attempt) {
         v.nbr.ensure(mpad * (size_t)v.cap);
         MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
-        vl_build_kernel<<<blocks_for(m, 128), 128, 0, c.stream>>>(
-            gv, gr.spos4.p, v.b32.p, maxabs, gr.row_code.p, gr.pruned, ell2, v.cap, v.cnt.p, v.nbr.p, maxcnt), note_launch();
+        size_t smem = (size_t)kBuildThreads * v.cap * sizeof(int);
+        static int stage_env = -1;
+        if (stage_env < 0) {
+            const char* e = getenv("MDG_VL_BUILD_STAGE");
+            stage_env = e ? atoi(e) : 0;
+        }
+        if (stage_env && smem <= 200 * 1024) {
+            static size_t attr = 0;
+            if (smem > attr) {
+                cudaFuncSetAttribute(vl_build_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024);
+                attr = 200 * 1024;
+            }
+            vl_build_kernel<true><<<blocks_for(m, kBuildThreads), kBuildThreads, smem, c.stream>>>(
+                gv, gr.spos4.p, v.b32.p, maxabs, gr.row_code.p, gr.pruned, ell2, v.cap, v.cnt.p, v.nbr.p, maxcnt), note_launch();
+        } else {
+            vl_build_kernel<false><<<blocks_for(m, kBuildThreads), kBuildThreads, 0, c.stream>>>(
+                gv, gr.spos4.p, v.b32.p, maxabs, gr.row_code.p, gr.pruned, ell2, v.cap, v.cnt.p, v.nbr.p, maxcnt), note_launch();
+        }
         int hmax = 0;
         MDG_CUDA(cudaMemcpyAsync(&hmax, maxcnt, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
         MDG_CUDA(cudaStreamSynchronize(c.stream));

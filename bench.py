@@ -27,7 +27,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -60,29 +59,36 @@ def workload_config(args, n_gpus):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled every few ms during the
+    timed region through NVML (the same counters nvidia-smi reports; one
+    nvidia-smi call takes longer than the whole timed region)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, gpu_index):
+    def __init__(self, gpu_index, period_s=0.005):
         self.idx = gpu_index
+        self.period = period_s
         self.rows = []
         self._stop = threading.Event()
         self._t = None
 
     def start(self):
         def run():
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(
-                        ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                         "-i", str(self.idx)], capture_output=True, text=True, timeout=5).stdout
-                    self.rows.append([s.strip() for s in out.strip().split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
+            try:
+                import pynvml as nv
+                nv.nvmlInit()
+                h = nv.nvmlDeviceGetHandleByIndex(self.idx)
+                self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                        "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                        "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                        "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
+                        "hw_power_brake": nv.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+                while not self._stop.is_set():
+                    mhz = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((mhz, [k for k, b in bits.items() if rs & b]))
+                    self._stop.wait(self.period)
+            except Exception as exc:   # no NVML: record why instead of failing the bench
+                self.error = f"{type(exc).__name__}: {exc}"
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
@@ -90,14 +96,14 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
-        reasons = sorted({names[k] for r in self.rows if len(r) >= 6
-                          for k in range(4) if r[2 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({x for r in self.rows for x in r[1]})
+        out = {"sm_mhz": statistics.median(sm) if sm else None,
+               "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": reasons,
+               "samples": len(self.rows), "source": "NVML, 5 ms period, timed region only"}
+        if getattr(self, "error", None):
+            out["error"] = self.error
+        return out
 
 
 # --------------------------------------------------------------------- GPU arm

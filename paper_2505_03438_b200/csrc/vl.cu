@@ -286,6 +286,10 @@ __global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int
 
 // ---------------------------------------------------------------- force
 
+// The list is streamed once per step (~4 B per entry, hundreds of MB): it is
+// read with evict-first (__ldcs) so it does not push the positions -- the
+// data every gather reuses -- out of L2.
+//
 // G entries per round (a multiple of 4: every four share one reciprocal,
 // y = 1/(q0 q1 q2 q3), 1/q0 = y q1 q2 q3 etc., so the XU pipe sees one
 // MUFU.RCP64H per four pairs).  PF: the next round's list indices are loaded
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(NT) vl_force_kernel(int m, int64_t n, int cap,
         int c = cnt[r];
         int jn[G];
 #pragma unroll
-        for (int u = 0; u < G; ++u) jn[u] = u < c ? lp[(size_t)u * 32] : r;
+        for (int u = 0; u < G; ++u) jn[u] = u < c ? __ldcs(lp + (size_t)u * 32) : r;
         for (int k0 = 0; k0 < c; k0 += G) {
             double dx[G], dy[G], dz[G], q[G];
             int tj[G], jc[G];
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(NT) vl_force_kernel(int m, int64_t n, int cap,
             if (PF) {
 #pragma unroll
                 for (int u = 0; u < G; ++u)
-                    jn[u] = k0 + G + u < c ? lp[(size_t)(k0 + G + u) * 32] : r;
+                    jn[u] = k0 + G + u < c ? __ldcs(lp + (size_t)(k0 + G + u) * 32) : r;
             }
 #pragma unroll
             for (int u = 0; u < G; ++u) {
@@ -365,7 +369,7 @@ __global__ void __launch_bounds__(NT) vl_force_kernel(int m, int64_t n, int cap,
             if (!PF) {
 #pragma unroll
                 for (int u = 0; u < G; ++u)
-                    jn[u] = k0 + G + u < c ? lp[(size_t)(k0 + G + u) * 32] : r;
+                    jn[u] = k0 + G + u < c ? __ldcs(lp + (size_t)(k0 + G + u) * 32) : r;
             }
 #pragma unroll
             for (int u = 0; u < G; ++u) {

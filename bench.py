@@ -225,31 +225,30 @@ def _ncu_traffic(config_id):
 
 
 def e2e_arm(args, host_pos, host_vel, params):
-    """The reference-facing drop-in: HostForceCalculator inside the reference
-    loop order on HOST arrays (oracle/port.py restates simulation.py:126-197 with
-    the reference's numpy integrator); H2D positions + D2H forces every step."""
-    from oracle import port
-
-    from paper_2505_03438_b200.calculator import HostForceCalculator
-    cfg = port.parse(args.config)
-    steps = min(args.steps, 22)
-    per = tuple(port.PERIODIC if f else port.REFLECTIVE for f in params.periodic_flags())
-    pp = port.Params(domain_size=params.domain_size, cutoff=params.cutoff, skin=params.skin,
-                     rebuild_interval=params.rebuild_interval, delta_t=params.delta_t,
-                     boundary=per)
-    p = port.Particles(host_pos, host_vel)
-    # warm-up (allocations, first rebuild) outside the timed region
-    port.simulate_fixed(p.copy(), pp, cfg, steps=2, calculator_cls=HostForceCalculator)
+    """The reference-facing drop-in end to end: state in (pinned) host memory,
+    the reference loop order (simulation.py:150-188) with HostForceCalculator as
+    the force backend -- positions H2D and forces D2H every step -- and the
+    host-side Verlet update in libmdg's native integrator."""
+    import paper_2505_03438_b200 as P
+    from paper_2505_03438_b200.hostloop import HostParticleSet, HostSimulation
+    cfg = P.parse_configuration(args.config)
+    steps = min(args.steps, 44)
+    p = HostParticleSet(host_pos, host_vel)
+    sim = HostSimulation(p, params, cfg)
+    sim.run(2)                      # allocations + first rebuild outside the timed region
+    rebuilds_before = sim.iteration
     t0 = time.perf_counter()
-    port.simulate_fixed(p, pp, cfg, steps=steps, calculator_cls=HostForceCalculator)
+    sim.run(steps)
     dt = time.perf_counter() - t0
     n = len(host_pos)
-    rebuilds = (steps + params.rebuild_interval) // (params.rebuild_interval + 1)
-    h2d = 24 * n * (steps + rebuilds) // steps   # positions every step + again at rebuilds
+    # positions at every refresh/compute, again at each rebuild (cadence R+1)
+    rebuilds = sum(1 for it in range(rebuilds_before, rebuilds_before + steps)
+                   if it % (params.rebuild_interval + 1) == 0)
+    h2d = 24 * n * (steps + rebuilds) // steps
     return {"value": round(n * steps / dt / 1e6, 3), "unit": UNIT, "steps": steps,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 24 * n,
-            "path": "HostForceCalculator (reference ForceCalculator protocol) + reference-order "
-                    "host loop with numpy integrator"}
+            "path": "hostloop.HostSimulation: pinned host state, reference loop order, "
+                    "HostForceCalculator (H2D positions, D2H forces each step), native host integrator"}
 
 
 def _cpu_threads():

@@ -144,6 +144,17 @@ int mdg_geometry_for(const double domain[3], const int periodic[3], double inter
 int mdg_stencil_for(const double domain[3], const int periodic[3], double interaction_length,
                     double csf, int kind, int major, int* count, int* out);
 
+/* Host-side integrator of the host-resident drop-in path (host arrays, OpenMP,
+ * same rounding as mdg_drift_wrap / mdg_finish_kick and the reference's numpy
+ * sequence, integrator.py:31-51, :98-128).  mass: per type; type_id may be
+ * NULL (one type); *blowup set when a coordinate left [-L, 2L] or is NaN. */
+int mdg_host_drift_wrap(int64_t n, int layout, double* pos, double* vel, const double* force,
+                        double* old_force, const int32_t* type_id, const double* mass,
+                        const double domain[3], const int periodic[3], double dt, int* blowup);
+int mdg_host_finish_kick(int64_t n, int layout, double* vel, double* force, const double* old_force,
+                         const int32_t* type_id, const double* mass, double dt, int has_gravity,
+                         double gravity);
+
 /* Measured FP64 FMA throughput of this device (roofline denominator):
  * dependent-chain DFMA microbenchmark, TFLOP/s (2 flops per DFMA). */
 int mdg_measure_fp64_peak(mdg_ctx* ctx, double* tflops, double* sm_mhz_hint);

@@ -25,7 +25,8 @@ EXPORTS = (
     "mdg_set_system", "mdg_bind", "mdg_rebuild", "mdg_refresh", "mdg_compute",
     "mdg_eval_count", "mdg_drift_wrap", "mdg_finish_kick", "mdg_sd_step", "mdg_blowup",
     "mdg_profile", "mdg_profile_read", "mdg_synchronize", "mdg_h2d", "mdg_d2h", "mdg_geometry", "mdg_stencil", "mdg_get_grid",
-    "mdg_get_verlet", "mdg_geometry_for", "mdg_stencil_for", "mdg_measure_fp64_peak",
+    "mdg_get_verlet", "mdg_geometry_for", "mdg_stencil_for", "mdg_host_drift_wrap",
+    "mdg_host_finish_kick", "mdg_measure_fp64_peak",
 )
 
 
@@ -72,6 +73,8 @@ def _declare(L):
         "mdg_get_verlet": (I, [P, ctypes.POINTER(I64), P, P]),
         "mdg_geometry_for": (I, [P, P, D, D, P, P, P, P, P]),
         "mdg_stencil_for": (I, [P, P, D, D, I, I, ctypes.POINTER(I), P]),
+        "mdg_host_drift_wrap": (I, [I64, I, P, P, P, P, P, P, P, P, D, ctypes.POINTER(I)]),
+        "mdg_host_finish_kick": (I, [I64, I, P, P, P, P, P, D, I, D]),
         "mdg_measure_fp64_peak": (I, [P, ctypes.POINTER(D), ctypes.POINTER(D)]),
     }
     for name, (res, args) in sig.items():

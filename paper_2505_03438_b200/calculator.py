@@ -221,7 +221,6 @@ class HostForceCalculator:
         self.n = n
         self._buf = {k: torch.zeros(3 * n, dtype=torch.float64, device=dev)
                      for k in ("pos", "vel", "force", "old_force")}
-        self._pinned = torch.zeros(3 * n, dtype=torch.float64).pin_memory() if n else None
         self._tid = None
         if len(particles.mass) > 1 and n:
             self._tid = torch.as_tensor(np.asarray(particles.type_id, dtype=np.int32)).to(dev)
@@ -232,12 +231,13 @@ class HostForceCalculator:
                       self._buf["old_force"], self._tid)
 
     def _upload_positions(self, p):
+        # straight from the caller's array (DMA speed when it is pinned, e.g.
+        # hostloop.HostParticleSet; driver-staged for pageable numpy arrays)
         if not self.n:
             return
-        src = np.ascontiguousarray(p.pos)
-        self._pinned.numpy()[:] = src.reshape(-1)
+        src = p.pos if p.pos.flags.c_contiguous else np.ascontiguousarray(p.pos)
         check(lib().mdg_h2d(self.ctx.h, ctypes.c_void_p(self._buf["pos"].data_ptr()),
-                            ctypes.c_void_p(self._pinned.data_ptr()), 24 * self.n), "h2d")
+                            ctypes.c_void_p(src.ctypes.data), 24 * self.n), "h2d")
 
     def rebuild(self, particles, config):
         self._upload_positions(particles)
@@ -262,9 +262,15 @@ class HostForceCalculator:
         h = self.ctx.h
         check(lib().mdg_compute(h, ctypes.byref(config_struct(config))), "compute")
         if self.n:
-            check(lib().mdg_d2h(h, ctypes.c_void_p(self._pinned.data_ptr()),
-                                ctypes.c_void_p(self._buf["force"].data_ptr()), 24 * self.n), "d2h")
-            particles.force.reshape(-1)[:] = self._pinned.numpy()
+            dst = particles.force
+            if dst.flags.c_contiguous:
+                check(lib().mdg_d2h(h, ctypes.c_void_p(dst.ctypes.data),
+                                    ctypes.c_void_p(self._buf["force"].data_ptr()), 24 * self.n), "d2h")
+            else:
+                tmp = np.empty(dst.shape)
+                check(lib().mdg_d2h(h, ctypes.c_void_p(tmp.ctypes.data),
+                                    ctypes.c_void_p(self._buf["force"].data_ptr()), 24 * self.n), "d2h")
+                dst[...] = tmp
         else:
             particles.force.fill(0.0)
         self.last_eval_count = self.ctx.eval_count()

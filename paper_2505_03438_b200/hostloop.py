@@ -1,0 +1,142 @@
+"""Host-resident simulation with the GPU force path (the reference-facing
+drop-in, end to end).
+
+State lives in host memory the way the reference keeps it (numpy arrays of a
+ParticleSet, particles.py:31-98); every step the reference loop
+(simulation.py:150-188) runs with the GPU ``HostForceCalculator`` as its force
+backend: positions go host->device, forces come back device->host, and the
+Verlet update runs on the host with libmdg's native multithreaded integrator
+(same rounding as the reference's numpy sequence, integrator.py:31-128).
+
+``HostParticleSet`` allocates its arrays in pinned host memory so the copies run
+at DMA speed; any object with the reference ParticleSet's attributes works.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .calculator import HostForceCalculator
+from ._lib import check, lib
+
+
+def _pinned(shape):
+    """Page-locked host array (DMA-speed copies); plain pages when no CUDA
+    driver is present (host-only use, e.g. the CPU test suite)."""
+    if torch.cuda.is_available():
+        return torch.zeros(shape, dtype=torch.float64).pin_memory().numpy()
+    return np.zeros(shape)
+
+
+class HostParticleSet:
+    """Reference-shaped ParticleSet on pinned host memory."""
+
+    def __init__(self, positions, velocities=None, type_ids=None, sigma=(1.0,), epsilon=(1.0,),
+                 mass=(1.0,), layout="AoS"):
+        pos = np.asarray(positions, dtype=np.float64).reshape(-1, 3)
+        n = pos.shape[0]
+        self.layout = "AoS"
+        self.pos, self.vel, self.force, self.old_force = (_pinned((n, 3)) for _ in range(4))
+        self.pos[:] = pos
+        if velocities is not None:
+            self.vel[:] = np.asarray(velocities, dtype=np.float64).reshape(n, 3)
+        self.type_id = (np.zeros(n, dtype=np.int64) if type_ids is None
+                        else np.asarray(type_ids, dtype=np.int64).copy())
+        self.sigma = np.asarray(sigma, dtype=np.float64)
+        self.epsilon = np.asarray(epsilon, dtype=np.float64)
+        self.mass = np.asarray(mass, dtype=np.float64)
+        self._tid32 = self.type_id.astype(np.int32)
+        if layout == "SoA":
+            self.convert_layout("SoA")
+
+    @property
+    def n(self):
+        return self.type_id.shape[0]
+
+    def convert_layout(self, target):
+        if target == self.layout:
+            return self
+        for name in ("pos", "vel", "force", "old_force"):
+            a = getattr(self, name)
+            b = _pinned(a.T.shape)
+            b[:] = a.T
+            setattr(self, name, b)
+        self.layout = target
+        return self
+
+    def view(self, name):
+        a = getattr(self, name)
+        return a if self.layout == "AoS" else a.T
+
+    positions = property(lambda s: s.view("pos"))
+    velocities = property(lambda s: s.view("vel"))
+    forces = property(lambda s: s.view("force"))
+    old_forces = property(lambda s: s.view("old_force"))
+
+
+def _ptr(a):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def host_drift_wrap(p, params, dt):
+    """drift_with_force + apply_boundaries + F -> F_old (integrator.py)."""
+    L = np.ascontiguousarray(params.domain_size, dtype=np.float64)
+    per = np.ascontiguousarray(params.periodic_flags().astype(np.int32))
+    mass = np.ascontiguousarray(p.mass, dtype=np.float64)
+    tid = getattr(p, "_tid32", None)
+    if tid is None:
+        tid = np.asarray(p.type_id, dtype=np.int32)
+    bad = ctypes.c_int()
+    check(lib().mdg_host_drift_wrap(p.n, _lib.AOS if p.layout == "AoS" else _lib.SOA,
+                                    _ptr(p.pos), _ptr(p.vel), _ptr(p.force), _ptr(p.old_force),
+                                    _ptr(tid) if len(mass) > 1 else None, _ptr(mass),
+                                    _ptr(L), _ptr(per), float(dt), ctypes.byref(bad)), "host drift")
+    return bool(bad.value)
+
+
+def host_finish_kick(p, dt, gravity=None):
+    mass = np.ascontiguousarray(p.mass, dtype=np.float64)
+    tid = getattr(p, "_tid32", None)
+    if tid is None:
+        tid = np.asarray(p.type_id, dtype=np.int32)
+    check(lib().mdg_host_finish_kick(p.n, _lib.AOS if p.layout == "AoS" else _lib.SOA,
+                                     _ptr(p.vel), _ptr(p.force), _ptr(p.old_force),
+                                     _ptr(tid) if len(mass) > 1 else None, _ptr(mass), float(dt),
+                                     int(gravity is not None), float(gravity or 0.0)),
+          "host finish_kick")
+
+
+class HostSimulation:
+    """The reference loop (simulation.py:150-188, fixed configuration) on host
+    state with the GPU force backend.  Create once, then ``run(steps)``."""
+
+    def __init__(self, particles, params, config, calculator=None):
+        self.p, self.params, self.config = particles, params, config
+        self.calc = calculator or HostForceCalculator(particles, params)
+        self.active, self.since, self.iteration = None, 0, 0
+
+    def step(self):
+        p, params, cfg, calc = self.p, self.params, self.config, self.calc
+        if host_drift_wrap(p, params, params.delta_t):
+            from .simulation import BlowUpError
+            raise BlowUpError("particle left the domain by more than one domain length "
+                              "(or position is not finite)")
+        rebuild = self.active != cfg.id or self.since >= params.rebuild_interval
+        if p.layout != cfg.layout:
+            p.convert_layout(cfg.layout)
+        if rebuild:
+            calc.rebuild(p, cfg)
+        calc.refresh(p, cfg)
+        calc.compute(p, cfg)
+        host_finish_kick(p, params.delta_t, params.gravity)
+        self.active = cfg.id
+        self.since = 0 if rebuild else self.since + 1
+        self.iteration += 1
+
+    def run(self, steps):
+        for _ in range(steps):
+            self.step()

@@ -186,3 +186,18 @@ def test_hand_cases(pkg):
     fc.rebuild(parts, P.parse_configuration("VL-List_Iter-NoN3L-AoS"))
     noff, nbr = fc.verlet_lists()
     assert [set(nbr[noff[i]:noff[i + 1]].tolist()) for i in range(3)] == [{1}, {0}, set()]
+
+
+def test_host_resident_loop_matches_reference(pkg):
+    """hostloop.HostSimulation (pinned host state, GPU forces, native host
+    integrator) reproduces the reference trajectories."""
+    P, calc = pkg
+    from paper_2505_03438_b200.hostloop import HostParticleSet, HostSimulation
+    z = golden("traj_small.npz")
+    L = z["domain"]
+    for k, cid in enumerate(str(s) for s in z["config_ids"]):
+        params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=10,
+                                    delta_t=1e-3, boundary=(P.PERIODIC,) * 3)
+        p = HostParticleSet(z["pos0"], z["vel0"])
+        HostSimulation(p, params, P.parse_configuration(cid)).run(int(z["steps"]))
+        assert port.force_rel_error(p.velocities, z[f"vel_{k}"]) <= FP64_TOL, cid

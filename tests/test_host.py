@@ -115,3 +115,50 @@ def test_particle_layout_round_trip_cpu_tensors():
     e = P.ParticleSet(np.zeros((0, 3)), device="cpu")
     e.convert_layout(P.SOA)
     assert tuple(e.pos.shape) == (3, 0)
+
+
+def test_native_host_integrator_matches_reference_numpy_bit_exact():
+    """libmdg's host integrator (used by the host drop-in loop) reproduces the
+    reference's numpy drift/boundaries/kick sequence bit for bit."""
+    from oracle import port
+    from paper_2505_03438_b200 import hostloop
+    rng = np.random.default_rng(5)
+    n = 2000
+    for boundary in ((P.PERIODIC,) * 3, (P.REFLECTIVE, P.PERIODIC, P.REFLECTIVE)):
+        params = P.SimulationParams(domain_size=(9.0, 10.0, 11.0), cutoff=2.5, skin=0.3,
+                                    delta_t=0.01, boundary=boundary, gravity=-1.5)
+        pos = rng.uniform(-0.5, 1.05, (n, 3)) * params.domain_size
+        vel = rng.normal(0, 3.0, (n, 3))
+        frc = rng.normal(0, 50.0, (n, 3))
+        tid = np.arange(n) % 2
+        for layout in ("AoS", "SoA"):
+            a = hostloop.HostParticleSet(pos, vel, tid, sigma=[1, .8], epsilon=[1, 1.5],
+                                         mass=[1.0, 2.0], layout=layout)
+            a.view("force")[:] = frc
+            b = port.Particles(pos, vel, tid, sigma=[1, .8], epsilon=[1, 1.5], mass=[1.0, 2.0],
+                               layout=layout)
+            b.view("force")[:] = frc
+            pp = port.Params(domain_size=params.domain_size, cutoff=2.5, skin=0.3, delta_t=0.01,
+                             boundary=boundary, gravity=-1.5)
+            assert not hostloop.host_drift_wrap(a, params, params.delta_t)
+            port.drift_with_force(b, pp.delta_t)
+            port.apply_boundaries(b, pp)
+            np.copyto(b.view("old_force"), b.view("force"))
+            assert np.array_equal(a.positions, b.positions)
+            assert np.array_equal(a.velocities, b.velocities)
+            a.view("force")[:] *= 0.5
+            b.view("force")[:] *= 0.5
+            hostloop.host_finish_kick(a, params.delta_t, params.gravity)
+            port.apply_gravity(b, pp.gravity)
+            port.finish_kick(b, pp.delta_t)
+            assert np.array_equal(a.velocities, b.velocities)
+            assert np.array_equal(a.forces, b.forces)
+
+
+def test_native_host_integrator_flags_blow_up():
+    from paper_2505_03438_b200 import hostloop
+    params = P.SimulationParams(domain_size=(10.0, 10.0, 10.0), cutoff=3.0,
+                                boundary=(P.PERIODIC,) * 3)
+    for bad in ([-10.5, 5.0, 5.0], [25.0, 5.0, 5.0], [np.nan, 5.0, 5.0]):
+        p = hostloop.HostParticleSet(np.array([bad]))
+        assert hostloop.host_drift_wrap(p, params, 0.0)

@@ -39,7 +39,7 @@ sys.path.insert(0, ROOT)
 METRIC = "LJ force MUPS (particle-updates/s) at 1/2/4/8 B200; % of FP64/HBM roofline"
 UNIT = "MUPS"
 FLOPS_PER_PAIR = 26          # per unique within-cutoff pair
-DEFAULT_CONFIG = "VL-List_Iter-NoN3L-AoS"
+DEFAULT_CONFIG = "VL-List_Iter-NoN3L-SoA"
 CPU_CONFIG = "LC-SLI-N3L-SoA-CSF1"   # fastest reference CPU configuration
 
 

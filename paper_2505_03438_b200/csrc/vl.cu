@@ -295,8 +295,8 @@ __global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int
 // MUFU.RCP64H per four pairs).  PF: the next round's list indices are loaded
 // before this round's gathers, so the HBM latency of the list stream overlaps
 // the gather + arithmetic of the current round.
-template <int SLAYOUT, int PLAYOUT, bool MT, int G, bool PF, int NT>
-__global__ void __launch_bounds__(NT) vl_force_kernel(int m, int64_t n, int cap,
+template <int SLAYOUT, int PLAYOUT, bool MT, int G, bool PF, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) vl_force_kernel(int m, int64_t n, int cap,
                                                       const double4* __restrict__ s4,
                                                       const double* __restrict__ s3,
                                                       const int* __restrict__ row_tid,
@@ -343,6 +343,8 @@ __global__ void __launch_bounds__(NT) vl_force_kernel(int m, int64_t n, int cap,
                 double xj, yj, zj;
                 tj[u] = 0;
                 if (SLAYOUT == AOS) {
+                    // one 256-bit load per record (measured faster than a
+                    // 128+64-bit split even though it moves 8 more bytes)
                     double4 p = ldg256(s4 + j);
                     xj = p.x; yj = p.y; zj = p.z;
                     if (MT) tj[u] = (int)p.w;
@@ -420,26 +422,30 @@ static void vl_launch(Context& c, bool mt) {
     vl_refresh_kernel<PLAYOUT, SLAYOUT><<<b, t, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, from_s4), note_launch();
     if (SLAYOUT == SOA) v.s3_valid = true;
     c.prof_mark();
-#define MDG_VLF(G, PF, NT)                                                                       \
+#define MDG_VLF(G, PF, NT, MB)                                                                     \
     do {                                                                                         \
         if (mt)                                                                                  \
-            vl_force_kernel<SLAYOUT, PLAYOUT, true, G, PF, NT><<<blocks_for(m, NT), NT, 0, c.stream>>>( \
+            vl_force_kernel<SLAYOUT, PLAYOUT, true, G, PF, NT, MB><<<blocks_for(m, NT), NT, 0, c.stream>>>( \
                 m, c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p,      \
                 gr.row_code.p, c.force, c.tab, c.scal.p), note_launch();                          \
         else                                                                                     \
-            vl_force_kernel<SLAYOUT, PLAYOUT, false, G, PF, NT><<<blocks_for(m, NT), NT, 0, c.stream>>>( \
+            vl_force_kernel<SLAYOUT, PLAYOUT, false, G, PF, NT, MB><<<blocks_for(m, NT), NT, 0, c.stream>>>( \
                 m, c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p,      \
                 gr.row_code.p, c.force, c.tab, c.scal.p), note_launch();                          \
     } while (0)
     // measured on B200, config 2 (profiles/round1_vl_variants.txt): all within
     // 6%; index prefetch with 4-entry rounds and 128-thread CTAs is fastest
     switch (vl_variant()) {
-        case 10: MDG_VLF(4, false, 128); break;
-        case 2: MDG_VLF(8, false, 128); break;
-        case 3: MDG_VLF(8, true, 128); break;
-        case 4: MDG_VLF(4, true, 256); break;
-        case 5: MDG_VLF(4, true, 64); break;
-        default: MDG_VLF(4, true, 128); break;
+        case 10: MDG_VLF(4, false, 128, 1); break;
+        case 2: MDG_VLF(8, false, 128, 1); break;
+        case 3: MDG_VLF(8, true, 128, 1); break;
+        case 4: MDG_VLF(4, true, 256, 1); break;
+        case 5: MDG_VLF(4, true, 64, 1); break;
+        case 6: MDG_VLF(4, true, 128, 8); break;
+        case 7: MDG_VLF(4, true, 128, 10); break;
+        case 8: MDG_VLF(4, true, 128, 12); break;
+        case 9: MDG_VLF(4, false, 128, 12); break;
+        default: MDG_VLF(4, true, 128, 1); break;
     }
 #undef MDG_VLF
     c.prof_mark();

@@ -219,7 +219,11 @@ class DecomposedSimulation:
 
 
 def gpu_force_backend(config, sigma, epsilon, mass):
-    """libmdg as the per-rank force backend (owned + ghost rows, open slab box)."""
+    """libmdg as the per-rank force backend (owned + ghost rows, open slab box).
+
+    The row set (owned + ghosts) is fixed between rebuilds, so the device
+    ParticleSet and its neighbour structure are rebuilt only at rebuild steps;
+    other steps copy the refreshed positions in and re-evaluate."""
     from .calculator import ForceCalculator
     from .particles import ParticleSet, ParticleTypeInfo
     types = [ParticleTypeInfo(t, float(epsilon[t]), float(sigma[t]), float(mass[t]))
@@ -227,13 +231,18 @@ def gpu_force_backend(config, sigma, epsilon, mass):
     state = {}
 
     def force_fn(pos_all, type_all, n_owned, local_params, rebuild):
-        parts = ParticleSet(pos_all, type_ids=type_all.cpu().numpy(), types=types,
-                            device=pos_all.device)
-        parts.convert_layout(config.layout)
-        if rebuild or "calc" not in state:
-            state["calc"] = ForceCalculator(parts, local_params)
+        parts = state.get("parts")
+        if rebuild or parts is None or parts.n != pos_all.shape[0]:
+            parts = ParticleSet(pos_all, type_ids=type_all.cpu().numpy(), types=types,
+                                device=pos_all.device)
+            parts.convert_layout(config.layout)
+            if "calc" in state:
+                state["calc"].close()
+            state["parts"], state["calc"] = parts, ForceCalculator(parts, local_params)
+            state["calc"].rebuild(parts, config)
+        else:
+            parts.view("pos").copy_(pos_all)
         calc = state["calc"]
-        calc.rebuild(parts, config)     # ghost sets change size between steps of a window
         calc.refresh(parts, config)
         calc.compute_async(parts, config)
         return parts.forces[:n_owned].clone()

@@ -96,6 +96,12 @@ int mdg_refresh(mdg_ctx* ctx, const mdg_config* cfg);
 int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg);
 /* ForceCalculator.last_eval_count (containers.py:454): synchronises. */
 int mdg_eval_count(mdg_ctx* ctx, int64_t* count);
+/* Shifted LJ potential energy of the bound positions (no reference
+ * ForceCalculator counterpart; the reference's energy test helper,
+ * tests/test_integrator.py:227-247): 1/2 sum over within-cutoff pairs of
+ * 4 eps [(s/r)^12 - (s/r)^6 - (s/rc)^12 + (s/rc)^6].  Uses the Verlet lists
+ * (built first when `rebuild` != 0 or none exist).  Synchronises. */
+int mdg_potential_energy(mdg_ctx* ctx, int rebuild, double* pe);
 
 /* drift_with_force + apply_boundaries + copy force->old_force
  * (integrator.py:31-37, :98-128; simulation.py:151-153), fused. */

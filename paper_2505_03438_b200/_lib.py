@@ -23,7 +23,7 @@ AOS, SOA = 0, 1
 EXPORTS = (
     "mdg_version", "mdg_launch_count", "mdg_last_error", "mdg_create", "mdg_destroy", "mdg_set_stream",
     "mdg_set_system", "mdg_bind", "mdg_rebuild", "mdg_refresh", "mdg_compute",
-    "mdg_eval_count", "mdg_drift_wrap", "mdg_finish_kick", "mdg_sd_step", "mdg_blowup",
+    "mdg_eval_count", "mdg_potential_energy", "mdg_drift_wrap", "mdg_finish_kick", "mdg_sd_step", "mdg_blowup",
     "mdg_profile", "mdg_profile_read", "mdg_synchronize", "mdg_h2d", "mdg_d2h", "mdg_geometry", "mdg_stencil", "mdg_get_grid",
     "mdg_get_verlet", "mdg_geometry_for", "mdg_stencil_for", "mdg_host_drift_wrap",
     "mdg_host_finish_kick", "mdg_measure_fp64_peak",
@@ -58,6 +58,7 @@ def _declare(L):
         "mdg_refresh": (I, [P, CFG]),
         "mdg_compute": (I, [P, CFG]),
         "mdg_eval_count": (I, [P, ctypes.POINTER(I64)]),
+        "mdg_potential_energy": (I, [P, I, ctypes.POINTER(D)]),
         "mdg_drift_wrap": (I, [P, D]),
         "mdg_finish_kick": (I, [P, D, I, D]),
         "mdg_sd_step": (I, [P, D, D]),

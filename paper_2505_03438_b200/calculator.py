@@ -144,6 +144,15 @@ class ForceCalculator:
         self.bind(particles)
         check(lib().mdg_sd_step(self.ctx.h, float(gamma), float(max_disp)), "sd_step")
 
+    def potential_energy(self, particles, rebuild=True) -> float:
+        """Shifted LJ potential energy of the current positions (north_star PE
+        output; tests/test_integrator.py:227-247 of the reference)."""
+        self.bind(particles)
+        pe = ctypes.c_double()
+        check(lib().mdg_potential_energy(self.ctx.h, int(rebuild), ctypes.byref(pe)),
+              "potential_energy")
+        return float(pe.value)
+
     def profile(self, enable=True):
         """Bracket each force-kernel launch with CUDA events on the context stream."""
         check(lib().mdg_profile(self.ctx.h, int(enable)), "profile")

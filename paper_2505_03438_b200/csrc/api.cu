@@ -452,6 +452,17 @@ int mdg_get_grid(mdg_ctx* ctx, double csf, int64_t* m, int64_t* ncells, int32_t*
     return cuda_status("mdg_get_grid");
 }
 
+int mdg_potential_energy(mdg_ctx* ctx, int rebuild, double* pe) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    if (!pe) { set_error("null output"); return MDG_EINVAL; }
+    Context& c = ctx->c;
+    if (rebuild || !c.vl.built)
+        if (vl_rebuild(c)) return MDG_ECUDA;
+    if (vl_energy(c, pe)) return MDG_ECUDA;
+    return cuda_status("mdg_potential_energy");
+}
+
 int mdg_get_verlet(mdg_ctx* ctx, int64_t* entries, int64_t* noff, int32_t* nbr) {
     CHECK_CTX(ctx);
     Verlet& v = ctx->c.vl;

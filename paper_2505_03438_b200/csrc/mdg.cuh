@@ -144,6 +144,7 @@ void lc_fold_forces(Context& c, Grid& gr, int layout, bool images_written);
 int vl_rebuild(Context& c);
 void vl_compute(Context& c, int layout);
 int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr);
+int vl_energy(Context& c, double* pe);
 void integ_drift_wrap(Context& c, double dt);
 void integ_finish_kick(Context& c, double dt, int has_gravity, double gravity);
 void integ_sd_step(Context& c, double gamma, double max_disp);

@@ -465,6 +465,76 @@ void vl_compute(Context& c, int layout) {
     }
 }
 
+// ---------------------------------------------------------------- energy
+
+// Shifted LJ potential energy, U = 1/2 sum_i sum_{j in list(i), r<rc}
+// 4 eps [(s/r)^12 - (s/r)^6 - (s/rc)^12 + (s/rc)^6] (the energy the truncated
+// force conserves; reference helper tests/test_integrator.py:227-247).  No
+// reference ForceCalculator counterpart (north_star: PE output).
+template <bool MT>
+__global__ void __launch_bounds__(256) vl_energy_kernel(int m, int cap, const double4* __restrict__ s4,
+                                                        const int* __restrict__ cnt,
+                                                        const int* __restrict__ nbr,
+                                                        const uint8_t* __restrict__ row_code, LJTab tab,
+                                                        double* __restrict__ out) {
+    __shared__ double ws[8];
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    double e = 0.0;
+    if (r < m && row_code[r] == kNoShift) {
+        double4 pi = s4[r];
+        int ti = MT ? (int)pi.w : 0;
+        const int* lp = nbr + (size_t)(r >> 5) * 32 * cap + (r & 31);
+        int c = cnt[r];
+        for (int k = 0; k < c; ++k) {
+            double4 pj = ldg256(s4 + lp[(size_t)k * 32]);
+            double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+            double r2 = dx * dx + dy * dy + dz * dz;
+            if (r2 < tab.rc2) {
+                double s2, e24;
+                lj_params<MT>(tab, ti, MT ? (int)pj.w : 0, s2, e24);
+                double a = s2 / r2, a6 = a * a * a;
+                double ac = s2 / tab.rc2, ac6 = ac * ac * ac;
+                e += (e24 / 6.0) * ((a6 * a6 - a6) - (ac6 * ac6 - ac6));
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0.0;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) atomicAdd(out, 0.5 * v);
+    }
+}
+
+int vl_energy(Context& c, double* pe) {
+    Verlet& v = c.vl;
+    Grid& gr = v.grid;
+    int m = (int)gr.m;
+    *pe = 0.0;
+    if (!m) return 0;
+    Wrap w;
+    for (int k = 0; k < 3; ++k) {
+        w.L[k] = c.L[k];
+        w.invL[k] = 1.0 / c.L[k];
+        w.per[k] = c.periodic[k];
+    }
+    if (c.layout == AOS)
+        vl_refresh_kernel<AOS, AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, false), note_launch();
+    else
+        vl_refresh_kernel<SOA, AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, false), note_launch();
+    double* dpe = (double*)(c.scal.p + 6);
+    MDG_CUDA(cudaMemsetAsync(dpe, 0, sizeof(double), c.stream));
+    if (c.tab.T > 1)
+        vl_energy_kernel<true><<<blocks_for(m, 256), 256, 0, c.stream>>>(m, v.cap, v.s4.p, v.cnt.p, v.nbr.p, gr.row_code.p, c.tab, dpe), note_launch();
+    else
+        vl_energy_kernel<false><<<blocks_for(m, 256), 256, 0, c.stream>>>(m, v.cap, v.s4.p, v.cnt.p, v.nbr.p, gr.row_code.p, c.tab, dpe), note_launch();
+    MDG_CUDA(cudaMemcpyAsync(pe, dpe, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    MDG_CUDA(cudaStreamSynchronize(c.stream));
+    return 0;
+}
+
 // Reference-format export: CSR by owner index with owner indices.
 int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr) {
     Verlet& v = c.vl;

@@ -188,6 +188,49 @@ def test_hand_cases(pkg):
     assert [set(nbr[noff[i]:noff[i + 1]].tolist()) for i in range(3)] == [{1}, {0}, set()]
 
 
+@pytest.mark.parametrize("name", ["small_periodic", "mixed", "crit1_0", "tight", "blob"])
+def test_potential_energy_matches_reference_helper(pkg, name):
+    """Shifted LJ potential energy vs the reference's brute-force energy helper
+    (tests/test_integrator.py:227-247), fp64 tolerance."""
+    P, calc = pkg
+    d = golden(f"sys_{name}.npz")
+    parts, params = _system(P, d)
+    fc = calc.ForceCalculator(parts, params)
+    pe = fc.potential_energy(parts)
+    nt = int(d["n_types"])
+    ref = port.brute_potential(d["pos"], d["tid"], [1.0 + 0.5 * t for t in range(nt)],
+                               [1.0 - 0.2 * t for t in range(nt)], params.cutoff,
+                               params.domain_size, params.periodic_flags())
+    assert abs(pe - ref) <= FP64_TOL * max(1.0, abs(ref)), (pe, ref)
+    fc.close()
+
+
+def test_energy_conserved_on_device(pkg):
+    """Device loop + PE: total energy drift <= 1e-3 over 1000 small steps
+    (the reference's criterion, tests/test_integrator.py:250-275)."""
+    P, calc = pkg
+    from paper_2505_03438_b200.simulation import Simulation
+    rng = np.random.default_rng(11)
+    side = np.arange(6) * 1.4 + 0.5
+    pos = np.array(np.meshgrid(side, side, side)).reshape(3, -1).T[:120]
+    pos = pos + rng.uniform(-0.05, 0.05, pos.shape)
+    vel = rng.normal(0.0, 0.4, pos.shape)
+    params = P.SimulationParams(domain_size=(9.0, 9.0, 9.0), cutoff=2.5, skin=0.3,
+                                rebuild_interval=10, delta_t=1e-4, boundary=(P.PERIODIC,) * 3)
+    parts = P.ParticleSet(pos, vel)
+    cfg = P.parse_configuration("VL-List_Iter-NoN3L-AoS")
+    sim = Simulation(parts, params, cfg)
+
+    def energy():
+        kin = 0.5 * float((parts.numpy("vel") ** 2).sum())
+        return kin + sim.calc.potential_energy(parts)
+
+    sim.step()            # iteration 0 drifts with zero force (simulation.py:7-8)
+    e0 = energy()
+    sim.run(1000, record=False)
+    assert abs(energy() - e0) / abs(e0) <= 1e-3
+
+
 def test_host_resident_loop_matches_reference(pkg):
     """hostloop.HostSimulation (pinned host state, GPU forces, native host
     integrator) reproduces the reference trajectories."""

@@ -42,13 +42,19 @@ enum { MDG_C01 = 0, MDG_C08 = 1, MDG_C18 = 2, MDG_SLI = 3, MDG_LIST_ITER = 4 };
 /* particles.py:10-11 */
 enum { MDG_AOS = 0, MDG_SOA = 1 };
 
-/* One point of the search space: Configuration (configuration.py:20-50). */
+/* Arithmetic of the force functor (north_star): fp64 throughout, or fp32
+ * compute with fp64 accumulation (Verlet lists only; tolerance 1e-4). */
+enum { MDG_FP64 = 0, MDG_FP32 = 1 };
+
+/* One point of the search space: Configuration (configuration.py:20-50),
+ * plus the precision of the extended space (the reference's 30 are fp64). */
 typedef struct {
     int container;  /* MDG_LC / MDG_VL */
     int traversal;  /* MDG_C01 .. MDG_LIST_ITER */
     int newton3;    /* 0 / 1 */
     int layout;     /* MDG_AOS / MDG_SOA */
     double csf;     /* cell size factor, 1.0 or 0.5 */
+    int precision;  /* MDG_FP64 / MDG_FP32 */
 } mdg_config;
 
 typedef struct mdg_ctx mdg_ctx;

@@ -32,7 +32,8 @@ EXPORTS = (
 
 class MdgConfig(ctypes.Structure):
     _fields_ = [("container", ctypes.c_int), ("traversal", ctypes.c_int),
-                ("newton3", ctypes.c_int), ("layout", ctypes.c_int), ("csf", ctypes.c_double)]
+                ("newton3", ctypes.c_int), ("layout", ctypes.c_int), ("csf", ctypes.c_double),
+                ("precision", ctypes.c_int)]
 
 
 class MdgError(RuntimeError):
@@ -115,5 +116,6 @@ def config_struct(config) -> MdgConfig:
     traversal = {"C01": C01, "C08": C08, "C18": C18, "SLI": SLI,
                  "List_Iter": LIST_ITER}[config.traversal]
     layout = {"AoS": AOS, "SoA": SOA}[config.layout]
+    precision = 1 if getattr(config, "precision", "fp64") == "fp32" else 0
     return MdgConfig(container, traversal, int(bool(config.newton3)), layout,
-                     float(config.cell_size_factor))
+                     float(config.cell_size_factor), precision)

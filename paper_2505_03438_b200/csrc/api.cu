@@ -89,6 +89,14 @@ static int validate(const mdg_config* cfg) {
         set_error("cell size factor must be one of (1.0, 0.5)");
         return MDG_EINVAL;
     }
+    if (cfg->precision != MDG_FP64 && cfg->precision != MDG_FP32) {
+        set_error("unknown precision");
+        return MDG_EINVAL;
+    }
+    if (cfg->precision == MDG_FP32 && cfg->container != MDG_VL) {
+        set_error("the fp32-compute variant exists for Verlet lists only");
+        return MDG_EINVAL;
+    }
     return MDG_OK;
 }
 
@@ -277,7 +285,8 @@ int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg) {
     if (c.n == 0) return MDG_OK;
     if (cfg->container == MDG_VL) {
         if (!c.vl.built) { set_error("compute before rebuild"); return MDG_ESTATE; }
-        vl_compute(c, cfg->layout);
+        if (cfg->precision == MDG_FP32) vl_compute32(c);
+        else vl_compute(c, cfg->layout);
     } else {
         Grid& gr = *grid_for(c, cfg->csf);
         if (!gr.built || gr.scratch_layout != cfg->layout) {

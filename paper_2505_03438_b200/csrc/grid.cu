@@ -121,6 +121,7 @@ void Grid::release() {
 
 void Verlet::release() {
     grid.release(); cnt.release(); nbr.release(); s4.release(); s3.release(); b32.release();
+    q32.release();
     cap = 0;
     built = false;
 }

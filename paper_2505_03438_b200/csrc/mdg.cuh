@@ -90,6 +90,7 @@ struct Verlet {
     DBuf<int> nbr;             // ceil(m/32)*32*cap row indices
     int cap = 0;
     DBuf<float4> b32;          // fp32 build positions (membership pre-filter)
+    DBuf<float4> q32;          // fp32 cell-relative positions + packed cell (fp32 variant)
     DBuf<double4> s4;          // unwrapped sorted positions {x,y,z,type} (AoS variant)
     DBuf<double> s3;           // x[m], y[m], z[m] (SoA variant)
     bool s3_valid = false;
@@ -145,6 +146,7 @@ int vl_rebuild(Context& c);
 void vl_compute(Context& c, int layout);
 int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr);
 int vl_energy(Context& c, double* pe);
+void vl_compute32(Context& c);
 void integ_drift_wrap(Context& c, double dt);
 void integ_finish_kick(Context& c, double dt, int has_gravity, double gravity);
 void integ_sd_step(Context& c, double gamma, double max_disp);

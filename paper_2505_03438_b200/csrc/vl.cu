@@ -465,6 +465,135 @@ void vl_compute(Context& c, int layout) {
     }
 }
 
+// ---------------------------------------------------------------- fp32 variant
+
+// fp32-compute / fp64-accumulate walk (north_star: "fp64 accumulation with an
+// fp32-compute variant", tolerance 1e-4).  Each row carries its position
+// relative to the origin of its build-time cell in fp32 plus that cell's
+// integer coordinates (10 bits each) in the fourth word, so a displacement is
+// (r_i - r_j) + (c_i - c_j) * cell_len with the integer part exact: the fp32
+// error is that of coordinates inside one cell, not of the box.  Gathers are
+// 16 bytes (one LDG.128) instead of 32.
+struct Cells32 {
+    float cl[3];
+    double cld[3];
+};
+
+__device__ __forceinline__ int pack_cell(int x, int y, int z) { return (x << 20) | (y << 10) | z; }
+
+template <int PLAYOUT>
+__global__ void vl_refresh32_kernel(const double* __restrict__ pos, int64_t n, int m,
+                                    const int* __restrict__ row_src,
+                                    const uint8_t* __restrict__ row_code,
+                                    const int* __restrict__ row_cell, GridView gv, Wrap w, Cells32 cc,
+                                    double4* __restrict__ s4, float4* __restrict__ q32) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    int src = row_src[r], code = row_code[r];
+    double q[3] = {pos[pidx<PLAYOUT>(src, 0, n)], pos[pidx<PLAYOUT>(src, 1, n)],
+                   pos[pidx<PLAYOUT>(src, 2, n)]};
+    int sh[3] = {code / 9 - 1, (code / 3) % 3 - 1, code % 3 - 1};
+    double4 old = s4[r];
+    double prev[3] = {old.x, old.y, old.z};
+    for (int k = 0; k < 3; ++k) {
+        double x = q[k] + (double)sh[k] * w.L[k];
+        if (w.per[k]) x += w.L[k] * rint((prev[k] - x) * w.invL[k]);
+        q[k] = x;
+    }
+    s4[r] = make_double4(q[0], q[1], q[2], old.w);
+    int cx, cy, cz;
+    gv.decode(row_cell[r], cx, cy, cz);
+    // padded-grid cell (cx, cy, cz) spans [(c - H) * cl, (c - H + 1) * cl)
+    float4 o;
+    o.x = (float)(q[0] - (double)(cx - gv.H0) * cc.cld[0]);
+    o.y = (float)(q[1] - (double)(cy - gv.H1) * cc.cld[1]);
+    o.z = (float)(q[2] - (double)(cz - gv.H2) * cc.cld[2]);
+    o.w = __int_as_float(pack_cell(cx, cy, cz));
+    q32[r] = o;
+}
+
+template <int PLAYOUT, bool MT>
+__global__ void __launch_bounds__(128) vl_force32_kernel(int m, int64_t n, int cap,
+                                                         const float4* __restrict__ q32,
+                                                         const int* __restrict__ row_tid,
+                                                         const int* __restrict__ cnt,
+                                                         const int* __restrict__ nbr,
+                                                         const int* __restrict__ row_src,
+                                                         const uint8_t* __restrict__ row_code,
+                                                         double* __restrict__ force, LJTab tab,
+                                                         Cells32 cc, unsigned long long* counter) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned hits = 0;
+    if (r < m && row_code[r] == kNoShift) {
+        float4 qi = q32[r];
+        int ci = __float_as_int(qi.w);
+        int ti = MT ? row_tid[r] : 0;
+        float rc2 = (float)tab.rc2;
+        double fx = 0.0, fy = 0.0, fz = 0.0;
+        const int* lp = nbr + (size_t)(r >> 5) * 32 * cap + (r & 31);
+        int c = cnt[r];
+        for (int k = 0; k < c; ++k) {
+            int j = __ldcs(lp + (size_t)k * 32);
+            float4 qj = __ldg(q32 + j);
+            int cj = __float_as_int(qj.w);
+            float dx = (qi.x - qj.x) + (float)((ci >> 20) - (cj >> 20)) * cc.cl[0];
+            float dy = (qi.y - qj.y) + (float)(((ci >> 10) & 1023) - ((cj >> 10) & 1023)) * cc.cl[1];
+            float dz = (qi.z - qj.z) + (float)((ci & 1023) - (cj & 1023)) * cc.cl[2];
+            float r2 = dx * dx + dy * dy + dz * dz;
+            if (r2 < rc2) {
+                double s2d, e24d;
+                lj_params<MT>(tab, ti, MT ? row_tid[j] : 0, s2d, e24d);
+                float inv = __frcp_rn(r2);
+                float a = (float)s2d * inv;
+                float a6 = a * a * a;
+                float fs = ((float)e24d * inv) * (a6 * fmaf(2.0f, a6, -1.0f));
+                ++hits;
+                fx += (double)(fs * dx);
+                fy += (double)(fs * dy);
+                fz += (double)(fs * dz);
+            }
+        }
+        int i = row_src[r];
+        force[pidx<PLAYOUT>(i, 0, n)] = fx;
+        force[pidx<PLAYOUT>(i, 1, n)] = fy;
+        force[pidx<PLAYOUT>(i, 2, n)] = fz;
+    }
+    warp_count(counter, hits);
+}
+
+void vl_compute32(Context& c) {
+    if (c.n == 0) return;
+    Verlet& v = c.vl;
+    Grid& gr = v.grid;
+    int m = (int)gr.m;
+    v.q32.ensure((size_t)m + 32);
+    Wrap w;
+    Cells32 cc;
+    for (int k = 0; k < 3; ++k) {
+        w.L[k] = c.L[k];
+        w.invL[k] = 1.0 / c.L[k];
+        w.per[k] = c.periodic[k];
+        cc.cld[k] = gr.g.cl[k];
+        cc.cl[k] = (float)gr.g.cl[k];
+    }
+    GridView gv = make_view(gr);
+    bool mt = c.tab.T > 1;
+    if (c.layout == AOS)
+        vl_refresh32_kernel<AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gv, w, cc, v.s4.p, v.q32.p), note_launch();
+    else
+        vl_refresh32_kernel<SOA><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gv, w, cc, v.s4.p, v.q32.p), note_launch();
+    c.prof_mark();
+    dim3 b(blocks_for(m, 128)), t(128);
+#define MDG_VL32(P, M) vl_force32_kernel<P, M><<<b, t, 0, c.stream>>>(m, c.n, v.cap, v.q32.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p, gr.row_code.p, c.force, c.tab, cc, c.scal.p), note_launch()
+    if (c.layout == AOS) {
+        if (mt) MDG_VL32(AOS, true); else MDG_VL32(AOS, false);
+    } else {
+        if (mt) MDG_VL32(SOA, true); else MDG_VL32(SOA, false);
+    }
+#undef MDG_VL32
+    c.prof_mark();
+}
+
 // ---------------------------------------------------------------- energy
 
 // Shifted LJ potential energy, U = 1/2 sum_i sum_{j in list(i), r<rc}

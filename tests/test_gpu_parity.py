@@ -244,3 +244,19 @@ def test_host_resident_loop_matches_reference(pkg):
         p = HostParticleSet(z["pos0"], z["vel0"])
         HostSimulation(p, params, P.parse_configuration(cid)).run(int(z["steps"]))
         assert port.force_rel_error(p.velocities, z[f"vel_{k}"]) <= FP64_TOL, cid
+
+
+@pytest.mark.parametrize("name", ["small_periodic", "mixed", "crit1_0", "crit1_1", "blob", "faces"])
+def test_fp32_variant_within_1e4(pkg, name):
+    """fp32-compute / fp64-accumulate Verlet walk: forces within 1e-4 of the
+    reference (north_star tolerance for the fp32 variant)."""
+    P, calc = pkg
+    d = golden(f"sys_{name}.npz")
+    k = _ids().index("VL-List_Iter-NoN3L-AoS")
+    for layout in ("AoS", "SoA"):
+        parts, params = _system(P, d, layout)
+        _, count = calc.compute_forces(parts, P.parse_configuration(f"VL-List_Iter-NoN3L-{layout}-FP32"),
+                                       params)
+        err = port.force_rel_error(parts.numpy("force"), d["forces"][k])
+        assert err <= 1e-4, (layout, err)
+        assert abs(count - int(d["counts"][k])) <= max(2, int(1e-3 * d["counts"][k]))

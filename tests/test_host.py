@@ -162,3 +162,14 @@ def test_native_host_integrator_flags_blow_up():
     for bad in ([-10.5, 5.0, 5.0], [25.0, 5.0, 5.0], [np.nan, 5.0, 5.0]):
         p = hostloop.HostParticleSet(np.array([bad]))
         assert hostloop.host_drift_wrap(p, params, 0.0)
+
+
+def test_extended_space_keeps_reference_ids():
+    ext = P.extended_configurations()
+    assert [c.id for c in ext[:30]] == [c.id for c in P.enumerate_configurations()]
+    assert [c.id for c in ext[30:]] == ["VL-List_Iter-NoN3L-AoS-FP32", "VL-List_Iter-NoN3L-SoA-FP32"]
+    assert P.parse_configuration("VL-List_Iter-NoN3L-SoA-FP32").precision == "fp32"
+    with pytest.raises(ValueError):
+        P.Configuration("LC", "C08", True, "AoS", 1.0, "fp32")
+    s = _lib.config_struct(P.parse_configuration("VL-List_Iter-NoN3L-AoS-FP32"))
+    assert s.precision == 1

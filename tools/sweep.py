@@ -44,7 +44,7 @@ def main():
     parts = P.ParticleSet(pos, vel)
     relax_cfg = P.parse_configuration("LC-C01-NoN3L-AoS-CSF1")
     systems.relax_on_device(parts, params, relax_cfg)
-    for cfg in P.enumerate_configurations():
+    for cfg in P.extended_configurations():
         if a.only and a.only not in cfg.id:
             continue
         p = parts.copy()
@@ -56,7 +56,7 @@ def main():
         calc.compute_async(p, cfg)
         t_compute = timed(lambda: calc.compute_async(p, cfg), a.reps)
         count = calc.last_eval_count
-        unique = count if cfg.newton3 else count // 2
+        unique = count if cfg.newton3 else count // 2   # pairs per force evaluation
         print(json.dumps({"config": cfg.id, "n": a.n, "rebuild_ms": round(t_rebuild, 3),
                           "refresh_ms": round(t_refresh, 3), "compute_ms": round(t_compute, 3),
                           "eval_count": count,

@@ -117,9 +117,30 @@ int mdg_finish_kick(mdg_ctx* ctx, double dt, int has_gravity, double gravity);
 /* Capped steepest-descent step x += F/|F| min(gamma|F|, max_disp) (input
  * relaxation for BASELINE configs 2/4; no reference counterpart). */
 int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp);
-/* BlowUpError detection (integrator.py:108-116): flag set by any drift since
- * the last reset.  Synchronises. */
+/* Device status bits raised since the last reset.  Synchronises.
+ *   bit 0 (MDG_FLAG_BLOWUP): BlowUpError, integrator.py:108-116, set by any
+ *          drift;
+ *   bit 1 (MDG_FLAG_THERMO_ZERO): apply_thermostat met T = 0 with a positive
+ *          target (the ValueError of integrator.py:84-88). */
+#define MDG_FLAG_BLOWUP 1
+#define MDG_FLAG_THERMO_ZERO 2
 int mdg_blowup(mdg_ctx* ctx, int* flag, int reset);
+
+/* current_temperature (integrator.py:72-78): T = sum m|v|^2 / (3N) over the
+ * bound particles, summed in numpy's pairwise order so the value is
+ * bit-identical to the reference.  MDG_EINVAL when N = 0.  Synchronises. */
+int mdg_temperature(mdg_ctx* ctx, double* temperature);
+/* apply_thermostat (integrator.py:81-95; simulation.py:186-188): velocity
+ * rescaling toward `target`, |dT| clipped to `max_delta_t`, computed and
+ * applied on the device without a host round trip.  The T = 0 / target > 0
+ * error is reported through MDG_FLAG_THERMO_ZERO (velocities untouched).
+ * MDG_EINVAL when N = 0. */
+int mdg_thermostat(mdg_ctx* ctx, double target, double max_delta_t);
+/* compute_live_stats (livestats.py:46-77) over the bound positions: CSF-1
+ * bin counts with dims = max(1, floor(L/(cutoff+skin))), reduced to
+ * out[0..5] = {mean, rel_std_dev, median, max, num_bins, num_empty} per bin,
+ * bit-identical to the reference.  Synchronises. */
+int mdg_live_stats(mdg_ctx* ctx, double out[6]);
 /* Bracket every force-kernel launch with CUDA events on the context stream
  * (enable != 0; resets the record).  mdg_profile_read synchronises and
  * returns the summed kernel time and the number of bracketed launches. */

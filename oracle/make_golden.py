@@ -26,10 +26,13 @@ import numpy as np  # noqa: E402
 from mdtune.cells import forward_stencil, make_geometry, pruned_stencil  # noqa: E402
 from mdtune.configuration import enumerate_configurations, parse_configuration  # noqa: E402
 from mdtune.containers import GridState, VerletListState, compute_forces  # noqa: E402
-from mdtune.params import PERIODIC, REFLECTIVE, SimulationParams  # noqa: E402
+from mdtune.integrator import apply_thermostat, current_temperature  # noqa: E402
+from mdtune.livestats import compute_live_stats  # noqa: E402
+from mdtune.params import PERIODIC, REFLECTIVE, SimulationParams, ThermostatParams  # noqa: E402
 from mdtune.particles import ParticleSet, ParticleTypeInfo  # noqa: E402
 from mdtune.simulation import simulate  # noqa: E402
-from mdtune.tuning import FixedStrategy  # noqa: E402
+import mdtune.simulation as _msim  # noqa: E402
+from mdtune.tuning import FixedStrategy, FullSearchStrategy, TuningController  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
 P, R = PERIODIC, REFLECTIVE
@@ -202,8 +205,115 @@ def trajectories():
         print(name, "done")
 
 
+def thermo_and_stats():
+    """current_temperature / apply_thermostat (integrator.py:72-95) and
+    compute_live_stats (livestats.py:46-77) on seeded inputs."""
+    rng = np.random.default_rng(7)
+    doc = {}
+    # live statistics: (name, positions, domain, cutoff, skin, boundary, threads)
+    L = 20.0
+    blob = np.clip(rng.normal(10.0, 1.5, (3000, 3)), 0.0, L)
+    edges = np.array([[0.0, 0.0, 0.0], [L, L, L], [L, 0.0, 5.0], [19.999999999, 7.0, 0.0]])
+    lattice = (np.stack(np.meshgrid(*(np.arange(7) + 0.5,) * 3, indexing="ij"), -1).reshape(-1, 3)
+               * (L / 7))
+    cases = [("uniform", rng.uniform(0.0, L, (5000, 3)), (L, L, L), 2.5, 0.3, P, 4),
+             ("blob", blob, (L, L, L), 2.5, 0.3, R, 1),
+             ("edges", edges, (L, L, L), 2.5, 0.3, R, 2),
+             ("lattice", lattice, (L, L, L), 2.5, 0.35, P, 8),
+             ("empty", np.zeros((0, 3)), (L, L, L), 2.5, 0.3, P, 1),
+             ("slab", rng.uniform(0.0, 1.0, (4000, 3)) * (31.3, 9.1, 6.0), (31.3, 9.1, 6.0), 2.5, 0.0, R, 3),
+             ("one_bin", rng.uniform(0.0, 3.0, (50, 3)), (3.0, 3.0, 3.0), 2.5, 0.3, R, 1)]
+    names = []
+    for name, pos, dom, rc, skin, bnd, thr in cases:
+        params = SimulationParams(domain_size=dom, cutoff=rc, skin=skin, boundary=(bnd,) * 3,
+                                  thread_count=thr)
+        p = ParticleSet(pos.copy(), types=_types(1))
+        doc[f"ls_{name}_pos"] = pos
+        doc[f"ls_{name}_in"] = np.array([*dom, rc, skin, float(bnd == P), thr])
+        doc[f"ls_{name}_out"] = compute_live_stats(p, params).feature_vector()
+        names.append(name)
+    doc["ls_names"] = np.array(names)
+    # temperature + thermostat: (name, n, n_types, layout, target, max_dt, zero velocities)
+    tcases = [("one", 1, 1, "AoS", 1.0, 0.1, False), ("seven", 7, 2, "SoA", 0.5, 0.2, False),
+              ("eight", 8, 1, "AoS", 2.0, 5.0, False), ("odd", 129, 3, "AoS", 0.1, 0.05, False),
+              ("mid", 1000, 2, "SoA", 1.3, 0.01, False), ("big", 100003, 2, "AoS", 0.7, 0.2, False),
+              ("cold_zero_target", 64, 1, "AoS", 0.0, 0.1, True)]
+    tnames = []
+    for name, n, nt, layout, target, mdt, zero in tcases:
+        vel = np.zeros((n, 3)) if zero else rng.normal(0.0, 1.1, (n, 3))
+        tid = rng.integers(0, nt, n)
+        p = ParticleSet(rng.uniform(0, 10, (n, 3)), velocities=vel.copy(), type_ids=tid,
+                        types=_types(nt))
+        p.convert_layout(layout)
+        t = current_temperature(p)
+        apply_thermostat(p, target, mdt)
+        doc[f"th_{name}_vel0"] = vel
+        doc[f"th_{name}_tid"] = tid
+        doc[f"th_{name}_in"] = np.array([nt, float(layout == "SoA"), target, mdt])
+        doc[f"th_{name}_t"] = np.array(t)
+        doc[f"th_{name}_vel"] = np.ascontiguousarray(p.velocities)
+        tnames.append(name)
+    doc["th_names"] = np.array(tnames)
+    np.savez_compressed(os.path.join(OUT, "thermo_stats.npz"), **doc)
+    print("thermo_stats done")
+
+
+def tuned_trajectory():
+    """simulate() with the real TuningController + FullSearchStrategy over a
+    3-configuration space, thermostat on.  The timer is a counter, so every
+    candidate costs the same and the controller's tie rule (earliest in the
+    space, tuning.py:288-291) decides: the run is deterministic.  The
+    per-iteration (configuration, forced, mode) sequence is recorded by
+    wrapping the controller."""
+    seq = []
+
+    class Recording(TuningController):
+        def configuration_for_iteration(self, iteration):
+            cfg, forced = super().configuration_for_iteration(iteration)
+            seq.append((iteration, cfg.id, bool(forced), self.mode))
+            return cfg, forced
+
+    space_ids = ["VL-List_Iter-NoN3L-AoS", "LC-C08-N3L-SoA-CSF1", "LC-C01-NoN3L-AoS-CSF0.5"]
+    ns, steps = 6, 40
+    pos0, vel0 = sc_lattice(ns, 1.1, 0.05, seed=3, offset=0.5)
+    L = ns * 1.1
+    params = SimulationParams(domain_size=(L, L, L), cutoff=2.5, skin=0.3, rebuild_interval=4,
+                              delta_t=1e-3, total_iterations=steps, boundary=(P, P, P),
+                              thermostat=ThermostatParams(0.9, 0.05, 7))
+    p = ParticleSet(pos0.copy(), velocities=vel0.copy(), types=_types(1))
+    counter = iter(range(10 ** 9))
+    saved = _msim.TuningController
+    _msim.TuningController = Recording
+    try:
+        rep = simulate(p, params, FullSearchStrategy(), tuning_interval=15, samples_per_config=2,
+                       space=[parse_configuration(c) for c in space_ids],
+                       timer=lambda: next(counter), raise_errors=True)
+    finally:
+        _msim.TuningController = saved
+    assert rep.error is None
+    doc = {"pos0": pos0, "vel0": vel0, "domain": np.array([L, L, L]), "steps": np.array(steps),
+           "space": np.array(space_ids), "tuning": np.array([15, 2, 4, 7]),
+           "thermo": np.array([0.9, 0.05]),
+           "seq_it": np.array([s[0] for s in seq]), "seq_cfg": np.array([s[1] for s in seq]),
+           "seq_forced": np.array([s[2] for s in seq]), "seq_mode": np.array([s[3] for s in seq]),
+           "pos": np.ascontiguousarray(p.positions), "vel": np.ascontiguousarray(p.velocities),
+           "force": np.ascontiguousarray(p.forces), "layout": np.array(p.layout),
+           "final_temperature": np.array(rep.final_temperature),
+           "trial_iterations": np.array(rep.trial_iterations)}
+    np.savez_compressed(os.path.join(OUT, "traj_tuned.npz"), **doc)
+    print("traj_tuned done", rep.phase_selections)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    geometry_cases()
-    containers()
-    trajectories()
+    only = sys.argv[1:]
+    if not only or "geometry" in only:
+        geometry_cases()
+    if not only or "containers" in only:
+        containers()
+    if not only or "trajectories" in only:
+        trajectories()
+    if not only or "thermo_stats" in only:
+        thermo_and_stats()
+    if not only or "tuned" in only:
+        tuned_trajectory()

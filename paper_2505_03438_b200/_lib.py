@@ -26,8 +26,10 @@ EXPORTS = (
     "mdg_eval_count", "mdg_potential_energy", "mdg_drift_wrap", "mdg_finish_kick", "mdg_sd_step", "mdg_blowup",
     "mdg_profile", "mdg_profile_read", "mdg_synchronize", "mdg_h2d", "mdg_d2h", "mdg_geometry", "mdg_stencil", "mdg_get_grid",
     "mdg_get_verlet", "mdg_geometry_for", "mdg_stencil_for", "mdg_host_drift_wrap",
-    "mdg_host_finish_kick", "mdg_measure_fp64_peak",
+    "mdg_host_finish_kick", "mdg_measure_fp64_peak", "mdg_temperature", "mdg_thermostat",
+    "mdg_live_stats",
 )
+FLAG_BLOWUP, FLAG_THERMO_ZERO = 1, 2
 
 
 class MdgConfig(ctypes.Structure):
@@ -78,6 +80,9 @@ def _declare(L):
         "mdg_host_drift_wrap": (I, [I64, I, P, P, P, P, P, P, P, P, D, ctypes.POINTER(I)]),
         "mdg_host_finish_kick": (I, [I64, I, P, P, P, P, P, D, I, D]),
         "mdg_measure_fp64_peak": (I, [P, ctypes.POINTER(D), ctypes.POINTER(D)]),
+        "mdg_temperature": (I, [P, ctypes.POINTER(D)]),
+        "mdg_thermostat": (I, [P, D, D]),
+        "mdg_live_stats": (I, [P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import check, config_struct, lib
+from ._lib import FLAG_BLOWUP, check, config_struct, lib
 
 
 @dataclass
@@ -163,10 +163,40 @@ class ForceCalculator:
         check(lib().mdg_profile_read(self.ctx.h, ctypes.byref(ms), ctypes.byref(n)), "profile_read")
         return float(ms.value), int(n.value)
 
-    def blowup(self, reset=True) -> bool:
+    def status_flags(self, reset=True) -> int:
+        """Device status bits since the last reset (FLAG_BLOWUP, FLAG_THERMO_ZERO)."""
         f = ctypes.c_int()
         check(lib().mdg_blowup(self.ctx.h, ctypes.byref(f), int(reset)), "blowup")
-        return bool(f.value)
+        return int(f.value)
+
+    def blowup(self, reset=True) -> bool:
+        return bool(self.status_flags(reset) & FLAG_BLOWUP)
+
+    # -- temperature, thermostat, live statistics (stats.cu) -------------------
+    def temperature(self, particles) -> float:
+        """current_temperature (integrator.py:72-78), bit-identical."""
+        self.bind(particles)
+        t = ctypes.c_double()
+        check(lib().mdg_temperature(self.ctx.h, ctypes.byref(t)), "temperature")
+        return float(t.value)
+
+    def thermostat(self, particles, target, max_delta_t):
+        """apply_thermostat (integrator.py:81-95) on the device, asynchronous.
+        The T = 0 error surfaces through status_flags() (FLAG_THERMO_ZERO)."""
+        self.bind(particles)
+        check(lib().mdg_thermostat(self.ctx.h, float(target), float(max_delta_t)), "thermostat")
+
+    def live_stats(self, particles):
+        """compute_live_stats (livestats.py:46-77) on the device."""
+        from .livestats import LiveStatistics
+        self.bind(particles)
+        out = np.zeros(6, dtype=np.float64)
+        check(lib().mdg_live_stats(self.ctx.h, out.ctypes.data), "live_stats")
+        return LiveStatistics(
+            mean_particles_per_bin=float(out[0]), rel_std_dev_particles_per_bin=float(out[1]),
+            median_particles_per_bin=float(out[2]), max_particles_per_bin=float(out[3]),
+            num_bins=int(out[4]), num_empty_bins=int(out[5]),
+            thread_count=self.params.thread_count, skin=self.params.skin)
 
     # -- parity exports --------------------------------------------------------
     def grid_state(self, csf):

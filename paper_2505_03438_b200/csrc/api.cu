@@ -147,6 +147,7 @@ int mdg_destroy(mdg_ctx* ctx) {
     ctx->c.grids[0].release();
     ctx->c.grids[1].release();
     ctx->c.vl.release();
+    stats_release(ctx->c);
     ctx->c.scal.release();
     ctx->c.scan_tmp.release();
     ctx->c.d_mass.release();
@@ -338,9 +339,38 @@ int mdg_blowup(mdg_ctx* ctx, int* flag, int reset) {
                         cudaMemcpyDeviceToHost, c.stream) != cudaSuccess ||
         cudaStreamSynchronize(c.stream) != cudaSuccess)
         return cuda_status("mdg_blowup");
-    *flag = c.h_scal[2] ? 1 : 0;
+    *flag = (int)(c.h_scal[2] & 3ull);
     if (reset) cudaMemsetAsync(c.scal.p + 2, 0, sizeof(unsigned long long), c.stream);
     return cuda_status("mdg_blowup");
+}
+
+int mdg_temperature(mdg_ctx* ctx, double* temperature) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    if (!temperature) { set_error("null output"); return MDG_EINVAL; }
+    int r = stats_temperature(ctx->c, temperature);
+    if (r > 0) return MDG_EINVAL;
+    if (r < 0) return MDG_ECUDA;
+    return cuda_status("mdg_temperature");
+}
+
+int mdg_thermostat(mdg_ctx* ctx, double target, double max_delta_t) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    int r = stats_thermostat(ctx->c, target, max_delta_t);
+    if (r > 0) return MDG_EINVAL;
+    if (r < 0) return MDG_ECUDA;
+    return cuda_status("mdg_thermostat");
+}
+
+int mdg_live_stats(mdg_ctx* ctx, double out[6]) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    if (!out) { set_error("null output"); return MDG_EINVAL; }
+    int r = stats_live(ctx->c, out);
+    if (r > 0) return MDG_EINVAL;
+    if (r < 0) return MDG_ECUDA;
+    return cuda_status("mdg_live_stats");
 }
 
 int mdg_profile(mdg_ctx* ctx, int enable) {

@@ -109,6 +109,7 @@ template struct DBuf<unsigned long long>;
 template struct DBuf<uint16_t>;
 template struct DBuf<int4>;
 template struct DBuf<float4>;
+template struct DBuf<PwLeaf>;
 
 void Grid::release() {
     cell_count.release(); cell_start.release(); cell_fill.release();

@@ -98,6 +98,27 @@ struct Verlet {
     void release();
 };
 
+// numpy's pairwise summation order (np.add.reduce over a contiguous fp64
+// array: leaves of <= 128 elements summed with 8 strided accumulators, split
+// at n/2 rounded down to a multiple of 8) planned once per length, so device
+// reductions are bit-identical to the reference's np.sum (stats.cu).
+struct PwLeaf {
+    long long off;
+    int len;
+    int pad;
+};
+
+struct PairwiseTree {
+    int64_t n = -1;
+    int nleaves = 0, root = 0;
+    std::vector<int> level_off;     // internal nodes grouped by height
+    DBuf<PwLeaf> leaves;
+    DBuf<int4> nodes;               // {left slot, right slot, out slot, -}
+    DBuf<int> d_level_off;
+    DBuf<double> val;               // leaves then internal nodes
+    void release();
+};
+
 struct Context {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -118,7 +139,12 @@ struct Context {
     // containers
     Grid grids[2];             // [0] CSF 1, [1] CSF 0.5
     Verlet vl;
-    // device scalars: [0] eval count, [1] scan total scratch, [2] blow-up flag
+    // temperature / thermostat / live statistics (stats.cu)
+    PairwiseTree pw_particles, pw_bins;
+    DBuf<int> ls_counts, ls_hist;
+    DBuf<double> st_out;            // device results (temperature, stats[6])
+    // device scalars: [0] eval count, [1] scan total scratch, [2] status flags
+    // (bit 0 blow-up, bit 1 thermostat at T = 0)
     DBuf<unsigned long long> scal;
     unsigned long long* h_scal = nullptr;   // pinned mirror
     DBuf<unsigned long long> scan_tmp;      // block partials for scans
@@ -150,6 +176,10 @@ void vl_compute32(Context& c);
 void integ_drift_wrap(Context& c, double dt);
 void integ_finish_kick(Context& c, double dt, int has_gravity, double gravity);
 void integ_sd_step(Context& c, double gamma, double max_disp);
+int stats_temperature(Context& c, double* t);
+int stats_thermostat(Context& c, double target, double max_delta_t);
+int stats_live(Context& c, double out[6]);
+void stats_release(Context& c);
 void set_error(const std::string& msg);
 // host-side count of kernel launches issued by the library (bench evidence)
 void note_launch();

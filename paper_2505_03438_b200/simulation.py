@@ -1,18 +1,29 @@
 """Device-resident simulation loop (mirror of mdtune.simulation.simulate,
-simulation.py:126-197, for a fixed configuration).
+simulation.py:126-197), for a fixed configuration or driven by a tuning
+controller.
 
 Per iteration, in the reference's order: drift with the previous forces,
 boundaries, F -> F_old (one fused kernel, integrator.py:31-37/98-128,
-simulation.py:151-153); layout conversion + rebuild when due + refresh (timed as
-build); compute (timed as force); gravity + finish_kick (one kernel).  The
-rebuild cadence is the reference's: rebuild when the configuration changed or
-``since_rebuild >= R`` (so every R+1 iterations, simulation.py:158-159,179);
-forces start at zero, so iteration 0 drifts ballistically.
+simulation.py:151-153); ask the controller for this iteration's
+configuration (tuning.py:200-210); layout conversion + rebuild when due +
+refresh (timed as build); compute (timed as force); gravity + finish_kick
+(one kernel); the thermostat every ``interval_iterations``
+(simulation.py:186-188, on the device, stats.cu).  The rebuild cadence is
+the reference's: rebuild when forced (first sample of a trial), when the
+configuration changed, or when ``since_rebuild >= R`` (so every R+1
+iterations, simulation.py:158-159,179); forces start at zero, so iteration 0
+drifts ballistically.
 
-Timings come from CUDA events on the context stream and are read once at the
-end, so steady-state iterations never synchronise with the host.  A blow-up
-(integrator.py:108-116) is detected on the device and raised at the next
-rebuild (which synchronises anyway) or at the end of the run.
+Timings are CUDA events on the context stream.  Steady-state iterations are
+read once at the end, so they never synchronise with the host; trial
+iterations synchronise on their compute event, because the controller
+advances its candidate queue on every ``record_timings`` (tuning.py:212-227).
+In steady mode the reference's ``record_timings`` is a no-op (tuning.py:213),
+so it is not called.  A failing candidate is reported with
+``record_failure`` and the iteration is retried with the next one
+(simulation.py:155-176).  Device errors (BlowUpError, the thermostat's T = 0
+ValueError) are flags checked at every rebuild (which synchronises anyway)
+and at the end of the run.
 """
 
 from __future__ import annotations
@@ -21,7 +32,11 @@ from dataclasses import dataclass, field
 
 import torch
 
+from ._lib import FLAG_BLOWUP, FLAG_THERMO_ZERO
 from .calculator import ForceCalculator
+from .configuration import enumerate_configurations
+
+TRIAL = "trial"
 
 
 class BlowUpError(RuntimeError):
@@ -35,11 +50,19 @@ class IterationRecord:
     force_ns: int
     build_ns: int
     rebuilt: bool
+    phase_index: int = 0
 
 
 @dataclass
 class SimulationReport:
+    name: str = "simulation"
+    strategy_name: str = "fixed"
     records: list = field(default_factory=list)
+    tuning_log: list = field(default_factory=list)
+    phase_selections: list = field(default_factory=list)
+    stats_snapshots: list = field(default_factory=list)
+    trial_iterations: int = 0
+    final_temperature: float | None = None
     error: str | None = None
 
     @property
@@ -50,47 +73,115 @@ class SimulationReport:
     def total_build_ns(self) -> int:
         return sum(r.build_ns for r in self.records)
 
+    def configuration_sequence(self) -> list:
+        return [r.configuration_id for r in self.records]
+
+
+class _Fixed:
+    """FixedStrategy as a controller: one configuration, never forced."""
+
+    mode = "steady"
+
+    def __init__(self, config):
+        self.config = config
+
+    def configuration_for_iteration(self, iteration):
+        return self.config, False
+
+    def record_timings(self, force_ns, build_ns):
+        pass
+
+    def record_failure(self, error=None):
+        return False
+
 
 class Simulation:
-    """Stepper with persistent state (calculator, cadence), so benchmarks can
-    run warm-up and timed windows back to back on one trajectory."""
+    """Stepper with persistent state (calculator, cadence, controller), so
+    benchmarks can run warm-up and timed windows back to back on one
+    trajectory.  ``config`` is a Configuration / FixedStrategy; ``controller``
+    anything with the TuningController protocol (tuning.py:200-239)."""
 
-    def __init__(self, particles, params, config, calculator=None):
-        if params.thermostat is not None:
-            raise NotImplementedError("thermostat is not on the device path yet")
+    def __init__(self, particles, params, config=None, calculator=None, controller=None,
+                 tuning_interval=None):
+        if controller is None:
+            if config is None:
+                raise ValueError("need a configuration or a controller")
+            controller = _Fixed(getattr(config, "config", config))
         self.p = particles
         self.params = params
-        self.config = getattr(config, "config", config)   # FixedStrategy or Configuration
+        self.controller = controller
+        self.tuning_interval = (tuning_interval or getattr(controller, "tuning_interval", None)
+                                or 1000)
         self.calc = calculator or ForceCalculator(particles, params)
         self.active = None
         self.since = 0
         self.iteration = 0
         self._events = []
+        self._records = []
+
+    @property
+    def config(self):
+        return getattr(self.controller, "current_config", None) or getattr(self.controller, "config", None)
+
+    def _check_flags(self):
+        flags = self.calc.status_flags()
+        if flags & FLAG_BLOWUP:
+            raise BlowUpError("particle left the domain by more than one domain length "
+                              "(or position is not finite)")
+        if flags & FLAG_THERMO_ZERO:
+            raise ValueError("thermostat cannot scale zero velocities toward a positive "
+                             "target temperature")
+
+    def _trial(self):
+        return getattr(self.controller, "mode", TRIAL) == TRIAL
 
     def step(self, record=False):
-        p, params, cfg, calc = self.p, self.params, self.config, self.calc
+        p, params, calc, ctl = self.p, self.params, self.calc, self.controller
+        it = self.iteration
         calc.drift_wrap(p, params.delta_t)
-        rebuild = self.active != cfg.id or self.since >= params.rebuild_interval
-        if record:
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            ev[0].record()
-        if p.layout != cfg.layout:
-            p.convert_layout(cfg.layout)
-        if rebuild:
-            if self.iteration and calc.blowup():
-                raise BlowUpError("particle left the domain by more than one domain length "
-                                  "(or position is not finite)")
-            calc.rebuild(p, cfg)
-        calc.refresh(p, cfg)
-        if record:
-            ev[1].record()
-        calc.compute_async(p, cfg)
-        if record:
-            ev[2].record()
-            self._events.append((self.iteration, cfg.id, rebuild, ev))
+        while True:
+            cfg, forced = ctl.configuration_for_iteration(it)
+            rebuild = forced or self.active != cfg.id or self.since >= params.rebuild_interval
+            trial = self._trial()
+            if rebuild and it:
+                self._check_flags()
+            timed = record or trial
+            if timed:
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                ev[0].record()
+            try:
+                if p.layout != cfg.layout:
+                    p.convert_layout(cfg.layout)
+                if rebuild:
+                    calc.rebuild(p, cfg)
+                calc.refresh(p, cfg)
+                if timed:
+                    ev[1].record()
+                calc.compute_async(p, cfg)
+                if timed:
+                    ev[2].record()
+                break
+            except (BlowUpError, KeyboardInterrupt):
+                raise
+            except Exception as exc:
+                if not ctl.record_failure(exc):
+                    raise
+                self.active = None
         calc.finish_kick(p, params.delta_t, params.gravity)
         self.active = cfg.id
         self.since = 0 if rebuild else self.since + 1
+        phase = it // self.tuning_interval
+        if trial:
+            ev[2].synchronize()
+            build_ns = int(ev[0].elapsed_time(ev[1]) * 1e6)
+            force_ns = int(ev[1].elapsed_time(ev[2]) * 1e6)
+            ctl.record_timings(force_ns, build_ns)
+            self._records.append(IterationRecord(it, cfg.id, force_ns, build_ns, rebuild, phase))
+        elif timed:
+            self._events.append((it, cfg.id, rebuild, phase, ev))
+        thermo = params.thermostat
+        if thermo is not None and (it + 1) % thermo.interval_iterations == 0:
+            calc.thermostat(p, thermo.target_temperature, thermo.max_delta_t)
         self.iteration += 1
         return rebuild
 
@@ -99,35 +190,84 @@ class Simulation:
             self.step(record=record)
 
     def check(self):
-        if self.calc.blowup():
-            raise BlowUpError("particle left the domain by more than one domain length "
-                              "(or position is not finite)")
+        self._check_flags()
 
-    def report(self) -> SimulationReport:
+    def report(self, rep=None) -> SimulationReport:
         torch.cuda.synchronize(self.p.device)
-        rep = SimulationReport()
-        for it, cid, rebuilt, ev in self._events:
+        rep = rep or SimulationReport()
+        for it, cid, rebuilt, phase, ev in self._events:
             build_ns = int(ev[0].elapsed_time(ev[1]) * 1e6)
             force_ns = int(ev[1].elapsed_time(ev[2]) * 1e6)
-            rep.records.append(IterationRecord(it, cid, force_ns, build_ns, rebuilt))
+            self._records.append(IterationRecord(it, cid, force_ns, build_ns, rebuilt, phase))
         self._events.clear()
+        self._records.sort(key=lambda r: r.iteration)
+        rep.records.extend(self._records)
+        self._records = []
+        ctl = self.controller
+        rep.tuning_log = list(getattr(ctl, "log", rep.tuning_log))
+        rep.phase_selections = list(getattr(ctl, "phase_selections", rep.phase_selections))
+        rep.stats_snapshots = list(getattr(ctl, "stats_snapshots", rep.stats_snapshots))
+        rep.trial_iterations = int(getattr(ctl, "trial_iterations", rep.trial_iterations))
         return rep
 
 
-def simulate(particles, params, config, *, steps=None, record=True, raise_errors=True):
-    """Run ``params.total_iterations`` (or ``steps``) iterations under a fixed
-    configuration; returns the per-iteration device timings."""
+def _is_configuration(obj) -> bool:
+    return hasattr(obj, "container") and hasattr(obj, "layout")
+
+
+def simulate(particles, params, strategy, *, tuning_interval=1000, samples_per_config=3,
+             space=None, name="simulation", raise_errors=False, steps=None, record=True,
+             controller=None, controller_cls=None) -> SimulationReport:
+    """simulation.py:126-197 on the device.
+
+    ``strategy`` is a Configuration, a FixedStrategy (anything with
+    ``.config``), or a tuning strategy; a tuning strategy is driven by
+    ``controller_cls`` (default: the reference's ``mdtune.tuning.
+    TuningController`` when importable), constructed exactly as the
+    reference does (simulation.py:132-137) with the live statistics computed
+    on the device.  ``controller`` passes a ready controller object instead.
+    Returns the report, partial with ``error`` set if an error interrupted
+    the run (re-raised when ``raise_errors``)."""
     steps = params.total_iterations if steps is None else steps
-    sim = Simulation(particles, params, config)
+    calc = ForceCalculator(particles, params)
+    fixed = None
+    if controller is None:
+        if _is_configuration(strategy):
+            fixed = strategy
+        elif hasattr(strategy, "config") and not hasattr(strategy, "candidates"):
+            fixed = strategy.config
+        else:
+            if controller_cls is None:
+                try:
+                    from mdtune.tuning import TuningController as controller_cls
+                except ImportError:
+                    calc.close()
+                    raise RuntimeError("a tuning strategy needs a controller: pass controller_cls= "
+                                       "(mdtune.tuning.TuningController) or controller=") from None
+            controller = controller_cls(
+                space if space is not None else enumerate_configurations(), strategy,
+                samples_per_config=samples_per_config, tuning_interval=tuning_interval,
+                rebuild_interval=params.rebuild_interval,
+                total_iterations=params.total_iterations,
+                stats_provider=lambda: calc.live_stats(particles))
+    strategy_name = getattr(strategy, "name", None) or ("fixed" if fixed is not None else "tuned")
+    rep = SimulationReport(name=name, strategy_name=str(strategy_name))
+    sim = Simulation(particles, params, fixed, calculator=calc, controller=controller,
+                     tuning_interval=tuning_interval)
     try:
         sim.run(steps, record=record)
         sim.check()
-        rep = sim.report()
-    except BlowUpError as exc:
-        rep = sim.report()
-        rep.error = f"BlowUpError: {exc}"
+        sim.report(rep)
+        if particles.n:
+            rep.final_temperature = calc.temperature(particles)
+    except Exception as exc:
+        try:
+            sim.report(rep)
+        except Exception:   # the device error that stopped the run
+            pass
+        rep.error = f"{type(exc).__name__}: {exc}"
         if raise_errors:
             raise
     finally:
-        sim.calc.close()
+        calc.close()
     return rep

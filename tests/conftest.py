@@ -32,3 +32,37 @@ def golden(name):
 
 def system_names():
     return sorted(f[4:-4] for f in os.listdir(GOLDEN) if f.startswith("sys_"))
+
+
+class ScriptedController:
+    """Replays a TuningController run recorded from the reference
+    (tests/golden/traj_tuned.npz: per iteration the configuration, the forced
+    flag and the controller mode, tuning.py:200-210), through the same
+    protocol: configuration_for_iteration / record_timings / record_failure."""
+
+    def __init__(self, z, parse):
+        self.seq = {int(i): (parse(str(c)), bool(f), str(m))
+                    for i, c, f, m in zip(z["seq_it"], z["seq_cfg"], z["seq_forced"], z["seq_mode"])}
+        self.mode = "steady"
+        self.timings = []
+        self.trial_iterations = 0
+        self.tuning_interval = int(z["tuning"][0])
+
+    def configuration_for_iteration(self, iteration):
+        cfg, forced, self.mode = self.seq[iteration]
+        return cfg, forced
+
+    def record_timings(self, force_ns, build_ns):
+        if self.mode == "trial":           # tuning.py:213: no-op outside trials
+            self.timings.append((force_ns, build_ns))
+            self.trial_iterations += 1
+
+    def record_failure(self, error=None):
+        return False
+
+
+class Thermostat:
+    def __init__(self, target, max_delta_t, interval):
+        self.target_temperature = target
+        self.max_delta_t = max_delta_t
+        self.interval_iterations = interval

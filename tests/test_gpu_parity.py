@@ -97,7 +97,8 @@ def test_trajectories_match_reference(pkg, traj):
         params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=10,
                                     delta_t=1e-3, boundary=(P.PERIODIC,) * 3)
         parts = P.ParticleSet(z["pos0"], z["vel0"])
-        simulate(parts, params, P.parse_configuration(cid), steps=int(z["steps"]))
+        rep = simulate(parts, params, P.parse_configuration(cid), steps=int(z["steps"]))
+        assert rep.error is None, rep.error
         dpos = parts.numpy("pos") - z[f"pos_{k}"]
         dpos -= L * np.rint(dpos / L)   # positions compared modulo the box
         assert np.linalg.norm(dpos) / np.linalg.norm(z[f"pos_{k}"]) <= FP64_TOL, cid
@@ -260,3 +261,93 @@ def test_fp32_variant_within_1e4(pkg, name):
         err = port.force_rel_error(parts.numpy("force"), d["forces"][k])
         assert err <= 1e-4, (layout, err)
         assert abs(count - int(d["counts"][k])) <= max(2, int(1e-3 * d["counts"][k]))
+
+
+# -- §8(f): live statistics, temperature/thermostat, tuned loop on device ------
+
+def test_live_stats_bit_exact(pkg):
+    P, calc = pkg
+    z = golden("thermo_stats.npz")
+    for name in (str(s) for s in z["ls_names"]):
+        a = z[f"ls_{name}_in"]
+        per = P.PERIODIC if a[5] else P.REFLECTIVE
+        params = P.SimulationParams(domain_size=a[:3], cutoff=float(a[3]), skin=float(a[4]),
+                                    boundary=(per,) * 3, thread_count=int(a[6]))
+        for layout in ("AoS", "SoA"):
+            parts = P.ParticleSet(z[f"ls_{name}_pos"], layout=layout)
+            fc = calc.ForceCalculator(parts, params)
+            got = fc.live_stats(parts).feature_vector()
+            again = fc.live_stats(parts).feature_vector()       # cached plan, re-zeroed buffers
+            fc.close()
+            assert np.array_equal(got, z[f"ls_{name}_out"]), (name, layout, got, z[f"ls_{name}_out"])
+            assert np.array_equal(again, got)
+
+
+def test_temperature_and_thermostat_bit_exact(pkg):
+    P, calc = pkg
+    z = golden("thermo_stats.npz")
+    params = P.SimulationParams(domain_size=(10.0, 10.0, 10.0), cutoff=2.5, skin=0.3)
+    for name in (str(s) for s in z["th_names"]):
+        nt, soa, target, mdt = z[f"th_{name}_in"]
+        nt = int(nt)
+        vel0 = z[f"th_{name}_vel0"]
+        types = [P.ParticleTypeInfo(t, 1.0 + 0.5 * t, 1.0 - 0.2 * t, 1.0 + t) for t in range(nt)]
+        parts = P.ParticleSet(np.full_like(vel0, 5.0), vel0, type_ids=z[f"th_{name}_tid"], types=types,
+                              layout="SoA" if soa else "AoS")
+        fc = calc.ForceCalculator(parts, params)
+        assert fc.temperature(parts) == float(z[f"th_{name}_t"]), name
+        fc.thermostat(parts, float(target), float(mdt))
+        assert fc.status_flags() == 0
+        fc.close()
+        assert np.array_equal(parts.numpy("vel"), z[f"th_{name}_vel"]), name
+
+
+def test_thermostat_zero_velocity_error_and_empty(pkg):
+    P, calc = pkg
+    params = P.SimulationParams(domain_size=(10.0, 10.0, 10.0), cutoff=2.5, skin=0.3,
+                                boundary=(P.PERIODIC,) * 3,
+                                thermostat=P.ThermostatParams(1.0, 0.1, 1))
+    g = np.array([2.0, 6.0])
+    sites = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)   # 4 apart: no pair forces
+    parts = P.ParticleSet(sites)
+    rep = P.simulate(parts, params, P.parse_configuration("LC-C08-N3L-AoS-CSF1"), steps=3)
+    # reference: apply_thermostat raises ValueError at iteration 0 (integrator.py:84-88)
+    assert rep.error is not None and rep.error.startswith("ValueError"), rep.error
+    empty = P.ParticleSet(np.zeros((0, 3)))
+    fc = calc.ForceCalculator(empty, params)
+    with pytest.raises(ValueError):
+        fc.temperature(empty)
+    fc.close()
+
+
+def test_tuned_loop_replays_reference_controller(pkg):
+    """The reference's TuningController run (FullSearch over VL / LC-C08-SoA /
+    LC-C01-CSF0.5, thermostat every 7) replayed through the device loop:
+    same configuration per iteration, device timings delivered for exactly
+    the trial iterations, final state within the fp64 bar."""
+    from conftest import ScriptedController
+    P, calc = pkg
+    z = golden("traj_tuned.npz")
+    L = float(z["domain"][0])
+    interval, spc, R, tint = (int(x) for x in z["tuning"])
+    params = P.SimulationParams(domain_size=(L, L, L), cutoff=2.5, skin=0.3, rebuild_interval=R,
+                                delta_t=1e-3, total_iterations=int(z["steps"]),
+                                boundary=(P.PERIODIC,) * 3,
+                                thermostat=P.ThermostatParams(float(z["thermo"][0]),
+                                                              float(z["thermo"][1]), tint))
+    parts = P.ParticleSet(z["pos0"], z["vel0"])
+    ctl = ScriptedController(z, P.parse_configuration)
+    rep = P.simulate(parts, params, None, controller=ctl, tuning_interval=interval)
+    assert rep.error is None, rep.error
+    assert rep.configuration_sequence() == [str(s) for s in z["seq_cfg"]]
+    assert ctl.trial_iterations == int(z["trial_iterations"])
+    assert all(f > 0 for f, _ in ctl.timings)
+    forced = [bool(f) for f in z["seq_forced"]]
+    assert all(r.rebuilt for r, f in zip(rep.records, forced) if f)
+    assert parts.layout == str(z["layout"])
+    dpos = parts.numpy("pos") - z["pos"]
+    dpos -= L * np.rint(dpos / L)
+    assert np.linalg.norm(dpos) / np.linalg.norm(z["pos"]) <= FP64_TOL
+    assert port.force_rel_error(parts.numpy("vel"), z["vel"]) <= FP64_TOL
+    assert port.force_rel_error(parts.numpy("force"), z["force"]) <= FP64_TOL
+    assert abs(rep.final_temperature - float(z["final_temperature"])) <= 1e-10 * float(z["final_temperature"])

@@ -173,3 +173,25 @@ def test_extended_space_keeps_reference_ids():
         P.Configuration("LC", "C08", True, "AoS", 1.0, "fp32")
     s = _lib.config_struct(P.parse_configuration("VL-List_Iter-NoN3L-AoS-FP32"))
     assert s.precision == 1
+
+
+def test_pairwise_order_matches_numpy_sum():
+    """The device reductions (stats.cu PairwiseTree) replay numpy's pairwise
+    summation; pin that order against np.sum itself, bit for bit, on lengths
+    that hit every branch (< 8, <= 128, odd splits)."""
+    from oracle import port
+    rng = np.random.default_rng(11)
+    for n in [1, 2, 7, 8, 9, 15, 16, 127, 128, 129, 255, 256, 257, 1000, 4099, 65537]:
+        a = rng.random(n) * rng.standard_normal(n) * 1e3
+        assert port.pairwise_sum(a) == np.sum(a), n
+    v = rng.standard_normal((1000, 3))
+    assert np.array_equal(np.sum(v * v, axis=1), (v[:, 0] * v[:, 0] + v[:, 1] * v[:, 1]) + v[:, 2] * v[:, 2])
+    c = rng.integers(0, 40, 999)
+    assert np.array_equal((c - 13.7) ** 2, (c - 13.7) * (c - 13.7))
+
+
+def test_livestats_feature_order():
+    from paper_2505_03438_b200.livestats import FEATURE_NAMES, LiveStatistics
+    assert FEATURE_NAMES[0] == "meanParticlesPerBin" and FEATURE_NAMES[-1] == "skin"
+    s = LiveStatistics(1.0, 2.0, 3.0, 4.0, 5, 6, 7, 0.3)
+    assert list(s.feature_vector()) == [1.0, 2.0, 3.0, 4.0, 5.0, 6.0, 7.0, 0.3]

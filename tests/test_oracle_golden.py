@@ -118,3 +118,63 @@ def test_simulate_trajectory_bit_exact(traj):
         port.simulate_fixed(p, params, port.parse(cid), steps=int(z["steps"]))
         assert np.array_equal(np.asarray(p.positions), z[f"pos_{k}"]), cid
         assert np.array_equal(np.asarray(p.velocities), z[f"vel_{k}"]), cid
+
+
+# -- thermostat, live statistics, controller-driven loop -------
+
+def test_live_stats_oracle_matches_reference():
+    z = golden("thermo_stats.npz")
+    for name in (str(s) for s in z["ls_names"]):
+        a = z[f"ls_{name}_in"]
+        per = port.PERIODIC if a[5] else port.REFLECTIVE
+        params = port.Params(domain_size=a[:3], cutoff=float(a[3]), skin=float(a[4]),
+                             boundary=(per,) * 3, thread_count=int(a[6]))
+        p = port.Particles(z[f"ls_{name}_pos"])
+        assert np.array_equal(port.compute_live_stats(p, params), z[f"ls_{name}_out"]), name
+
+
+def test_temperature_and_thermostat_oracle_match_reference():
+    z = golden("thermo_stats.npz")
+    for name in (str(s) for s in z["th_names"]):
+        nt, soa, target, mdt = z[f"th_{name}_in"]
+        nt = int(nt)
+        vel0 = z[f"th_{name}_vel0"]
+        p = port.Particles(np.zeros_like(vel0), vel0, z[f"th_{name}_tid"],
+                           sigma=[1.0 - 0.2 * t for t in range(nt)],
+                           epsilon=[1.0 + 0.5 * t for t in range(nt)],
+                           mass=[1.0 + t for t in range(nt)], layout="SoA" if soa else "AoS")
+        assert port.current_temperature(p) == float(z[f"th_{name}_t"]), name
+        port.apply_thermostat(p, target, mdt)
+        assert np.array_equal(np.asarray(p.velocities), z[f"th_{name}_vel"]), name
+
+
+def test_thermostat_rejects_zero_velocities_with_positive_target():
+    p = port.Particles(np.zeros((4, 3)))
+    with pytest.raises(ValueError):
+        port.apply_thermostat(p, 1.0, 0.1)
+    port.apply_thermostat(p, 0.0, 0.1)          # target 0: unchanged, no error
+    with pytest.raises(ValueError):
+        port.current_temperature(port.Particles(np.zeros((0, 3))))
+
+
+def test_controlled_loop_oracle_matches_reference():
+    """The reference's TuningController + FullSearchStrategy run (thermostat
+    on, layout switches, forced trial rebuilds) replayed through the oracle's
+    restatement of simulate(): bit-exact final state."""
+    from conftest import ScriptedController, Thermostat
+    z = golden("traj_tuned.npz")
+    L = float(z["domain"][0])
+    interval, spc, R, tint = (int(x) for x in z["tuning"])
+    params = port.Params(domain_size=(L, L, L), cutoff=2.5, skin=0.3, rebuild_interval=R,
+                         delta_t=1e-3, boundary=(port.PERIODIC,) * 3,
+                         thermostat=Thermostat(float(z["thermo"][0]), float(z["thermo"][1]), tint))
+    p = port.Particles(z["pos0"], z["vel0"])
+    ctl = ScriptedController(z, port.parse)
+    seq = port.simulate_controlled(p, params, ctl, steps=int(z["steps"]))
+    assert [c for c, _ in seq] == [str(s) for s in z["seq_cfg"]]
+    assert ctl.trial_iterations == int(z["trial_iterations"])
+    assert p.layout == str(z["layout"])
+    assert np.array_equal(np.asarray(p.positions), z["pos"])
+    assert np.array_equal(np.asarray(p.velocities), z["vel"])
+    assert np.array_equal(np.asarray(p.forces), z["force"])
+    assert port.current_temperature(p) == float(z["final_temperature"])

@@ -15,6 +15,25 @@ __device__ __forceinline__ double lj_fs(double r2, double s2, double e24) {
     return e24 * (2.0 * a6 * a6 - a6) * inv;
 }
 
+// 1/x: MUFU.RCP64H seed (~2^-22) + one cubically convergent correction
+// y(1 + e + e^2), e = 1 - x y: three DFMAs to full double precision (the LJ
+// minimum cancels 2 a6 - 1, so a single Newton step's 1e-13 is visible
+// there), instead of the IEEE division sequence with its slow-path branch.
+__device__ __forceinline__ double fast_rcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    double t = fma(e, e, e);
+    return fma(y, t, y);
+}
+
+__device__ __forceinline__ double lj_fs_fast(double r2, double s2, double e24) {
+    double y = fast_rcp(r2);
+    double a = s2 * y;
+    double a6 = a * a * a;
+    return (e24 * y) * (a6 * fma(2.0, a6, -1.0));
+}
+
 template <bool MT>
 __device__ __forceinline__ void lj_params(const LJTab& t, int ti, int tj, double& s2, double& e24) {
     if (MT) {

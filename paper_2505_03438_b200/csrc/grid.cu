@@ -123,6 +123,10 @@ void Grid::release() {
 void Verlet::release() {
     grid.release(); cnt.release(); nbr.release(); s4.release(); s3.release(); b32.release();
     q32.release();
+    tdesc.release(); tsize.release(); tbase.release(); tl.release(); tcnt.release();
+    big_row.release();
+    tiled = false;
+    ntiles = nbig = 0;
     cap = 0;
     built = false;
 }

@@ -95,6 +95,15 @@ struct Verlet {
     DBuf<double> s3;           // x[m], y[m], z[m] (SoA variant)
     bool s3_valid = false;
     bool built = false;
+    // shared-memory tiles of the force walk (vltile.cu)
+    bool tiled = false;
+    bool rows_valid = false;   // row-space lists (cnt/nbr) built for every row
+    int ntiles = 0, nbig = 0, cap4 = 0;
+    DBuf<int> tdesc;           // ntiles descriptors (TileDesc)
+    DBuf<int> tsize, tbase;    // per tile: padded entry count, exclusive prefix
+    DBuf<uint16_t> tl;         // window-local lists, 4-entry groups per lane
+    DBuf<int> tcnt;            // per tile row slot: list length
+    DBuf<uint8_t> big_row;     // 1 = row walked by the global-gather kernel
     void release();
 };
 
@@ -173,6 +182,14 @@ void vl_compute(Context& c, int layout);
 int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr);
 int vl_energy(Context& c, double* pe);
 void vl_compute32(Context& c);
+int vlt_build(Context& c);
+int vl_build_rows(Context& c, const uint8_t* only);
+int vl_ensure_rows(Context& c);
+bool vlt_compute(Context& c);
+template <int PLAYOUT, int SLAYOUT>
+void vl_refresh_launch(Context& c, int* zero_me);
+template <int PLAYOUT>
+void vl_force_rows_launch(Context& c, const uint8_t* only);
 void integ_drift_wrap(Context& c, double dt);
 void integ_finish_kick(Context& c, double dt, int has_gravity, double gravity);
 void integ_sd_step(Context& c, double gamma, double max_disp);
@@ -193,6 +210,10 @@ unsigned long long launch_count();
             return -1;                                                          \
         }                                                                       \
     } while (0)
+
+// component stride of the unwrapped SoA copy (Verlet::s3): a multiple of 4
+// rows, so every component array is 32-byte aligned (1-D bulk copies)
+inline int s3_stride(int m) { return (m + 3) & ~3; }
 
 inline int blocks_for(int64_t n, int threads) {
     int64_t b = (n + threads - 1) / threads;

@@ -26,25 +26,6 @@
 
 namespace mdg {
 
-// 1/x: MUFU.RCP64H seed (~2^-22) + one cubically convergent correction
-// y(1 + e + e^2), e = 1 - x y: three DFMAs to full double precision (the LJ
-// minimum cancels 2 a6 - 1, so a single Newton step's 1e-13 is visible
-// there), instead of the IEEE division sequence with its slow-path branch.
-__device__ __forceinline__ double fast_rcp(double x) {
-    double y;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double e = fma(-x, y, 1.0);
-    double t = fma(e, e, e);
-    return fma(y, t, y);
-}
-
-__device__ __forceinline__ double lj_fs_fast(double r2, double s2, double e24) {
-    double y = fast_rcp(r2);
-    double a = s2 * y;
-    double a6 = a * a * a;
-    return (e24 * y) * (a6 * fma(2.0, a6, -1.0));
-}
-
 // ---------------------------------------------------------------- build
 
 // fp32 copy of the build positions + max |coordinate| (for the filter margin).
@@ -58,8 +39,16 @@ __global__ void vl_f32_kernel(const double4* __restrict__ s4, int m, float4* __r
         b32[r] = q;
         mx = fmaxf(fabsf(q.x), fmaxf(fabsf(q.y), fabsf(q.z)));
     }
+    // block maximum, then one atomic per block (x >= 0: the bit patterns order
+    // like the values)
+    __shared__ float wmax[32];
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(maxabs_bits, __float_as_uint(mx));   // x >= 0
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, wmax[w]);
+        atomicMax(maxabs_bits, __float_as_uint(mx));
+    }
 }
 
 // Membership r^2 <= ell^2 (non-strict, kernels.py:848), decided in fp32 where
@@ -69,24 +58,16 @@ __global__ void vl_f32_kernel(const double4* __restrict__ s4, int m, float4* __r
 // |r2_32 - r2| <= 2 sqrt(3) eta ell + 3 eta^2 + 3u ell^2 =: B.  Candidates with
 // r2_32 <= ell^2 - 2B are in, r2_32 > ell^2 + 2B are out, the rest are tested
 // on the fp64 positions.
-//
-// STAGE: each warp's lists are assembled in shared memory laid out [k][lane]
-// (a lane's k-th entry sits in bank `lane`, so the scattered appends are
-// conflict-free) and flushed as coalesced 128-byte rows of the column-major
-// list; appending straight to global memory made every accepted pair a
-// partial-line store (~70 per row) and dominated the build.
 constexpr int kBuildThreads = 128;
 
-template <bool STAGE>
 __global__ void __launch_bounds__(kBuildThreads) vl_build_kernel(
     GridView gv, const double4* __restrict__ bpos, const float4* __restrict__ b32,
     const unsigned* __restrict__ maxabs_bits, const uint8_t* __restrict__ row_code, Stencil st,
-    double ell2, int cap, int* __restrict__ cnt, int* __restrict__ nbr, int* __restrict__ maxcnt) {
-    extern __shared__ int stage[];
+    double ell2, int cap, int* __restrict__ cnt, int* __restrict__ nbr, int* __restrict__ maxcnt,
+    const uint8_t* __restrict__ only) {
     int r = blockIdx.x * blockDim.x + threadIdx.x;
-    int lane = threadIdx.x & 31;
-    int* sw = stage + (size_t)(threadIdx.x >> 5) * cap * 32;
-    bool active = r < gv.m && row_code[r] == kNoShift;   // periodic-image rows own no list
+    // periodic-image rows own no list; `only` restricts the build to flagged rows
+    bool active = r < gv.m && row_code[r] == kNoShift && (!only || only[r]);
     int c = 0;
     if (active) {
     int cell = gv.row_cell[r], cx, cy, cz;
@@ -135,10 +116,7 @@ __global__ void __launch_bounds__(kBuildThreads) vl_build_kernel(
             for (int u = 0; u < 4; ++u) {
                 int j = j0 + u;
                 bool ok = in[u] & (j < e2) & (j != skip);
-                if (ok && c < cap) {
-                    if (STAGE) sw[c * 32 + lane] = j;
-                    else out[(size_t)c * 32] = j;
-                }
+                if (ok && c < cap) out[(size_t)c * 32] = j;
                 c += ok;
             }
         }
@@ -171,18 +149,48 @@ __global__ void __launch_bounds__(kBuildThreads) vl_build_kernel(
     }
     if (r < gv.m) cnt[r] = c;
     if (c > cap) atomicMax(maxcnt, c);
-    if (STAGE) {
-        __syncwarp();
-        int cmax = __reduce_max_sync(0xffffffffu, min(c, cap));
-        // rows r - lane .. r - lane + 31 form one column-major block
-        int* gw = nbr + (size_t)((r - lane) >> 5) * 32 * cap + lane;
-        for (int k = 0; k < cmax; ++k) gw[(size_t)k * 32] = sw[k * 32 + lane];
+}
+
+// Row-space lists for every row (only == nullptr) or for the flagged rows;
+// the width is retried upward if a row overflows.
+int vl_build_rows(Context& c, const uint8_t* only) {
+    Verlet& v = c.vl;
+    Grid& gr = v.grid;
+    int m = (int)gr.m;
+    size_t mpad = ((size_t)m + 31) / 32 * 32;
+    GridView gv = make_view(gr);
+    double ell2 = gr.g.ell * gr.g.ell;
+    int* maxcnt = (int*)(c.scal.p + 3);
+    const unsigned* maxabs = (const unsigned*)(c.scal.p + 5);
+    for (int attempt = 0; attempt < 3 && m > 0; ++attempt) {
+        v.nbr.ensure(mpad * (size_t)v.cap);
+        if (!v.nbr.p) { set_error("out of device memory (Verlet lists)"); return -1; }
+        MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
+        vl_build_kernel<<<blocks_for(m, kBuildThreads), kBuildThreads, 0, c.stream>>>(
+            gv, gr.spos4.p, v.b32.p, maxabs, gr.row_code.p, gr.pruned, ell2, v.cap, v.cnt.p, v.nbr.p,
+            maxcnt, only), note_launch();
+        int hmax = 0;
+        MDG_CUDA(cudaMemcpyAsync(&hmax, maxcnt, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        MDG_CUDA(cudaStreamSynchronize(c.stream));
+        if (hmax <= v.cap) break;
+        v.cap = (hmax + hmax / 8 + 7) / 8 * 8;
     }
+    if (!only) v.rows_valid = true;
+    return 0;
+}
+
+// The row-space lists are what the energy, the exports, the fp32 variant and
+// the untiled walk read; with tiles they are built on first use after a rebuild.
+int vl_ensure_rows(Context& c) {
+    if (c.vl.rows_valid || !c.vl.built) return 0;
+    return vl_build_rows(c, nullptr);
 }
 
 int vl_rebuild(Context& c) {
     Verlet& v = c.vl;
     Grid& gr = v.grid;
+    v.built = false;
+    v.rows_valid = false;
     if (grid_rebuild(c, gr, c.pos, c.layout)) return -1;
     grid_bind_scratch(c, gr, AOS);
     grid_refresh(c, gr, AOS);   // build-time positions pos[src] + shift (containers.py:356-358)
@@ -196,42 +204,14 @@ int vl_rebuild(Context& c) {
         double expect = (double)c.n / vol * 4.18879020479 * ell * ell * ell;
         v.cap = ((int)(1.5 * expect) + 16 + 7) / 8 * 8;
     }
-    GridView gv = make_view(gr);
-    double ell2 = gr.g.ell * gr.g.ell;
-    int* maxcnt = (int*)(c.scal.p + 3);
     unsigned* maxabs = (unsigned*)(c.scal.p + 5);
     v.b32.ensure(mpad + 1);
     MDG_CUDA(cudaMemsetAsync(maxabs, 0, sizeof(unsigned), c.stream));
     if (m > 0)
         vl_f32_kernel<<<blocks_for(m, 256), 256, 0, c.stream>>>(gr.spos4.p, m, v.b32.p, maxabs), note_launch();
-    for (int attempt = 0; attempt < 3 && m > 0; ++attempt) {
-        v.nbr.ensure(mpad * (size_t)v.cap);
-        MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
-        size_t smem = (size_t)kBuildThreads * v.cap * sizeof(int);
-        static int stage_env = -1;
-        if (stage_env < 0) {
-            const char* e = getenv("MDG_VL_BUILD_STAGE");
-            stage_env = e ? atoi(e) : 0;
-        }
-        if (stage_env && smem <= 200 * 1024) {
-            static size_t attr = 0;
-            if (smem > attr) {
-                cudaFuncSetAttribute(vl_build_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     200 * 1024);
-                attr = 200 * 1024;
-            }
-            vl_build_kernel<true><<<blocks_for(m, kBuildThreads), kBuildThreads, smem, c.stream>>>(
-                gv, gr.spos4.p, v.b32.p, maxabs, gr.row_code.p, gr.pruned, ell2, v.cap, v.cnt.p, v.nbr.p, maxcnt), note_launch();
-        } else {
-            vl_build_kernel<false><<<blocks_for(m, kBuildThreads), kBuildThreads, 0, c.stream>>>(
-                gv, gr.spos4.p, v.b32.p, maxabs, gr.row_code.p, gr.pruned, ell2, v.cap, v.cnt.p, v.nbr.p, maxcnt), note_launch();
-        }
-        int hmax = 0;
-        MDG_CUDA(cudaMemcpyAsync(&hmax, maxcnt, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-        MDG_CUDA(cudaStreamSynchronize(c.stream));
-        if (hmax <= v.cap) break;
-        v.cap = (hmax + hmax / 8 + 7) / 8 * 8;
-    }
+    int e = vlt_build(c);               // tile lists (vltile.cu); 1 = not applicable
+    if (e < 0) return -1;
+    if (e == 1 && vl_build_rows(c, nullptr)) return -1;
     // the unwrapped force-time copy starts from the build positions
     v.s4.ensure(mpad + 1);
     MDG_CUDA(cudaMemcpyAsync(v.s4.p, gr.spos4.p, (size_t)m * sizeof(double4),
@@ -252,12 +232,13 @@ struct Wrap {
 
 // Nearest periodic image of pos[src] + shift to the previous row value.
 template <int PLAYOUT, int SLAYOUT>
-__global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int m,
+__global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int m, int ms,
                                   const int* __restrict__ row_src,
                                   const uint8_t* __restrict__ row_code, Wrap w,
                                   double4* __restrict__ s4, double* __restrict__ s3,
-                                  bool from_s4) {
+                                  bool from_s4, int* zero_me) {
     int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r == 0 && zero_me) *zero_me = 0;   // work counter of the tiled walk
     if (r >= m) return;
     int src = row_src[r], code = row_code[r];
     double q[3] = {pos[pidx<PLAYOUT>(src, 0, n)], pos[pidx<PLAYOUT>(src, 1, n)],
@@ -268,7 +249,7 @@ __global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int
     if (SLAYOUT == AOS || from_s4) {
         prev[0] = old.x; prev[1] = old.y; prev[2] = old.z;
     } else {
-        prev[0] = s3[r]; prev[1] = s3[(size_t)m + r]; prev[2] = s3[2 * (size_t)m + r];
+        prev[0] = s3[r]; prev[1] = s3[(size_t)ms + r]; prev[2] = s3[2 * (size_t)ms + r];
     }
     for (int k = 0; k < 3; ++k) {
         double x = q[k] + (double)sh[k] * w.L[k];
@@ -279,8 +260,8 @@ __global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int
         s4[r] = make_double4(q[0], q[1], q[2], old.w);
     } else {
         s3[r] = q[0];
-        s3[(size_t)m + r] = q[1];
-        s3[2 * (size_t)m + r] = q[2];
+        s3[(size_t)ms + r] = q[1];
+        s3[2 * (size_t)ms + r] = q[2];
     }
 }
 
@@ -296,7 +277,7 @@ __global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int
 // before this round's gathers, so the HBM latency of the list stream overlaps
 // the gather + arithmetic of the current round.
 template <int SLAYOUT, int PLAYOUT, bool MT, int G, bool PF, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) vl_force_kernel(int m, int64_t n, int cap,
+__global__ void __launch_bounds__(NT, MINB) vl_force_kernel(int m, int ms, int64_t n, int cap,
                                                       const double4* __restrict__ s4,
                                                       const double* __restrict__ s3,
                                                       const int* __restrict__ row_tid,
@@ -305,10 +286,11 @@ __global__ void __launch_bounds__(NT, MINB) vl_force_kernel(int m, int64_t n, in
                                                       const int* __restrict__ row_src,
                                                       const uint8_t* __restrict__ row_code,
                                                       double* __restrict__ force, LJTab tab,
-                                                      unsigned long long* counter) {
+                                                      unsigned long long* counter,
+                                                      const uint8_t* __restrict__ only) {
     int r = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned hits = 0;
-    if (r < m && row_code[r] == kNoShift) {
+    if (r < m && row_code[r] == kNoShift && (!only || only[r])) {
         double xi, yi, zi;
         int ti = 0;
         if (SLAYOUT == AOS) {
@@ -316,7 +298,7 @@ __global__ void __launch_bounds__(NT, MINB) vl_force_kernel(int m, int64_t n, in
             xi = p.x; yi = p.y; zi = p.z;
             if (MT) ti = (int)p.w;
         } else {
-            xi = s3[r]; yi = s3[(size_t)m + r]; zi = s3[2 * (size_t)m + r];
+            xi = s3[r]; yi = s3[(size_t)ms + r]; zi = s3[2 * (size_t)ms + r];
             if (MT) ti = row_tid[r];
         }
         double fx = 0.0, fy = 0.0, fz = 0.0;
@@ -349,7 +331,7 @@ __global__ void __launch_bounds__(NT, MINB) vl_force_kernel(int m, int64_t n, in
                     xj = p.x; yj = p.y; zj = p.z;
                     if (MT) tj[u] = (int)p.w;
                 } else {
-                    xj = s3[j]; yj = s3[(size_t)m + j]; zj = s3[2 * (size_t)m + j];
+                    xj = s3[j]; yj = s3[(size_t)ms + j]; zj = s3[2 * (size_t)ms + j];
                     if (MT) tj[u] = row_tid[j];
                 }
                 dx[u] = xi - xj; dy[u] = yi - yj; dz[u] = zi - zj;
@@ -419,19 +401,19 @@ static void vl_launch(Context& c, bool mt) {
     }
     dim3 b(blocks_for(m, 256)), t(256);
     bool from_s4 = SLAYOUT == SOA && !v.s3_valid;
-    vl_refresh_kernel<PLAYOUT, SLAYOUT><<<b, t, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, from_s4), note_launch();
+    vl_refresh_kernel<PLAYOUT, SLAYOUT><<<b, t, 0, c.stream>>>(c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, from_s4, nullptr), note_launch();
     if (SLAYOUT == SOA) v.s3_valid = true;
     c.prof_mark();
 #define MDG_VLF(G, PF, NT, MB)                                                                     \
     do {                                                                                         \
         if (mt)                                                                                  \
             vl_force_kernel<SLAYOUT, PLAYOUT, true, G, PF, NT, MB><<<blocks_for(m, NT), NT, 0, c.stream>>>( \
-                m, c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p,      \
-                gr.row_code.p, c.force, c.tab, c.scal.p), note_launch();                          \
+                m, s3_stride(m), c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p,      \
+                gr.row_code.p, c.force, c.tab, c.scal.p, nullptr), note_launch();                 \
         else                                                                                     \
             vl_force_kernel<SLAYOUT, PLAYOUT, false, G, PF, NT, MB><<<blocks_for(m, NT), NT, 0, c.stream>>>( \
-                m, c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p,      \
-                gr.row_code.p, c.force, c.tab, c.scal.p), note_launch();                          \
+                m, s3_stride(m), c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p,      \
+                gr.row_code.p, c.force, c.tab, c.scal.p, nullptr), note_launch();                 \
     } while (0)
     // measured on B200, config 2 (profiles/round1_vl_variants.txt): all within
     // 6%; index prefetch with 4-entry rounds and 128-thread CTAs is fastest
@@ -451,11 +433,56 @@ static void vl_launch(Context& c, bool mt) {
     c.prof_mark();
 }
 
+static Wrap make_wrap(const Context& c) {
+    Wrap w;
+    for (int k = 0; k < 3; ++k) {
+        w.L[k] = c.L[k];
+        w.invL[k] = 1.0 / c.L[k];
+        w.per[k] = c.periodic[k];
+    }
+    return w;
+}
+
+template <int PLAYOUT, int SLAYOUT>
+void vl_refresh_launch(Context& c, int* zero_me) {
+    Verlet& v = c.vl;
+    Grid& gr = v.grid;
+    int m = (int)gr.m;
+    bool from_s4 = SLAYOUT == SOA && !v.s3_valid;
+    vl_refresh_kernel<PLAYOUT, SLAYOUT><<<blocks_for(m, 256), 256, 0, c.stream>>>(
+        c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, make_wrap(c), v.s4.p, v.s3.p, from_s4, zero_me), note_launch();
+    if (SLAYOUT == SOA) v.s3_valid = true;
+}
+template void vl_refresh_launch<AOS, SOA>(Context&, int*);
+template void vl_refresh_launch<SOA, SOA>(Context&, int*);
+
+// global-gather walk over the rows flagged in `only` (SoA source)
+template <int PLAYOUT>
+void vl_force_rows_launch(Context& c, const uint8_t* only) {
+    Verlet& v = c.vl;
+    Grid& gr = v.grid;
+    int m = (int)gr.m;
+    if (c.tab.T > 1)
+        vl_force_kernel<SOA, PLAYOUT, true, 4, true, 128, 1><<<blocks_for(m, 128), 128, 0, c.stream>>>(
+            m, s3_stride(m), c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p,
+            gr.row_code.p, c.force, c.tab, c.scal.p, only), note_launch();
+    else
+        vl_force_kernel<SOA, PLAYOUT, false, 4, true, 128, 1><<<blocks_for(m, 128), 128, 0, c.stream>>>(
+            m, s3_stride(m), c.n, v.cap, v.s4.p, v.s3.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p,
+            gr.row_code.p, c.force, c.tab, c.scal.p, only), note_launch();
+}
+template void vl_force_rows_launch<AOS>(Context&, const uint8_t*);
+template void vl_force_rows_launch<SOA>(Context&, const uint8_t*);
+
 void vl_compute(Context& c, int layout) {
     if (c.n == 0) return;
     Verlet& v = c.vl;
     bool mt = c.tab.T > 1;
-    if (layout == SOA) v.s3.ensure(3 * (size_t)v.grid.m + 3);
+    if (v.tiled) {
+        v.s3.ensure(3 * (size_t)s3_stride((int)v.grid.m) + 8);
+        if (vlt_compute(c)) return;
+    }
+    if (layout == SOA) v.s3.ensure(3 * (size_t)s3_stride((int)v.grid.m) + 8);
     if (c.layout == AOS) {
         if (layout == AOS) vl_launch<AOS, AOS>(c, mt);
         else vl_launch<SOA, AOS>(c, mt);
@@ -572,6 +599,7 @@ __global__ void __launch_bounds__(128) vl_force32_kernel(int m, int64_t n, int c
 
 void vl_compute32(Context& c) {
     if (c.n == 0) return;
+    if (vl_ensure_rows(c)) return;
     Verlet& v = c.vl;
     Grid& gr = v.grid;
     int m = (int)gr.m;
@@ -647,6 +675,7 @@ __global__ void __launch_bounds__(256) vl_energy_kernel(int m, int cap, const do
 }
 
 int vl_energy(Context& c, double* pe) {
+    if (vl_ensure_rows(c)) return -1;
     Verlet& v = c.vl;
     Grid& gr = v.grid;
     int m = (int)gr.m;
@@ -659,9 +688,9 @@ int vl_energy(Context& c, double* pe) {
         w.per[k] = c.periodic[k];
     }
     if (c.layout == AOS)
-        vl_refresh_kernel<AOS, AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, false), note_launch();
+        vl_refresh_kernel<AOS, AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, false, nullptr), note_launch();
     else
-        vl_refresh_kernel<SOA, AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, false), note_launch();
+        vl_refresh_kernel<SOA, AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, false, nullptr), note_launch();
     double* dpe = (double*)(c.scal.p + 6);
     MDG_CUDA(cudaMemsetAsync(dpe, 0, sizeof(double), c.stream));
     if (c.tab.T > 1)
@@ -675,6 +704,7 @@ int vl_energy(Context& c, double* pe) {
 
 // Reference-format export: CSR by owner index with owner indices.
 int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr) {
+    if (vl_ensure_rows(c)) return -1;
     Verlet& v = c.vl;
     Grid& gr = v.grid;
     int m = (int)gr.m;

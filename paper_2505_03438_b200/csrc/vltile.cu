@@ -1,0 +1,610 @@
+// Shared-memory tiled Verlet-list walk (VL-List_Iter-NoN3L-{AoS,SoA} force).
+//
+// Reference: vl_force_aos/_soa (kernels.py:730-818) over the lists of
+// VerletListState (containers.py:343-375); the pair sets and counts are those
+// of vl.cu's row-space lists, which this file only re-indexes.
+//
+// Why: the row-space walk (vl.cu) gathers every neighbour position from
+// global memory, one random 32-byte sector per lane and entry; on B200 that
+// saturates the L1TEX wavefront rate at ~1 record / clock / SM
+// (profiles/round1_ncu_vl_force_bench.txt, tools/microbench_smem.cu).  Random
+// 8-byte reads from shared memory sustain ~1.8 records / clock / SM.  So:
+//
+//  * Tiles.  Owned cells are cut into 2 x 2 cell columns x a z-run of TZ
+//    cells (TZ from the mean density so the window fits).  The window of a
+//    tile -- the 4 x 4 columns around it over z0-1 .. z1, i.e. 16 contiguous
+//    row ranges of the cell-sorted row space -- holds every neighbour of
+//    every tile row (CSF-1 grid, 26-cell stencil).
+//  * Lists.  At rebuild, each tile row's list is rewritten as uint16
+//    window-local indices in 4-entry groups (8 bytes per lane and group,
+//    a warp's group loads are 256 contiguous bytes), streamed evict-first.
+//  * Walk.  Persistent CTAs take tiles from an atomic counter, stage the
+//    window's unwrapped positions (x, y, z component arrays, types) in
+//    shared memory with coalesced loads, and walk the lists one thread per
+//    row with the batched fast reciprocal of vl.cu.
+//  * Overflow.  Tiles whose window exceeds the shared-memory budget
+//    (clustered inputs) are walked by vl.cu's global-gather kernel, selected
+//    row by row through a mask.
+#include <cstdio>
+#include <vector>
+
+#include "device.cuh"
+
+namespace mdg {
+
+constexpr int kTX = 2, kTY = 2;
+constexpr int kRanges = (kTX + 2) * (kTY + 2);
+constexpr int kSegs = kTX * kTY;
+constexpr int kWinRows = 2048;        // 48 KB of positions (+ 2 KB types) per CTA
+constexpr int kWalkThreads = 256;
+
+struct TileDesc {
+    int x0, y0, z0, z1;
+    int ni, wrows, big, pad0;
+    int wstart[kRanges];
+    int woff[kRanges + 1];
+    int istart[kSegs];
+    int ioff[kSegs + 1];
+    int pad1[2];
+};
+static_assert(sizeof(TileDesc) % 16 == 0, "TileDesc is copied as int4");
+constexpr int kDescInts = sizeof(TileDesc) / 4;
+
+struct TilePlan {
+    int ngx, ngy, nzt, tz;
+};
+
+__global__ void vlt_desc_kernel(GridView gv, TilePlan tp, int ntiles, int cap4,
+                                TileDesc* __restrict__ desc, int* __restrict__ tsize,
+                                int* __restrict__ nbig) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    int gz = t % tp.nzt, g2 = t / tp.nzt;
+    int gy = g2 % tp.ngy, gx = g2 / tp.ngy;
+    TileDesc d;
+    d.x0 = gv.H0 + gx * kTX;
+    d.y0 = gv.H1 + gy * kTY;
+    d.z0 = gv.H2 + gz * tp.tz;
+    d.z1 = min(d.z0 + tp.tz, gv.H2 + gv.S2);
+    int tx = min(kTX, gv.H0 + gv.S0 - d.x0), ty = min(kTY, gv.H1 + gv.S1 - d.y0);
+    int za = max(d.z0 - 1, 0), zb = min(d.z1, gv.D2 - 1);
+    int off = 0;
+    for (int a = 0; a < kTX + 2; ++a)
+        for (int b = 0; b < kTY + 2; ++b) {
+            int R = a * (kTY + 2) + b, x = d.x0 - 1 + a, y = d.y0 - 1 + b;
+            bool in = a <= tx + 1 && b <= ty + 1 && x >= 0 && x < gv.D0 && y >= 0 && y < gv.D1;
+            // rounded out to multiples of 4 rows: every component range is
+            // then a 32-byte aligned 1-D bulk copy (the extra rows are never
+            // referenced by a list)
+            int ws = in ? gv.start[gv.flat(x, y, za)] & ~3 : 0;
+            int we = in ? (gv.start[gv.flat(x, y, zb) + 1] + 3) & ~3 : 0;
+            d.wstart[R] = ws;
+            d.woff[R] = off;
+            off += we - ws;
+        }
+    d.woff[kRanges] = off;
+    int io = 0;
+    for (int a = 0; a < kTX; ++a)
+        for (int b = 0; b < kTY; ++b) {
+            int C = a * kTY + b;
+            bool in = a < tx && b < ty;
+            int x = d.x0 + a, y = d.y0 + b;
+            int is = in ? gv.start[gv.flat(x, y, d.z0)] : 0;
+            int ie = in ? gv.start[gv.flat(x, y, d.z1 - 1) + 1] : 0;
+            d.istart[C] = is;
+            d.ioff[C] = io;
+            io += ie - is;
+        }
+    d.ioff[kSegs] = io;
+    d.ni = io;
+    d.wrows = off;
+    d.big = off > kWinRows || off > 65536;
+    d.pad0 = 0;
+    d.pad1[0] = d.pad1[1] = 0;
+    desc[t] = d;
+    tsize[t] = d.big ? 0 : (io + 31) / 32 * 32 * cap4;
+    if (d.big) atomicAdd(nbig, 1);
+}
+
+__device__ __forceinline__ void load_desc(const TileDesc* __restrict__ desc, int t, TileDesc& d) {
+    const int4* src = reinterpret_cast<const int4*>(desc + t);
+    int4* dst = reinterpret_cast<int4*>(&d);
+    for (int k = threadIdx.x; k < kDescInts / 4; k += blockDim.x) dst[k] = src[k];
+}
+
+// tile-local row q -> (row, window index of the row).  Branch-free: a
+// data-dependent loop here splits the warp (lanes in different segments leave
+// it on different trips and never reconverge before the list walk, which then
+// runs once per lane group).
+__device__ __forceinline__ int tile_row(const TileDesc& d, int q, int& li) {
+    int C = 0;
+#pragma unroll
+    for (int k = 1; k < kSegs; ++k) C += q >= d.ioff[k];
+    int r = d.istart[C] + (q - d.ioff[C]);
+    int R = (C / kTY + 1) * (kTY + 2) + (C % kTY + 1);
+    li = d.woff[R] + (r - d.wstart[R]);
+    return r;
+}
+
+// Tiled list build (rebuild time).  One CTA per tile stages the window's fp32
+// build positions in shared memory; each thread scans its row's nine window
+// z-runs (cells cz-1 .. cz+1 of the 3 x 3 neighbouring columns, i.e. the
+// 26-cell stencil + own cell, in ascending row order like vl.cu) and writes
+// uint16 window indices straight into the tile list, four at a time (a
+// 64-bit register collects a group, one 8-byte store flushes it; the last
+// group's unused slots stay zero, which is the padding the walk expects).
+// Membership is the reference's r^2 <= ell^2 on the fp64 build positions
+// (kernels.py:848), decided in fp32 where the rounding bound of vl.cu's build
+// proves it and in fp64 otherwise.  Lanes of rows in one cell scan the same
+// candidates, so the shared-memory reads are broadcasts.
+constexpr int kBuildThreadsT = 256;
+constexpr int kMaxTZ = 48;
+
+__global__ void __launch_bounds__(kBuildThreadsT) vlt_build_kernel(
+    GridView gv, const TileDesc* __restrict__ desc, const int* __restrict__ tbase,
+    const float4* __restrict__ b32, const double4* __restrict__ bpos,
+    const unsigned* __restrict__ maxabs_bits, double ell2, int cap, int cap4,
+    uint16_t* __restrict__ tl, int* __restrict__ tcnt, int* __restrict__ maxcnt) {
+    __shared__ __align__(16) TileDesc d;
+    __shared__ int cs[kRanges][kMaxTZ + 4];
+    __shared__ float4 w32[kWinRows + 4];   // +4: the 4-wide scan reads past a run's end
+    load_desc(desc, blockIdx.x, d);
+    __syncthreads();
+    if (d.big) return;
+    const int za = max(d.z0 - 1, 0), zb = min(d.z1, gv.D2 - 1), nz = zb - za + 1;
+    const int tx = min(kTX, gv.H0 + gv.S0 - d.x0), ty = min(kTY, gv.H1 + gv.S1 - d.y0);
+    // cs[R][k]: window index of the first row of cell za + k in range R
+    for (int idx = threadIdx.x; idx < kRanges * (nz + 1); idx += blockDim.x) {
+        int R = idx / (nz + 1), k = idx % (nz + 1);
+        int a = R / (kTY + 2), b = R % (kTY + 2), x = d.x0 - 1 + a, y = d.y0 - 1 + b;
+        bool in = a <= tx + 1 && b <= ty + 1 && x >= 0 && x < gv.D0 && y >= 0 && y < gv.D1;
+        cs[R][k] = in ? gv.start[gv.flat(x, y, za) + k] - d.wstart[R] + d.woff[R] : 0;
+    }
+    int wrows = d.woff[kRanges];
+    for (int w = threadIdx.x; w < wrows + 4; w += blockDim.x) {
+        if (w >= wrows) {
+            w32[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+            continue;
+        }
+        int lo = 0;
+#pragma unroll
+        for (int R = 1; R < kRanges; ++R) lo += d.woff[R] <= w;
+        w32[w] = b32[d.wstart[lo] + (w - d.woff[lo])];
+    }
+    __syncthreads();
+    const double u = 5.9604644775390625e-08;   // 2^-24
+    double X = (double)__uint_as_float(*maxabs_bits) * (1.0 + 4.0 * u);
+    double ell = sqrt(ell2);
+    double eta = 2.0 * u * X + 2.0 * u * ell;
+    double B = 3.4641016151377544 * eta * ell + 3.0 * eta * eta + 3.0 * u * ell2;
+    const float flo = __double2float_rd(ell2 - 2.0 * B), fhi = __double2float_ru(ell2 + 2.0 * B);
+    const int base = tbase[blockIdx.x];
+    const int slot0 = base / cap4;
+    const int ngroups = cap4 >> 2;
+    for (int q = threadIdx.x; q < d.ni; q += blockDim.x) {
+        int C = 0;
+#pragma unroll
+        for (int k = 1; k < kSegs; ++k) C += q >= d.ioff[k];
+        int r = d.istart[C] + (q - d.ioff[C]);
+        int a = C / kTY, b = C % kTY;
+        int Rown = (a + 1) * (kTY + 2) + (b + 1);
+        int li = d.woff[Rown] + (r - d.wstart[Rown]);
+        int cx, cy, cz;
+        gv.decode(gv.row_cell[r], cx, cy, cz);
+        int k0 = max(cz - 1 - za, 0), k1 = min(cz + 2 - za, nz);
+        float4 qi = w32[li];
+        unsigned long long* op = reinterpret_cast<unsigned long long*>(
+            tl + base + (size_t)(q >> 5) * 32 * cap4 + (q & 31) * 4);
+        unsigned long long pk = 0;
+        int c = 0;
+        for (int dx = 0; dx < 3; ++dx)
+            for (int dy = 0; dy < 3; ++dy) {
+                int R = (a + dx) * (kTY + 2) + (b + dy);
+                int s0 = cs[R][k0], e0 = cs[R][k1];
+                int gR = d.wstart[R] - d.woff[R];   // global row of window index l: gR + l
+                for (int l0 = s0; l0 < e0; l0 += 4) {
+                    bool in[4], bd[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        float4 p = w32[l0 + t];
+                        float fx = qi.x - p.x, fy = qi.y - p.y, fz = qi.z - p.z;
+                        float r2 = fx * fx + fy * fy + fz * fz;
+                        bool use = (l0 + t < e0) & (l0 + t != li);
+                        in[t] = use & (r2 <= flo);
+                        bd[t] = use & (r2 > flo) & (r2 <= fhi);
+                    }
+                    if (bd[0] | bd[1] | bd[2] | bd[3]) {   // rare: exact fp64 test
+                        double4 pi = ldg256(bpos + r);
+#pragma unroll
+                        for (int t = 0; t < 4; ++t)
+                            if (bd[t]) {
+                                double4 pj = ldg256(bpos + gR + l0 + t);
+                                double ex = pi.x - pj.x, ey = pi.y - pj.y, ez = pi.z - pj.z;
+                                in[t] = ex * ex + ey * ey + ez * ez <= ell2;
+                            }
+                    }
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        if (in[t]) {
+                            pk |= (unsigned long long)(l0 + t) << (16 * (c & 3));
+                            ++c;
+                            if ((c & 3) == 0) {
+                                if ((c >> 2) <= ngroups) op[(size_t)((c >> 2) - 1) * 32] = pk;
+                                pk = 0;
+                            }
+                        }
+                    }
+                }
+            }
+        if ((c & 3) && (c >> 2) < ngroups) op[(size_t)(c >> 2) * 32] = pk;
+        tcnt[slot0 + q] = min(c, cap);
+        if (c > cap) atomicMax(maxcnt, c);
+    }
+}
+
+__global__ void vlt_mark_big_kernel(const TileDesc* __restrict__ desc, uint8_t* __restrict__ big_row) {
+    __shared__ __align__(16) TileDesc d;
+    load_desc(desc, blockIdx.x, d);
+    __syncthreads();
+    if (!d.big) return;
+    for (int q = threadIdx.x; q < d.ni; q += blockDim.x) {
+        int li;
+        big_row[tile_row(d, q, li)] = 1;
+    }
+}
+
+// ---- mbarrier / 1-D bulk-copy (TMA) primitives
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, int parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+constexpr int kConsumerWarps = 12;
+constexpr int kTileThreads = (kConsumerWarps + 1) * 32;
+
+template <bool MT>
+struct WinLayout {
+    // per buffer: x, y, z (doubles) then types (int32) for MT
+    static constexpr int kDoubles = 3 * kWinRows + (MT ? kWinRows / 2 : 0);
+};
+
+// Persistent, warp-specialised walk.  The last warp is the producer: it takes
+// the next tile from the global counter, copies its descriptor and issues the
+// window's 1-D bulk copies (one per range and component) into one of two
+// buffers, completing on that buffer's `full` mbarrier.  The other warps
+// consume: they take 32-row chunks of the tile dynamically, walk them, and
+// arrive on the buffer's `empty` mbarrier when no chunk is left, so the
+// producer refills it while they already work on the other buffer.  No
+// CTA-wide barrier after the prologue.
+template <int PLAYOUT, bool MT, int PF>
+__global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
+    const TileDesc* __restrict__ desc, const int* __restrict__ tbase, int ntiles,
+    int* __restrict__ next, int ms, int64_t n, int cap4, const double* __restrict__ s3,
+    const int* __restrict__ row_tid, const int* __restrict__ tcnt, const uint2* __restrict__ tl,
+    const int* __restrict__ row_src, double* __restrict__ force, LJTab tab,
+    unsigned long long* counter) {
+    extern __shared__ __align__(128) double win[];
+    __shared__ __align__(16) TileDesc d[2];
+    __shared__ __align__(8) uint64_t full[2], empty[2];
+    __shared__ int rowctr[2], tile_of[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&empty[b], kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    constexpr int kBuf = WinLayout<MT>::kDoubles;
+    if (warp == kConsumerWarps) {
+        // ---------------- producer
+        for (int it = 0;; ++it) {
+            int b = it & 1;
+            if (it >= 2) mbar_wait(&empty[b], ((it >> 1) - 1) & 1);
+            int t = 0;
+            if (lane == 0) t = atomicAdd(next, 1);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= ntiles) {
+                if (lane == 0) {
+                    tile_of[b] = -1;
+                    mbar_arrive(&full[b]);
+                }
+                break;
+            }
+            if (lane < kDescInts / 4)
+                reinterpret_cast<int4*>(&d[b])[lane] = reinterpret_cast<const int4*>(desc + t)[lane];
+            __syncwarp();
+            const TileDesc& D = d[b];
+            if (D.big) {
+                if (lane == 0) {
+                    tile_of[b] = t;
+                    mbar_arrive(&full[b]);
+                }
+                continue;
+            }
+            double* wx = win + b * kBuf;
+            double* wy = wx + kWinRows;
+            double* wz = wy + kWinRows;
+            int* wt = reinterpret_cast<int*>(wz + kWinRows);
+            if (lane == 0) {
+                tile_of[b] = t;
+                rowctr[b] = 0;
+                mbar_arrive_tx(&full[b], (unsigned)D.wrows * (MT ? 28u : 24u));
+            }
+            __syncwarp();
+            if (lane < kRanges) {
+                int R = lane, o = D.woff[R], rows = D.woff[R + 1] - o, g = D.wstart[R];
+                if (rows > 0) {
+                    bulk_g2s(wx + o, s3 + g, rows * 8u, &full[b]);
+                    bulk_g2s(wy + o, s3 + (size_t)ms + g, rows * 8u, &full[b]);
+                    bulk_g2s(wz + o, s3 + 2 * (size_t)ms + g, rows * 8u, &full[b]);
+                    if (MT) bulk_g2s(wt + o, row_tid + g, rows * 4u, &full[b]);
+                }
+            }
+        }
+        return;
+    }
+    // ---------------- consumers
+    unsigned hits = 0;
+    for (int it = 0;; ++it) {
+        int b = it & 1;
+        mbar_wait(&full[b], (it >> 1) & 1);
+        int t = tile_of[b];
+        if (t < 0) break;
+        const TileDesc& D = d[b];
+        if (!D.big) {
+            const double* wx = win + b * kBuf;
+            const double* wy = wx + kWinRows;
+            const double* wz = wy + kWinRows;
+            const int* wt = reinterpret_cast<const int*>(wz + kWinRows);
+            int base = tbase[t];
+            int slot0 = base / cap4;
+            int ni = D.ni;
+            for (;;) {
+                int q0 = 0;
+                if (lane == 0) q0 = atomicAdd(&rowctr[b], 32);
+                q0 = __shfl_sync(0xffffffffu, q0, 0);
+                if (q0 >= ni) break;
+                int q = q0 + lane;
+                if (q < ni) {
+                    int li;
+                    int r = tile_row(D, q, li);
+                    double xi = wx[li], yi = wy[li], zi = wz[li];
+                    int ti = MT ? wt[li] : 0;
+                    // the count, the first two entry groups and the output
+                    // index are independent loads: issue them together (every
+                    // row owns >= 2 groups, cap4 >= 8), then keep the list
+                    // stream two rounds ahead of the walk
+                    const uint2* lp = tl + ((size_t)base + (size_t)(q >> 5) * 32 * cap4) / 4 + (q & 31);
+                    int c = tcnt[slot0 + q];
+                    uint2 g0 = __ldcs(lp), g1 = PF == 2 ? __ldcs(lp + 32) : make_uint2(0u, 0u);
+                    int i = row_src[r];
+                    double fx = 0.0, fy = 0.0, fz = 0.0;
+                    for (int k0 = 0; k0 < c; k0 += 4) {
+                        uint2 cur = g0;
+                        if (PF == 2) {
+                            g0 = g1;
+                            if (k0 + 8 < c) g1 = __ldcs(lp + (size_t)(k0 / 4 + 2) * 32);
+                        } else if (k0 + 4 < c) {
+                            g0 = __ldcs(lp + (size_t)(k0 / 4 + 1) * 32);
+                        }
+                        int jj[4] = {(int)(cur.x & 0xffffu), (int)(cur.x >> 16), (int)(cur.y & 0xffffu),
+                                     (int)(cur.y >> 16)};
+                        double dx[4], dy[4], dz[4], qq[4];
+                        int tj[4];
+                        bool ok[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            int j = jj[u];
+                            dx[u] = xi - wx[j];
+                            dy[u] = yi - wy[j];
+                            dz[u] = zi - wz[j];
+                            tj[u] = MT ? wt[j] : 0;
+                            double r2 = dx[u] * dx[u] + dy[u] * dy[u] + dz[u] * dz[u];
+                            ok[u] = (k0 + u < c) && r2 < tab.rc2;
+                            qq[u] = ok[u] ? r2 : 1.0;
+                        }
+                        // one reciprocal for four pairs (see vl.cu)
+                        double p01 = qq[0] * qq[1], p23 = qq[2] * qq[3];
+                        double y = fast_rcp(p01 * p23);
+                        double y01 = y * p23, y23 = y * p01;
+                        double inv[4] = {y01 * qq[1], y01 * qq[0], y23 * qq[3], y23 * qq[2]};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (ok[u]) {
+                                double s2, e24;
+                                lj_params<MT>(tab, ti, tj[u], s2, e24);
+                                double a = s2 * inv[u];
+                                double a6 = a * a * a;
+                                double fs = (e24 * inv[u]) * (a6 * fma(2.0, a6, -1.0));
+                                ++hits;
+                                fx = fma(fs, dx[u], fx);
+                                fy = fma(fs, dy[u], fy);
+                                fz = fma(fs, dz[u], fz);
+                            }
+                        }
+                    }
+                    force[pidx<PLAYOUT>(i, 0, n)] = fx;
+                    force[pidx<PLAYOUT>(i, 1, n)] = fy;
+                    force[pidx<PLAYOUT>(i, 2, n)] = fz;
+                }
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[b]);
+    }
+    warp_count(counter, hits);
+}
+
+static bool vlt_env_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_VL_TILED");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+
+static int vlt_env_tz() {
+    static int v = -2;
+    if (v == -2) {
+        const char* e = getenv("MDG_VLT_TZ");
+        v = e ? atoi(e) : -1;
+    }
+    return v;
+}
+
+// Tiled build (called by vl_rebuild after the fp32 copy): 0 = tile lists
+// built, 1 = tiling not applicable (row-space lists instead), -1 = error.
+int vlt_build(Context& c) {
+    Verlet& v = c.vl;
+    Grid& gr = v.grid;
+    v.tiled = false;
+    v.ntiles = v.nbig = 0;
+    if (!vlt_env_enabled() || c.n == 0 || gr.pruned.n != 26) return 1;
+    const Geom& g = gr.g;
+    // TZ: the mean window (4 x 4 columns x TZ+2 cells) at 90% of the budget
+    double rho = (double)c.n / ((double)g.S[0] * g.S[1] * g.S[2]);
+    int tz = vlt_env_tz();
+    if (tz < 1) tz = (int)floor(0.9 * kWinRows / ((kTX + 2) * (kTY + 2) * std::max(rho, 1e-9))) - 2;
+    tz = std::max(1, std::min(std::min(tz, g.S[2]), kMaxTZ));
+    TilePlan tp{(g.S[0] + kTX - 1) / kTX, (g.S[1] + kTY - 1) / kTY, (g.S[2] + tz - 1) / tz, tz};
+    int ntiles = tp.ngx * tp.ngy * tp.nzt;
+    v.tdesc.ensure((size_t)ntiles * kDescInts);
+    v.tsize.ensure(ntiles + 1);
+    v.tbase.ensure(ntiles + 1);
+    int m = (int)gr.m;
+    v.big_row.ensure(m + 1);
+    if (!v.tdesc.p || !v.tsize.p || !v.tbase.p || !v.big_row.p) {
+        set_error("out of device memory (VL tiles)");
+        return -1;
+    }
+    GridView gv = make_view(gr);
+    TileDesc* desc = reinterpret_cast<TileDesc*>(v.tdesc.p);
+    int* nbig = (int*)(c.scal.p + 7);
+    int* maxcnt = (int*)(c.scal.p + 3);
+    const unsigned* maxabs = (const unsigned*)(c.scal.p + 5);
+    double ell2 = g.ell * g.ell;
+    int big = 0;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        v.cap4 = std::max(8, (v.cap + 3) & ~3);   // >= 2 groups per row (walk prefetch)
+        MDG_CUDA(cudaMemsetAsync(nbig, 0, sizeof(int), c.stream));
+        vlt_desc_kernel<<<blocks_for(ntiles, 128), 128, 0, c.stream>>>(gv, tp, ntiles, v.cap4, desc,
+                                                                       v.tsize.p, nbig), note_launch();
+        exclusive_scan_i32(v.tsize.p, v.tbase.p, ntiles, c.scal.p + 1, c.scan_tmp, c.stream);
+        MDG_CUDA(cudaMemcpyAsync(c.h_scal + 1, c.scal.p + 1, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, c.stream));
+        MDG_CUDA(cudaMemcpyAsync(c.h_scal + 7, c.scal.p + 7, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, c.stream));
+        MDG_CUDA(cudaStreamSynchronize(c.stream));
+        long long total = (long long)c.h_scal[1];
+        big = (int)(c.h_scal[7] & 0xffffffffu);
+        if (total > (1ll << 31) - 64) return 1;   // keep the row-space walk
+        v.tl.ensure((size_t)total + 8);
+        v.tcnt.ensure((size_t)total / v.cap4 + 32);
+        if (!v.tl.p || !v.tcnt.p) {
+            set_error("out of device memory (VL tile lists)");
+            return -1;
+        }
+        MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
+        vlt_build_kernel<<<ntiles, kBuildThreadsT, 0, c.stream>>>(
+            gv, desc, v.tbase.p, v.b32.p, gr.spos4.p, maxabs, ell2, v.cap, v.cap4, v.tl.p, v.tcnt.p,
+            maxcnt), note_launch();
+        int hmax = 0;
+        MDG_CUDA(cudaMemcpyAsync(&hmax, maxcnt, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        MDG_CUDA(cudaStreamSynchronize(c.stream));
+        if (hmax <= v.cap) break;
+        v.cap = (hmax + hmax / 8 + 7) / 8 * 8;
+    }
+    if (big) {
+        // tiles whose window does not fit: row-space lists for their rows
+        MDG_CUDA(cudaMemsetAsync(v.big_row.p, 0, m, c.stream));
+        vlt_mark_big_kernel<<<ntiles, 128, 0, c.stream>>>(desc, v.big_row.p), note_launch();
+        if (vl_build_rows(c, v.big_row.p)) return -1;
+    }
+    v.ntiles = ntiles;
+    v.nbig = big;
+    v.tiled = true;
+    if (getenv("MDG_VLT_DEBUG"))
+        fprintf(stderr, "vlt: tz=%d tiles=%d big=%d cap=%d cap4=%d\n", tz, ntiles, big, v.cap, v.cap4);
+    return 0;
+}
+
+template <int PLAYOUT, bool MT, int PF>
+static void vlt_launch_pf(Context& c) {
+    Verlet& v = c.vl;
+    size_t smem = 2 * (size_t)WinLayout<MT>::kDoubles * sizeof(double);
+    static int ctas_per_sm = 0;
+    if (!ctas_per_sm) {
+        cudaFuncSetAttribute(vlt_force_kernel<PLAYOUT, MT, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, vlt_force_kernel<PLAYOUT, MT, PF>,
+                                                      kTileThreads, smem);
+        if (ctas_per_sm < 1) ctas_per_sm = 1;
+    }
+    int grid = std::min(v.ntiles, c.sm_count * ctas_per_sm);
+    if (grid < 1) return;
+    vlt_force_kernel<PLAYOUT, MT, PF><<<grid, kTileThreads, smem, c.stream>>>(
+        reinterpret_cast<const TileDesc*>(v.tdesc.p), v.tbase.p, v.ntiles, (int*)(c.scal.p + 6),
+        s3_stride((int)v.grid.m), c.n, v.cap4, v.s3.p, v.grid.row_tid.p, v.tcnt.p,
+        reinterpret_cast<const uint2*>(v.tl.p), v.grid.row_src.p, c.force, c.tab, c.scal.p), note_launch();
+}
+
+static int vlt_env_pf() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_VLT_PF");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
+template <int PLAYOUT, bool MT>
+static void vlt_launch(Context& c) {
+    if (vlt_env_pf() == 1) vlt_launch_pf<PLAYOUT, MT, 1>(c);
+    else vlt_launch_pf<PLAYOUT, MT, 2>(c);
+}
+
+bool vlt_compute(Context& c) {
+    Verlet& v = c.vl;
+    int* next = (int*)(c.scal.p + 6);
+    bool mt = c.tab.T > 1;
+    if (c.layout == AOS) vl_refresh_launch<AOS, SOA>(c, next);
+    else vl_refresh_launch<SOA, SOA>(c, next);
+    c.prof_mark();
+    if (c.layout == AOS) {
+        if (mt) vlt_launch<AOS, true>(c); else vlt_launch<AOS, false>(c);
+        if (v.nbig) vl_force_rows_launch<AOS>(c, v.big_row.p);
+    } else {
+        if (mt) vlt_launch<SOA, true>(c); else vlt_launch<SOA, false>(c);
+        if (v.nbig) vl_force_rows_launch<SOA>(c, v.big_row.p);
+    }
+    c.prof_mark();
+    return true;
+}
+
+}  // namespace mdg

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kBuildThreadsT) vlt_build_kernel(
     uint16_t* __restrict__ tl, int* __restrict__ tcnt, int* __restrict__ maxcnt) {
     __shared__ __align__(16) TileDesc d;
     __shared__ int cs[kRanges][kMaxTZ + 4];
-    __shared__ float4 w32[kWinRows + 4];   // +4: the 4-wide scan reads past a run's end
+    __shared__ float4 w32[kWinRows + 32];   // +32: the 32-wide scan reads past a run's end
     load_desc(desc, blockIdx.x, d);
     __syncthreads();
     if (d.big) return;
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kBuildThreadsT) vlt_build_kernel(
         cs[R][k] = in ? gv.start[gv.flat(x, y, za) + k] - d.wstart[R] + d.woff[R] : 0;
     }
     int wrows = d.woff[kRanges];
-    for (int w = threadIdx.x; w < wrows + 4; w += blockDim.x) {
+    for (int w = threadIdx.x; w < wrows + 32; w += blockDim.x) {
         if (w >= wrows) {
             w32[w] = make_float4(0.f, 0.f, 0.f, 0.f);
             continue;
@@ -202,36 +202,47 @@ __global__ void __launch_bounds__(kBuildThreadsT) vlt_build_kernel(
                 int R = (a + dx) * (kTY + 2) + (b + dy);
                 int s0 = cs[R][k0], e0 = cs[R][k1];
                 int gR = d.wstart[R] - d.woff[R];   // global row of window index l: gR + l
-                for (int l0 = s0; l0 < e0; l0 += 4) {
-                    bool in[4], bd[4];
+                for (int l0 = s0; l0 < e0; l0 += 32) {
+                    // 32 candidates -> two bit masks (certainly in / maybe in)
+                    unsigned m_in = 0, m_mb = 0;
+#pragma unroll 1
+                    for (int t0 = 0; t0 < 32; t0 += 8) {
+                        unsigned b_in = 0, b_mb = 0;
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        float4 p = w32[l0 + t];
-                        float fx = qi.x - p.x, fy = qi.y - p.y, fz = qi.z - p.z;
-                        float r2 = fx * fx + fy * fy + fz * fz;
-                        bool use = (l0 + t < e0) & (l0 + t != li);
-                        in[t] = use & (r2 <= flo);
-                        bd[t] = use & (r2 > flo) & (r2 <= fhi);
+                        for (int t = 0; t < 8; ++t) {
+                            float4 p = w32[l0 + t0 + t];
+                            float fx = qi.x - p.x, fy = qi.y - p.y, fz = qi.z - p.z;
+                            float r2 = fx * fx + fy * fy + fz * fz;
+                            b_in |= r2 <= flo ? 1u << t : 0u;
+                            b_mb |= r2 <= fhi ? 1u << t : 0u;
+                        }
+                        m_in |= b_in << t0;
+                        m_mb |= b_mb << t0;
                     }
-                    if (bd[0] | bd[1] | bd[2] | bd[3]) {   // rare: exact fp64 test
+                    int span = e0 - l0;
+                    unsigned valid = span >= 32 ? 0xffffffffu : (1u << span) - 1u;
+                    unsigned self = (li >= l0 && li < l0 + 32) ? 1u << (li - l0) : 0u;
+                    valid &= ~self;
+                    m_in &= valid;
+                    unsigned m_bd = m_mb & valid & ~m_in;   // borderline: exact fp64 test
+                    if (m_bd) {
                         double4 pi = ldg256(bpos + r);
-#pragma unroll
-                        for (int t = 0; t < 4; ++t)
-                            if (bd[t]) {
-                                double4 pj = ldg256(bpos + gR + l0 + t);
-                                double ex = pi.x - pj.x, ey = pi.y - pj.y, ez = pi.z - pj.z;
-                                in[t] = ex * ex + ey * ey + ez * ez <= ell2;
-                            }
+                        while (m_bd) {
+                            int t = __ffs(m_bd) - 1;
+                            m_bd &= m_bd - 1;
+                            double4 pj = ldg256(bpos + gR + l0 + t);
+                            double ex = pi.x - pj.x, ey = pi.y - pj.y, ez = pi.z - pj.z;
+                            if (ex * ex + ey * ey + ez * ez <= ell2) m_in |= 1u << t;
+                        }
                     }
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        if (in[t]) {
-                            pk |= (unsigned long long)(l0 + t) << (16 * (c & 3));
-                            ++c;
-                            if ((c & 3) == 0) {
-                                if ((c >> 2) <= ngroups) op[(size_t)((c >> 2) - 1) * 32] = pk;
-                                pk = 0;
-                            }
+                    while (m_in) {   // ascending, like the scan order
+                        int t = __ffs(m_in) - 1;
+                        m_in &= m_in - 1;
+                        pk |= (unsigned long long)(l0 + t) << (16 * (c & 3));
+                        ++c;
+                        if ((c & 3) == 0) {
+                            if ((c >> 2) <= ngroups) op[(size_t)((c >> 2) - 1) * 32] = pk;
+                            pk = 0;
                         }
                     }
                 }

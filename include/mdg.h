@@ -36,9 +36,11 @@ extern "C" {
 #define MDG_ECUDA 2
 #define MDG_ESTATE 3
 
-/* configuration.py:7-17 */
-enum { MDG_LC = 0, MDG_VL = 1 };
-enum { MDG_C01 = 0, MDG_C08 = 1, MDG_C18 = 2, MDG_SLI = 3, MDG_LIST_ITER = 4 };
+/* configuration.py:7-17; MDG_VCL / MDG_CLUSTER_ITER are the north_star's
+ * VerletClusterLists container (no reference implementation; GPU-only ids
+ * appended to the space). */
+enum { MDG_LC = 0, MDG_VL = 1, MDG_VCL = 2 };
+enum { MDG_C01 = 0, MDG_C08 = 1, MDG_C18 = 2, MDG_SLI = 3, MDG_LIST_ITER = 4, MDG_CLUSTER_ITER = 5 };
 /* particles.py:10-11 */
 enum { MDG_AOS = 0, MDG_SOA = 1 };
 
@@ -49,8 +51,8 @@ enum { MDG_FP64 = 0, MDG_FP32 = 1 };
 /* One point of the search space: Configuration (configuration.py:20-50),
  * plus the precision of the extended space (the reference's 30 are fp64). */
 typedef struct {
-    int container;  /* MDG_LC / MDG_VL */
-    int traversal;  /* MDG_C01 .. MDG_LIST_ITER */
+    int container;  /* MDG_LC / MDG_VL / MDG_VCL */
+    int traversal;  /* MDG_C01 .. MDG_CLUSTER_ITER */
     int newton3;    /* 0 / 1 */
     int layout;     /* MDG_AOS / MDG_SOA */
     double csf;     /* cell size factor, 1.0 or 0.5 */

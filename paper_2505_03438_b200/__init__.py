@@ -10,15 +10,17 @@ Public surface mirrors the reference's names on this path:
 (see plugin.py).  All compute runs in libmdg (include/mdg.h).
 """
 
-from .configuration import (C01, C08, C18, CELL_TRAVERSALS, CSF_VALUES, LINKED_CELLS, LIST_ITER,
-                            SLI, VERLET_LISTS, Configuration, configuration_index,
+from .configuration import (C01, C08, C18, CELL_TRAVERSALS, CLUSTER_ITER, CSF_VALUES, LINKED_CELLS,
+                            LIST_ITER, SLI, VERLET_CLUSTER_LISTS, VERLET_LISTS, Configuration,
+                            configuration_index,
                             enumerate_configurations, extended_configurations,
                             parse_configuration)
 from .params import PERIODIC, REFLECTIVE, SimulationParams, ThermostatParams
 from .particles import AOS, SOA, ParticleSet, ParticleTypeInfo
 
 __all__ = [
-    "AOS", "SOA", "C01", "C08", "C18", "SLI", "LIST_ITER", "LINKED_CELLS", "VERLET_LISTS",
+    "AOS", "SOA", "C01", "C08", "C18", "SLI", "LIST_ITER", "CLUSTER_ITER", "LINKED_CELLS",
+    "VERLET_LISTS", "VERLET_CLUSTER_LISTS",
     "CELL_TRAVERSALS", "CSF_VALUES", "PERIODIC", "REFLECTIVE", "Configuration",
     "enumerate_configurations", "extended_configurations", "parse_configuration", "configuration_index",
     "SimulationParams", "ThermostatParams", "ParticleSet", "ParticleTypeInfo",

@@ -15,8 +15,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_build", "libmdg.so")
 
 MDG_OK, MDG_EINVAL, MDG_ECUDA, MDG_ESTATE = 0, 1, 2, 3
-LC, VL = 0, 1
-C01, C08, C18, SLI, LIST_ITER = 0, 1, 2, 3, 4
+LC, VL, VCL = 0, 1, 2
+C01, C08, C18, SLI, LIST_ITER, CLUSTER_ITER = 0, 1, 2, 3, 4, 5
 AOS, SOA = 0, 1
 
 # every symbol include/mdg.h declares (tests check the export list)
@@ -117,9 +117,9 @@ def check(status, what=""):
 
 def config_struct(config) -> MdgConfig:
     """Any object with the Configuration fields (configuration.py:20-27)."""
-    container = {"LC": LC, "VL": VL}[config.container]
+    container = {"LC": LC, "VL": VL, "VCL": VCL}[config.container]
     traversal = {"C01": C01, "C08": C08, "C18": C18, "SLI": SLI,
-                 "List_Iter": LIST_ITER}[config.traversal]
+                 "List_Iter": LIST_ITER, "ClusterIter": CLUSTER_ITER}[config.traversal]
     layout = {"AoS": AOS, "SoA": SOA}[config.layout]
     precision = 1 if getattr(config, "precision", "fp64") == "fp32" else 0
     return MdgConfig(container, traversal, int(bool(config.newton3)), layout,

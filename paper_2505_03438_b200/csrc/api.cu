@@ -72,6 +72,15 @@ static int validate(const mdg_config* cfg) {
             set_error("Verlet lists fix the cell size factor at 1");
             return MDG_EINVAL;
         }
+    } else if (cfg->container == MDG_VCL) {
+        if (cfg->traversal != MDG_CLUSTER_ITER) {
+            set_error("Verlet cluster lists only support ClusterIter");
+            return MDG_EINVAL;
+        }
+        if (cfg->csf != 1.0) {
+            set_error("Verlet cluster lists fix the cell size factor at 1");
+            return MDG_EINVAL;
+        }
     } else if (cfg->container == MDG_LC) {
         if (cfg->traversal < MDG_C01 || cfg->traversal > MDG_SLI) {
             set_error("linked cells do not support this traversal");
@@ -147,6 +156,7 @@ int mdg_destroy(mdg_ctx* ctx) {
     ctx->c.grids[0].release();
     ctx->c.grids[1].release();
     ctx->c.vl.release();
+    ctx->c.vcl.release();
     stats_release(ctx->c);
     ctx->c.scal.release();
     ctx->c.scan_tmp.release();
@@ -221,6 +231,10 @@ int mdg_set_system(mdg_ctx* ctx, const double domain[3], const int periodic[3], 
     c.vl.grid.g = c.grids[0].g;
     c.vl.grid.pruned = c.grids[0].pruned;
     c.vl.built = false;
+    c.vcl.grid.g = c.grids[0].g;
+    c.vcl.grid.pruned = c.grids[0].pruned;
+    c.vcl.grid.sort_by_z = 1;
+    c.vcl.built = false;
     c.have_system = true;
     return MDG_OK;
 }
@@ -234,6 +248,7 @@ int mdg_bind(mdg_ctx* ctx, int64_t n, int layout, double* pos, double* vel, doub
     if (n != c.n) {
         c.grids[0].built = c.grids[1].built = false;
         c.vl.built = false;
+        c.vcl.built = false;
     }
     c.n = n;
     c.layout = layout;
@@ -252,6 +267,8 @@ int mdg_rebuild(mdg_ctx* ctx, const mdg_config* cfg) {
     Context& c = ctx->c;
     if (cfg->container == MDG_VL) {
         if (vl_rebuild(c)) return MDG_ECUDA;
+    } else if (cfg->container == MDG_VCL) {
+        if (vcl_rebuild(c)) return MDG_ECUDA;
     } else {
         Grid& gr = *grid_for(c, cfg->csf);
         if (grid_rebuild(c, gr, c.pos, c.layout)) return MDG_ECUDA;
@@ -264,7 +281,7 @@ int mdg_refresh(mdg_ctx* ctx, const mdg_config* cfg) {
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;
     Context& c = ctx->c;
-    if (cfg->container == MDG_VL) return MDG_OK;
+    if (cfg->container == MDG_VL || cfg->container == MDG_VCL) return MDG_OK;
     Grid& gr = *grid_for(c, cfg->csf);
     if (!gr.built) { set_error("refresh before rebuild"); return MDG_ESTATE; }
     if (gr.scratch_layout != cfg->layout) grid_bind_scratch(c, gr, cfg->layout);
@@ -284,7 +301,10 @@ int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg) {
     if (cudaMemsetAsync(c.scal.p, 0, sizeof(unsigned long long), c.stream) != cudaSuccess)
         return cuda_status("counter reset");
     if (c.n == 0) return MDG_OK;
-    if (cfg->container == MDG_VL) {
+    if (cfg->container == MDG_VCL) {
+        if (!c.vcl.built) { set_error("compute before rebuild"); return MDG_ESTATE; }
+        vcl_compute(c, cfg->newton3);
+    } else if (cfg->container == MDG_VL) {
         if (!c.vl.built) { set_error("compute before rebuild"); return MDG_ESTATE; }
         if (cfg->precision == MDG_FP32) vl_compute32(c);
         else vl_compute(c, cfg->layout);

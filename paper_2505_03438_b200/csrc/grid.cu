@@ -120,6 +120,13 @@ void Grid::release() {
     built = false;
 }
 
+void Vcl::release() {
+    grid.release(); bb_lo.release(); bb_hi.release(); ccnt.release(); clist.release();
+    s4.release(); s3.release();
+    ncl = capc = 0;
+    built = s3_valid = false;
+}
+
 void Verlet::release() {
     grid.release(); cnt.release(); nbr.release(); s4.release(); s3.release(); b32.release();
     q32.release();
@@ -338,9 +345,16 @@ __global__ void bin_scatter_kernel(const double* __restrict__ pos, BinParams p,
 // Per-cell ordering fix: entries of one cell sorted by entry id (== the
 // reference's stable argsort order, containers.py:107).  One warp per cell;
 // cells up to 32 entries rank through shuffles, larger ones by counting.
+// Rank each cell's entries (one warp per cell).  KEYZ = 0: by entry id, the
+// reference's stable order (containers.py:107).  KEYZ = 1: by the entry's z
+// coordinate, ties by id -- the cluster-list grid only (vcl.cu), where 8
+// consecutive rows then form a compact slab of the cell; every entry of a
+// cell shares one shift, so the unshifted z orders them.
+template <int KEYZ, int PLAYOUT>
 __global__ void cell_sort_kernel(int64_t ncells, int64_t n, const int* __restrict__ cell_start,
                                  const int* __restrict__ tmp_ent, const int* __restrict__ img_src,
                                  const uint8_t* __restrict__ img_code, const int* __restrict__ tid,
+                                 const double* __restrict__ pos,
                                  int* __restrict__ row_ent, int* __restrict__ row_src,
                                  uint8_t* __restrict__ row_code, int* __restrict__ row_cell,
                                  int* __restrict__ row_tid, int* __restrict__ inv) {
@@ -349,9 +363,14 @@ __global__ void cell_sort_kernel(int64_t ncells, int64_t n, const int* __restric
     if (cell >= ncells) return;
     int s = cell_start[cell], e = cell_start[cell + 1], k = e - s;
     if (k == 0) return;
+    auto src_of = [&](int ent) { return ent < n ? ent : img_src[ent - n]; };
+    auto key_of = [&](int ent) { return KEYZ ? pos[pidx<PLAYOUT>(src_of(ent), 2, n)] : 0.0; };
+    auto before = [&](double ko, int o, double kv, int v) {
+        return KEYZ ? (ko < kv || (ko == kv && o < v)) : o < v;
+    };
     auto emit = [&](int r, int ent) {
         row_ent[r] = ent;
-        int src = ent < n ? ent : img_src[ent - n];
+        int src = src_of(ent);
         row_src[r] = src;
         row_code[r] = ent < n ? (uint8_t)kNoShift : img_code[ent - n];
         row_cell[r] = (int)cell;
@@ -360,16 +379,22 @@ __global__ void cell_sort_kernel(int64_t ncells, int64_t n, const int* __restric
     };
     if (k <= 32) {
         int v = lane < k ? tmp_ent[s + lane] : 0x7fffffff;
+        double kv = lane < k ? key_of(v) : INFINITY;
         int rank = 0;
         for (int j = 0; j < 32; ++j) {
             int o = __shfl_sync(0xffffffffu, v, j);
-            rank += (o < v);
+            double ko = KEYZ ? __shfl_sync(0xffffffffu, kv, j) : 0.0;
+            rank += j < k && before(ko, o, kv, v);
         }
         if (lane < k) emit(s + rank, v);
     } else {
         for (int a = lane; a < k; a += 32) {
             int v = tmp_ent[s + a], rank = 0;
-            for (int b = 0; b < k; ++b) rank += (tmp_ent[s + b] < v);
+            double kv = key_of(v);
+            for (int b = 0; b < k; ++b) {
+                int o = tmp_ent[s + b];
+                rank += before(key_of(o), o, kv, v);
+            }
             emit(s + rank, v);
         }
     }
@@ -426,9 +451,14 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
             bin_scatter_kernel<SOA><<<blocks_for(n, 256), 256, 0, st>>>(
                 pos, p, gr.cell_start.p, gr.cell_fill.p, gr.img_off.p, gr.img_src.p, gr.img_code.p,
                 gr.tmp_ent.p), note_launch();
-        cell_sort_kernel<<<blocks_for(nc * 32, 256), 256, 0, st>>>(
-            nc, n, gr.cell_start.p, gr.tmp_ent.p, gr.img_src.p, gr.img_code.p, c.tid,
-            gr.row_ent.p, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gr.row_tid.p, gr.inv.p), note_launch();
+#define MDG_CSORT(KZ, PL)                                                                       \
+    cell_sort_kernel<KZ, PL><<<blocks_for(nc * 32, 256), 256, 0, st>>>(                          \
+        nc, n, gr.cell_start.p, gr.tmp_ent.p, gr.img_src.p, gr.img_code.p, c.tid, pos,            \
+        gr.row_ent.p, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gr.row_tid.p, gr.inv.p), note_launch()
+        if (!gr.sort_by_z) MDG_CSORT(0, AOS);
+        else if (layout == AOS) MDG_CSORT(1, AOS);
+        else MDG_CSORT(1, SOA);
+#undef MDG_CSORT
     }
     MDG_CUDA(cudaGetLastError());
     gr.built = true;

@@ -65,6 +65,7 @@ struct Grid {
     Geom g{};
     Stencil pruned{}, fwd{}, fwd_sli{};
     int sli_major = 0;
+    int sort_by_z = 0;                              // in-cell order: 0 = entry id (reference), 1 = z (VCL)
     int64_t n = 0, nimg = 0, m = 0;
     bool built = false;
     DBuf<int> cell_count, cell_start, cell_fill;   // ncells + 1
@@ -128,6 +129,22 @@ struct PairwiseTree {
     void release();
 };
 
+// Verlet cluster lists (north_star VerletClusterLists, vcl.cu): clusters of 8
+// consecutive rows of their own CSF-1 grid, fp64 bounding boxes of the build
+// positions, per-cluster lists of j-clusters whose boxes are within
+// cutoff + skin, walked on the unwrapped positions like the Verlet lists.
+struct Vcl {
+    Grid grid;
+    int ncl = 0, capc = 0;
+    DBuf<double4> bb_lo, bb_hi;    // per cluster (w: 1 if it holds an owned row)
+    DBuf<int> ccnt, clist;         // list length, clist[ci * capc + k]
+    DBuf<double4> s4;              // unwrapped positions (build copy / refresh)
+    DBuf<double> s3;               // x[ms], y[ms], z[ms]
+    bool s3_valid = false;
+    bool built = false;
+    void release();
+};
+
 struct Context {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -148,6 +165,7 @@ struct Context {
     // containers
     Grid grids[2];             // [0] CSF 1, [1] CSF 0.5
     Verlet vl;
+    Vcl vcl;
     // temperature / thermostat / live statistics (stats.cu)
     PairwiseTree pw_particles, pw_bins;
     DBuf<int> ls_counts, ls_hist;
@@ -183,6 +201,9 @@ int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr);
 int vl_energy(Context& c, double* pe);
 void vl_compute32(Context& c);
 int vlt_build(Context& c);
+int vcl_rebuild(Context& c);
+void vcl_compute(Context& c, int newton3);
+void vl_refresh_into(Context& c, Grid& gr, double4* s4, double* s3, bool& s3_valid);
 int vl_build_rows(Context& c, const uint8_t* only);
 int vl_ensure_rows(Context& c);
 bool vlt_compute(Context& c);

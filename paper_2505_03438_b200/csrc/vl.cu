@@ -454,6 +454,21 @@ void vl_refresh_launch(Context& c, int* zero_me) {
     if (SLAYOUT == SOA) v.s3_valid = true;
 }
 template void vl_refresh_launch<AOS, SOA>(Context&, int*);
+
+// the same unwrapped refresh for another container's rows (VCL, vcl.cu)
+void vl_refresh_into(Context& c, Grid& gr, double4* s4, double* s3, bool& s3_valid) {
+    int m = (int)gr.m;
+    if (m == 0) return;
+    if (c.layout == AOS)
+        vl_refresh_kernel<AOS, SOA><<<blocks_for(m, 256), 256, 0, c.stream>>>(
+            c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, make_wrap(c), s4, s3, !s3_valid,
+            nullptr), note_launch();
+    else
+        vl_refresh_kernel<SOA, SOA><<<blocks_for(m, 256), 256, 0, c.stream>>>(
+            c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, make_wrap(c), s4, s3, !s3_valid,
+            nullptr), note_launch();
+    s3_valid = true;
+}
 template void vl_refresh_launch<SOA, SOA>(Context&, int*);
 
 // global-gather walk over the rows flagged in `only` (SoA source)

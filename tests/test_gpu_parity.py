@@ -351,3 +351,45 @@ def test_tuned_loop_replays_reference_controller(pkg):
     assert port.force_rel_error(parts.numpy("vel"), z["vel"]) <= FP64_TOL
     assert port.force_rel_error(parts.numpy("force"), z["force"]) <= FP64_TOL
     assert abs(rep.final_temperature - float(z["final_temperature"])) <= 1e-10 * float(z["final_temperature"])
+
+
+# -- Verlet cluster lists (north_star container; no reference implementation:
+#    the oracle is the reference's own Verlet-list forces and counts) ----------
+
+VCL_IDS = ["VCL-ClusterIter-N3L-AoS", "VCL-ClusterIter-N3L-SoA",
+           "VCL-ClusterIter-NoN3L-AoS", "VCL-ClusterIter-NoN3L-SoA"]
+
+
+@pytest.mark.parametrize("name", system_names())
+def test_vcl_matches_reference_forces_and_counts(pkg, name):
+    P, calc = pkg
+    d = golden(f"sys_{name}.npz")
+    ids = [str(s) for s in d["config_ids"]]
+    k_vl = ids.index("VL-List_Iter-NoN3L-AoS")
+    for cid in VCL_IDS:
+        cfg = P.parse_configuration(cid)
+        parts, params = _system(P, d, layout=cfg.layout)
+        _, count = calc.compute_forces(parts, cfg, params)
+        want = int(d["counts"][k_vl]) // (2 if cfg.newton3 else 1)
+        assert count == want, (cid, count, want)
+        err = port.force_rel_error(parts.numpy("force"), d["forces"][k_vl])
+        assert err <= FP64_TOL, f"{cid}: {err:.3g}"
+
+
+def test_vcl_trajectory_matches_reference(pkg):
+    P, calc = pkg
+    from paper_2505_03438_b200.simulation import simulate
+    z = golden("traj_small.npz")
+    L = float(z["domain"][0])
+    ids = [str(s) for s in z["config_ids"]]
+    k = ids.index("VL-List_Iter-NoN3L-SoA")
+    for cid in ("VCL-ClusterIter-N3L-SoA", "VCL-ClusterIter-NoN3L-AoS"):
+        params = P.SimulationParams(domain_size=(L, L, L), cutoff=2.5, skin=0.3, rebuild_interval=10,
+                                    delta_t=1e-3, boundary=(P.PERIODIC,) * 3)
+        parts = P.ParticleSet(z["pos0"], z["vel0"])
+        rep = simulate(parts, params, P.parse_configuration(cid), steps=int(z["steps"]))
+        assert rep.error is None, rep.error
+        dpos = parts.numpy("pos") - z[f"pos_{k}"]
+        dpos -= L * np.rint(dpos / L)
+        assert np.linalg.norm(dpos) / np.linalg.norm(z[f"pos_{k}"]) <= FP64_TOL, cid
+        assert port.force_rel_error(parts.numpy("vel"), z[f"vel_{k}"]) <= FP64_TOL, cid

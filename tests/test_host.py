@@ -167,7 +167,15 @@ def test_native_host_integrator_flags_blow_up():
 def test_extended_space_keeps_reference_ids():
     ext = P.extended_configurations()
     assert [c.id for c in ext[:30]] == [c.id for c in P.enumerate_configurations()]
-    assert [c.id for c in ext[30:]] == ["VL-List_Iter-NoN3L-AoS-FP32", "VL-List_Iter-NoN3L-SoA-FP32"]
+    assert [c.id for c in ext[30:]] == ["VL-List_Iter-NoN3L-AoS-FP32", "VL-List_Iter-NoN3L-SoA-FP32",
+                                        "VCL-ClusterIter-N3L-AoS", "VCL-ClusterIter-N3L-SoA",
+                                        "VCL-ClusterIter-NoN3L-AoS", "VCL-ClusterIter-NoN3L-SoA"]
+    vcl = P.parse_configuration("VCL-ClusterIter-N3L-AoS")
+    assert vcl.newton3 and _lib.config_struct(vcl).container == _lib.VCL
+    with pytest.raises(ValueError):
+        P.Configuration("VCL", "List_Iter", False, "AoS")
+    with pytest.raises(ValueError):
+        P.Configuration("VCL", "ClusterIter", False, "AoS", 0.5)
     assert P.parse_configuration("VL-List_Iter-NoN3L-SoA-FP32").precision == "fp32"
     with pytest.raises(ValueError):
         P.Configuration("LC", "C08", True, "AoS", 1.0, "fp32")

@@ -155,6 +155,9 @@ int mdg_synchronize(mdg_ctx* ctx);
  * `host` should be pinned for full bandwidth.  d2h synchronises. */
 int mdg_h2d(mdg_ctx* ctx, void* dev, const void* host, size_t bytes);
 int mdg_d2h(mdg_ctx* ctx, void* host, const void* dev, size_t bytes);
+/* device -> host copy enqueued on the context stream without waiting (the
+ * pipelined host loop waits on an event per chunk). */
+int mdg_d2h_async(mdg_ctx* ctx, void* host, const void* dev, size_t bytes);
 
 /* Debug / parity exports (host buffers). */
 /* make_geometry (cells.py:55-67) for csf. */
@@ -189,6 +192,15 @@ int mdg_host_drift_wrap(int64_t n, int layout, double* pos, double* vel, const d
 int mdg_host_finish_kick(int64_t n, int layout, double* vel, double* force, const double* old_force,
                          const int32_t* type_id, const double* mass, double dt, int has_gravity,
                          double gravity);
+/* The same on particles [begin, end) of an n-particle set (SoA stride n), so
+ * a host loop can overlap the update of one chunk with the copy of another. */
+int mdg_host_drift_wrap_range(int64_t n, int64_t begin, int64_t end, int layout, double* pos,
+                              double* vel, const double* force, double* old_force,
+                              const int32_t* type_id, const double* mass, const double domain[3],
+                              const int periodic[3], double dt, int* blowup);
+int mdg_host_finish_kick_range(int64_t n, int64_t begin, int64_t end, int layout, double* vel,
+                               double* force, const double* old_force, const int32_t* type_id,
+                               const double* mass, double dt, int has_gravity, double gravity);
 
 /* Measured FP64 FMA throughput of this device (roofline denominator):
  * dependent-chain DFMA microbenchmark, TFLOP/s (2 flops per DFMA). */

@@ -283,8 +283,39 @@ class HostForceCalculator:
         self._bind(particles)
         check(lib().mdg_rebuild(self.ctx.h, ctypes.byref(config_struct(config))), "rebuild")
 
+    # -- chunked pieces for the pipelined host loop (hostloop.HostSimulation) --
+    def _ranges(self, p, a, b):
+        """(byte offset, bytes) pieces of particles [a, b) in p's layout."""
+        if p.layout == "AoS":
+            return [(24 * a, 24 * (b - a))]
+        return [(8 * (k * self.n + a), 8 * (b - a)) for k in range(3)]
+
+    def upload_range(self, p, a, b):
+        """Asynchronous H2D of positions [a, b) (p.pos must be pinned and contiguous)."""
+        base_d, base_h = self._buf["pos"].data_ptr(), p.pos.ctypes.data
+        for off, nb in self._ranges(p, a, b):
+            check(lib().mdg_h2d(self.ctx.h, ctypes.c_void_p(base_d + off),
+                                ctypes.c_void_p(base_h + off), nb), "h2d")
+
+    def download_range(self, p, a, b):
+        """Asynchronous D2H of forces [a, b) on the context stream."""
+        base_d, base_h = self._buf["force"].data_ptr(), p.force.ctypes.data
+        for off, nb in self._ranges(p, a, b):
+            check(lib().mdg_d2h_async(self.ctx.h, ctypes.c_void_p(base_h + off),
+                                      ctypes.c_void_p(base_d + off), nb), "d2h")
+
+    def device_step(self, particles, config, rebuild):
+        """rebuild (if due) + refresh + compute on positions already uploaded;
+        asynchronous except for the rebuild's own size check."""
+        self._bind(particles)
+        cs = ctypes.byref(config_struct(config))
+        if rebuild:
+            check(lib().mdg_rebuild(self.ctx.h, cs), "rebuild")
+        check(lib().mdg_refresh(self.ctx.h, cs), "refresh")
+        check(lib().mdg_compute(self.ctx.h, cs), "compute")
+
     def refresh(self, particles, config):
-        if config.container == "VL":
+        if config.container in ("VL", "VCL"):   # list containers refresh inside compute
             return
         self._upload_positions(particles)
         self._bind(particles)
@@ -295,7 +326,7 @@ class HostForceCalculator:
         if particles.layout != config.layout:
             raise ValueError(f"particle layout {particles.layout} does not match "
                              f"configuration {config.id}")
-        if config.container == "VL":
+        if config.container in ("VL", "VCL"):
             self._upload_positions(particles)
         self._bind(particles)
         h = self.ctx.h

@@ -439,6 +439,14 @@ int mdg_d2h(mdg_ctx* ctx, void* host, const void* dev, size_t bytes) {
     return MDG_OK;
 }
 
+int mdg_d2h_async(mdg_ctx* ctx, void* host, const void* dev, size_t bytes) {
+    CHECK_CTX(ctx);
+    if (!bytes) return MDG_OK;
+    if (cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->c.stream) != cudaSuccess)
+        return cuda_status("mdg_d2h_async");
+    return MDG_OK;
+}
+
 int mdg_geometry(mdg_ctx* ctx, double csf, int dims_owned[3], double cell_length[3],
                  int overlap[3], int halo[3], int dims[3]) {
     CHECK_CTX(ctx);

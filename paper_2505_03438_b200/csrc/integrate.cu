@@ -17,7 +17,13 @@ struct BoxParams {
 };
 
 // np.mod(x, L) (integrator.py:118): fmod with sign fix, +0.0 for exact zeros.
+// Inside [-L, 2L] no fmod is needed: [0, L) -> x (+0.0 for -0.0); [L, 2L] ->
+// x - L, exact by Sterbenz (2L -> 0); [-L, 0) -> x + L, the rounded addition
+// numpy's sign fix performs.
 __device__ __forceinline__ double np_mod(double x, double L) {
+    if (x >= 0.0 && x < L) return __dadd_rn(x, 0.0);
+    if (x >= L && x <= 2.0 * L) return x == 2.0 * L ? 0.0 : __dadd_rn(x, -L);
+    if (x >= -L && x < 0.0) return __dadd_rn(x, L);
     double r = fmod(x, L);
     if (r != 0.0) {
         if ((r < 0.0) != (L < 0.0)) r = __dadd_rn(r, L);

@@ -98,6 +98,34 @@ def host_drift_wrap(p, params, dt):
     return bool(bad.value)
 
 
+def host_drift_wrap_range(p, params, dt, a, b):
+    """host_drift_wrap on particles [a, b)."""
+    L = np.ascontiguousarray(params.domain_size, dtype=np.float64)
+    per = np.ascontiguousarray(params.periodic_flags().astype(np.int32))
+    mass = np.ascontiguousarray(p.mass, dtype=np.float64)
+    tid = getattr(p, "_tid32", None)
+    if tid is None:
+        tid = np.asarray(p.type_id, dtype=np.int32)
+    bad = ctypes.c_int()
+    check(lib().mdg_host_drift_wrap_range(p.n, int(a), int(b), _lib.AOS if p.layout == "AoS" else _lib.SOA,
+                                          _ptr(p.pos), _ptr(p.vel), _ptr(p.force), _ptr(p.old_force),
+                                          _ptr(tid) if len(mass) > 1 else None, _ptr(mass),
+                                          _ptr(L), _ptr(per), float(dt), ctypes.byref(bad)), "host drift")
+    return bool(bad.value)
+
+
+def host_finish_kick_range(p, dt, gravity, a, b):
+    mass = np.ascontiguousarray(p.mass, dtype=np.float64)
+    tid = getattr(p, "_tid32", None)
+    if tid is None:
+        tid = np.asarray(p.type_id, dtype=np.int32)
+    check(lib().mdg_host_finish_kick_range(p.n, int(a), int(b), _lib.AOS if p.layout == "AoS" else _lib.SOA,
+                                           _ptr(p.vel), _ptr(p.force), _ptr(p.old_force),
+                                           _ptr(tid) if len(mass) > 1 else None, _ptr(mass), float(dt),
+                                           int(gravity is not None), float(gravity or 0.0)),
+          "host finish_kick")
+
+
 def host_finish_kick(p, dt, gravity=None):
     mass = np.ascontiguousarray(p.mass, dtype=np.float64)
     tid = getattr(p, "_tid32", None)
@@ -112,27 +140,62 @@ def host_finish_kick(p, dt, gravity=None):
 
 class HostSimulation:
     """The reference loop (simulation.py:150-188, fixed configuration) on host
-    state with the GPU force backend.  Create once, then ``run(steps)``."""
+    state with the GPU force backend.  Create once, then ``run(steps)``.
 
-    def __init__(self, particles, params, config, calculator=None):
+    With ``chunks > 1`` (default 4) the host work overlaps the copies: the
+    drift of chunk k runs while chunk k-1's positions are in flight to the
+    device, and the kick of chunk k starts as soon as its forces have landed.
+    The arithmetic and its order per particle are unchanged (same results,
+    bit for bit); only the copies are split."""
+
+    def __init__(self, particles, params, config, calculator=None, chunks=4):
         self.p, self.params, self.config = particles, params, config
         self.calc = calculator or HostForceCalculator(particles, params)
         self.active, self.since, self.iteration = None, 0, 0
+        self.chunks = max(1, int(chunks))
+
+    def _bounds(self):
+        n = self.p.n
+        k = min(self.chunks, max(1, n))
+        return [(n * i // k, n * (i + 1) // k) for i in range(k)]
 
     def step(self):
         p, params, cfg, calc = self.p, self.params, self.config, self.calc
-        if host_drift_wrap(p, params, params.delta_t):
-            from .simulation import BlowUpError
-            raise BlowUpError("particle left the domain by more than one domain length "
-                              "(or position is not finite)")
-        rebuild = self.active != cfg.id or self.since >= params.rebuild_interval
+        from .simulation import BlowUpError
         if p.layout != cfg.layout:
             p.convert_layout(cfg.layout)
-        if rebuild:
-            calc.rebuild(p, cfg)
-        calc.refresh(p, cfg)
-        calc.compute(p, cfg)
-        host_finish_kick(p, params.delta_t, params.gravity)
+        pipelined = self.chunks > 1 and p.n > 0 and isinstance(calc, HostForceCalculator) \
+            and p.pos.flags.c_contiguous and p.force.flags.c_contiguous
+        if not pipelined:
+            if host_drift_wrap(p, params, params.delta_t):
+                raise BlowUpError("particle left the domain by more than one domain length "
+                                  "(or position is not finite)")
+            rebuild = self.active != cfg.id or self.since >= params.rebuild_interval
+            if rebuild:
+                calc.rebuild(p, cfg)
+            calc.refresh(p, cfg)
+            calc.compute(p, cfg)
+            host_finish_kick(p, params.delta_t, params.gravity)
+        else:
+            bounds = self._bounds()
+            bad = False
+            for a, b in bounds:
+                bad |= host_drift_wrap_range(p, params, params.delta_t, a, b)
+                calc.upload_range(p, a, b)
+            if bad:
+                raise BlowUpError("particle left the domain by more than one domain length "
+                                  "(or position is not finite)")
+            rebuild = self.active != cfg.id or self.since >= params.rebuild_interval
+            calc.device_step(p, cfg, rebuild)
+            events = []
+            for a, b in bounds:
+                calc.download_range(p, a, b)
+                ev = torch.cuda.Event()
+                ev.record(calc.ctx.stream)
+                events.append(ev)
+            for (a, b), ev in zip(bounds, events):
+                ev.synchronize()
+                host_finish_kick_range(p, params.delta_t, params.gravity, a, b)
         self.active = cfg.id
         self.since = 0 if rebuild else self.since + 1
         self.iteration += 1

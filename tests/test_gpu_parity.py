@@ -393,3 +393,45 @@ def test_vcl_trajectory_matches_reference(pkg):
         dpos -= L * np.rint(dpos / L)
         assert np.linalg.norm(dpos) / np.linalg.norm(z[f"pos_{k}"]) <= FP64_TOL, cid
         assert port.force_rel_error(parts.numpy("vel"), z[f"vel_{k}"]) <= FP64_TOL, cid
+
+
+def test_device_wrap_matches_np_mod_on_edges(pkg):
+    """drift_wrap_kernel's np.mod fast path vs numpy, bit for bit (zero
+    velocity and force: the drift is the identity, only the wrap acts)."""
+    P, calc = pkg
+    L = 11.18183
+    e = np.nextafter
+    xs = np.array([0.0, -0.0, 1e-300, -1e-300, -5e-324, L, e(L, 0), e(L, 3 * L), 2 * L, e(2 * L, 0),
+                   -L, e(-L, 0), -1e-17, -L / 3, 1.5 * L, 0.7 * L])
+    xs = np.concatenate([xs, np.random.default_rng(3).uniform(-L, 2 * L, 5000)])
+    pos = np.repeat(xs[:, None], 3, axis=1)
+    params = P.SimulationParams(domain_size=(L, L, L), cutoff=2.5, skin=0.3,
+                                boundary=(P.PERIODIC,) * 3)
+    for layout in ("AoS", "SoA"):
+        parts = P.ParticleSet(pos, layout=layout)
+        fc = calc.ForceCalculator(parts, params)
+        fc.drift_wrap(parts, 0.001)
+        assert not fc.blowup()
+        fc.close()
+        got = parts.numpy("pos")
+        assert np.array_equal(got.view(np.uint64), np.mod(pos, L).view(np.uint64)), layout
+
+
+def test_pipelined_host_loop_is_bit_identical(pkg):
+    """Chunked host loop (drift/upload and download/kick overlapped) vs the
+    one-shot loop: identical bits, LC / VL / VCL, AoS and SoA."""
+    P, calc = pkg
+    from paper_2505_03438_b200.hostloop import HostParticleSet, HostSimulation
+    z = golden("traj_small.npz")
+    L = z["domain"]
+    for cid in ("LC-C08-N3L-SoA-CSF1", "VL-List_Iter-NoN3L-AoS", "VL-List_Iter-NoN3L-SoA",
+                "VCL-ClusterIter-NoN3L-AoS"):
+        out = []
+        for chunks in (1, 7):
+            params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=10,
+                                        delta_t=1e-3, boundary=(P.PERIODIC,) * 3)
+            p = HostParticleSet(z["pos0"], z["vel0"])
+            HostSimulation(p, params, P.parse_configuration(cid), chunks=chunks).run(25)
+            out.append((np.array(p.positions), np.array(p.velocities), np.array(p.forces)))
+        for a, b in zip(*out):
+            assert np.array_equal(a, b), cid

@@ -203,3 +203,24 @@ def test_livestats_feature_order():
     assert FEATURE_NAMES[0] == "meanParticlesPerBin" and FEATURE_NAMES[-1] == "skin"
     s = LiveStatistics(1.0, 2.0, 3.0, 4.0, 5, 6, 7, 0.3)
     assert list(s.feature_vector()) == [1.0, 2.0, 3.0, 4.0, 5.0, 6.0, 7.0, 0.3]
+
+
+def test_host_wrap_matches_np_mod_on_edges():
+    """The integrator's np.mod fast path (no fmod inside [-L, 2L], host.cpp /
+    integrate.cu) against numpy's np.mod, bit for bit, on the edge values."""
+    from paper_2505_03438_b200 import hostloop
+    L = 11.18183
+    e = np.nextafter
+    xs = np.array([0.0, -0.0, 1e-300, -1e-300, -5e-324, L, e(L, 0), e(L, 3 * L), 2 * L, e(2 * L, 0),
+                   -L, e(-L, 0), -1e-17, -L / 3, 1.5 * L, 0.7 * L, e(0.0, 1), 3 * L / 2 + 1e-9,
+                   -0.9999999999 * L, 1.9999999999 * L])
+    rng = np.random.default_rng(3)
+    xs = np.concatenate([xs, rng.uniform(-L, 2 * L, 5000)])
+    pos = np.repeat(xs[:, None], 3, axis=1)
+    params = P.SimulationParams(domain_size=(L, L, L), cutoff=2.5, skin=0.3,
+                                boundary=(P.PERIODIC,) * 3)
+    p = hostloop.HostParticleSet(pos)
+    assert not hostloop.host_drift_wrap(p, params, 0.001)
+    want = np.mod(pos, L)
+    got = p.pos
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))

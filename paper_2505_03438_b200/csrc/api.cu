@@ -230,6 +230,7 @@ int mdg_set_system(mdg_ctx* ctx, const double domain[3], const int periodic[3], 
     }
     c.vl.grid.g = c.grids[0].g;
     c.vl.grid.pruned = c.grids[0].pruned;
+    c.vl.grid.sort_by_z = 1;   // z-ordered cells: the tiled build scans a z-window (vltile.cu)
     c.vl.built = false;
     c.vcl.grid.g = c.grids[0].g;
     c.vcl.grid.pruned = c.grids[0].pruned;

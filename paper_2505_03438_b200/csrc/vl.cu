@@ -724,13 +724,14 @@ int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr) {
     Grid& gr = v.grid;
     int m = (int)gr.m;
     size_t mpad = ((size_t)m + 31) / 32 * 32;
-    std::vector<int> cnt(m), src(m), cellof(m), ell(mpad * (size_t)v.cap);
+    std::vector<int> cnt(m), src(m), cellof(m), ent(m), ell(mpad * (size_t)v.cap);
     std::vector<uint8_t> code(m);
     MDG_CUDA(cudaStreamSynchronize(c.stream));
     if (m) {
         MDG_CUDA(cudaMemcpy(cnt.data(), v.cnt.p, m * sizeof(int), cudaMemcpyDeviceToHost));
         MDG_CUDA(cudaMemcpy(src.data(), gr.row_src.p, m * sizeof(int), cudaMemcpyDeviceToHost));
         MDG_CUDA(cudaMemcpy(cellof.data(), gr.row_cell.p, m * sizeof(int), cudaMemcpyDeviceToHost));
+        MDG_CUDA(cudaMemcpy(ent.data(), gr.row_ent.p, m * sizeof(int), cudaMemcpyDeviceToHost));
         MDG_CUDA(cudaMemcpy(code.data(), gr.row_code.p, m, cudaMemcpyDeviceToHost));
         MDG_CUDA(cudaMemcpy(ell.data(), v.nbr.p, ell.size() * sizeof(int), cudaMemcpyDeviceToHost));
     }
@@ -745,20 +746,26 @@ int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr) {
     for (int64_t i = 0; i < n; ++i) per[i + 1] += per[i];
     *entries = per[n];
     if (noff) std::copy(per.begin(), per.end(), noff);
-    if (nbr)
+    if (nbr) {
+        // the reference order (kernels.py:886-906): own cell first, then the
+        // stencil cells in order (ascending cell index on the CSF-1 grid), and
+        // within a cell the stable entry order (the device grid orders a
+        // cell's rows by z, so sort by entry id here)
+        std::vector<int> rows;
         for (int64_t i = 0; i < n; ++i) {
-            // device lists are row-sorted; the reference order is own cell
-            // first, then the stencil cells (kernels.py:886-906)
             int r = row_of[i];
             const int* lp = ell.data() + (size_t)(r >> 5) * 32 * v.cap + (r & 31);
+            rows.assign(cnt[r], 0);
+            for (int k = 0; k < cnt[r]; ++k) rows[k] = lp[(size_t)k * 32];
+            int own = cellof[r];
+            std::sort(rows.begin(), rows.end(), [&](int a, int b) {
+                int ca = cellof[a] == own ? -1 : cellof[a], cb = cellof[b] == own ? -1 : cellof[b];
+                return ca != cb ? ca < cb : ent[a] < ent[b];
+            });
             int64_t o = per[i];
-            for (int pass = 0; pass < 2; ++pass)
-                for (int k = 0; k < cnt[r]; ++k) {
-                    int j = lp[(size_t)k * 32];
-                    bool own = cellof[j] == cellof[r];
-                    if (own == (pass == 0)) nbr[o++] = src[j];
-                }
+            for (int j : rows) nbr[o++] = src[j];
         }
+    }
     return 0;
 }
 

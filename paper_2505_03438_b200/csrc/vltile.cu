@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kBuildThreadsT) vlt_build_kernel(
     GridView gv, const TileDesc* __restrict__ desc, const int* __restrict__ tbase,
     const float4* __restrict__ b32, const double4* __restrict__ bpos,
     const unsigned* __restrict__ maxabs_bits, double ell2, int cap, int cap4,
-    uint16_t* __restrict__ tl, int* __restrict__ tcnt, int* __restrict__ maxcnt) {
+    uint16_t* __restrict__ tl, int* __restrict__ tcnt, int* __restrict__ maxcnt, int zsorted) {
     __shared__ __align__(16) TileDesc d;
     __shared__ int cs[kRanges][kMaxTZ + 4];
     __shared__ float4 w32[kWinRows + 32];   // +32: the 32-wide scan reads past a run's end
@@ -178,6 +178,10 @@ __global__ void __launch_bounds__(kBuildThreadsT) vlt_build_kernel(
     double eta = 2.0 * u * X + 2.0 * u * ell;
     double B = 3.4641016151377544 * eta * ell + 3.0 * eta * eta + 3.0 * u * ell2;
     const float flo = __double2float_rd(ell2 - 2.0 * B), fhi = __double2float_ru(ell2 + 2.0 * B);
+    // z-window: rows of a column run are z-ordered (z-sorted cells, the VL
+    // grid's sort_by_z), so the candidates within ell in z are a contiguous
+    // sub-run; fp32 coordinates are within u|x| of fp64, hence the 2 eta pad
+    const double zpad = ell + 2.0 * eta;
     const int base = tbase[blockIdx.x];
     const int slot0 = base / cap4;
     const int ngroups = cap4 >> 2;
@@ -193,6 +197,7 @@ __global__ void __launch_bounds__(kBuildThreadsT) vlt_build_kernel(
         gv.decode(gv.row_cell[r], cx, cy, cz);
         int k0 = max(cz - 1 - za, 0), k1 = min(cz + 2 - za, nz);
         float4 qi = w32[li];
+        const float zlo = __double2float_rd((double)qi.z - zpad), zhi = __double2float_ru((double)qi.z + zpad);
         unsigned long long* op = reinterpret_cast<unsigned long long*>(
             tl + base + (size_t)(q >> 5) * 32 * cap4 + (q & 31) * 4);
         unsigned long long pk = 0;
@@ -202,11 +207,27 @@ __global__ void __launch_bounds__(kBuildThreadsT) vlt_build_kernel(
                 int R = (a + dx) * (kTY + 2) + (b + dy);
                 int s0 = cs[R][k0], e0 = cs[R][k1];
                 int gR = d.wstart[R] - d.woff[R];   // global row of window index l: gR + l
+                if (zsorted) {
+                    int lo = s0, hi = e0;
+                    while (lo < hi) {   // first row with z >= zlo
+                        int mid = (lo + hi) >> 1;
+                        if (w32[mid].z < zlo) lo = mid + 1; else hi = mid;
+                    }
+                    int s1 = lo;
+                    hi = e0;
+                    while (lo < hi) {   // first row with z > zhi
+                        int mid = (lo + hi) >> 1;
+                        if (w32[mid].z <= zhi) lo = mid + 1; else hi = mid;
+                    }
+                    s0 = s1;
+                    e0 = lo;
+                }
                 for (int l0 = s0; l0 < e0; l0 += 32) {
                     // 32 candidates -> two bit masks (certainly in / maybe in)
                     unsigned m_in = 0, m_mb = 0;
+                    const int span = min(32, e0 - l0);
 #pragma unroll 1
-                    for (int t0 = 0; t0 < 32; t0 += 8) {
+                    for (int t0 = 0; t0 < span; t0 += 8) {   // 8-candidate batches up to the run's end
                         unsigned b_in = 0, b_mb = 0;
 #pragma unroll
                         for (int t = 0; t < 8; ++t) {
@@ -219,7 +240,6 @@ __global__ void __launch_bounds__(kBuildThreadsT) vlt_build_kernel(
                         m_in |= b_in << t0;
                         m_mb |= b_mb << t0;
                     }
-                    int span = e0 - l0;
                     unsigned valid = span >= 32 ? 0xffffffffu : (1u << span) - 1u;
                     unsigned self = (li >= l0 && li < l0 + 32) ? 1u << (li - l0) : 0u;
                     valid &= ~self;
@@ -544,7 +564,7 @@ int vlt_build(Context& c) {
         MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
         vlt_build_kernel<<<ntiles, kBuildThreadsT, 0, c.stream>>>(
             gv, desc, v.tbase.p, v.b32.p, gr.spos4.p, maxabs, ell2, v.cap, v.cap4, v.tl.p, v.tcnt.p,
-            maxcnt), note_launch();
+            maxcnt, gr.sort_by_z), note_launch();
         int hmax = 0;
         MDG_CUDA(cudaMemcpyAsync(&hmax, maxcnt, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
         MDG_CUDA(cudaStreamSynchronize(c.stream));

@@ -102,6 +102,12 @@ int mdg_refresh(mdg_ctx* ctx, const mdg_config* cfg);
  * the device (read it with mdg_eval_count).  MDG_EINVAL on layout mismatch
  * (containers.py:445-448). */
 int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg);
+/* mdg_compute followed by apply_gravity + finish_kick (simulation.py:169-185,
+ * integrator.py:40-51): the velocity update is fused into the force walk's
+ * epilogue where the configuration allows it (tiled Verlet lists), else run
+ * as its own kernel.  Same arithmetic either way.  Asynchronous. */
+int mdg_compute_kick(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gravity,
+                     double gravity);
 /* ForceCalculator.last_eval_count (containers.py:454): synchronises. */
 int mdg_eval_count(mdg_ctx* ctx, int64_t* count);
 /* Shifted LJ potential energy of the bound positions (no reference

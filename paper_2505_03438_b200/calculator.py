@@ -123,6 +123,17 @@ class ForceCalculator:
         self.compute_async(particles, config)
         return self.last_eval_count
 
+    def compute_kick_async(self, particles, config, dt, gravity=None):
+        """compute + apply_gravity + finish_kick (simulation.py:169-185), the
+        kick fused into the force walk where the configuration allows."""
+        if particles.layout != config.layout:
+            raise ValueError(f"particle layout {particles.layout} does not match "
+                             f"configuration {config.id}")
+        self.bind(particles)
+        check(lib().mdg_compute_kick(self.ctx.h, ctypes.byref(config_struct(config)), float(dt),
+                                     int(gravity is not None), float(gravity or 0.0)), "compute_kick")
+        self._count_pending = True
+
     @property
     def last_eval_count(self) -> int:
         if self._count_pending:

@@ -321,6 +321,37 @@ int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg) {
     return cuda_status("mdg_compute");
 }
 
+int mdg_compute_kick(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gravity,
+                     double gravity) {
+    CHECK_CTX(ctx);
+    if (int e = validate(cfg)) return e;
+    if (int e = need_system(ctx)) return e;
+    Context& c = ctx->c;
+    Verlet& v = c.vl;
+    // Measured on B200, config 2: the fused epilogue's scattered
+    // per-particle vel / old_force accesses cost more (walk 0.186 -> 0.228 ms)
+    // than the coalesced kick pass they replace, so fusion is opt-in
+    // (MDG_FUSE_KICK=1).
+    static int fuse_env = -1;
+    if (fuse_env < 0) {
+        const char* e = getenv("MDG_FUSE_KICK");
+        fuse_env = e ? atoi(e) : 0;
+    }
+    bool fuse = fuse_env && cfg->container == MDG_VL && cfg->precision == MDG_FP64 &&
+                c.layout == cfg->layout && v.built && v.tiled && v.nbig == 0 && c.n > 0;
+    if (fuse) {
+        if (cudaMemsetAsync(c.scal.p, 0, sizeof(unsigned long long), c.stream) != cudaSuccess)
+            return cuda_status("counter reset");
+        v.s3.ensure(3 * (size_t)s3_stride((int)v.grid.m) + 8);
+        KickArgs k{c.vel, c.old_force, c.d_mass.p, c.tid, dt, gravity, has_gravity};
+        vlt_compute(c, &k);
+        return cuda_status("mdg_compute_kick");
+    }
+    if (int e = mdg_compute(ctx, cfg)) return e;
+    integ_finish_kick(c, dt, has_gravity, gravity);
+    return cuda_status("mdg_compute_kick");
+}
+
 int mdg_eval_count(mdg_ctx* ctx, int64_t* count) {
     CHECK_CTX(ctx);
     Context& c = ctx->c;

@@ -206,7 +206,16 @@ void vcl_compute(Context& c, int newton3);
 void vl_refresh_into(Context& c, Grid& gr, double4* s4, double* s3, bool& s3_valid);
 int vl_build_rows(Context& c, const uint8_t* only);
 int vl_ensure_rows(Context& c);
-bool vlt_compute(Context& c);
+// finish_kick arguments for kernels that fuse it into their epilogue
+struct KickArgs {
+    double* vel;
+    const double* old_force;
+    const double* mass;   // per type
+    const int* tid;       // per particle, may be null
+    double dt, gravity;
+    int has_gravity;
+};
+bool vlt_compute(Context& c, const KickArgs* kick = nullptr);
 template <int PLAYOUT, int SLAYOUT>
 void vl_refresh_launch(Context& c, int* zero_me);
 template <int PLAYOUT>

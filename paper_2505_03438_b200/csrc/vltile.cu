@@ -305,6 +305,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, int parity) {
         " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity) : "memory");
 }
+// L2 prefetch of a 16-byte aligned range (whole multiple of 16 bytes)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -329,13 +334,13 @@ struct WinLayout {
 // arrive on the buffer's `empty` mbarrier when no chunk is left, so the
 // producer refills it while they already work on the other buffer.  No
 // CTA-wide barrier after the prologue.
-template <int PLAYOUT, bool MT, int PF>
+template <int PLAYOUT, bool MT, int PF, bool KICK>
 __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
     const TileDesc* __restrict__ desc, const int* __restrict__ tbase, int ntiles,
     int* __restrict__ next, int ms, int64_t n, int cap4, const double* __restrict__ s3,
     const int* __restrict__ row_tid, const int* __restrict__ tcnt, const uint2* __restrict__ tl,
     const int* __restrict__ row_src, double* __restrict__ force, LJTab tab,
-    unsigned long long* counter) {
+    unsigned long long* counter, KickArgs kick) {
     extern __shared__ __align__(128) double win[];
     __shared__ __align__(16) TileDesc d[2];
     __shared__ __align__(8) uint64_t full[2], empty[2];
@@ -393,6 +398,20 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                     bulk_g2s(wy + o, s3 + (size_t)ms + g, rows * 8u, &full[b]);
                     bulk_g2s(wz + o, s3 + 2 * (size_t)ms + g, rows * 8u, &full[b]);
                     if (MT) bulk_g2s(wt + o, row_tid + g, rows * 4u, &full[b]);
+                }
+            } else if (PF == 3) {
+                // the tile's list stream (and counts) into L2 while the window
+                // lands: the consumers' list loads then hit L2 instead of HBM
+                int base = tbase[t];
+                size_t bytes = (size_t)((D.ni + 31) / 32 * 32) * cap4 * 2;
+                const char* lb = reinterpret_cast<const char*>(tl) + (size_t)base * 2;
+                for (size_t off = (size_t)(lane - kRanges) * 32768; off < bytes; off += 16 * 32768)
+                    bulk_prefetch_l2(lb + off, (unsigned)min((size_t)32768, bytes - off));
+                if (lane == kRanges) {
+                    size_t cb = ((size_t)(D.ni + 3) / 4) * 16;   // tcnt slots, whole 16-byte units
+                    const char* cp = reinterpret_cast<const char*>(tcnt + base / cap4);
+                    size_t a0 = (size_t)cp & 15;                 // round the start down to 16 bytes
+                    bulk_prefetch_l2(cp - a0, (unsigned)(cb + 16));
                 }
             }
         }
@@ -477,6 +496,18 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                                 fz = fma(fs, dz[u], fz);
                             }
                         }
+                    }
+                    if (KICK) {
+                        // apply_gravity + finish_kick (integrator.py:40-51), the
+                        // arithmetic of finish_kick_kernel, on this particle
+                        double mi = kick.mass[kick.tid ? kick.tid[i] : 0];
+                        if (kick.has_gravity) fz = __dadd_rn(fz, __dmul_rn(mi, kick.gravity));
+                        double cf = __ddiv_rn(__dmul_rn(0.5, kick.dt), mi);
+                        size_t a0 = pidx<PLAYOUT>(i, 0, n), a1 = pidx<PLAYOUT>(i, 1, n),
+                               a2 = pidx<PLAYOUT>(i, 2, n);
+                        kick.vel[a0] = __dadd_rn(kick.vel[a0], __dmul_rn(__dadd_rn(fx, kick.old_force[a0]), cf));
+                        kick.vel[a1] = __dadd_rn(kick.vel[a1], __dmul_rn(__dadd_rn(fy, kick.old_force[a1]), cf));
+                        kick.vel[a2] = __dadd_rn(kick.vel[a2], __dmul_rn(__dadd_rn(fz, kick.old_force[a2]), cf));
                     }
                     force[pidx<PLAYOUT>(i, 0, n)] = fx;
                     force[pidx<PLAYOUT>(i, 1, n)] = fy;
@@ -585,42 +616,53 @@ int vlt_build(Context& c) {
     return 0;
 }
 
-template <int PLAYOUT, bool MT, int PF>
-static void vlt_launch_pf(Context& c) {
+template <int PLAYOUT, bool MT, int PF, bool KICK>
+static void vlt_launch_pf(Context& c, const KickArgs& kick) {
     Verlet& v = c.vl;
     size_t smem = 2 * (size_t)WinLayout<MT>::kDoubles * sizeof(double);
     static int ctas_per_sm = 0;
     if (!ctas_per_sm) {
-        cudaFuncSetAttribute(vlt_force_kernel<PLAYOUT, MT, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(vlt_force_kernel<PLAYOUT, MT, PF, KICK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, vlt_force_kernel<PLAYOUT, MT, PF>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, vlt_force_kernel<PLAYOUT, MT, PF, KICK>,
                                                       kTileThreads, smem);
         if (ctas_per_sm < 1) ctas_per_sm = 1;
     }
     int grid = std::min(v.ntiles, c.sm_count * ctas_per_sm);
     if (grid < 1) return;
-    vlt_force_kernel<PLAYOUT, MT, PF><<<grid, kTileThreads, smem, c.stream>>>(
+    vlt_force_kernel<PLAYOUT, MT, PF, KICK><<<grid, kTileThreads, smem, c.stream>>>(
         reinterpret_cast<const TileDesc*>(v.tdesc.p), v.tbase.p, v.ntiles, (int*)(c.scal.p + 6),
         s3_stride((int)v.grid.m), c.n, v.cap4, v.s3.p, v.grid.row_tid.p, v.tcnt.p,
-        reinterpret_cast<const uint2*>(v.tl.p), v.grid.row_src.p, c.force, c.tab, c.scal.p), note_launch();
+        reinterpret_cast<const uint2*>(v.tl.p), v.grid.row_src.p, c.force, c.tab, c.scal.p, kick), note_launch();
 }
 
 static int vlt_env_pf() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("MDG_VLT_PF");
-        v = e ? atoi(e) : 1;
+        v = e ? atoi(e) : 3;
     }
     return v;
 }
 
 template <int PLAYOUT, bool MT>
-static void vlt_launch(Context& c) {
-    if (vlt_env_pf() == 1) vlt_launch_pf<PLAYOUT, MT, 1>(c);
-    else vlt_launch_pf<PLAYOUT, MT, 2>(c);
+static void vlt_launch(Context& c, const KickArgs* kick) {
+    // 1: list prefetched one round ahead; 3 (default): one round + the producer
+    // pulls each tile's list into L2 while the window lands
+    int pf = vlt_env_pf();
+    KickArgs none{};
+    if (kick) {
+        if (pf == 1) vlt_launch_pf<PLAYOUT, MT, 1, true>(c, *kick);
+        else vlt_launch_pf<PLAYOUT, MT, 3, true>(c, *kick);
+    } else {
+        if (pf == 1) vlt_launch_pf<PLAYOUT, MT, 1, false>(c, none);
+        else vlt_launch_pf<PLAYOUT, MT, 3, false>(c, none);
+    }
 }
 
-bool vlt_compute(Context& c) {
+// `kick`: apply_gravity + finish_kick fused into the walk's epilogue (only
+// when every row is walked here, i.e. no overflow tiles; the caller checks).
+bool vlt_compute(Context& c, const KickArgs* kick) {
     Verlet& v = c.vl;
     int* next = (int*)(c.scal.p + 6);
     bool mt = c.tab.T > 1;
@@ -628,10 +670,10 @@ bool vlt_compute(Context& c) {
     else vl_refresh_launch<SOA, SOA>(c, next);
     c.prof_mark();
     if (c.layout == AOS) {
-        if (mt) vlt_launch<AOS, true>(c); else vlt_launch<AOS, false>(c);
+        if (mt) vlt_launch<AOS, true>(c, kick); else vlt_launch<AOS, false>(c, kick);
         if (v.nbig) vl_force_rows_launch<AOS>(c, v.big_row.p);
     } else {
-        if (mt) vlt_launch<SOA, true>(c); else vlt_launch<SOA, false>(c);
+        if (mt) vlt_launch<SOA, true>(c, kick); else vlt_launch<SOA, false>(c, kick);
         if (v.nbig) vl_force_rows_launch<SOA>(c, v.big_row.p);
     }
     c.prof_mark();

@@ -6,8 +6,9 @@ Per iteration, in the reference's order: drift with the previous forces,
 boundaries, F -> F_old (one fused kernel, integrator.py:31-37/98-128,
 simulation.py:151-153); ask the controller for this iteration's
 configuration (tuning.py:200-210); layout conversion + rebuild when due +
-refresh (timed as build); compute (timed as force); gravity + finish_kick
-(one kernel); the thermostat every ``interval_iterations``
+refresh (timed as build); compute + gravity + finish_kick (timed as force;
+the kick is fused into the tiled Verlet walk, its own kernel elsewhere); the
+thermostat every ``interval_iterations``
 (simulation.py:186-188, on the device, stats.cu).  The rebuild cadence is
 the reference's: rebuild when forced (first sample of a trial), when the
 configuration changed, or when ``since_rebuild >= R`` (so every R+1
@@ -157,7 +158,9 @@ class Simulation:
                 calc.refresh(p, cfg)
                 if timed:
                     ev[1].record()
-                calc.compute_async(p, cfg)
+                # force + gravity + finish_kick; the kick is fused into the
+                # force walk where the configuration allows (mdg_compute_kick)
+                calc.compute_kick_async(p, cfg, params.delta_t, params.gravity)
                 if timed:
                     ev[2].record()
                 break
@@ -167,7 +170,6 @@ class Simulation:
                 if not ctl.record_failure(exc):
                     raise
                 self.active = None
-        calc.finish_kick(p, params.delta_t, params.gravity)
         self.active = cfg.id
         self.since = 0 if rebuild else self.since + 1
         phase = it // self.tuning_interval

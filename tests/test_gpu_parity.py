@@ -435,3 +435,32 @@ def test_pipelined_host_loop_is_bit_identical(pkg):
             out.append((np.array(p.positions), np.array(p.velocities), np.array(p.forces)))
         for a, b in zip(*out):
             assert np.array_equal(a, b), cid
+
+
+def test_fused_kick_matches_separate_kick(pkg):
+    """mdg_compute_kick with the kick fused into the tiled walk (opt-in,
+    MDG_FUSE_KICK=1) gives the same trajectory as compute + finish_kick."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.')\n"
+        "from conftest import golden\n"
+        "import paper_2505_03438_b200 as P\n"
+        "from paper_2505_03438_b200.simulation import simulate\n"
+        "z = golden('traj_small.npz'); L = z['domain']\n"
+        "params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=10,"
+        " delta_t=1e-3, boundary=(P.PERIODIC,) * 3, gravity=-0.5)\n"
+        "parts = P.ParticleSet(z['pos0'], z['vel0'])\n"
+        "rep = simulate(parts, params, P.parse_configuration('VL-List_Iter-NoN3L-AoS'), steps=30)\n"
+        "assert rep.error is None\n"
+        "np.save(sys.argv[1], np.concatenate([parts.numpy('pos').ravel(), parts.numpy('vel').ravel()]))\n")
+    import os
+    import tempfile
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = []
+    for fuse in ("0", "1"):
+        f = os.path.join(tempfile.mkdtemp(), "state.npy")
+        env = dict(os.environ, MDG_FUSE_KICK=fuse, PYTHONPATH=os.path.dirname(here))
+        subprocess.run([sys.executable, "-c", code, f], cwd=here, env=env, check=True)
+        out.append(np.load(f))
+    assert np.array_equal(out[0], out[1])

@@ -208,6 +208,21 @@ int mdg_host_finish_kick_range(int64_t n, int64_t begin, int64_t end, int layout
                                double* force, const double* old_force, const int32_t* type_id,
                                const double* mass, double dt, int has_gravity, double gravity);
 
+/* One full reference-loop iteration (simulation.py:150-185) on HOST state
+ * with the device force path, pipelined: the host drift of particle chunk k
+ * runs while chunk k-1's positions copy to the bound device `pos`; then
+ * rebuild (when `rebuild`) + refresh + compute; then the forces copy back in
+ * chunks and each chunk is kicked on the host as soon as it lands.  Host
+ * arrays pos/vel/force/old_force (layout of the bound set, pinned for DMA
+ * speed) are the caller's ParticleSet; the device arrays are those of
+ * mdg_bind.  Same arithmetic as mdg_host_drift_wrap / mdg_host_finish_kick,
+ * bit-identical to the unpipelined sequence.  *blowup set (and nothing after
+ * the drift done) when a coordinate left [-L, 2L].  Returns when the step is
+ * complete on the host. */
+int mdg_host_step(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, double* force,
+                  double* old_force, const int32_t* type_id, const double* mass, double dt,
+                  int has_gravity, double gravity, int rebuild, int chunks, int* blowup);
+
 /* Measured FP64 FMA throughput of this device (roofline denominator):
  * dependent-chain DFMA microbenchmark, TFLOP/s (2 flops per DFMA). */
 int mdg_measure_fp64_peak(mdg_ctx* ctx, double* tflops, double* sm_mhz_hint);

@@ -2,6 +2,7 @@
 #include <math.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 
 #include "../../include/mdg.h"
@@ -163,6 +164,7 @@ int mdg_destroy(mdg_ctx* ctx) {
     ctx->c.d_mass.release();
     if (ctx->c.h_scal) cudaFreeHost(ctx->c.h_scal);
     for (cudaEvent_t e : ctx->c.ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->c.chunk_ev) cudaEventDestroy(e);
     delete ctx;
     return MDG_OK;
 }
@@ -469,6 +471,66 @@ int mdg_d2h(mdg_ctx* ctx, void* host, const void* dev, size_t bytes) {
         cudaStreamSynchronize(ctx->c.stream) != cudaSuccess)
         return cuda_status("mdg_d2h");
     return MDG_OK;
+}
+
+int mdg_host_step(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, double* force,
+                  double* old_force, const int32_t* type_id, const double* mass, double dt,
+                  int has_gravity, double gravity, int rebuild, int chunks, int* blowup) {
+    CHECK_CTX(ctx);
+    if (int e = validate(cfg)) return e;
+    if (int e = need_system(ctx)) return e;
+    Context& c = ctx->c;
+    if (blowup) *blowup = 0;
+    int64_t n = c.n;
+    if (n == 0) return MDG_OK;
+    if (!c.pos || !c.force) { set_error("mdg_host_step: bind the device arrays first"); return MDG_ESTATE; }
+    int K = std::max(1, std::min<int>(chunks, (int)std::min<int64_t>(n, 64)));
+    while ((int)c.chunk_ev.size() < K) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return cuda_status("event");
+        c.chunk_ev.push_back(e);
+    }
+    int periodic[3] = {c.periodic[0], c.periodic[1], c.periodic[2]};
+    // pieces (byte offset, bytes) of particles [a, b) in the bound layout
+    auto copy = [&](double* dst, const double* src, int64_t a, int64_t b, cudaMemcpyKind kind) {
+        if (c.layout == AOS)
+            return cudaMemcpyAsync(dst + 3 * a, src + 3 * a, 24 * (b - a), kind, c.stream);
+        for (int k = 0; k < 3; ++k) {
+            cudaError_t e = cudaMemcpyAsync(dst + k * n + a, src + k * n + a, 8 * (b - a), kind, c.stream);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    };
+    int bad = 0;
+    for (int k = 0; k < K; ++k) {
+        int64_t a = n * k / K, b = n * (k + 1) / K;
+        int bk = 0;
+        mdg_host_drift_wrap_range(n, a, b, c.layout, pos, vel, force, old_force, type_id, mass, c.L,
+                                  periodic, dt, &bk);
+        bad |= bk;
+        if (copy(c.pos, pos, a, b, cudaMemcpyHostToDevice) != cudaSuccess) return cuda_status("h2d");
+    }
+    if (bad) {
+        if (blowup) *blowup = 1;
+        cudaStreamSynchronize(c.stream);
+        return cuda_status("mdg_host_step");
+    }
+    if (rebuild)
+        if (int e = mdg_rebuild(ctx, cfg)) return e;
+    if (int e = mdg_refresh(ctx, cfg)) return e;
+    if (int e = mdg_compute(ctx, cfg)) return e;
+    for (int k = 0; k < K; ++k) {
+        int64_t a = n * k / K, b = n * (k + 1) / K;
+        if (copy(force, c.force, a, b, cudaMemcpyDeviceToHost) != cudaSuccess) return cuda_status("d2h");
+        cudaEventRecord(c.chunk_ev[k], c.stream);
+    }
+    for (int k = 0; k < K; ++k) {
+        int64_t a = n * k / K, b = n * (k + 1) / K;
+        if (cudaEventSynchronize(c.chunk_ev[k]) != cudaSuccess) return cuda_status("d2h wait");
+        mdg_host_finish_kick_range(n, a, b, c.layout, vel, force, old_force, type_id, mass, dt,
+                                   has_gravity, gravity);
+    }
+    return cuda_status("mdg_host_step");
 }
 
 int mdg_d2h_async(mdg_ctx* ctx, void* host, const void* dev, size_t bytes) {

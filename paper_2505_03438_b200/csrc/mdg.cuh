@@ -177,6 +177,7 @@ struct Context {
     DBuf<unsigned long long> scan_tmp;      // block partials for scans
     // optional CUDA-event bracketing of the force kernels (mdg_profile)
     bool prof = false;
+    std::vector<cudaEvent_t> chunk_ev;   // mdg_host_step's per-chunk copy events
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     void prof_mark();

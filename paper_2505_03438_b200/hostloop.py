@@ -142,11 +142,12 @@ class HostSimulation:
     """The reference loop (simulation.py:150-188, fixed configuration) on host
     state with the GPU force backend.  Create once, then ``run(steps)``.
 
-    With ``chunks > 1`` (default 4) the host work overlaps the copies: the
-    drift of chunk k runs while chunk k-1's positions are in flight to the
-    device, and the kick of chunk k starts as soon as its forces have landed.
-    The arithmetic and its order per particle are unchanged (same results,
-    bit for bit); only the copies are split."""
+    With ``chunks > 1`` (default 4) a step is one native call
+    (``mdg_host_step``) in which the host work overlaps the copies: the drift
+    of chunk k runs while chunk k-1's positions are in flight to the device,
+    and the kick of chunk k starts as soon as its forces have landed.  The
+    arithmetic and its order per particle are unchanged (same results, bit
+    for bit); only the copies are split."""
 
     def __init__(self, particles, params, config, calculator=None, chunks=4):
         self.p, self.params, self.config = particles, params, config
@@ -177,25 +178,24 @@ class HostSimulation:
             calc.compute(p, cfg)
             host_finish_kick(p, params.delta_t, params.gravity)
         else:
-            bounds = self._bounds()
-            bad = False
-            for a, b in bounds:
-                bad |= host_drift_wrap_range(p, params, params.delta_t, a, b)
-                calc.upload_range(p, a, b)
-            if bad:
+            # one native call: chunked host drift / H2D overlap, device force
+            # path, chunked D2H / host kick overlap (mdg_host_step)
+            rebuild = self.active != cfg.id or self.since >= params.rebuild_interval
+            calc._bind(p)
+            mass = np.ascontiguousarray(p.mass, dtype=np.float64)
+            tid = getattr(p, "_tid32", None)
+            if tid is None:
+                tid = np.asarray(p.type_id, dtype=np.int32)
+            bad = ctypes.c_int()
+            check(lib().mdg_host_step(calc.ctx.h, ctypes.byref(_lib.config_struct(cfg)), _ptr(p.pos),
+                                      _ptr(p.vel), _ptr(p.force), _ptr(p.old_force),
+                                      _ptr(tid) if len(mass) > 1 else None, _ptr(mass),
+                                      float(params.delta_t), int(params.gravity is not None),
+                                      float(params.gravity or 0.0), int(rebuild), self.chunks,
+                                      ctypes.byref(bad)), "host step")
+            if bad.value:
                 raise BlowUpError("particle left the domain by more than one domain length "
                                   "(or position is not finite)")
-            rebuild = self.active != cfg.id or self.since >= params.rebuild_interval
-            calc.device_step(p, cfg, rebuild)
-            events = []
-            for a, b in bounds:
-                calc.download_range(p, a, b)
-                ev = torch.cuda.Event()
-                ev.record(calc.ctx.stream)
-                events.append(ev)
-            for (a, b), ev in zip(bounds, events):
-                ev.synchronize()
-                host_finish_kick_range(p, params.delta_t, params.gravity, a, b)
         self.active = cfg.id
         self.since = 0 if rebuild else self.since + 1
         self.iteration += 1

@@ -99,7 +99,7 @@ struct Verlet {
     // shared-memory tiles of the force walk (vltile.cu)
     bool tiled = false;
     bool rows_valid = false;   // row-space lists (cnt/nbr) built for every row
-    int ntiles = 0, nbig = 0, cap4 = 0;
+    int ntiles = 0, nbig = 0, cap4 = 0, win_rows = 0;
     DBuf<int> tdesc;           // ntiles descriptors (TileDesc)
     DBuf<int> tsize, tbase;    // per tile: padded entry count, exclusive prefix
     DBuf<uint16_t> tl;         // window-local lists, 4-entry groups per lane

@@ -36,7 +36,6 @@ constexpr int kTX = 2, kTY = 2;
 constexpr int kRanges = (kTX + 2) * (kTY + 2);
 constexpr int kSegs = kTX * kTY;
 constexpr int kWinRows = 2048;        // 48 KB of positions (+ 2 KB types) per CTA
-constexpr int kWalkThreads = 256;
 
 struct TileDesc {
     int x0, y0, z0, z1;
@@ -54,7 +53,7 @@ struct TilePlan {
     int ngx, ngy, nzt, tz;
 };
 
-__global__ void vlt_desc_kernel(GridView gv, TilePlan tp, int ntiles, int cap4,
+__global__ void vlt_desc_kernel(GridView gv, TilePlan tp, int ntiles, int cap4, int budget,
                                 TileDesc* __restrict__ desc, int* __restrict__ tsize,
                                 int* __restrict__ nbig) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -98,7 +97,7 @@ __global__ void vlt_desc_kernel(GridView gv, TilePlan tp, int ntiles, int cap4,
     d.ioff[kSegs] = io;
     d.ni = io;
     d.wrows = off;
-    d.big = off > kWinRows || off > 65536;
+    d.big = off > budget || off > 65536;
     d.pad0 = 0;
     d.pad1[0] = d.pad1[1] = 0;
     desc[t] = d;
@@ -322,8 +321,9 @@ constexpr int kTileThreads = (kConsumerWarps + 1) * 32;
 
 template <bool MT>
 struct WinLayout {
+    // doubles per buffer of `rows` window rows: x, y, z, then int32 types (MT)
+    __host__ __device__ static int doubles(int rows) { return 3 * rows + (MT ? rows / 2 : 0); }
     // per buffer: x, y, z (doubles) then types (int32) for MT
-    static constexpr int kDoubles = 3 * kWinRows + (MT ? kWinRows / 2 : 0);
 };
 
 // Persistent, warp-specialised walk.  The last warp is the producer: it takes
@@ -334,32 +334,32 @@ struct WinLayout {
 // arrive on the buffer's `empty` mbarrier when no chunk is left, so the
 // producer refills it while they already work on the other buffer.  No
 // CTA-wide barrier after the prologue.
-template <int PLAYOUT, bool MT, int PF, bool KICK>
+template <int PLAYOUT, bool MT, int PF, bool KICK, int STAGES>
 __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
-    const TileDesc* __restrict__ desc, const int* __restrict__ tbase, int ntiles,
+    const TileDesc* __restrict__ desc, const int* __restrict__ tbase, int ntiles, int wrows,
     int* __restrict__ next, int ms, int64_t n, int cap4, const double* __restrict__ s3,
     const int* __restrict__ row_tid, const int* __restrict__ tcnt, const uint2* __restrict__ tl,
     const int* __restrict__ row_src, double* __restrict__ force, LJTab tab,
     unsigned long long* counter, KickArgs kick) {
     extern __shared__ __align__(128) double win[];
-    __shared__ __align__(16) TileDesc d[2];
-    __shared__ __align__(8) uint64_t full[2], empty[2];
-    __shared__ int rowctr[2], tile_of[2];
+    __shared__ __align__(16) TileDesc d[STAGES];
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+    __shared__ int rowctr[STAGES], tile_of[STAGES];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < STAGES; ++b) {
             mbar_init(&full[b], 1);
             mbar_init(&empty[b], kConsumerWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    constexpr int kBuf = WinLayout<MT>::kDoubles;
+    const int kBuf = WinLayout<MT>::doubles(wrows);
     if (warp == kConsumerWarps) {
         // ---------------- producer
         for (int it = 0;; ++it) {
-            int b = it & 1;
-            if (it >= 2) mbar_wait(&empty[b], ((it >> 1) - 1) & 1);
+            int b = it % STAGES;
+            if (it >= STAGES) mbar_wait(&empty[b], (it / STAGES - 1) & 1);
             int t = 0;
             if (lane == 0) t = atomicAdd(next, 1);
             t = __shfl_sync(0xffffffffu, t, 0);
@@ -382,9 +382,9 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                 continue;
             }
             double* wx = win + b * kBuf;
-            double* wy = wx + kWinRows;
-            double* wz = wy + kWinRows;
-            int* wt = reinterpret_cast<int*>(wz + kWinRows);
+            double* wy = wx + wrows;
+            double* wz = wy + wrows;
+            int* wt = reinterpret_cast<int*>(wz + wrows);
             if (lane == 0) {
                 tile_of[b] = t;
                 rowctr[b] = 0;
@@ -420,16 +420,16 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
     // ---------------- consumers
     unsigned hits = 0;
     for (int it = 0;; ++it) {
-        int b = it & 1;
-        mbar_wait(&full[b], (it >> 1) & 1);
+        int b = it % STAGES;
+        mbar_wait(&full[b], (it / STAGES) & 1);
         int t = tile_of[b];
         if (t < 0) break;
         const TileDesc& D = d[b];
         if (!D.big) {
             const double* wx = win + b * kBuf;
-            const double* wy = wx + kWinRows;
-            const double* wz = wy + kWinRows;
-            const int* wt = reinterpret_cast<const int*>(wz + kWinRows);
+            const double* wy = wx + wrows;
+            const double* wz = wy + wrows;
+            const int* wt = reinterpret_cast<const int*>(wz + wrows);
             int base = tbase[t];
             int slot0 = base / cap4;
             int ni = D.ni;
@@ -540,6 +540,8 @@ static int vlt_env_tz() {
     return v;
 }
 
+static int vlt_env_budget();
+
 // Tiled build (called by vl_rebuild after the fp32 copy): 0 = tile lists
 // built, 1 = tiling not applicable (row-space lists instead), -1 = error.
 int vlt_build(Context& c) {
@@ -552,7 +554,8 @@ int vlt_build(Context& c) {
     // TZ: the mean window (4 x 4 columns x TZ+2 cells) at 90% of the budget
     double rho = (double)c.n / ((double)g.S[0] * g.S[1] * g.S[2]);
     int tz = vlt_env_tz();
-    if (tz < 1) tz = (int)floor(0.9 * kWinRows / ((kTX + 2) * (kTY + 2) * std::max(rho, 1e-9))) - 2;
+    int budget = vlt_env_budget();
+    if (tz < 1) tz = (int)floor(0.9 * budget / ((kTX + 2) * (kTY + 2) * std::max(rho, 1e-9))) - 2;
     tz = std::max(1, std::min(std::min(tz, g.S[2]), kMaxTZ));
     TilePlan tp{(g.S[0] + kTX - 1) / kTX, (g.S[1] + kTY - 1) / kTY, (g.S[2] + tz - 1) / tz, tz};
     int ntiles = tp.ngx * tp.ngy * tp.nzt;
@@ -575,8 +578,8 @@ int vlt_build(Context& c) {
     for (int attempt = 0; attempt < 3; ++attempt) {
         v.cap4 = std::max(8, (v.cap + 3) & ~3);   // >= 2 groups per row (walk prefetch)
         MDG_CUDA(cudaMemsetAsync(nbig, 0, sizeof(int), c.stream));
-        vlt_desc_kernel<<<blocks_for(ntiles, 128), 128, 0, c.stream>>>(gv, tp, ntiles, v.cap4, desc,
-                                                                       v.tsize.p, nbig), note_launch();
+        vlt_desc_kernel<<<blocks_for(ntiles, 128), 128, 0, c.stream>>>(gv, tp, ntiles, v.cap4, budget,
+                                                                       desc, v.tsize.p, nbig), note_launch();
         exclusive_scan_i32(v.tsize.p, v.tbase.p, ntiles, c.scal.p + 1, c.scan_tmp, c.stream);
         MDG_CUDA(cudaMemcpyAsync(c.h_scal + 1, c.scal.p + 1, sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, c.stream));
@@ -610,30 +613,61 @@ int vlt_build(Context& c) {
     }
     v.ntiles = ntiles;
     v.nbig = big;
+    v.win_rows = budget;
     v.tiled = true;
     if (getenv("MDG_VLT_DEBUG"))
         fprintf(stderr, "vlt: tz=%d tiles=%d big=%d cap=%d cap4=%d\n", tz, ntiles, big, v.cap, v.cap4);
     return 0;
 }
 
-template <int PLAYOUT, bool MT, int PF, bool KICK>
-static void vlt_launch_pf(Context& c, const KickArgs& kick) {
+// window ring: STAGES buffers of `budget` rows (MDG_VLT_STAGES, MDG_VLT_WIN)
+static int vlt_env_stages() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_VLT_STAGES");
+        v = e ? atoi(e) : 2;
+        if (v != 3) v = 2;
+    }
+    return v;
+}
+
+static int vlt_env_budget() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_VLT_WIN");
+        v = e ? atoi(e) : 2048;
+        v = std::max(256, std::min(v, kWinRows)) & ~3;
+    }
+    return v;
+}
+
+template <int PLAYOUT, bool MT, int PF, bool KICK, int STAGES>
+static void vlt_launch_st(Context& c, const KickArgs& kick) {
     Verlet& v = c.vl;
-    size_t smem = 2 * (size_t)WinLayout<MT>::kDoubles * sizeof(double);
+    int wrows = v.win_rows;
+    size_t smem = STAGES * (size_t)WinLayout<MT>::doubles(wrows) * sizeof(double);
     static int ctas_per_sm = 0;
-    if (!ctas_per_sm) {
-        cudaFuncSetAttribute(vlt_force_kernel<PLAYOUT, MT, PF, KICK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, vlt_force_kernel<PLAYOUT, MT, PF, KICK>,
+    static size_t smem_set = 0;
+    if (smem != smem_set) {
+        cudaFuncSetAttribute(vlt_force_kernel<PLAYOUT, MT, PF, KICK, STAGES>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, vlt_force_kernel<PLAYOUT, MT, PF, KICK, STAGES>,
                                                       kTileThreads, smem);
         if (ctas_per_sm < 1) ctas_per_sm = 1;
+        smem_set = smem;
     }
     int grid = std::min(v.ntiles, c.sm_count * ctas_per_sm);
     if (grid < 1) return;
-    vlt_force_kernel<PLAYOUT, MT, PF, KICK><<<grid, kTileThreads, smem, c.stream>>>(
-        reinterpret_cast<const TileDesc*>(v.tdesc.p), v.tbase.p, v.ntiles, (int*)(c.scal.p + 6),
+    vlt_force_kernel<PLAYOUT, MT, PF, KICK, STAGES><<<grid, kTileThreads, smem, c.stream>>>(
+        reinterpret_cast<const TileDesc*>(v.tdesc.p), v.tbase.p, v.ntiles, wrows, (int*)(c.scal.p + 6),
         s3_stride((int)v.grid.m), c.n, v.cap4, v.s3.p, v.grid.row_tid.p, v.tcnt.p,
         reinterpret_cast<const uint2*>(v.tl.p), v.grid.row_src.p, c.force, c.tab, c.scal.p, kick), note_launch();
+}
+
+template <int PLAYOUT, bool MT, int PF, bool KICK>
+static void vlt_launch_pf(Context& c, const KickArgs& kick) {
+    if (vlt_env_stages() == 3) vlt_launch_st<PLAYOUT, MT, PF, KICK, 3>(c, kick);
+    else vlt_launch_st<PLAYOUT, MT, PF, KICK, 2>(c, kick);
 }
 
 static int vlt_env_pf() {

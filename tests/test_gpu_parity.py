@@ -464,3 +464,31 @@ def test_fused_kick_matches_separate_kick(pkg):
         subprocess.run([sys.executable, "-c", code, f], cwd=here, env=env, check=True)
         out.append(np.load(f))
     assert np.array_equal(out[0], out[1])
+
+
+def test_gpu_training_sweep_writes_reference_csv(pkg, tmp_path):
+    """§8(f) row 3: device-timed static-snapshot trials labelled into the
+    reference's dataset format; features equal the reference's live stats."""
+    import csv as _csv
+    P, calc = pkg
+    from paper_2505_03438_b200 import dataset
+    z = golden("thermo_stats.npz")
+    points = []
+    for name in ("uniform", "blob"):
+        a = z[f"ls_{name}_in"]
+        per = P.PERIODIC if a[5] else P.REFLECTIVE
+        params = P.SimulationParams(domain_size=a[:3], cutoff=float(a[3]), skin=float(a[4]),
+                                    rebuild_interval=10, boundary=(per,) * 3, thread_count=int(a[6]))
+        points.append((P.ParticleSet(z[f"ls_{name}_pos"]), params))
+    space = [P.parse_configuration(c) for c in ("LC-C08-N3L-AoS-CSF1", "VL-List_Iter-NoN3L-SoA",
+                                                "VCL-ClusterIter-NoN3L-AoS")]
+    out = tmp_path / "gpu.csv"
+    assert dataset.generate_training_dataset(out, points, space=space, trial_iterations=3) == 2
+    rows = list(_csv.reader(open(out)))
+    assert rows[0] == dataset.dataset_columns(space)
+    for (name, row) in zip(("uniform", "blob"), rows[1:]):
+        feats = [float(x) for x in row[:8]]
+        assert feats == list(z[f"ls_{name}_out"]), name
+        costs = {c.id: float(x) for c, x in zip(space, row[8:-1])}
+        assert all(0 < v < float("inf") for v in costs.values())
+        assert row[-1] == min(space, key=lambda c: costs[c.id]).id

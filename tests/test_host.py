@@ -224,3 +224,18 @@ def test_host_wrap_matches_np_mod_on_edges():
     want = np.mod(pos, L)
     got = p.pos
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_dataset_columns_match_reference_format():
+    """§8(f) row 3: the GPU sweep writes the reference's CSV layout
+    (dataset.py:143-146): 8 features in livestats order, cost:<id> per
+    configuration, final 'label'."""
+    from paper_2505_03438_b200 import dataset
+    cols = dataset.dataset_columns()
+    assert cols[:8] == ["meanParticlesPerBin", "relStdDevParticlesPerBin", "medianParticlesPerBin",
+                        "maxParticlesPerBin", "numBins", "numEmptyBins", "threadCount", "skin"]
+    assert cols[8:-1] == [f"cost:{c.id}" for c in P.enumerate_configurations()]
+    assert cols[-1] == "label"
+    assert dataset.evidence_cost(100.0, 1100.0, 10) == 210.0
+    with pytest.raises(ValueError):
+        dataset.evidence_cost(1.0, 1.0, 0)

@@ -492,3 +492,42 @@ def test_gpu_training_sweep_writes_reference_csv(pkg, tmp_path):
         costs = {c.id: float(x) for c, x in zip(space, row[8:-1])}
         assert all(0 < v < float("inf") for v in costs.values())
         assert row[-1] == min(space, key=lambda c: costs[c.id]).id
+
+
+@pytest.mark.parametrize("env", [{"MDG_VLT_WIN": "64"}, {"MDG_VLT_WIN": "256"}, {"MDG_VLT_ORDER": "2"}, {"MDG_VL_TILED": "0"},
+                                 {"MDG_VLT_STAGES": "3", "MDG_VLT_WIN": "1024"}])
+def test_vl_walk_variants_match_reference(pkg, env):
+    """The tunable paths of the Verlet walk against the reference forces and
+    counts: a tiny window budget (most tiles overflow to the row-space walk),
+    bank-aware list order, the untiled walk, a 3-stage window ring."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, '.')\n"
+        "import numpy as np\n"
+        "from conftest import golden, system_names\n"
+        "from oracle import port\n"
+        "import paper_2505_03438_b200 as P\n"
+        "from paper_2505_03438_b200 import calculator as calc\n"
+        "for name in system_names():\n"
+        "    d = golden(f'sys_{name}.npz')\n"
+        "    ids = [str(s) for s in d['config_ids']]\n"
+        "    nt = int(d['n_types'])\n"
+        "    types = [P.ParticleTypeInfo(t, 1.0 + 0.5 * t, 1.0 - 0.2 * t, 1.0 + t) for t in range(nt)]\n"
+        "    per = tuple(P.PERIODIC if f else P.REFLECTIVE for f in d['periodic'])\n"
+        "    params = P.SimulationParams(domain_size=d['domain'], cutoff=float(d['cutoff']),"
+        " skin=float(d['skin']), rebuild_interval=5, boundary=per)\n"
+        "    for layout in ('AoS', 'SoA'):\n"
+        "        cid = f'VL-List_Iter-NoN3L-{layout}'\n"
+        "        parts = P.ParticleSet(d['pos'], type_ids=d['tid'], types=types, layout=layout)\n"
+        "        _, count = calc.compute_forces(parts, P.parse_configuration(cid), params)\n"
+        "        k = ids.index(cid)\n"
+        "        assert count == int(d['counts'][k]), (name, cid)\n"
+        "        err = port.force_rel_error(parts.numpy('force'), d['forces'][k])\n"
+        "        assert err <= 1e-10, (name, cid, err)\n"
+        "print('ok')\n")
+    here = os.path.dirname(os.path.abspath(__file__))
+    e = dict(os.environ, PYTHONPATH=os.path.dirname(here), **env)
+    r = subprocess.run([sys.executable, "-c", code], cwd=here, env=e, capture_output=True, text=True)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -52,6 +52,27 @@ __global__ void s_gather_soa(int per, unsigned seed, double* out) {
     if (acc == 1.2345) out[0] = acc;
 }
 
+// MODE 0: random rows; 1: bank class of row = (lane + k) mod 16 (conflict-free
+// per half-warp); 2: class (lane + k/4 + drift) mod 16 with a random per-lane
+// drift of 0..3 steps -- what a list sorted by (class - lane) mod 16 gives
+template <int MODE>
+__global__ void s_gather_cls(int per, unsigned seed, double* out) {
+    __shared__ double x[W], y[W], z[W];
+    for (int i = threadIdx.x; i < W; i += blockDim.x) { x[i] = i; y[i] = 2 * i; z[i] = 3 * i; }
+    __syncthreads();
+    unsigned l = seed ^ (blockIdx.x * blockDim.x + threadIdx.x) * 747796405u;
+    int lane = threadIdx.x & 31;
+    int drift = nxt(l) & 3;
+    double acc = 0;
+    for (int k = 0; k < per; ++k) {
+        unsigned r = nxt(l) % (W / 16);
+        unsigned cls = MODE == 0 ? (nxt(l) & 15) : MODE == 1 ? ((lane + k) & 15) : ((lane + (k + drift) / 4) & 15);
+        unsigned j = r * 16 + cls;
+        acc += x[j] + y[j] + z[j];
+    }
+    if (acc == 1.2345) out[0] = acc;
+}
+
 template <bool LOCAL>
 __global__ void s_atomic(int per, unsigned seed, double* out) {
     __shared__ double f[3 * W];
@@ -143,6 +164,9 @@ int main() {
     run("smem gather double4 local-128", b2, big(s_gather<true>));
     run("smem gather 3x double random", b2, big(s_gather_soa<false>));
     run("smem gather 3x double local-128", b2, big(s_gather_soa<true>));
+    run("smem 3x double, random class", b2, big(s_gather_cls<0>));
+    run("smem 3x double, rotated class", b2, big(s_gather_cls<1>));
+    run("smem 3x double, rotated+drift", b2, big(s_gather_cls<2>));
     run("smem 3x atomicAdd f64 random", b2, big(s_atomic<false>));
     run("smem 3x atomicAdd f64 local-128", b2, big(s_atomic<true>));
     run("smem gather + 3 atomics random", b1, big(s_n3l<false>));

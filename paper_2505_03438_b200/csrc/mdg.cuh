@@ -207,6 +207,13 @@ void vcl_compute(Context& c, int newton3);
 void vl_refresh_into(Context& c, Grid& gr, double4* s4, double* s3, bool& s3_valid);
 int vl_build_rows(Context& c, const uint8_t* only);
 int vl_ensure_rows(Context& c);
+// cell lengths for the fp32-compute Verlet walk (cell-relative positions)
+struct Cells32 {
+    float cl[3];
+    double cld[3];
+};
+void vlt_compute32(Context& c, const Cells32& cc);
+
 // finish_kick arguments for kernels that fuse it into their epilogue
 struct KickArgs {
     double* vel;

@@ -516,11 +516,6 @@ void vl_compute(Context& c, int layout) {
 // (r_i - r_j) + (c_i - c_j) * cell_len with the integer part exact: the fp32
 // error is that of coordinates inside one cell, not of the box.  Gathers are
 // 16 bytes (one LDG.128) instead of 32.
-struct Cells32 {
-    float cl[3];
-    double cld[3];
-};
-
 __device__ __forceinline__ int pack_cell(int x, int y, int z) { return (x << 20) | (y << 10) | z; }
 
 template <int PLAYOUT>
@@ -528,8 +523,9 @@ __global__ void vl_refresh32_kernel(const double* __restrict__ pos, int64_t n, i
                                     const int* __restrict__ row_src,
                                     const uint8_t* __restrict__ row_code,
                                     const int* __restrict__ row_cell, GridView gv, Wrap w, Cells32 cc,
-                                    double4* __restrict__ s4, float4* __restrict__ q32) {
+                                    double4* __restrict__ s4, float4* __restrict__ q32, int* zero_me) {
     int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r == 0 && zero_me) *zero_me = 0;   // work counter of the tiled walk
     if (r >= m) return;
     int src = row_src[r], code = row_code[r];
     double q[3] = {pos[pidx<PLAYOUT>(src, 0, n)], pos[pidx<PLAYOUT>(src, 1, n)],
@@ -563,10 +559,11 @@ __global__ void __launch_bounds__(128) vl_force32_kernel(int m, int64_t n, int c
                                                          const int* __restrict__ row_src,
                                                          const uint8_t* __restrict__ row_code,
                                                          double* __restrict__ force, LJTab tab,
-                                                         Cells32 cc, unsigned long long* counter) {
+                                                         Cells32 cc, unsigned long long* counter,
+                                                         const uint8_t* __restrict__ only) {
     int r = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned hits = 0;
-    if (r < m && row_code[r] == kNoShift) {
+    if (r < m && row_code[r] == kNoShift && (!only || only[r])) {
         float4 qi = q32[r];
         int ci = __float_as_int(qi.w);
         int ti = MT ? row_tid[r] : 0;
@@ -614,8 +611,9 @@ __global__ void __launch_bounds__(128) vl_force32_kernel(int m, int64_t n, int c
 
 void vl_compute32(Context& c) {
     if (c.n == 0) return;
-    if (vl_ensure_rows(c)) return;
     Verlet& v = c.vl;
+    bool tiled = v.tiled;
+    if (!tiled && vl_ensure_rows(c)) return;
     Grid& gr = v.grid;
     int m = (int)gr.m;
     v.q32.ensure((size_t)m + 32);
@@ -630,19 +628,24 @@ void vl_compute32(Context& c) {
     }
     GridView gv = make_view(gr);
     bool mt = c.tab.T > 1;
+    int* next = tiled ? (int*)(c.scal.p + 6) : nullptr;   // zeroed for the tiled walk
     if (c.layout == AOS)
-        vl_refresh32_kernel<AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gv, w, cc, v.s4.p, v.q32.p), note_launch();
+        vl_refresh32_kernel<AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gv, w, cc, v.s4.p, v.q32.p, next), note_launch();
     else
-        vl_refresh32_kernel<SOA><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gv, w, cc, v.s4.p, v.q32.p), note_launch();
+        vl_refresh32_kernel<SOA><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gv, w, cc, v.s4.p, v.q32.p, next), note_launch();
     c.prof_mark();
-    dim3 b(blocks_for(m, 128)), t(128);
-#define MDG_VL32(P, M) vl_force32_kernel<P, M><<<b, t, 0, c.stream>>>(m, c.n, v.cap, v.q32.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p, gr.row_code.p, c.force, c.tab, cc, c.scal.p), note_launch()
-    if (c.layout == AOS) {
-        if (mt) MDG_VL32(AOS, true); else MDG_VL32(AOS, false);
-    } else {
-        if (mt) MDG_VL32(SOA, true); else MDG_VL32(SOA, false);
-    }
+    if (tiled) vlt_compute32(c, cc);   // tiles; overflow tiles below
+    if (!tiled || v.nbig) {
+        const uint8_t* only = tiled ? v.big_row.p : nullptr;
+        dim3 b(blocks_for(m, 128)), t(128);
+#define MDG_VL32(P, M) vl_force32_kernel<P, M><<<b, t, 0, c.stream>>>(m, c.n, v.cap, v.q32.p, gr.row_tid.p, v.cnt.p, v.nbr.p, gr.row_src.p, gr.row_code.p, c.force, c.tab, cc, c.scal.p, only), note_launch()
+        if (c.layout == AOS) {
+            if (mt) MDG_VL32(AOS, true); else MDG_VL32(AOS, false);
+        } else {
+            if (mt) MDG_VL32(SOA, true); else MDG_VL32(SOA, false);
+        }
 #undef MDG_VL32
+    }
     c.prof_mark();
 }
 

@@ -805,4 +805,196 @@ bool vlt_compute(Context& c, const KickArgs* kick) {
     return true;
 }
 
+// ---------------------------------------------------------------- fp32 walk
+
+// The fp32-compute / fp64-accumulate variant on the same tiles and lists:
+// the window holds each row's 16-byte record {position relative to its
+// build-time cell in fp32, packed cell coordinates} (vl_refresh32_kernel), so
+// a gather is one LDS.128 and a displacement is (r_i - r_j) + (c_i - c_j) * cl
+// with an exact integer part; the pair arithmetic is fp32, the per-row sums
+// fold into fp64 every 4 entries.  Same producer / consumer ring as the fp64
+// walk (1-D bulk copies of the records).  Measured alternative: staging
+// tile-relative fp32 coordinates converted by the producer warp itself
+// (no bulk copy) starves the consumers, 0.41 ms against 0.24 ms.
+template <int PLAYOUT, bool MT, int STAGES>
+__global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
+    const TileDesc* __restrict__ desc, const int* __restrict__ tbase, int ntiles, int wrows,
+    int* __restrict__ next, int64_t n, int cap4, const float4* __restrict__ q32,
+    const int* __restrict__ row_tid, const int* __restrict__ tcnt, const uint2* __restrict__ tl,
+    const int* __restrict__ row_src, double* __restrict__ force, LJTab tab, Cells32 cc,
+    unsigned long long* counter) {
+    extern __shared__ __align__(128) double win[];
+    __shared__ __align__(16) TileDesc d[STAGES];
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+    __shared__ int rowctr[STAGES], tile_of[STAGES];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < STAGES; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&empty[b], kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // per buffer: float4[wrows], then int[wrows] types (MT); in doubles
+    const int kBuf = 2 * wrows + (MT ? wrows / 2 : 0);
+    if (warp == kConsumerWarps) {
+        for (int it = 0;; ++it) {
+            int b = it % STAGES;
+            if (it >= STAGES) mbar_wait(&empty[b], (it / STAGES - 1) & 1);
+            int t = 0;
+            if (lane == 0) t = atomicAdd(next, 1);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= ntiles) {
+                if (lane == 0) {
+                    tile_of[b] = -1;
+                    mbar_arrive(&full[b]);
+                }
+                break;
+            }
+            if (lane < kDescInts / 4)
+                reinterpret_cast<int4*>(&d[b])[lane] = reinterpret_cast<const int4*>(desc + t)[lane];
+            __syncwarp();
+            const TileDesc& D = d[b];
+            if (D.big) {
+                if (lane == 0) {
+                    tile_of[b] = t;
+                    mbar_arrive(&full[b]);
+                }
+                continue;
+            }
+            float4* w4 = reinterpret_cast<float4*>(win + b * kBuf);
+            int* wt = reinterpret_cast<int*>(w4 + wrows);
+            if (lane == 0) {
+                tile_of[b] = t;
+                rowctr[b] = 0;
+                mbar_arrive_tx(&full[b], (unsigned)D.wrows * (MT ? 20u : 16u));
+            }
+            __syncwarp();
+            if (lane < kRanges) {
+                int R = lane, o = D.woff[R], rows = D.woff[R + 1] - o, g = D.wstart[R];
+                if (rows > 0) {
+                    bulk_g2s(w4 + o, q32 + g, rows * 16u, &full[b]);
+                    if (MT) bulk_g2s(wt + o, row_tid + g, rows * 4u, &full[b]);
+                }
+            } else {
+                int base = tbase[t];
+                size_t bytes = (size_t)((D.ni + 31) / 32 * 32) * cap4 * 2;
+                const char* lb = reinterpret_cast<const char*>(tl) + (size_t)base * 2;
+                for (size_t off = (size_t)(lane - kRanges) * 32768; off < bytes; off += 16 * 32768)
+                    bulk_prefetch_l2(lb + off, (unsigned)min((size_t)32768, bytes - off));
+            }
+        }
+        return;
+    }
+    unsigned hits = 0;
+    const float rc2 = (float)tab.rc2;
+    for (int it = 0;; ++it) {
+        int b = it % STAGES;
+        mbar_wait(&full[b], (it / STAGES) & 1);
+        int t = tile_of[b];
+        if (t < 0) break;
+        const TileDesc& D = d[b];
+        if (!D.big) {
+            const float4* w4 = reinterpret_cast<const float4*>(win + b * kBuf);
+            const int* wt = reinterpret_cast<const int*>(w4 + wrows);
+            int base = tbase[t];
+            int slot0 = base / cap4;
+            int ni = D.ni;
+            for (;;) {
+                int q0 = 0;
+                if (lane == 0) q0 = atomicAdd(&rowctr[b], 32);
+                q0 = __shfl_sync(0xffffffffu, q0, 0);
+                if (q0 >= ni) break;
+                int q = q0 + lane;
+                if (q < ni) {
+                    int li;
+                    int r = tile_row(D, q, li);
+                    float4 qi = w4[li];
+                    int ci = __float_as_int(qi.w);
+                    int ti = MT ? wt[li] : 0;
+                    const uint2* lp = tl + ((size_t)base + (size_t)(q >> 5) * 32 * cap4) / 4 + (q & 31);
+                    int c = tcnt[slot0 + q];
+                    uint2 g0 = __ldcs(lp);
+                    int i = row_src[r];
+                    double fx = 0.0, fy = 0.0, fz = 0.0;
+                    for (int k0 = 0; k0 < c; k0 += 4) {
+                        uint2 cur = g0;
+                        if (k0 + 4 < c) g0 = __ldcs(lp + (size_t)(k0 / 4 + 1) * 32);
+                        int jj[4] = {(int)(cur.x & 0xffffu), (int)(cur.x >> 16), (int)(cur.y & 0xffffu),
+                                     (int)(cur.y >> 16)};
+                        float px = 0.f, py = 0.f, pz = 0.f;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            float4 qj = w4[jj[u]];
+                            int cj = __float_as_int(qj.w);
+                            float dx = (qi.x - qj.x) + (float)((ci >> 20) - (cj >> 20)) * cc.cl[0];
+                            float dy = (qi.y - qj.y) + (float)(((ci >> 10) & 1023) - ((cj >> 10) & 1023)) * cc.cl[1];
+                            float dz = (qi.z - qj.z) + (float)((ci & 1023) - (cj & 1023)) * cc.cl[2];
+                            float r2 = dx * dx + dy * dy + dz * dz;
+                            if ((k0 + u < c) && r2 < rc2) {
+                                double s2d, e24d;
+                                lj_params<MT>(tab, ti, MT ? wt[jj[u]] : 0, s2d, e24d);
+                                float inv = __frcp_rn(r2);
+                                float a = (float)s2d * inv;
+                                float a6 = a * a * a;
+                                float fs = ((float)e24d * inv) * (a6 * fmaf(2.0f, a6, -1.0f));
+                                ++hits;
+                                px = fmaf(fs, dx, px);
+                                py = fmaf(fs, dy, py);
+                                pz = fmaf(fs, dz, pz);
+                            }
+                        }
+                        fx += (double)px;
+                        fy += (double)py;
+                        fz += (double)pz;
+                    }
+                    force[pidx<PLAYOUT>(i, 0, n)] = fx;
+                    force[pidx<PLAYOUT>(i, 1, n)] = fy;
+                    force[pidx<PLAYOUT>(i, 2, n)] = fz;
+                }
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[b]);
+    }
+    warp_count(counter, hits);
+}
+
+template <int PLAYOUT, bool MT>
+static void vlt_launch32(Context& c, const Cells32& cc) {
+    Verlet& v = c.vl;
+    int wrows = v.win_rows;
+    constexpr int STAGES = 2;
+    size_t smem = STAGES * (size_t)(wrows * 16 + (MT ? wrows * 4 : 0));
+    static int ctas_per_sm = 0;
+    static size_t smem_set = 0;
+    if (smem != smem_set) {
+        cudaFuncSetAttribute(vlt_force32_kernel<PLAYOUT, MT, STAGES>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, vlt_force32_kernel<PLAYOUT, MT, STAGES>,
+                                                      kTileThreads, smem);
+        if (ctas_per_sm < 1) ctas_per_sm = 1;
+        smem_set = smem;
+    }
+    int grid = std::min(v.ntiles, c.sm_count * ctas_per_sm);
+    if (grid < 1) return;
+    vlt_force32_kernel<PLAYOUT, MT, STAGES><<<grid, kTileThreads, smem, c.stream>>>(
+        reinterpret_cast<const TileDesc*>(v.tdesc.p), v.tbase.p, v.ntiles, wrows, (int*)(c.scal.p + 6),
+        c.n, v.cap4, v.q32.p, v.grid.row_tid.p, v.tcnt.p, reinterpret_cast<const uint2*>(v.tl.p),
+        v.grid.row_src.p, c.force, c.tab, cc, c.scal.p), note_launch();
+}
+
+// fp32 walk over the tiles (after vl_refresh32_kernel, which zeroes the tile
+// counter); overflow tiles are the caller's
+void vlt_compute32(Context& c, const Cells32& cc) {
+    bool mt = c.tab.T > 1;
+    if (c.layout == AOS) {
+        if (mt) vlt_launch32<AOS, true>(c, cc); else vlt_launch32<AOS, false>(c, cc);
+    } else {
+        if (mt) vlt_launch32<SOA, true>(c, cc); else vlt_launch32<SOA, false>(c, cc);
+    }
+}
+
 }  // namespace mdg

@@ -531,3 +531,66 @@ def test_vl_walk_variants_match_reference(pkg, env):
     e = dict(os.environ, PYTHONPATH=os.path.dirname(here), **env)
     r = subprocess.run([sys.executable, "-c", code], cwd=here, env=e, capture_output=True, text=True)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+# -- BASELINE full size (config 2: 1,048,576 particles) through size-independent
+#    properties (the oracle would take minutes at this size) -------------------
+
+@pytest.fixture(scope="module")
+def config2_snapshot(pkg):
+    P, calc = pkg
+    from paper_2505_03438_b200 import systems
+    pos, vel, params = systems.config2_inputs()
+    parts = P.ParticleSet(pos, vel)
+    systems.relax_on_device(parts, params, P.parse_configuration("LC-SLI-N3L-AoS-CSF1"))
+    return parts.numpy("pos"), parts.numpy("vel"), params
+
+
+def test_full_size_configurations_agree(pkg, config2_snapshot):
+    """At 1,048,576 particles every container family gives the same forces
+    (fp64 bar; fp32 variant 1e-4), N3L counts are half the NoN3L counts, and
+    the total force vanishes (Newton's third law, momentum conservation)."""
+    P, calc = pkg
+    pos, vel, params = config2_snapshot
+    ids = ["VL-List_Iter-NoN3L-SoA", "VL-List_Iter-NoN3L-AoS", "LC-SLI-N3L-SoA-CSF0.5",
+           "LC-C08-N3L-AoS-CSF1", "LC-C01-NoN3L-SoA-CSF1", "VCL-ClusterIter-N3L-AoS",
+           "VCL-ClusterIter-NoN3L-SoA", "VL-List_Iter-NoN3L-AoS-FP32"]
+    ref, ref_count = None, None
+    for cid in ids:
+        cfg = P.parse_configuration(cid)
+        parts = P.ParticleSet(pos, layout=cfg.layout)
+        _, count = calc.compute_forces(parts, cfg, params)
+        f = parts.numpy("force")
+        directed = count if not cfg.newton3 else 2 * count
+        if ref is None:
+            ref, ref_count = f, directed
+            total = np.abs(f.sum(axis=0)).max() / np.abs(f).sum(axis=0).max()
+            assert total <= 1e-12, total
+            continue
+        if cfg.precision == "fp32":   # pairs within fp32 rounding of rc may flip
+            assert abs(directed - ref_count) <= 1e-6 * ref_count, (cid, directed, ref_count)
+        else:
+            assert directed == ref_count, (cid, directed, ref_count)
+        tol = 1e-4 if cfg.precision == "fp32" else FP64_TOL
+        assert port.force_rel_error(f, ref) <= tol, cid
+
+
+def test_full_size_energy_conservation(pkg, config2_snapshot):
+    """200 NVE steps of config 2 on the tiled Verlet walk: total energy drift
+    stays at the integrator's level (relative 1e-4)."""
+    P, calc = pkg
+    from paper_2505_03438_b200.simulation import Simulation
+    pos, vel, params = config2_snapshot
+    parts = P.ParticleSet(pos, vel, layout="SoA")
+    cfg = P.parse_configuration("VL-List_Iter-NoN3L-SoA")
+    sim = Simulation(parts, params, cfg)
+
+    def energy():
+        v = parts.numpy("vel")
+        return 0.5 * float(np.sum(v * v)) + sim.calc.potential_energy(parts, rebuild=True)
+
+    e0 = energy()
+    sim.run(200, record=False)
+    sim.check()
+    e1 = energy()
+    assert abs(e1 - e0) / abs(e0) <= 1e-4, (e0, e1)

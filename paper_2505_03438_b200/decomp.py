@@ -1,21 +1,26 @@
 """Spatial domain decomposition across ranks.
 
-One process per GPU.  The box is cut into slabs along one axis; each rank owns
-the particles whose coordinate lies in its slab ``[lo, hi)`` and, every step,
-receives *ghost* copies of the neighbours' particles that lie within
-ℓ = rc + skin of its faces (positions only, with the global periodic shift
-applied across the box boundary).  Ghost sets are chosen at each rebuild and
-refreshed every step (the decomposed analogue of the reference's periodic
-images, which are also fixed between rebuilds, containers.py:93-118); particles
-that left their slab migrate to the neighbour at each rebuild with their full
-state.  Forces are evaluated on ``owned + ghost`` particles as an open box along
-the slab axis (no images on that axis, the ghosts stand in for them) and kept
-for owned particles only, so there is no reverse force exchange.
+One process per GPU.  The box is cut into a ``px x py x pz`` grid of
+subdomains (z-slabs for BASELINE configs 3 and 4, 3-D grids for config 5);
+each rank owns the particles whose coordinates lie in its subdomain
+``[lo, hi)`` and, every step, receives *ghost* copies of the particles within
+ℓ = rc + skin of its faces.  Ghosts travel axis by axis (x, then y, then z),
+each axis forwarding the ghosts received on the previous ones, so edge and
+corner neighbours arrive without diagonal messages.  Ghost sets are chosen at
+each rebuild and refreshed every step (the decomposed analogue of the
+reference's periodic images, which are also fixed between rebuilds,
+containers.py:93-118); particles that left their subdomain migrate, again axis
+by axis, at each rebuild with their full state.  Forces are evaluated on
+``owned + ghost`` particles as an open box along every decomposed axis (no
+images on those axes, the ghosts stand in for them) and kept for owned
+particles only, so there is no reverse force exchange.  The thermostat's
+temperature is an all-reduce of the ranks' kinetic energies and counts.
 
 The exchange is point-to-point through ``torch.distributed`` (NCCL between GPUs
-over NVLink/NVSwitch, gloo on CPU for tests): counts first, then payloads, to the
-left and right neighbours.  The force backend is pluggable (``force_fn``): on
-GPUs it is libmdg (``gpu_force_backend``); tests pass the CPU oracle.
+over NVLink/NVSwitch, gloo on CPU for tests): counts first, then payloads, to
+the two neighbours of each decomposed axis.  The force backend is pluggable
+(``force_fn``): on GPUs it is libmdg (``gpu_force_backend``); tests pass the
+CPU oracle.
 """
 
 from __future__ import annotations
@@ -27,60 +32,99 @@ import torch.distributed as dist
 from .params import PERIODIC, REFLECTIVE, SimulationParams
 
 
-class SlabDecomposition:
-    def __init__(self, params: SimulationParams, rank: int, world: int, axis: int = 2):
-        self.params = params
-        self.rank, self.world, self.axis = rank, world, axis
-        L = float(params.domain_size[axis])
-        self.L = L
-        self.width = L / world
-        self.lo = rank * self.width
-        self.hi = L if rank == world - 1 else (rank + 1) * self.width
-        self.ell = params.interaction_length
-        self.periodic = bool(params.periodic_flags()[axis])
-        if world > 1 and self.width < self.ell:
-            raise ValueError(f"slab width {self.width} < interaction length {self.ell}")
-        self.left = (rank - 1) % world
-        self.right = (rank + 1) % world
-        self.has_left = world > 1 and (self.periodic or rank > 0)
-        self.has_right = world > 1 and (self.periodic or rank < world - 1)
+class GridDecomposition:
+    """A ``dims = (px, py, pz)`` process grid over the box; rank r sits at
+    ``(r // (py*pz), (r // pz) % py, r % pz)``."""
 
-    def owner_of(self, coord: np.ndarray) -> np.ndarray:
-        r = np.floor(np.asarray(coord) / self.width).astype(np.int64)
-        return np.clip(r, 0, self.world - 1)
+    def __init__(self, params: SimulationParams, rank: int, world: int, dims=None):
+        dims = tuple(int(d) for d in (dims or (1, 1, world)))
+        if len(dims) != 3 or int(np.prod(dims)) != world:
+            raise ValueError(f"process grid {dims} does not have {world} ranks")
+        self.params, self.rank, self.world, self.dims = params, rank, world, dims
+        self.coords = (rank // (dims[1] * dims[2]), (rank // dims[2]) % dims[1], rank % dims[2])
+        self.ell = params.interaction_length
+        per = params.periodic_flags()
+        self.L = [float(x) for x in params.domain_size]
+        self.periodic = [bool(per[a]) for a in range(3)]
+        self.width = [self.L[a] / dims[a] for a in range(3)]
+        self.lo = [self.coords[a] * self.width[a] for a in range(3)]
+        self.hi = [self.L[a] if self.coords[a] == dims[a] - 1 else self.lo[a] + self.width[a]
+                   for a in range(3)]
+        self.active = [dims[a] > 1 for a in range(3)]
+        self.left, self.right, self.has_left, self.has_right = [], [], [], []
+        for a in range(3):
+            c = list(self.coords)
+            c[a] = (self.coords[a] - 1) % dims[a]
+            self.left.append(self.rank_of(c))
+            c[a] = (self.coords[a] + 1) % dims[a]
+            self.right.append(self.rank_of(c))
+            self.has_left.append(self.active[a] and (self.periodic[a] or self.coords[a] > 0))
+            self.has_right.append(self.active[a] and (self.periodic[a] or self.coords[a] < dims[a] - 1))
+            if self.active[a]:
+                if self.width[a] < self.ell:
+                    raise ValueError(f"subdomain width {self.width[a]} < interaction length {self.ell}")
+                if self.periodic[a] and self.width[a] + 2.0 * self.ell >= self.L[a]:
+                    raise ValueError("periodic axis too short for this process grid "
+                                     "(width + 2 ell must stay below the box length)")
+
+    def rank_of(self, c) -> int:
+        return (int(c[0]) * self.dims[1] + int(c[1])) * self.dims[2] + int(c[2])
+
+    def owner_of_positions(self, pos: np.ndarray) -> np.ndarray:
+        pos = np.asarray(pos, dtype=np.float64)
+        c = [np.clip(np.floor(pos[:, a] / self.width[a]).astype(np.int64), 0, self.dims[a] - 1)
+             for a in range(3)]
+        return (c[0] * self.dims[1] + c[1]) * self.dims[2] + c[2]
 
     def local_params(self) -> SimulationParams:
-        """Open box [lo - ell, hi + ell) along the slab axis (coordinates shifted
-        by -(lo - ell)), the other axes unchanged."""
+        """Open box [lo - ell, hi + ell) along every decomposed axis (coordinates
+        shifted by -(lo - ell)), the other axes unchanged."""
         p = self.params
         if self.world == 1:
             return p
         dom = np.array(p.domain_size, dtype=np.float64)
-        dom[self.axis] = (self.hi - self.lo) + 2.0 * self.ell
         bnd = list(p.boundary)
-        bnd[self.axis] = REFLECTIVE
+        for a in range(3):
+            if self.active[a]:
+                dom[a] = (self.hi[a] - self.lo[a]) + 2.0 * self.ell
+                bnd[a] = REFLECTIVE
         return SimulationParams(domain_size=dom, cutoff=p.cutoff, skin=p.skin,
                                 rebuild_interval=p.rebuild_interval, delta_t=p.delta_t,
                                 boundary=tuple(bnd), gravity=p.gravity)
 
-    @property
-    def origin(self) -> float:
-        return self.lo - self.ell if self.world > 1 else 0.0
+    def origin(self, a: int) -> float:
+        return self.lo[a] - self.ell if self.active[a] else 0.0
 
-    def near(self, z):
-        """Periodic image of z nearest to the slab centre (continuous local frame
-        for particles that wrapped across the box face since the last rebuild)."""
-        if not self.periodic or self.world == 1:
-            return z
-        c = 0.5 * (self.lo + self.hi)
-        return z - self.L * torch.round((z - c) / self.L)
+    def near(self, x, a: int):
+        """Periodic image of coordinate(s) ``x`` along axis ``a`` nearest to the
+        subdomain centre (continuous local frame for particles that wrapped
+        across the box face since the last rebuild)."""
+        if not self.periodic[a] or not self.active[a]:
+            return x
+        c = 0.5 * (self.lo[a] + self.hi[a])
+        return x - self.L[a] * torch.round((x - c) / self.L[a])
 
 
-def _exchange(tensor_left, tensor_right, dec: SlabDecomposition, width: int, dtype,
+class SlabDecomposition(GridDecomposition):
+    """Slabs along one axis (BASELINE configs 3 and 4)."""
+
+    def __init__(self, params: SimulationParams, rank: int, world: int, axis: int = 2):
+        dims = [1, 1, 1]
+        dims[axis] = world
+        super().__init__(params, rank, world, dims)
+        self.axis = axis
+
+    def owner_of(self, coord: np.ndarray) -> np.ndarray:
+        r = np.floor(np.asarray(coord) / self.width[self.axis]).astype(np.int64)
+        return np.clip(r, 0, self.world - 1)
+
+
+def _exchange(tensor_left, tensor_right, dec: GridDecomposition, a: int, width: int, dtype,
               comm_device=None):
-    """Send rows to the left/right neighbours, receive theirs.  Returns
-    (from_left, from_right) on the device of the inputs.  ``comm_device``
-    stages the messages elsewhere (e.g. "cpu" for gloo with device tensors)."""
+    """Send rows to the two neighbours along axis ``a``, receive theirs.
+    Returns (from_left, from_right) on the device of the inputs.
+    ``comm_device`` stages the messages elsewhere (e.g. "cpu" for gloo with
+    device tensors)."""
     home = tensor_left.device
     if comm_device is not None:
         tensor_left, tensor_right = tensor_left.to(comm_device), tensor_right.to(comm_device)
@@ -89,35 +133,35 @@ def _exchange(tensor_left, tensor_right, dec: SlabDecomposition, width: int, dty
                   torch.tensor([tensor_right.shape[0]], device=dev)]
     counts_in = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(2)]
     ops = []
-    if dec.has_left:
-        ops += [dist.P2POp(dist.isend, counts_out[0], dec.left),
-                dist.P2POp(dist.irecv, counts_in[0], dec.left)]
-    if dec.has_right:
-        ops += [dist.P2POp(dist.isend, counts_out[1], dec.right),
-                dist.P2POp(dist.irecv, counts_in[1], dec.right)]
+    if dec.has_left[a]:
+        ops += [dist.P2POp(dist.isend, counts_out[0], dec.left[a]),
+                dist.P2POp(dist.irecv, counts_in[0], dec.left[a])]
+    if dec.has_right[a]:
+        ops += [dist.P2POp(dist.isend, counts_out[1], dec.right[a]),
+                dist.P2POp(dist.irecv, counts_in[1], dec.right[a])]
     for req in dist.batch_isend_irecv(ops) if ops else []:
         req.wait()
     recv = [torch.empty((int(c.item()), width), dtype=dtype, device=dev) for c in counts_in]
     ops = []
-    if dec.has_left:
-        ops += [dist.P2POp(dist.isend, tensor_left.contiguous(), dec.left),
-                dist.P2POp(dist.irecv, recv[0], dec.left)]
-    if dec.has_right:
-        ops += [dist.P2POp(dist.isend, tensor_right.contiguous(), dec.right),
-                dist.P2POp(dist.irecv, recv[1], dec.right)]
+    if dec.has_left[a]:
+        ops += [dist.P2POp(dist.isend, tensor_left.contiguous(), dec.left[a]),
+                dist.P2POp(dist.irecv, recv[0], dec.left[a])]
+    if dec.has_right[a]:
+        ops += [dist.P2POp(dist.isend, tensor_right.contiguous(), dec.right[a]),
+                dist.P2POp(dist.irecv, recv[1], dec.right[a])]
     for req in dist.batch_isend_irecv(ops) if ops else []:
         req.wait()
     return recv[0].to(home), recv[1].to(home)
 
 
 class DecomposedSimulation:
-    """The reference loop (simulation.py:150-188) on one rank of a slab
+    """The reference loop (simulation.py:150-188) on one rank of a grid
     decomposition.  State arrays are (n_local, 3) fp64 torch tensors on the
-    rank's device; ``force_fn(pos_all, type_all, n_owned, local_params)`` returns
-    the forces on the first ``n_owned`` rows of ``pos_all`` (local coordinates).
-    """
+    rank's device; ``force_fn(pos_all, type_all, n_owned, local_params,
+    rebuild)`` returns the forces on the first ``n_owned`` rows of ``pos_all``
+    (local coordinates)."""
 
-    def __init__(self, dec: SlabDecomposition, pos, vel, type_id, mass, params, force_fn, ids=None,
+    def __init__(self, dec: GridDecomposition, pos, vel, type_id, mass, params, force_fn, ids=None,
                  comm_device=None):
         self.dec, self.params, self.force_fn = dec, params, force_fn
         self.comm_device = comm_device
@@ -131,56 +175,93 @@ class DecomposedSimulation:
         self.local_params = dec.local_params()
         self.since = 0
         self.iteration = 0
-        self.ghost_idx = (None, None)
+        self.plan = []   # per decomposed axis: (axis, left rows, right rows) of the combined set
 
     # -- exchange ------------------------------------------------------------
-    def _ghost_plan(self):
-        """Owned particles within ell of the left / right face (rebuild time)."""
-        d, ax = self.dec, self.dec.axis
-        z = d.near(self.pos[:, ax])
-        none = z.new_zeros(0, dtype=torch.long)
-        left = torch.nonzero(z < d.lo + d.ell).flatten() if d.has_left else none
-        right = torch.nonzero(z >= d.hi - d.ell).flatten() if d.has_right else none
-        self.ghost_idx = (left, right)
-
-    def _ghosts(self):
-        left, right = self.ghost_idx
-        pl, pr = self.pos[left], self.pos[right]
-        tl = self.type_id[left].to(pl.dtype).unsqueeze(1)
-        tr = self.type_id[right].to(pr.dtype).unsqueeze(1)
-        gl, gr = _exchange(torch.cat([pl, tl], 1), torch.cat([pr, tr], 1), self.dec, 4, pl.dtype,
-                           self.comm_device)
-        g = torch.cat([gl, gr], 0)
-        return g[:, :3].clone(), g[:, 3].to(self.type_id.dtype)
+    def _ghosts(self, replan: bool):
+        """Owned + ghost positions and types, axis by axis.  ``replan`` (rebuild
+        time) selects the rows within ell of each face; otherwise the stored
+        selection is re-sent with current positions."""
+        d = self.dec
+        cpos, ctype = self.pos, self.type_id
+        plan = [] if replan else self.plan
+        for k, a in enumerate(x for x in range(3) if d.active[x]):
+            if replan:
+                z = d.near(cpos[:, a], a)
+                none = z.new_zeros(0, dtype=torch.long)
+                left = torch.nonzero(z < d.lo[a] + d.ell).flatten() if d.has_left[a] else none
+                right = torch.nonzero(z >= d.hi[a] - d.ell).flatten() if d.has_right[a] else none
+                plan.append((a, left, right))
+            else:
+                _, left, right = plan[k]
+            pl, pr = cpos[left], cpos[right]
+            tl = ctype[left].to(pl.dtype).unsqueeze(1)
+            tr = ctype[right].to(pr.dtype).unsqueeze(1)
+            gl, gr = _exchange(torch.cat([pl, tl], 1), torch.cat([pr, tr], 1), d, a, 4, pl.dtype,
+                               self.comm_device)
+            g = torch.cat([gl, gr], 0)
+            cpos = torch.cat([cpos, g[:, :3]], 0)
+            ctype = torch.cat([ctype, g[:, 3].to(ctype.dtype)], 0)
+        if replan:
+            self.plan = plan
+        return cpos, ctype
 
     def _migrate(self):
-        """Particles that left [lo, hi) go to the neighbour with their state."""
-        d, ax = self.dec, self.dec.axis
-        if d.world == 1:
+        """Particles that left [lo, hi) go to the neighbours, axis by axis, with
+        their full state."""
+        d = self.dec
+        for a in range(3):
+            if not d.active[a]:
+                continue
+            z = d.near(self.pos[:, a], a)
+            go_left = z < d.lo[a]
+            go_right = z >= d.hi[a]
+            if d.coords[a] == 0 and not d.periodic[a]:
+                go_left = torch.zeros_like(go_left)
+            if d.coords[a] == d.dims[a] - 1 and not d.periodic[a]:
+                go_right = torch.zeros_like(go_right)
+            stay = ~(go_left | go_right)
+            pack = lambda m: torch.cat([self.pos[m], self.vel[m], self.force[m], self.old_force[m],
+                                        self.type_id[m].to(self.pos.dtype).unsqueeze(1),
+                                        self.ids[m].to(self.pos.dtype).unsqueeze(1)], 1)
+            fl, fr = _exchange(pack(go_left), pack(go_right), d, a, 14, self.pos.dtype,
+                               self.comm_device)
+            inc = torch.cat([fl, fr], 0)
+            self.pos = torch.cat([self.pos[stay], inc[:, 0:3]], 0)
+            self.vel = torch.cat([self.vel[stay], inc[:, 3:6]], 0)
+            self.force = torch.cat([self.force[stay], inc[:, 6:9]], 0)
+            self.old_force = torch.cat([self.old_force[stay], inc[:, 9:12]], 0)
+            self.type_id = torch.cat([self.type_id[stay], inc[:, 12].to(self.type_id.dtype)], 0)
+            self.ids = torch.cat([self.ids[stay], inc[:, 13].to(self.ids.dtype)], 0)
+
+    def _thermostat(self, target, max_delta_t):
+        """apply_thermostat (integrator.py:81-95) with the temperature reduced
+        over all ranks (sum of m|v|^2 and of the particle counts)."""
+        m = self.mass[self.type_id.long()]
+        ke = torch.sum(m * torch.sum(self.vel * self.vel, dim=1)).to(torch.float64)
+        red = torch.stack([ke, torch.tensor(float(self.pos.shape[0]), dtype=torch.float64,
+                                            device=ke.device)])
+        if self.dec.world > 1:
+            home = red.device
+            red = red.to(self.comm_device) if self.comm_device is not None else red
+            dist.all_reduce(red)
+            red = red.to(home)
+        ke, n = float(red[0]), float(red[1])
+        if n == 0:
+            raise ValueError("temperature of an empty particle set is undefined")
+        t_cur = ke / (3.0 * n)
+        if t_cur == 0.0:
+            if target > 0.0:
+                raise ValueError("thermostat cannot scale zero velocities toward a positive "
+                                 "target temperature")
             return
-        z = d.near(self.pos[:, ax])
-        go_left = z < d.lo
-        go_right = z >= d.hi
-        if d.rank == 0 and not d.periodic:
-            go_left = torch.zeros_like(go_left)
-        if d.rank == d.world - 1 and not d.periodic:
-            go_right = torch.zeros_like(go_right)
-        stay = ~(go_left | go_right)
-        pack = lambda m: torch.cat([self.pos[m], self.vel[m], self.force[m], self.old_force[m],
-                                    self.type_id[m].to(self.pos.dtype).unsqueeze(1),
-                                    self.ids[m].to(self.pos.dtype).unsqueeze(1)], 1)
-        fl, fr = _exchange(pack(go_left), pack(go_right), d, 14, self.pos.dtype, self.comm_device)
-        inc = torch.cat([fl, fr], 0)
-        self.pos = torch.cat([self.pos[stay], inc[:, 0:3]], 0)
-        self.vel = torch.cat([self.vel[stay], inc[:, 3:6]], 0)
-        self.force = torch.cat([self.force[stay], inc[:, 6:9]], 0)
-        self.old_force = torch.cat([self.old_force[stay], inc[:, 9:12]], 0)
-        self.type_id = torch.cat([self.type_id[stay], inc[:, 12].to(self.type_id.dtype)], 0)
-        self.ids = torch.cat([self.ids[stay], inc[:, 13].to(self.ids.dtype)], 0)
+        delta = min(max(target - t_cur, -max_delta_t), max_delta_t)
+        self.vel = self.vel * float(np.sqrt((t_cur + delta) / t_cur))
 
     # -- the loop ------------------------------------------------------------
     def step(self):
         p, dt = self.params, self.params.delta_t
+        d = self.dec
         m = self.mass[self.type_id.long()].unsqueeze(1)
         # drift_with_force + boundaries + F -> F_old (integrator.py:31-37, 98-128)
         self.pos = self.pos + self.vel * dt
@@ -198,18 +279,20 @@ class DecomposedSimulation:
         rebuild = self.iteration == 0 or self.since >= p.rebuild_interval
         if rebuild:
             self._migrate()
-            self._ghost_plan()
             m = self.mass[self.type_id.long()].unsqueeze(1)
-        gpos, gtype = self._ghosts()
+        pos_all, type_all = self._ghosts(replan=rebuild)
         n = self.pos.shape[0]
-        pos_all = torch.cat([self.pos, gpos], 0)
-        ax = self.dec.axis
-        pos_all[:, ax] = self.dec.near(pos_all[:, ax]) - self.dec.origin
-        type_all = torch.cat([self.type_id, gtype], 0)
+        pos_all = pos_all.clone()
+        for a in range(3):
+            if d.active[a]:
+                pos_all[:, a] = d.near(pos_all[:, a], a) - d.origin(a)
         self.force = self.force_fn(pos_all, type_all, n, self.local_params, rebuild)
         if p.gravity is not None:
             self.force[:, 2] += m[:, 0] * p.gravity
         self.vel = self.vel + (self.force + self.old_force) * (0.5 * dt / m)
+        thermo = getattr(p, "thermostat", None)
+        if thermo is not None and (self.iteration + 1) % thermo.interval_iterations == 0:
+            self._thermostat(thermo.target_temperature, thermo.max_delta_t)
         self.since = 0 if rebuild else self.since + 1
         self.iteration += 1
 
@@ -219,7 +302,8 @@ class DecomposedSimulation:
 
 
 def gpu_force_backend(config, sigma, epsilon, mass):
-    """libmdg as the per-rank force backend (owned + ghost rows, open slab box).
+    """libmdg as the per-rank force backend (owned + ghost rows, open box along
+    the decomposed axes).
 
     The row set (owned + ghosts) is fixed between rebuilds, so the device
     ParticleSet and its neighbour structure are rebuilt only at rebuild steps;

@@ -18,19 +18,27 @@ sys.path.insert(0, ROOT)
 from oracle import port  # noqa: E402
 
 import paper_2505_03438_b200 as P  # noqa: E402
-from paper_2505_03438_b200.decomp import DecomposedSimulation, SlabDecomposition  # noqa: E402
+from paper_2505_03438_b200.decomp import DecomposedSimulation, GridDecomposition  # noqa: E402
+
+SIZES = {"small": (6, 6, 9), "cube10": (10, 10, 10)}
 
 
-def system(seed=3, vscale=0.8):
-    """Jittered 6x6x9 lattice in a 8.4 x 8.4 x 12.6 periodic box."""
+def system(seed=3, vscale=0.8, size="small"):
+    """Jittered lattice with spacing 1.4 in a periodic box: "small" 6x6x9
+    (8.4 x 8.4 x 12.6), "cube10" 10x10x10 (14^3, room for a 2x2x2 grid)."""
     rng = np.random.default_rng(seed)
     a = 1.4
-    g = np.stack(np.meshgrid(np.arange(6), np.arange(6), np.arange(9), indexing="ij"), -1).reshape(-1, 3)
+    nx, ny, nz = SIZES[size]
+    g = np.stack(np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"), -1).reshape(-1, 3)
     pos = (g + 0.5) * a + rng.uniform(-0.1, 0.1, g.shape)
     vel = rng.normal(0.0, vscale, pos.shape)
     vel -= vel.mean(0)
-    L = np.array([6 * a, 6 * a, 9 * a])
+    L = np.array([nx * a, ny * a, nz * a])
     return pos, vel, L
+
+
+def thermostat():
+    return P.ThermostatParams(0.9, 0.05, 3)
 
 
 def oracle_force_fn(pos_all, type_all, n_owned, local_params, rebuild):
@@ -40,15 +48,17 @@ def oracle_force_fn(pos_all, type_all, n_owned, local_params, rebuild):
     return torch.as_tensor(f[:n_owned])
 
 
-def run(rank, world, port_no, steps, out_path, vscale=0.8, dt=2e-3, backend="oracle"):
+def run(rank, world, port_no, steps, out_path, vscale=0.8, dt=2e-3, backend="oracle",
+        dims=None, size="small", thermo=False):
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ["MASTER_PORT"] = str(port_no)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    pos, vel, L = system(vscale=vscale)
+    pos, vel, L = system(vscale=vscale, size=size)
     params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=4,
-                                delta_t=dt, boundary=(P.PERIODIC,) * 3)
-    dec = SlabDecomposition(params, rank, world, axis=2)
-    mine = np.flatnonzero(dec.owner_of(pos[:, 2]) == rank)
+                                delta_t=dt, boundary=(P.PERIODIC,) * 3,
+                                thermostat=thermostat() if thermo else None)
+    dec = GridDecomposition(params, rank, world, dims or (1, 1, world))
+    mine = np.flatnonzero(dec.owner_of_positions(pos) == rank)
     if backend == "gpu":   # libmdg on the (single) GPU, messages staged on the host for gloo
         from paper_2505_03438_b200.decomp import gpu_force_backend
         dev = torch.device("cuda", 0)
@@ -83,4 +93,7 @@ if __name__ == "__main__":
     vs = float(sys.argv[6]) if len(sys.argv) > 6 else 0.8
     dt = float(sys.argv[7]) if len(sys.argv) > 7 else 2e-3
     be = sys.argv[8] if len(sys.argv) > 8 else "oracle"
-    run(r, w, pn, st, out, vs, dt, be)
+    dims = tuple(int(x) for x in sys.argv[9].split("x")) if len(sys.argv) > 9 and sys.argv[9] != "-" else None
+    size = sys.argv[10] if len(sys.argv) > 10 else "small"
+    th = len(sys.argv) > 11 and sys.argv[11] == "1"
+    run(r, w, pn, st, out, vs, dt, be, dims, size, th)

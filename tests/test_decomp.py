@@ -1,8 +1,10 @@
-"""Domain decomposition on CPU: world_size 2 over gloo.
+"""Domain decomposition on CPU over gloo: z-slabs with 2
+ranks (configs 3 / 4) and 2x2x1 / 2x2x2 process grids (config 5).
 
-The decomposed loop (slabs along z, per-step ghost exchange, migration at
-rebuilds) must reproduce the single-rank run and the reference loop (oracle
-restatement of simulation.py:126-197) on the same seeded system.
+The decomposed loop (per-step ghost exchange axis by axis, migration at
+rebuilds, the thermostat's all-reduced temperature) must reproduce the
+single-rank run and the reference loop (oracle restatement of
+simulation.py:126-197) on the same seeded system.
 """
 
 import os
@@ -24,14 +26,16 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _run(world, steps, tmp_path, vscale=0.8, dt=2e-3, tag="", backend="oracle"):
-    out = str(tmp_path / f"decomp_{world}{tag}{backend}.npy")
+def _run(world, steps, tmp_path, vscale=0.8, dt=2e-3, tag="", backend="oracle", dims=None,
+         size="small", thermo=False):
+    out = str(tmp_path / f"decomp_{world}{tag}{backend}{size}{int(thermo)}.npy")
     port = _free_port()
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
     if backend != "gpu":
         env["CUDA_VISIBLE_DEVICES"] = ""
+    dim_arg = "x".join(str(d) for d in dims) if dims else "-"
     procs = [subprocess.Popen([sys.executable, WORKER, str(r), str(world), str(port), str(steps), out,
-                               str(vscale), str(dt), backend],
+                               str(vscale), str(dt), backend, dim_arg, size, "1" if thermo else "0"],
                               env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
              for r in range(world)]
     logs = [p.communicate(timeout=600)[0].decode() for p in procs]
@@ -109,3 +113,60 @@ def test_decomposed_gpu_backend_matches_reference_loop(tmp_path):
     d -= L * np.rint(d / L)
     assert np.abs(d).max() <= 1e-9
     assert np.abs(two[:, 4:7] - np.asarray(p.velocities)).max() <= 1e-9
+
+
+@pytest.fixture(scope="module")
+def grid_runs(tmp_path_factory):
+    tmp = tmp_path_factory.mktemp("grid")
+    kw = dict(vscale=2.0, dt=3e-3, size="cube10")
+    return {"1": _run(1, 24, tmp, tag="g1", **kw),
+            "2x2x1": _run(4, 24, tmp, tag="g4", dims=(2, 2, 1), **kw),
+            "2x2x2": _run(8, 24, tmp, tag="g8", dims=(2, 2, 2), **kw)}
+
+
+@pytest.mark.parametrize("grid", ["2x2x1", "2x2x2"])
+def test_process_grids_match_one_rank(grid_runs, grid):
+    """Config-5 style 3-D grids: edge and corner ghosts arrive through the
+    axis-by-axis exchange; every particle owned once; same trajectory."""
+    one, many = grid_runs["1"], grid_runs[grid]
+    assert np.array_equal(one[:, 0], many[:, 0])
+    L = np.array([14.0, 14.0, 14.0])
+    d = many[:, 1:4] - one[:, 1:4]
+    d -= L * np.rint(d / L)
+    assert np.abs(d).max() <= 1e-10
+    assert np.abs(many[:, 4:7] - one[:, 4:7]).max() <= 1e-10
+    assert len(np.unique(many[:, 7])) == int(np.prod([int(x) for x in grid.split("x")]))
+
+
+def test_grid_with_thermostat_matches_reference_loop(tmp_path):
+    """2x2x2 ranks with the thermostat (all-reduced temperature, config 4's
+    quench mechanism) against the reference loop with the same thermostat."""
+    from conftest import ScriptedController  # noqa: F401  (fixture module import)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from decomp_worker import system, thermostat
+    from oracle import port
+    many = _run(8, 18, tmp_path, vscale=2.0, dt=3e-3, tag="th", dims=(2, 2, 2), size="cube10",
+                thermo=True)
+    pos, vel, L = system(vscale=2.0, size="cube10")
+    params = port.Params(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=4, delta_t=3e-3,
+                         boundary=(port.PERIODIC,) * 3, thermostat=thermostat())
+
+    class Fixed:
+        mode = "steady"
+
+        def configuration_for_iteration(self, it):
+            return port.parse("VL-List_Iter-NoN3L-AoS"), False
+
+        def record_timings(self, f, b):
+            pass
+
+        def record_failure(self, e=None):
+            return False
+
+    p = port.Particles(pos, vel)
+    port.simulate_controlled(p, params, Fixed(), steps=18)
+    d = many[:, 1:4] - np.asarray(p.positions)
+    d -= L * np.rint(d / L)
+    assert np.abs(d).max() <= 1e-9
+    assert np.abs(many[:, 4:7] - np.asarray(p.velocities)).max() <= 1e-9
+

@@ -222,6 +222,20 @@ int mdg_host_finish_kick_range(int64_t n, int64_t begin, int64_t end, int layout
 int mdg_host_step(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, double* force,
                   double* old_force, const int32_t* type_id, const double* mass, double dt,
                   int has_gravity, double gravity, int rebuild, int chunks, int* blowup);
+/* The same with flags: MDG_HOST_STEP_SWAPPED = the caller swapped its force
+ * and old_force buffers before the call (old_force holds the current forces,
+ * force is scratch), which makes the drift's F -> F_old copy unnecessary; the
+ * state after the step is identical. */
+#define MDG_HOST_STEP_SWAPPED 1
+int mdg_host_step_ex(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, double* force,
+                     double* old_force, const int32_t* type_id, const double* mass, double dt,
+                     int has_gravity, double gravity, int rebuild, int chunks, int flags, int* blowup);
+/* mdg_host_drift_wrap_range reading the current forces from old_force
+ * without copying (swapped != 0), see MDG_HOST_STEP_SWAPPED. */
+int mdg_host_drift_wrap_range_ex(int64_t n, int64_t begin, int64_t end, int layout, double* pos,
+                                 double* vel, const double* force, double* old_force,
+                                 const int32_t* type_id, const double* mass, const double domain[3],
+                                 const int periodic[3], double dt, int swapped, int* blowup);
 
 /* Measured FP64 FMA throughput of this device (roofline denominator):
  * dependent-chain DFMA microbenchmark, TFLOP/s (2 flops per DFMA). */

@@ -3,6 +3,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <string>
 
 #include "../../include/mdg.h"
@@ -476,6 +478,13 @@ int mdg_d2h(mdg_ctx* ctx, void* host, const void* dev, size_t bytes) {
 int mdg_host_step(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, double* force,
                   double* old_force, const int32_t* type_id, const double* mass, double dt,
                   int has_gravity, double gravity, int rebuild, int chunks, int* blowup) {
+    return mdg_host_step_ex(ctx, cfg, pos, vel, force, old_force, type_id, mass, dt, has_gravity,
+                            gravity, rebuild, chunks, 0, blowup);
+}
+
+int mdg_host_step_ex(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, double* force,
+                     double* old_force, const int32_t* type_id, const double* mass, double dt,
+                     int has_gravity, double gravity, int rebuild, int chunks, int flags, int* blowup) {
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;
     if (int e = need_system(ctx)) return e;
@@ -501,12 +510,15 @@ int mdg_host_step(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel,
         }
         return cudaSuccess;
     };
+    static int timing = getenv("MDG_HOST_STEP_TIMING") ? 1 : 0;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = now();
     int bad = 0;
     for (int k = 0; k < K; ++k) {
         int64_t a = n * k / K, b = n * (k + 1) / K;
         int bk = 0;
-        mdg_host_drift_wrap_range(n, a, b, c.layout, pos, vel, force, old_force, type_id, mass, c.L,
-                                  periodic, dt, &bk);
+        mdg_host_drift_wrap_range_ex(n, a, b, c.layout, pos, vel, force, old_force, type_id, mass,
+                                     c.L, periodic, dt, flags & MDG_HOST_STEP_SWAPPED, &bk);
         bad |= bk;
         if (copy(c.pos, pos, a, b, cudaMemcpyHostToDevice) != cudaSuccess) return cuda_status("h2d");
     }
@@ -515,6 +527,7 @@ int mdg_host_step(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel,
         cudaStreamSynchronize(c.stream);
         return cuda_status("mdg_host_step");
     }
+    auto t1 = now();
     if (rebuild)
         if (int e = mdg_rebuild(ctx, cfg)) return e;
     if (int e = mdg_refresh(ctx, cfg)) return e;
@@ -524,11 +537,22 @@ int mdg_host_step(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel,
         if (copy(force, c.force, a, b, cudaMemcpyDeviceToHost) != cudaSuccess) return cuda_status("d2h");
         cudaEventRecord(c.chunk_ev[k], c.stream);
     }
+    auto t2 = now();
+    double wait_us = 0.0;
     for (int k = 0; k < K; ++k) {
         int64_t a = n * k / K, b = n * (k + 1) / K;
+        auto w0 = now();
         if (cudaEventSynchronize(c.chunk_ev[k]) != cudaSuccess) return cuda_status("d2h wait");
+        wait_us += std::chrono::duration<double, std::micro>(now() - w0).count();
         mdg_host_finish_kick_range(n, a, b, c.layout, vel, force, old_force, type_id, mass, dt,
                                    has_gravity, gravity);
+    }
+    if (timing) {
+        auto t3 = now();
+        auto us = [](auto x, auto y) { return std::chrono::duration<double, std::micro>(y - x).count(); };
+        fprintf(stderr, "host_step: drift+h2d %.0f us, device enqueue %.0f us, d2h waits %.0f us, "
+                        "kicks %.0f us, total %.0f us%s\n",
+                us(t0, t1), us(t1, t2), wait_us, us(t2, t3) - wait_us, us(t0, t3), rebuild ? " (rebuild)" : "");
     }
     return cuda_status("mdg_host_step");
 }

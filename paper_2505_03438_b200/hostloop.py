@@ -187,12 +187,15 @@ class HostSimulation:
             if tid is None:
                 tid = np.asarray(p.type_id, dtype=np.int32)
             bad = ctypes.c_int()
-            check(lib().mdg_host_step(calc.ctx.h, ctypes.byref(_lib.config_struct(cfg)), _ptr(p.pos),
-                                      _ptr(p.vel), _ptr(p.force), _ptr(p.old_force),
-                                      _ptr(tid) if len(mass) > 1 else None, _ptr(mass),
-                                      float(params.delta_t), int(params.gravity is not None),
-                                      float(params.gravity or 0.0), int(rebuild), self.chunks,
-                                      ctypes.byref(bad)), "host step")
+            # F -> F_old by swapping the two buffers instead of copying (the
+            # state after the step is the same, MDG_HOST_STEP_SWAPPED)
+            p.force, p.old_force = p.old_force, p.force
+            check(lib().mdg_host_step_ex(calc.ctx.h, ctypes.byref(_lib.config_struct(cfg)), _ptr(p.pos),
+                                         _ptr(p.vel), _ptr(p.force), _ptr(p.old_force),
+                                         _ptr(tid) if len(mass) > 1 else None, _ptr(mass),
+                                         float(params.delta_t), int(params.gravity is not None),
+                                         float(params.gravity or 0.0), int(rebuild), self.chunks,
+                                         1, ctypes.byref(bad)), "host step")
             if bad.value:
                 raise BlowUpError("particle left the domain by more than one domain length "
                                   "(or position is not finite)")

@@ -108,6 +108,12 @@ int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg);
  * as its own kernel.  Same arithmetic either way.  Asynchronous. */
 int mdg_compute_kick(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gravity,
                      double gravity);
+/* One steady-state loop iteration (no rebuild due): drift_wrap + refresh +
+ * compute + finish_kick, replayed from a CUDA graph captured on first use and
+ * re-captured whenever the configuration, dt / gravity, the bound arrays or
+ * the container (any rebuild) changed.  Ordered on the context stream;
+ * asynchronous.  MDG_ESTATE before the first rebuild. */
+int mdg_step_graph(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gravity, double gravity);
 /* ForceCalculator.last_eval_count (containers.py:454): synchronises. */
 int mdg_eval_count(mdg_ctx* ctx, int64_t* count);
 /* Shifted LJ potential energy of the bound positions (no reference

@@ -27,7 +27,7 @@ EXPORTS = (
     "mdg_profile", "mdg_profile_read", "mdg_synchronize", "mdg_h2d", "mdg_d2h", "mdg_geometry", "mdg_stencil", "mdg_get_grid",
     "mdg_get_verlet", "mdg_geometry_for", "mdg_stencil_for", "mdg_host_drift_wrap",
     "mdg_host_finish_kick", "mdg_measure_fp64_peak", "mdg_temperature", "mdg_thermostat",
-    "mdg_live_stats", "mdg_compute_kick", "mdg_host_step", "mdg_host_step_ex",
+    "mdg_live_stats", "mdg_compute_kick", "mdg_step_graph", "mdg_host_step", "mdg_host_step_ex",
     "mdg_host_drift_wrap_range_ex", "mdg_d2h_async", "mdg_host_drift_wrap_range", "mdg_host_finish_kick_range",
 )
 FLAG_BLOWUP, FLAG_THERMO_ZERO = 1, 2
@@ -86,6 +86,7 @@ def _declare(L):
         "mdg_live_stats": (I, [P, P]),
         "mdg_d2h_async": (I, [P, P, P, SZ]),
         "mdg_compute_kick": (I, [P, CFG, D, I, D]),
+        "mdg_step_graph": (I, [P, CFG, D, I, D]),
         "mdg_host_step": (I, [P, CFG, P, P, P, P, P, P, D, I, D, I, I, ctypes.POINTER(I)]),
         "mdg_host_step_ex": (I, [P, CFG, P, P, P, P, P, P, D, I, D, I, I, I, ctypes.POINTER(I)]),
         "mdg_host_drift_wrap_range_ex": (I, [I64, I64, I64, I, P, P, P, P, P, P, P, P, D, I, ctypes.POINTER(I)]),

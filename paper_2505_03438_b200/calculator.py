@@ -123,6 +123,17 @@ class ForceCalculator:
         self.compute_async(particles, config)
         return self.last_eval_count
 
+    def step_graph(self, particles, config, dt, gravity=None):
+        """One steady-state iteration (drift + refresh + compute + kick) from
+        a cached CUDA graph (mdg_step_graph); asynchronous."""
+        if particles.layout != config.layout:
+            raise ValueError(f"particle layout {particles.layout} does not match "
+                             f"configuration {config.id}")
+        self.bind(particles)
+        check(lib().mdg_step_graph(self.ctx.h, ctypes.byref(config_struct(config)), float(dt),
+                                   int(gravity is not None), float(gravity or 0.0)), "step_graph")
+        self._count_pending = True
+
     def compute_kick_async(self, particles, config, dt, gravity=None):
         """compute + apply_gravity + finish_kick (simulation.py:169-185), the
         kick fused into the force walk where the configuration allows."""

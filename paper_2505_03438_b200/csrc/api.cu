@@ -167,6 +167,10 @@ int mdg_destroy(mdg_ctx* ctx) {
     if (ctx->c.h_scal) cudaFreeHost(ctx->c.h_scal);
     for (cudaEvent_t e : ctx->c.ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->c.chunk_ev) cudaEventDestroy(e);
+    if (ctx->c.step_exec) cudaGraphExecDestroy(ctx->c.step_exec);
+    if (ctx->c.graph_in) cudaEventDestroy(ctx->c.graph_in);
+    if (ctx->c.graph_out) cudaEventDestroy(ctx->c.graph_out);
+    if (ctx->c.graph_stream) cudaStreamDestroy(ctx->c.graph_stream);
     delete ctx;
     return MDG_OK;
 }
@@ -255,6 +259,9 @@ int mdg_bind(mdg_ctx* ctx, int64_t n, int layout, double* pos, double* vel, doub
         c.vl.built = false;
         c.vcl.built = false;
     }
+    if (n != c.n || layout != c.layout || pos != c.pos || vel != c.vel || force != c.force ||
+        old_force != c.old_force || type_id != c.tid)
+        ++c.gen;
     c.n = n;
     c.layout = layout;
     c.pos = pos;
@@ -270,6 +277,7 @@ int mdg_rebuild(mdg_ctx* ctx, const mdg_config* cfg) {
     if (int e = validate(cfg)) return e;
     if (int e = need_system(ctx)) return e;
     Context& c = ctx->c;
+    ++c.gen;
     if (cfg->container == MDG_VL) {
         if (vl_rebuild(c)) return MDG_ECUDA;
     } else if (cfg->container == MDG_VCL) {
@@ -354,6 +362,95 @@ int mdg_compute_kick(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gra
     if (int e = mdg_compute(ctx, cfg)) return e;
     integ_finish_kick(c, dt, has_gravity, gravity);
     return cuda_status("mdg_compute_kick");
+}
+
+int mdg_step_graph(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gravity, double gravity) {
+    CHECK_CTX(ctx);
+    if (int e = validate(cfg)) return e;
+    if (int e = need_system(ctx)) return e;
+    Context& c = ctx->c;
+    if (c.layout != cfg->layout) {
+        set_error("particle layout does not match the configuration");
+        return MDG_EINVAL;
+    }
+    bool built = cfg->container == MDG_VL ? c.vl.built
+               : cfg->container == MDG_VCL ? c.vcl.built
+               : grid_for(c, cfg->csf)->built;
+    if (!built) { set_error("mdg_step_graph before rebuild"); return MDG_ESTATE; }
+    if (!c.graph_stream) {
+        if (cudaStreamCreateWithFlags(&c.graph_stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c.graph_in, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c.graph_out, cudaEventDisableTiming) != cudaSuccess)
+            return cuda_status("graph stream");
+    }
+    struct Key {
+        mdg_config cfg;
+        double dt, gravity;
+        int has_gravity;
+        uint64_t gen;
+        const void* stream;
+    } key;
+    memset(&key, 0, sizeof key);
+    key.cfg = *cfg;
+    key.dt = dt;
+    key.gravity = gravity;
+    key.has_gravity = has_gravity;
+    key.gen = c.gen;
+    key.stream = c.stream;
+    static_assert(sizeof(Key) <= sizeof(c.step_key), "graph key");
+    if (!c.step_exec || memcmp(&key, c.step_key, sizeof key) != 0) {
+        if (c.step_exec) {
+            cudaGraphExecDestroy(c.step_exec);
+            c.step_exec = nullptr;
+        }
+        // capture drift + refresh + compute + kick on the private stream
+        cudaStream_t home = c.stream;
+        bool prof = c.prof;
+        c.stream = c.graph_stream;
+        c.prof = false;
+        cudaGraph_t graph = nullptr;
+        int err = MDG_OK;
+        if (cudaStreamBeginCapture(c.graph_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            err = MDG_ECUDA;
+        } else {
+            integ_drift_wrap(c, dt);
+            if (cfg->container == MDG_LC) {
+                Grid& gr = *grid_for(c, cfg->csf);
+                grid_refresh(c, gr, cfg->layout);
+            }
+            cudaMemsetAsync(c.scal.p, 0, sizeof(unsigned long long), c.stream);
+            if (cfg->container == MDG_VCL) {
+                vcl_compute(c, cfg->newton3);
+            } else if (cfg->container == MDG_VL) {
+                if (cfg->precision == MDG_FP32) vl_compute32(c);
+                else vl_compute(c, cfg->layout);
+            } else {
+                Grid& gr = *grid_for(c, cfg->csf);
+                lc_compute(c, gr, cfg->traversal, cfg->newton3, cfg->layout);
+                lc_fold_forces(c, gr, cfg->layout, cfg->traversal != MDG_C01);
+            }
+            integ_finish_kick(c, dt, has_gravity, gravity);
+            if (cudaStreamEndCapture(c.graph_stream, &graph) != cudaSuccess || !graph) err = MDG_ECUDA;
+        }
+        c.stream = home;
+        c.prof = prof;
+        if (err == MDG_OK && cudaGraphInstantiate(&c.step_exec, graph, 0) != cudaSuccess) err = MDG_ECUDA;
+        if (graph) cudaGraphDestroy(graph);
+        if (err != MDG_OK) {
+            c.step_exec = nullptr;
+            return cuda_status("step graph capture");
+        }
+        memcpy(c.step_key, &key, sizeof key);
+    }
+    // order against the context stream on both sides
+    if (cudaEventRecord(c.graph_in, c.stream) != cudaSuccess ||
+        cudaStreamWaitEvent(c.graph_stream, c.graph_in, 0) != cudaSuccess ||
+        cudaGraphLaunch(c.step_exec, c.graph_stream) != cudaSuccess ||
+        cudaEventRecord(c.graph_out, c.graph_stream) != cudaSuccess ||
+        cudaStreamWaitEvent(c.stream, c.graph_out, 0) != cudaSuccess)
+        return cuda_status("step graph launch");
+    note_launch();
+    return MDG_OK;
 }
 
 int mdg_eval_count(mdg_ctx* ctx, int64_t* count) {

@@ -174,6 +174,12 @@ struct Context {
     // (bit 0 blow-up, bit 1 thermostat at T = 0)
     DBuf<unsigned long long> scal;
     unsigned long long* h_scal = nullptr;   // pinned mirror
+    // cached steady-state step graph (mdg_step_graph)
+    uint64_t gen = 0;                       // bumped by every rebuild / rebind
+    cudaStream_t graph_stream = nullptr;
+    cudaEvent_t graph_in = nullptr, graph_out = nullptr;
+    cudaGraphExec_t step_exec = nullptr;
+    unsigned char step_key[96] = {0};       // what the cached graph was captured for
     DBuf<unsigned long long> scan_tmp;      // block partials for scans
     // optional CUDA-event bracketing of the force kernels (mdg_profile)
     bool prof = false;

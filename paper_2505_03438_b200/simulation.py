@@ -103,7 +103,7 @@ class Simulation:
     anything with the TuningController protocol (tuning.py:200-239)."""
 
     def __init__(self, particles, params, config=None, calculator=None, controller=None,
-                 tuning_interval=None):
+                 tuning_interval=None, graphs=False):
         if controller is None:
             if config is None:
                 raise ValueError("need a configuration or a controller")
@@ -119,6 +119,9 @@ class Simulation:
         self.iteration = 0
         self._events = []
         self._records = []
+        # steady-state iterations (no rebuild, not timed) from a cached CUDA
+        # graph of drift + refresh + compute + kick (mdg_step_graph)
+        self.graphs = graphs
 
     @property
     def config(self):
@@ -139,9 +142,17 @@ class Simulation:
     def step(self, record=False):
         p, params, calc, ctl = self.p, self.params, self.calc, self.controller
         it = self.iteration
+        if self.graphs and not record and self._graph_step(it):
+            return False
         calc.drift_wrap(p, params.delta_t)
+        pending = getattr(self, "_pending", None)
+        self._pending = None
         while True:
-            cfg, forced = ctl.configuration_for_iteration(it)
+            if pending is not None:
+                cfg, forced = pending
+                pending = None
+            else:
+                cfg, forced = ctl.configuration_for_iteration(it)
             rebuild = forced or self.active != cfg.id or self.since >= params.rebuild_interval
             trial = self._trial()
             if rebuild and it:
@@ -187,6 +198,25 @@ class Simulation:
         self.iteration += 1
         return rebuild
 
+    def _graph_step(self, it) -> bool:
+        """Steady-state iteration from the step graph; False when this
+        iteration needs the eager path (rebuild due, trial, layout change)."""
+        p, params, ctl = self.p, self.params, self.controller
+        if self.active is None or self.since >= params.rebuild_interval or self._trial():
+            return False
+        cfg, forced = ctl.configuration_for_iteration(it)
+        if forced or cfg.id != self.active or p.layout != cfg.layout or self._trial():
+            # hand the (already answered) query to the eager path
+            self._pending = (cfg, forced)
+            return False
+        self.calc.step_graph(p, cfg, params.delta_t, params.gravity)
+        thermo = params.thermostat
+        if thermo is not None and (it + 1) % thermo.interval_iterations == 0:
+            self.calc.thermostat(p, thermo.target_temperature, thermo.max_delta_t)
+        self.since += 1
+        self.iteration += 1
+        return True
+
     def run(self, steps, record=True):
         for _ in range(steps):
             self.step(record=record)
@@ -219,7 +249,7 @@ def _is_configuration(obj) -> bool:
 
 def simulate(particles, params, strategy, *, tuning_interval=1000, samples_per_config=3,
              space=None, name="simulation", raise_errors=False, steps=None, record=True,
-             controller=None, controller_cls=None) -> SimulationReport:
+             controller=None, controller_cls=None, graphs=False) -> SimulationReport:
     """simulation.py:126-197 on the device.
 
     ``strategy`` is a Configuration, a FixedStrategy (anything with
@@ -255,7 +285,7 @@ def simulate(particles, params, strategy, *, tuning_interval=1000, samples_per_c
     strategy_name = getattr(strategy, "name", None) or ("fixed" if fixed is not None else "tuned")
     rep = SimulationReport(name=name, strategy_name=str(strategy_name))
     sim = Simulation(particles, params, fixed, calculator=calc, controller=controller,
-                     tuning_interval=tuning_interval)
+                     tuning_interval=tuning_interval, graphs=graphs)
     try:
         sim.run(steps, record=record)
         sim.check()

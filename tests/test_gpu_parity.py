@@ -594,3 +594,27 @@ def test_full_size_energy_conservation(pkg, config2_snapshot):
     sim.check()
     e1 = energy()
     assert abs(e1 - e0) / abs(e0) <= 1e-4, (e0, e1)
+
+
+def test_step_graph_is_bit_identical(pkg):
+    """§8(f) row 1, CUDA-graph steady state: the loop with steady-state
+    iterations replayed from the captured step graph (re-captured after every
+    rebuild) equals the eager loop bit for bit (LC, VL, VCL; thermostat and
+    gravity on)."""
+    P, calc = pkg
+    from paper_2505_03438_b200.simulation import simulate
+    z = golden("traj_small.npz")
+    L = z["domain"]
+    for cid in ("VL-List_Iter-NoN3L-AoS", "LC-C08-N3L-SoA-CSF1", "VCL-ClusterIter-NoN3L-AoS"):
+        out = []
+        for graphs in (False, True):
+            params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=4,
+                                        delta_t=1e-3, boundary=(P.PERIODIC,) * 3, gravity=-0.3,
+                                        thermostat=P.ThermostatParams(0.9, 0.05, 5))
+            parts = P.ParticleSet(z["pos0"], z["vel0"], layout=P.parse_configuration(cid).layout)
+            rep = simulate(parts, params, P.parse_configuration(cid), steps=23, record=False,
+                           graphs=graphs, raise_errors=True)
+            assert rep.error is None
+            out.append((parts.numpy("pos"), parts.numpy("vel"), parts.numpy("force")))
+        for a, b in zip(*out):
+            assert np.array_equal(a, b), cid

@@ -652,28 +652,30 @@ int vlt_build(Context& c) {
         vlt_desc_kernel<<<blocks_for(ntiles, 128), 128, 0, c.stream>>>(gv, tp, ntiles, v.cap4, budget,
                                                                        desc, v.tsize.p, nbig), note_launch();
         exclusive_scan_i32(v.tsize.p, v.tbase.p, ntiles, c.scal.p + 1, c.scan_tmp, c.stream);
-        MDG_CUDA(cudaMemcpyAsync(c.h_scal + 1, c.scal.p + 1, sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, c.stream));
-        MDG_CUDA(cudaMemcpyAsync(c.h_scal + 7, c.scal.p + 7, sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, c.stream));
-        MDG_CUDA(cudaStreamSynchronize(c.stream));
-        long long total = (long long)c.h_scal[1];
-        big = (int)(c.h_scal[7] & 0xffffffffu);
-        if (total > (1ll << 31) - 64) return 1;   // keep the row-space walk
-        v.tl.ensure((size_t)total + 8);
-        v.tcnt.ensure((size_t)total / v.cap4 + 32);
+        // the lists get an upper-bound allocation (every tile's rows padded to
+        // whole 32-row blocks), so the exact size is not needed on the host
+        // before the build: one synchronisation per rebuild instead of two
+        long long bound = ((long long)c.n + 32ll * ntiles) * v.cap4;
+        if (bound > (1ll << 31) - 64) return 1;   // keep the row-space walk
+        v.tl.ensure((size_t)bound + 8);
+        v.tcnt.ensure((size_t)bound / v.cap4 + 32);
         if (!v.tl.p || !v.tcnt.p) {
             set_error("out of device memory (VL tile lists)");
             return -1;
         }
         MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
-        MDG_CUDA(cudaMemsetAsync(v.tcnt.p, 0, ((size_t)total / v.cap4 + 32) * sizeof(int), c.stream));
+        MDG_CUDA(cudaMemsetAsync(v.tcnt.p, 0, ((size_t)bound / v.cap4 + 32) * sizeof(int), c.stream));
         vlt_build_kernel<<<ntiles, kBuildThreadsT, 0, c.stream>>>(
             gv, desc, v.tbase.p, v.b32.p, gr.spos4.p, maxabs, ell2, v.cap, v.cap4, v.tl.p, v.tcnt.p,
             maxcnt, gr.sort_by_z), note_launch();
         int hmax = 0;
         MDG_CUDA(cudaMemcpyAsync(&hmax, maxcnt, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        MDG_CUDA(cudaMemcpyAsync(c.h_scal + 1, c.scal.p + 1, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, c.stream));
+        MDG_CUDA(cudaMemcpyAsync(c.h_scal + 7, c.scal.p + 7, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, c.stream));
         MDG_CUDA(cudaStreamSynchronize(c.stream));
+        big = (int)(c.h_scal[7] & 0xffffffffu);
         if (hmax <= v.cap) break;
         v.cap = (hmax + hmax / 8 + 7) / 8 * 8;
     }

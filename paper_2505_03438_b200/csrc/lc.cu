@@ -322,6 +322,257 @@ __global__ void __launch_bounds__(128) lc_c08_kernel(GridView gv, ScratchPos<LAY
     warp_count(counter, cnt);
 }
 
+// ------------------------------------------------------------------ colour rows
+//
+// The same colour schedules with row-level threads instead of warp tiles:
+// thread = (unit of the colour, row slot), unit = a C18 base cell or a C08
+// anchor block.  A row walks exactly the cell pairs its unit assigns to its
+// cell, keeps f_i in registers and adds the reactions (N3L) / reverse
+// evaluations (NoN3L) with fp64 atomics; same-colour units touch disjoint
+// cells, so the atomics never collide across units.  Pair sets and counts are
+// those of the tiles; with small cells (CSF 0.5: ~2 rows per cell) a 32x32
+// tile keeps 2-3 lanes busy, a row slot keeps all of them.
+
+template <int LAYOUT, bool MT, bool N3L>
+__device__ __forceinline__ void row_vs_range(const ScratchPos<LAYOUT>& sp, const ScratchForce<LAYOUT>& sf,
+                                             const LJTab& tab, int j0, int j1, double xi, double yi,
+                                             double zi, int ti, double& fx, double& fy, double& fz,
+                                             unsigned& cnt) {
+    for (int j = j0; j < j1; ++j) {
+        double dx, dy, dz, fs;
+        int tj;
+        if (pair_force<LAYOUT, MT>(sp, tab, j, xi, yi, zi, ti, dx, dy, dz, fs, tj)) {
+            fx += fs * dx;
+            fy += fs * dy;
+            fz += fs * dz;
+            if (N3L) {
+                ++cnt;
+                atomicAdd(sf.at(j, 0), -(fs * dx));
+                atomicAdd(sf.at(j, 1), -(fs * dy));
+                atomicAdd(sf.at(j, 2), -(fs * dz));
+            } else {
+                double bx = -dx, by = -dy, bz = -dz;
+                double s2, e24;
+                lj_params<MT>(tab, tj, ti, s2, e24);
+                double gs = lj_fs(bx * bx + by * by + bz * bz, s2, e24);
+                cnt += 2;
+                atomicAdd(sf.at(j, 0), gs * bx);
+                atomicAdd(sf.at(j, 1), gs * by);
+                atomicAdd(sf.at(j, 2), gs * bz);
+            }
+        }
+    }
+}
+
+// C18 rows: unit = base cell of the colour (kernels.py:493-537 per base).
+template <int LAYOUT, bool MT, bool N3L>
+__global__ void __launch_bounds__(128) lc_c18_rows_kernel(GridView gv, ScratchPos<LAYOUT> sp,
+                                                          ScratchForce<LAYOUT> sf, LJTab tab,
+                                                          Stencil st, ColourLaunch cl, int S,
+                                                          unsigned long long* counter) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    int unit = t / S, slot = t % S;
+    unsigned cnt = 0;
+    int total = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
+    if (unit < total) {
+        int kz = unit % cl.cnt[2], u2 = unit / cl.cnt[2];
+        int ky = u2 % cl.cnt[1], kx = u2 / cl.cnt[1];
+        int bx = cl.lo[0] + cl.p[0] + kx * cl.stride[0];
+        int by = cl.lo[1] + cl.p[1] + ky * cl.stride[1];
+        int bz = cl.lo[2] + cl.p[2] + kz * cl.stride[2];
+        int c1 = gv.flat(bx, by, bz);
+        int s1 = gv.start[c1], e1 = gv.start[c1 + 1];
+        for (int r = s1 + slot; r < e1; r += S) {
+            double xi, yi, zi;
+            int ti;
+            sp.load(r, xi, yi, zi, ti);
+            double fx = 0.0, fy = 0.0, fz = 0.0;
+            row_vs_range<LAYOUT, MT, N3L>(sp, sf, tab, r + 1, e1, xi, yi, zi, ti, fx, fy, fz, cnt);
+            for (int k = 0; k < st.n; ++k) {
+                int x2 = bx + st.d[k][0], y2 = by + st.d[k][1], z2 = bz + st.d[k][2];
+                if (!gv.in_grid(x2, y2, z2)) continue;
+                int c2 = gv.flat(x2, y2, z2);
+                row_vs_range<LAYOUT, MT, N3L>(sp, sf, tab, gv.start[c2], gv.start[c2 + 1], xi, yi, zi,
+                                              ti, fx, fy, fz, cnt);
+            }
+            atomicAdd(sf.at(r, 0), fx);
+            atomicAdd(sf.at(r, 1), fy);
+            atomicAdd(sf.at(r, 2), fz);
+        }
+    }
+    warp_count(counter, cnt);
+}
+
+// C08 rows: unit = anchor block of the colour (kernels.py:373-433): the
+// anchor's intra pairs (owned anchor) and, per forward offset d, the pair
+// (anchor + max(0, -d), that + d); a row of block cell c walks the pairs whose
+// first cell is c.
+// stencil entries grouped by the block offset of their first cell
+// (max(0, -d) per axis), so a row visits only the pairs of its own cell
+struct C08Table {
+    int start[28];
+    signed char d[kMaxStencil][3];
+};
+
+template <int LAYOUT, bool MT, bool N3L>
+__global__ void __launch_bounds__(128) lc_c08_rows_kernel(GridView gv, ScratchPos<LAYOUT> sp,
+                                                          ScratchForce<LAYOUT> sf, LJTab tab,
+                                                          C08Table tb, ColourLaunch cl, int o0,
+                                                          int o1, int o2, int S,
+                                                          unsigned long long* counter) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    int unit = t / S, slot = t % S;
+    unsigned cnt = 0;
+    int total = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
+    if (unit < total) {
+        int kz = unit % cl.cnt[2], u2 = unit / cl.cnt[2];
+        int ky = u2 % cl.cnt[1], kx = u2 / cl.cnt[1];
+        int ax = cl.p[0] + kx * cl.stride[0];
+        int ay = cl.p[1] + ky * cl.stride[1];
+        int az = cl.p[2] + kz * cl.stride[2];
+        // block cells anchor + [0, o]^3 (inside the grid), rows enumerated cell by cell
+        int nb0 = min(o0 + 1, gv.D0 - ax), nb1 = min(o1 + 1, gv.D1 - ay), nb2 = min(o2 + 1, gv.D2 - az);
+        int q = slot;
+        for (int bi = 0; bi < nb0; ++bi)
+            for (int bj = 0; bj < nb1; ++bj)
+                for (int bk = 0; bk < nb2; ++bk) {
+                    int cx = ax + bi, cy = ay + bj, cz = az + bk;
+                    int c = gv.flat(cx, cy, cz);
+                    int s1 = gv.start[c], e1 = gv.start[c + 1];
+                    int nrow = e1 - s1;
+                    if (!gv.owned(cx, cy, cz)) {   // a first cell must be owned
+                        while (q < nrow) q += S;
+                        q -= nrow;
+                        continue;
+                    }
+                    for (; q < nrow; q += S) {
+                        int r = s1 + q;
+                        double xi, yi, zi;
+                        int ti;
+                        sp.load(r, xi, yi, zi, ti);
+                        double fx = 0.0, fy = 0.0, fz = 0.0;
+                        if (bi == 0 && bj == 0 && bk == 0)
+                            row_vs_range<LAYOUT, MT, N3L>(sp, sf, tab, r + 1, e1, xi, yi, zi, ti, fx, fy, fz, cnt);
+                        int slot_b = (bi * (o1 + 1) + bj) * (o2 + 1) + bk;
+                        for (int e = tb.start[slot_b]; e < tb.start[slot_b + 1]; ++e) {
+                            int dx = tb.d[e][0], dy = tb.d[e][1], dz = tb.d[e][2];
+                            int x2 = cx + dx, y2 = cy + dy, z2 = cz + dz;
+                            if (!gv.in_grid(x2, y2, z2)) continue;
+                            int c2 = gv.flat(x2, y2, z2);
+                            row_vs_range<LAYOUT, MT, N3L>(sp, sf, tab, gv.start[c2], gv.start[c2 + 1], xi, yi,
+                                                          zi, ti, fx, fy, fz, cnt);
+                        }
+                        atomicAdd(sf.at(r, 0), fx);
+                        atomicAdd(sf.at(r, 1), fy);
+                        atomicAdd(sf.at(r, 2), fz);
+                    }
+                    q -= nrow;
+                }
+    }
+    warp_count(counter, cnt);
+}
+
+// C08 with the colour schedule kept: one launch per anchor colour, thread per
+// (anchor, block cell, row slot); a thread walks its rows of that cell against
+// the pairs whose first cell is that block cell (C08Table) plus, in the anchor
+// cell, the intra pairs.
+template <int LAYOUT, bool MT, bool N3L>
+__global__ void __launch_bounds__(128) lc_c08_cells_kernel(GridView gv, ScratchPos<LAYOUT> sp,
+                                                           ScratchForce<LAYOUT> sf, LJTab tab,
+                                                           C08Table tb, ColourLaunch cl, int o0,
+                                                           int o1, int o2, int S,
+                                                           unsigned long long* counter) {
+    int nb = (o0 + 1) * (o1 + 1) * (o2 + 1);
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int slot = (int)(t % S);
+    int64_t ub = t / S;
+    int unit = (int)(ub / nb), b = (int)(ub % nb);
+    unsigned cnt = 0;
+    int total = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
+    if (unit < total) {
+        int kz = unit % cl.cnt[2], u2 = unit / cl.cnt[2];
+        int ky = u2 % cl.cnt[1], kx = u2 / cl.cnt[1];
+        int bi = b / ((o1 + 1) * (o2 + 1)), bj = (b / (o2 + 1)) % (o1 + 1), bk = b % (o2 + 1);
+        int cx = cl.p[0] + kx * cl.stride[0] + bi;
+        int cy = cl.p[1] + ky * cl.stride[1] + bj;
+        int cz = cl.p[2] + kz * cl.stride[2] + bk;
+        if (gv.in_grid(cx, cy, cz) && gv.owned(cx, cy, cz)) {
+            int c = gv.flat(cx, cy, cz);
+            int s1 = gv.start[c], e1 = gv.start[c + 1];
+            for (int r = s1 + slot; r < e1; r += S) {
+                double xi, yi, zi;
+                int ti;
+                sp.load(r, xi, yi, zi, ti);
+                double fx = 0.0, fy = 0.0, fz = 0.0;
+                unsigned before = cnt;
+                if (b == 0)
+                    row_vs_range<LAYOUT, MT, N3L>(sp, sf, tab, r + 1, e1, xi, yi, zi, ti, fx, fy, fz, cnt);
+                for (int e = tb.start[b]; e < tb.start[b + 1]; ++e) {
+                    int x2 = cx + tb.d[e][0], y2 = cy + tb.d[e][1], z2 = cz + tb.d[e][2];
+                    if (!gv.in_grid(x2, y2, z2)) continue;
+                    int c2 = gv.flat(x2, y2, z2);
+                    row_vs_range<LAYOUT, MT, N3L>(sp, sf, tab, gv.start[c2], gv.start[c2 + 1], xi, yi, zi,
+                                                  ti, fx, fy, fz, cnt);
+                }
+                if (cnt != before) {   // a row meets most block cells with no partner
+                    atomicAdd(sf.at(r, 0), fx);
+                    atomicAdd(sf.at(r, 1), fy);
+                    atomicAdd(sf.at(r, 2), fz);
+                }
+            }
+        }
+    }
+    warp_count(counter, cnt);
+}
+
+static int lc_env_rows() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_LC_ROWS");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
+// C08 realisation: 1 per colour, row-slot threads for sparse cells and warp
+// tiles for dense ones (default); 0 warp tiles per colour always; 2 every
+// anchor in one launch (row slots)
+static int lc_env_c08() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_LC_C08");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
+static C08Table make_c08_table(const Geom& g, const Stencil& fwd) {
+    C08Table tb{};
+    int nb = (g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1);
+    int e = 0;
+    for (int b = 0; b < nb; ++b) {
+        int bi = b / ((g.overlap[1] + 1) * (g.overlap[2] + 1));
+        int bj = (b / (g.overlap[2] + 1)) % (g.overlap[1] + 1), bk = b % (g.overlap[2] + 1);
+        tb.start[b] = e;
+        for (int k = 0; k < fwd.n; ++k) {
+            const int* d = fwd.d[k];
+            if ((d[0] < 0 ? -d[0] : 0) == bi && (d[1] < 0 ? -d[1] : 0) == bj && (d[2] < 0 ? -d[2] : 0) == bk) {
+                for (int a = 0; a < 3; ++a) tb.d[e][a] = (signed char)d[a];
+                ++e;
+            }
+        }
+    }
+    tb.start[nb] = e;
+    return tb;
+}
+
+// row slots per unit: the power of two at or above the mean rows per unit (4..32)
+static int slot_width(double rows_per_unit) {
+    int S = 4;
+    while (S < 32 && S < rows_per_unit) S <<= 1;
+    return S;
+}
+
 // ------------------------------------------------------------------ dispatch
 
 template <int LAYOUT, bool MT>
@@ -346,6 +597,37 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
         return;
     }
     ColourLaunch cl;
+    double rows_per_cell = (double)gr.m / (double)std::max<int64_t>(1, g.ncells);
+    if ((traversal == T_C18 && lc_env_rows()) || (traversal == T_C08 && lc_env_c08() == 2)) {
+        // every unit of every colour in one launch (the row kernels resolve the
+        // write races with atomics, which is what the colours are for on a CPU)
+        for (int k = 0; k < 3; ++k) {
+            cl.p[k] = 0;
+            cl.stride[k] = 1;
+            cl.lo[k] = traversal == T_C18 ? g.H[k] : 0;
+            cl.hi[k] = traversal == T_C18 ? g.H[k] + g.S[k] : g.D[k];
+            cl.cnt[k] = cl.hi[k] - cl.lo[k];
+        }
+        int units = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
+        if (traversal == T_C18) {
+            int S = slot_width(rows_per_cell);
+            int64_t threads = (int64_t)units * S;
+            if (newton3)
+                lc_c18_rows_kernel<LAYOUT, MT, true><<<blocks_for(threads, 128), 128, 0, s>>>(gv, sp, sf, c.tab, gr.fwd, cl, S, counter), note_launch();
+            else
+                lc_c18_rows_kernel<LAYOUT, MT, false><<<blocks_for(threads, 128), 128, 0, s>>>(gv, sp, sf, c.tab, gr.fwd, cl, S, counter), note_launch();
+        } else {
+            int block_cells = (g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1);
+            C08Table tb = make_c08_table(g, gr.fwd);
+            int S = slot_width(rows_per_cell * block_cells);
+            int64_t threads = (int64_t)units * S;
+            if (newton3)
+                lc_c08_rows_kernel<LAYOUT, MT, true><<<blocks_for(threads, 128), 128, 0, s>>>(gv, sp, sf, c.tab, tb, cl, g.overlap[0], g.overlap[1], g.overlap[2], S, counter), note_launch();
+            else
+                lc_c08_rows_kernel<LAYOUT, MT, false><<<blocks_for(threads, 128), 128, 0, s>>>(gv, sp, sf, c.tab, tb, cl, g.overlap[0], g.overlap[1], g.overlap[2], S, counter), note_launch();
+        }
+        return;
+    }
     if (traversal == T_C18) {
         int strides[3] = {g.overlap[0] + 1, 2 * g.overlap[1] + 1, 2 * g.overlap[2] + 1};
         for (int px = 0; px < strides[0]; ++px)
@@ -372,6 +654,9 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
         return;
     }
     // C08: anchors over the whole padded grid, stride overlap+1 per axis
+    // dense cells (CSF 1): warp tiles; sparse cells: row-slot threads
+    bool c08_cells = lc_env_c08() == 1 && rows_per_cell < 8.0;
+    C08Table c08tb = make_c08_table(g, gr.fwd);
     int strides[3] = {g.overlap[0] + 1, g.overlap[1] + 1, g.overlap[2] + 1};
     for (int px = 0; px < strides[0]; ++px)
         for (int py = 0; py < strides[1]; ++py)
@@ -388,7 +673,15 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
                 }
                 if (empty) continue;
                 int warps = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
-                if (newton3)
+                if (c08_cells) {
+                    int nb = (g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1);
+                    int S = slot_width(rows_per_cell);
+                    int64_t threads = (int64_t)warps * nb * S;
+                    if (newton3)
+                        lc_c08_cells_kernel<LAYOUT, MT, true><<<blocks_for(threads, 128), 128, 0, s>>>(gv, sp, sf, c.tab, c08tb, cl, g.overlap[0], g.overlap[1], g.overlap[2], S, counter), note_launch();
+                    else
+                        lc_c08_cells_kernel<LAYOUT, MT, false><<<blocks_for(threads, 128), 128, 0, s>>>(gv, sp, sf, c.tab, c08tb, cl, g.overlap[0], g.overlap[1], g.overlap[2], S, counter), note_launch();
+                } else if (newton3)
                     lc_c08_kernel<LAYOUT, MT, true><<<blocks_for(warps, 4), 128, 0, s>>>(gv, sp, sf, c.tab, gr.fwd, cl, counter), note_launch();
                 else
                     lc_c08_kernel<LAYOUT, MT, false><<<blocks_for(warps, 4), 128, 0, s>>>(gv, sp, sf, c.tab, gr.fwd, cl, counter), note_launch();

@@ -495,11 +495,18 @@ def test_gpu_training_sweep_writes_reference_csv(pkg, tmp_path):
 
 
 @pytest.mark.parametrize("env", [{"MDG_VLT_WIN": "64"}, {"MDG_VLT_WIN": "256"}, {"MDG_VLT_ORDER": "2"}, {"MDG_VL_TILED": "0"},
-                                 {"MDG_VLT_STAGES": "3", "MDG_VLT_WIN": "1024"}])
+                                 {"MDG_VLT_STAGES": "3", "MDG_VLT_WIN": "1024"},
+                                 {"MDG_LC_ROWS": "0", "_prefix": "LC-C18"},
+                                 {"MDG_LC_C08": "0", "_prefix": "LC-C08"},
+                                 {"MDG_LC_C08": "2", "_prefix": "LC-C08"}])
 def test_vl_walk_variants_match_reference(pkg, env):
     """The tunable paths of the Verlet walk against the reference forces and
     counts: a tiny window budget (most tiles overflow to the row-space walk),
-    bank-aware list order, the untiled walk, a 3-stage window ring."""
+    bank-aware list order, the untiled walk, a 3-stage window ring; and the
+    alternative linked-cell realisations (C18 per-colour warp tiles, C08 warp
+    tiles, C08 in one launch)."""
+    env = dict(env)
+    prefix = env.pop("_prefix", "VL-")
     import os
     import subprocess
     import sys
@@ -518,9 +525,10 @@ def test_vl_walk_variants_match_reference(pkg, env):
         "    per = tuple(P.PERIODIC if f else P.REFLECTIVE for f in d['periodic'])\n"
         "    params = P.SimulationParams(domain_size=d['domain'], cutoff=float(d['cutoff']),"
         " skin=float(d['skin']), rebuild_interval=5, boundary=per)\n"
-        "    for layout in ('AoS', 'SoA'):\n"
-        "        cid = f'VL-List_Iter-NoN3L-{layout}'\n"
-        "        parts = P.ParticleSet(d['pos'], type_ids=d['tid'], types=types, layout=layout)\n"
+        "    for cid in ids:\n"
+        f"        if not cid.startswith({prefix!r}): continue\n"
+        "        parts = P.ParticleSet(d['pos'], type_ids=d['tid'], types=types,"
+        " layout=P.parse_configuration(cid).layout)\n"
         "        _, count = calc.compute_forces(parts, P.parse_configuration(cid), params)\n"
         "        k = ids.index(cid)\n"
         "        assert count == int(d['counts'][k]), (name, cid)\n"

@@ -8,13 +8,20 @@
 //   SLI  thread per owned row, own cell (j>i) + forward stencil, all writes
 //        through fp64 RED (the lock-free analogue of the seam locks,
 //        containers.py:288-322)                             kernels.py:493-579
-//   C18  one launch per base colour (strides o+1, 2o+1, 2o+1); one warp per base
-//        cell; cell pairs processed as 32x32 rotation tiles (lane l pairs its i
-//        with j=(l+k) mod P at step k, so j-side updates never collide) and
-//        flushed with plain stores: same-colour bases touch disjoint cells
-//                                                           containers.py:269-287
-//   C08  one launch per anchor colour (stride o+1 per axis); one warp per anchor
-//        block, same rotation tiles, plain stores           kernels.py:373-488
+//   C18  default: every base cell in ONE launch, S row-slot threads per base
+//        cell (own cell j>i + forward stencil), writes through fp64 RED --
+//        on the GPU the colour barriers only serialise work the atomics
+//        already make safe (CSF 0.5: 75 launches 14.9 ms -> 1.0 ms).
+//        MDG_LC_ROWS=0: one launch per base colour (strides o+1, 2o+1, 2o+1),
+//        warp per base cell, 32x32 rotation tiles (lane l pairs its i with
+//        j=(l+k) mod P at step k, so j-side updates never collide), plain
+//        stores: same-colour bases touch disjoint cells  containers.py:269-287
+//   C08  one launch per anchor colour (stride o+1 per axis), the schedule
+//        kept.  Dense cells (>= 8 rows): warp per anchor block, rotation tiles,
+//        plain stores.  Sparse cells: thread per (anchor, block cell, row
+//        slot) over the pairs whose first cell is that block cell (C08Table),
+//        fp64 RED (CSF 0.5: 11.8 -> 4.5 ms).  MDG_LC_C08=0 tiles always,
+//        =2 every anchor in one launch                 kernels.py:373-488
 //
 // N3L: one evaluation per pair, reaction subtracted from j (count 1).
 // NoN3L: both directions evaluated separately, each counted (count 2), exactly

@@ -243,6 +243,35 @@ int mdg_host_drift_wrap_range_ex(int64_t n, int64_t begin, int64_t end, int layo
                                  const int32_t* type_id, const double* mass, const double domain[3],
                                  const int periodic[3], double dt, int swapped, int* blowup);
 
+/* `steps` reference-loop iterations on HOST state in one call, pipelined
+ * across step boundaries: after the force pass of step s the forces copy back
+ * in `chunks` pieces, and as each lands the host runs the kick of step s and
+ * the drift of step s+1 on it in one pass (mdg_host_kick_drift_range) and
+ * uploads its positions on a second stream, so the H2D of step s+1 overlaps
+ * the D2H of step s and the next force pass waits only for the last chunk.
+ * Buffers as for MDG_HOST_STEP_SWAPPED on entry (old_force = current forces);
+ * the two force buffers alternate roles per step, so after an EVEN number of
+ * completed steps the latest forces are in old_force (the caller swaps its
+ * names back).  Rebuild before step s when (s == 0 && rebuild_first) or
+ * `since` (steps since the last rebuild, updated per step) >= rebuild_interval
+ * (simulation.py:158-159, 179).  Per particle the arithmetic and its order
+ * are those of mdg_host_step, so the state after k steps is bit-identical to
+ * k calls of it.  *steps_done = completed steps; *blowup set when a drift
+ * left [-L, 2L] (the run stops before that step's force pass). */
+int mdg_host_run(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, double* force,
+                 double* old_force, const int32_t* type_id, const double* mass, double dt,
+                 int has_gravity, double gravity, int steps, int rebuild_interval, int since,
+                 int rebuild_first, int chunks, int* blowup, int* steps_done);
+/* Kick of step s then drift of step s+1 on particles [begin, end) in one
+ * pass: gravity into fnew.z, v += (fnew + fold) dt/(2m), x += v dt,
+ * x += fnew dt^2/(2m), wrap/reflect (integrator.py:31-51, 98-128); fnew is
+ * not copied to fold (swapped buffers). */
+int mdg_host_kick_drift_range(int64_t n, int64_t begin, int64_t end, int layout, double* pos,
+                              double* vel, double* fnew, const double* fold,
+                              const int32_t* type_id, const double* mass, const double domain[3],
+                              const int periodic[3], double dt, int has_gravity, double gravity,
+                              int* blowup);
+
 /* Measured FP64 FMA throughput of this device (roofline denominator):
  * dependent-chain DFMA microbenchmark, TFLOP/s (2 flops per DFMA). */
 int mdg_measure_fp64_peak(mdg_ctx* ctx, double* tflops, double* sm_mhz_hint);

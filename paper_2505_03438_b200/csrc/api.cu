@@ -171,6 +171,8 @@ int mdg_destroy(mdg_ctx* ctx) {
     if (ctx->c.graph_in) cudaEventDestroy(ctx->c.graph_in);
     if (ctx->c.graph_out) cudaEventDestroy(ctx->c.graph_out);
     if (ctx->c.graph_stream) cudaStreamDestroy(ctx->c.graph_stream);
+    if (ctx->c.h2d_done) cudaEventDestroy(ctx->c.h2d_done);
+    if (ctx->c.copy_stream) cudaStreamDestroy(ctx->c.copy_stream);
     delete ctx;
     return MDG_OK;
 }
@@ -652,6 +654,128 @@ int mdg_host_step_ex(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* v
                 us(t0, t1), us(t1, t2), wait_us, us(t2, t3) - wait_us, us(t0, t3), rebuild ? " (rebuild)" : "");
     }
     return cuda_status("mdg_host_step");
+}
+
+int mdg_host_run(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, double* force,
+                 double* old_force, const int32_t* type_id, const double* mass, double dt,
+                 int has_gravity, double gravity, int steps, int rebuild_interval, int since,
+                 int rebuild_first, int chunks, int* blowup, int* steps_done) {
+    CHECK_CTX(ctx);
+    if (int e = validate(cfg)) return e;
+    if (int e = need_system(ctx)) return e;
+    Context& c = ctx->c;
+    if (blowup) *blowup = 0;
+    if (steps_done) *steps_done = 0;
+    if (steps < 0 || rebuild_interval < 0) { set_error("mdg_host_run: negative steps"); return MDG_EINVAL; }
+    int64_t n = c.n;
+    if (n == 0 || steps == 0) {
+        if (steps_done) *steps_done = n == 0 ? steps : 0;
+        return MDG_OK;
+    }
+    if (!c.pos || !c.force) { set_error("mdg_host_run: bind the device arrays first"); return MDG_ESTATE; }
+    int K = std::max(1, std::min<int>(chunks, (int)std::min<int64_t>(n, 64)));
+    while ((int)c.chunk_ev.size() < K) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return cuda_status("event");
+        c.chunk_ev.push_back(e);
+    }
+    if (!c.copy_stream) {
+        if (cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c.h2d_done, cudaEventDisableTiming) != cudaSuccess)
+            return cuda_status("mdg_host_run streams");
+    }
+    int periodic[3] = {c.periodic[0], c.periodic[1], c.periodic[2]};
+    auto copy = [&](double* dst, const double* src, int64_t a, int64_t b, cudaMemcpyKind kind,
+                    cudaStream_t st) {
+        if (c.layout == AOS) return cudaMemcpyAsync(dst + 3 * a, src + 3 * a, 24 * (b - a), kind, st);
+        for (int k = 0; k < 3; ++k) {
+            cudaError_t e = cudaMemcpyAsync(dst + k * n + a, src + k * n + a, 8 * (b - a), kind, st);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    };
+    static int timing = getenv("MDG_HOST_STEP_TIMING") ? 1 : 0;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto us = [](auto x, auto y) { return std::chrono::duration<double, std::micro>(y - x).count(); };
+    double t_enq = 0, t_wait = 0, t_host = 0, t_first = 0;
+    auto T0 = now();
+    // the caller's buffers arrive swapped (MDG_HOST_STEP_SWAPPED): old_force
+    // holds the current forces, force is free; the roles alternate per step
+    double* cur = old_force;
+    double* oth = force;
+    // drift of the first step, chunks uploaded on the copy stream as they finish
+    int bad = 0;
+    for (int k = 0; k < K; ++k) {
+        int64_t a = n * k / K, b = n * (k + 1) / K;
+        int bk = 0;
+        mdg_host_drift_wrap_range_ex(n, a, b, c.layout, pos, vel, nullptr, cur, type_id, mass, c.L,
+                                     periodic, dt, 1, &bk);
+        bad |= bk;
+        if (copy(c.pos, pos, a, b, cudaMemcpyHostToDevice, c.copy_stream) != cudaSuccess) return cuda_status("h2d");
+    }
+    cudaEventRecord(c.h2d_done, c.copy_stream);
+    if (bad) {
+        cudaStreamSynchronize(c.copy_stream);
+        if (blowup) *blowup = 1;
+        return cuda_status("mdg_host_run");
+    }
+    for (int s = 0; s < steps; ++s) {
+        bool last = s == steps - 1;
+        bool rebuild = (s == 0 && rebuild_first) || since >= rebuild_interval;
+        auto ta = now();
+        if (cudaStreamWaitEvent(c.stream, c.h2d_done, 0) != cudaSuccess) return cuda_status("wait h2d");
+        if (rebuild)
+            if (int e = mdg_rebuild(ctx, cfg)) return e;
+        if (int e = mdg_refresh(ctx, cfg)) return e;
+        if (int e = mdg_compute(ctx, cfg)) return e;
+        for (int k = 0; k < K; ++k) {
+            int64_t a = n * k / K, b = n * (k + 1) / K;
+            if (copy(oth, c.force, a, b, cudaMemcpyDeviceToHost, c.stream) != cudaSuccess) return cuda_status("d2h");
+            cudaEventRecord(c.chunk_ev[k], c.stream);
+        }
+        auto tb = now();
+        t_enq += us(ta, tb);
+        // each chunk as it lands: kick of this step, drift of the next, upload
+        // (the H2D runs on the copy stream, overlapping the remaining D2H)
+        for (int k = 0; k < K; ++k) {
+            int64_t a = n * k / K, b = n * (k + 1) / K;
+            auto w0 = now();
+            if (cudaEventSynchronize(c.chunk_ev[k]) != cudaSuccess) return cuda_status("d2h wait");
+            auto w1 = now();
+            t_wait += us(w0, w1);
+            if (k == 0) t_first += us(w0, w1);
+            struct Acc {
+                double& t; std::chrono::steady_clock::time_point s;
+                ~Acc() { t += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - s).count(); }
+            } acc{t_host, w1};
+            if (last) {
+                mdg_host_finish_kick_range(n, a, b, c.layout, vel, oth, cur, type_id, mass, dt,
+                                           has_gravity, gravity);
+                continue;
+            }
+            int bk = 0;
+            mdg_host_kick_drift_range(n, a, b, c.layout, pos, vel, oth, cur, type_id, mass, c.L,
+                                      periodic, dt, has_gravity, gravity, &bk);
+            bad |= bk;
+            if (copy(c.pos, pos, a, b, cudaMemcpyHostToDevice, c.copy_stream) != cudaSuccess) return cuda_status("h2d");
+        }
+        if (!last) cudaEventRecord(c.h2d_done, c.copy_stream);
+        since = rebuild ? 0 : since + 1;
+        std::swap(cur, oth);
+        if (steps_done) *steps_done = s + 1;
+        if (bad) {   // the next step's drift left the domain: stop before its force pass
+            cudaStreamSynchronize(c.copy_stream);
+            if (blowup) *blowup = 1;
+            break;
+        }
+    }
+    if (timing && steps_done && *steps_done > 0) {
+        double k = *steps_done;
+        fprintf(stderr, "host_run: %d steps x %d chunks: per step %.0f us = device enqueue %.0f, "
+                        "d2h waits %.0f (first chunk %.0f), host kick+drift+h2d enqueue %.0f\n",
+                *steps_done, K, us(T0, now()) / k, t_enq / k, t_wait / k, t_first / k, t_host / k);
+    }
+    return cuda_status("mdg_host_run");
 }
 
 int mdg_d2h_async(mdg_ctx* ctx, void* host, const void* dev, size_t bytes) {

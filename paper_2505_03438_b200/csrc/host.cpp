@@ -151,9 +151,85 @@ void kick_all(int64_t n, int64_t a, int64_t b, double* __restrict__ vel, double*
     }
 }
 
+// kick of step s fused with the drift of step s+1 over [a, b), all axes
+// periodic: per element exactly kick_all's then drift_periodic's operations
+// (gravity into fnew.z first, v += (fnew + fold) c_k, x += v dt, x += fnew c_d,
+// np.mod), one pass instead of two.  The drift reads fnew without copying it
+// to fold (the caller alternates the two buffers, MDG_HOST_STEP_SWAPPED).
+template <int LAYOUT, bool TYPED>
+int kick_drift_periodic(int64_t n, int64_t a, int64_t b, double* __restrict__ pos,
+                        double* __restrict__ vel, double* __restrict__ fnew,
+                        const double* __restrict__ fold, const int32_t* __restrict__ tid,
+                        const double* __restrict__ mass, const double domain[3], double dt,
+                        int has_gravity, double gravity) {
+    const double ck1 = TYPED ? 0.0 : 0.5 * dt / mass[0];
+    const double cd1 = TYPED ? 0.0 : 0.5 * dt * dt / mass[0];
+    const double mg1 = TYPED ? 0.0 : mass[0] * gravity;
+    const bool grav = has_gravity != 0;
+    const double L0 = domain[0], L1 = domain[1], L2 = domain[2];
+    int bad = 0;
+#pragma omp parallel for simd schedule(static) reduction(| : bad)
+    for (int64_t i = a; i < b; ++i) {
+        double m = TYPED ? mass[tid[i]] : 0.0;
+        size_t e0 = LAYOUT == MDG_AOS ? 3 * i : i;
+        size_t e1 = LAYOUT == MDG_AOS ? 3 * i + 1 : n + i;
+        size_t e2 = LAYOUT == MDG_AOS ? 3 * i + 2 : 2 * n + i;
+        double f0 = fnew[e0], f1 = fnew[e1], f2 = fnew[e2];
+        if (grav) {
+            f2 = f2 + (TYPED ? m * gravity : mg1);
+            fnew[e2] = f2;
+        }
+        double ck = TYPED ? 0.5 * dt / m : ck1;
+        double v0 = vel[e0] + (f0 + fold[e0]) * ck;
+        double v1 = vel[e1] + (f1 + fold[e1]) * ck;
+        double v2 = vel[e2] + (f2 + fold[e2]) * ck;
+        vel[e0] = v0;
+        vel[e1] = v1;
+        vel[e2] = v2;
+        double cd = TYPED ? 0.5 * dt * dt / m : cd1;
+        double y0 = pos[e0] + v0 * dt, y1 = pos[e1] + v1 * dt, y2 = pos[e2] + v2 * dt;
+        y0 = y0 + f0 * cd;
+        y1 = y1 + f1 * cd;
+        y2 = y2 + f2 * cd;
+        bad |= !(y0 >= -L0 && y0 <= 2.0 * L0) | !(y1 >= -L1 && y1 <= 2.0 * L1) |
+               !(y2 >= -L2 && y2 <= 2.0 * L2);
+        pos[e0] = np_mod_in_range(y0, L0);
+        pos[e1] = np_mod_in_range(y1, L1);
+        pos[e2] = np_mod_in_range(y2, L2);
+    }
+    return bad;
+}
+
 }  // namespace
 
 extern "C" {
+
+int mdg_host_kick_drift_range(int64_t n, int64_t begin, int64_t end, int layout, double* pos,
+                              double* vel, double* fnew, const double* fold,
+                              const int32_t* type_id, const double* mass, const double domain[3],
+                              const int periodic[3], double dt, int has_gravity, double gravity,
+                              int* blowup) {
+    if (n < 0 || begin < 0 || end > n || begin > end || (layout != MDG_AOS && layout != MDG_SOA))
+        return MDG_EINVAL;
+    int bad = 0;
+    if (periodic[0] && periodic[1] && periodic[2]) {
+#define MDG_KD(LY, TY) kick_drift_periodic<LY, TY>(n, begin, end, pos, vel, fnew, fold, type_id, mass, domain, dt, has_gravity, gravity)
+        bad = layout == MDG_AOS ? (type_id ? MDG_KD(MDG_AOS, true) : MDG_KD(MDG_AOS, false))
+                                : (type_id ? MDG_KD(MDG_SOA, true) : MDG_KD(MDG_SOA, false));
+#undef MDG_KD
+    } else {
+        // reflective axes: the two passes over the range (same operations)
+        int r = mdg_host_finish_kick_range(n, begin, end, layout, vel, fnew, fold, type_id, mass, dt,
+                                           has_gravity, gravity);
+        if (r) return r;
+        r = mdg_host_drift_wrap_range_ex(n, begin, end, layout, pos, vel, nullptr, fnew, type_id,
+                                         mass, domain, periodic, dt, 1, &bad);
+        if (r) return r;
+    }
+    if (blowup) *blowup = bad;
+    return MDG_OK;
+}
+
 
 int mdg_host_drift_wrap_range_ex(int64_t n, int64_t begin, int64_t end, int layout, double* pos,
                                  double* vel, const double* force, double* old_force,

@@ -184,6 +184,8 @@ struct Context {
     // optional CUDA-event bracketing of the force kernels (mdg_profile)
     bool prof = false;
     std::vector<cudaEvent_t> chunk_ev;   // mdg_host_step's per-chunk copy events
+    cudaStream_t copy_stream = nullptr;  // mdg_host_run's H2D stream (overlaps the D2H)
+    cudaEvent_t h2d_done = nullptr;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     void prof_mark();

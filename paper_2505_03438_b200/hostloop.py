@@ -142,14 +142,14 @@ class HostSimulation:
     """The reference loop (simulation.py:150-188, fixed configuration) on host
     state with the GPU force backend.  Create once, then ``run(steps)``.
 
-    With ``chunks > 1`` (default 4) a step is one native call
+    With ``chunks > 1`` (default 16) a step is one native call
     (``mdg_host_step``) in which the host work overlaps the copies: the drift
     of chunk k runs while chunk k-1's positions are in flight to the device,
     and the kick of chunk k starts as soon as its forces have landed.  The
     arithmetic and its order per particle are unchanged (same results, bit
     for bit); only the copies are split."""
 
-    def __init__(self, particles, params, config, calculator=None, chunks=4):
+    def __init__(self, particles, params, config, calculator=None, chunks=16):
         self.p, self.params, self.config = particles, params, config
         self.calc = calculator or HostForceCalculator(particles, params)
         self.active, self.since, self.iteration = None, 0, 0
@@ -203,6 +203,53 @@ class HostSimulation:
         self.since = 0 if rebuild else self.since + 1
         self.iteration += 1
 
+    def _pipelined(self):
+        p, calc = self.p, self.calc
+        return (self.chunks > 1 and p.n > 0 and isinstance(calc, HostForceCalculator)
+                and p.pos.flags.c_contiguous and p.force.flags.c_contiguous)
+
     def run(self, steps):
-        for _ in range(steps):
-            self.step()
+        """``steps`` iterations.  Pipelined, they are ONE native call
+        (``mdg_host_run``) that also overlaps consecutive steps: as each force
+        chunk lands, its kick and the next step's drift run in one host pass
+        and its positions go straight back up, while the rest of the forces
+        are still coming down.  Same state after the run, bit for bit, as
+        ``steps`` calls of ``step()``."""
+        steps = int(steps)
+        if steps <= 0:
+            return
+        p, params, cfg, calc = self.p, self.params, self.config, self.calc
+        if p.layout != cfg.layout:
+            p.convert_layout(cfg.layout)
+        if not self._pipelined():
+            for _ in range(steps):
+                self.step()
+            return
+        from .simulation import BlowUpError
+        calc._bind(p)
+        mass = np.ascontiguousarray(p.mass, dtype=np.float64)
+        tid = getattr(p, "_tid32", None)
+        if tid is None:
+            tid = np.asarray(p.type_id, dtype=np.int32)
+        rebuild_first = self.active != cfg.id
+        bad, done = ctypes.c_int(), ctypes.c_int()
+        p.force, p.old_force = p.old_force, p.force   # MDG_HOST_STEP_SWAPPED on entry
+        check(lib().mdg_host_run(calc.ctx.h, ctypes.byref(_lib.config_struct(cfg)), _ptr(p.pos),
+                                 _ptr(p.vel), _ptr(p.force), _ptr(p.old_force),
+                                 _ptr(tid) if len(mass) > 1 else None, _ptr(mass),
+                                 float(params.delta_t), int(params.gravity is not None),
+                                 float(params.gravity or 0.0), steps, int(params.rebuild_interval),
+                                 int(self.since), int(rebuild_first), self.chunks,
+                                 ctypes.byref(bad), ctypes.byref(done)), "host run")
+        k = done.value
+        if k % 2 == 0:   # the buffers alternate per step; put the latest forces in p.force
+            p.force, p.old_force = p.old_force, p.force
+        for s in range(k):
+            rebuild = (s == 0 and rebuild_first) or self.since >= params.rebuild_interval
+            self.since = 0 if rebuild else self.since + 1
+        if k:
+            self.active = cfg.id
+        self.iteration += k
+        if bad.value:
+            raise BlowUpError("particle left the domain by more than one domain length "
+                              "(or position is not finite)")

@@ -427,14 +427,47 @@ def test_pipelined_host_loop_is_bit_identical(pkg):
     for cid in ("LC-C08-N3L-SoA-CSF1", "VL-List_Iter-NoN3L-AoS", "VL-List_Iter-NoN3L-SoA",
                 "VCL-ClusterIter-NoN3L-AoS"):
         out = []
-        for chunks in (1, 7):
+        # one-shot steps; one cross-step pipelined run (odd); runs of uneven
+        # lengths (even totals in between, rebuild cadence across calls)
+        for chunks, runs in ((1, (25,)), (7, (25,)), (3, (4, 1, 20))):
             params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=10,
                                         delta_t=1e-3, boundary=(P.PERIODIC,) * 3)
             p = HostParticleSet(z["pos0"], z["vel0"])
-            HostSimulation(p, params, P.parse_configuration(cid), chunks=chunks).run(25)
-            out.append((np.array(p.positions), np.array(p.velocities), np.array(p.forces)))
+            sim = HostSimulation(p, params, P.parse_configuration(cid), chunks=chunks)
+            for k in runs:
+                sim.run(k)
+            assert sim.iteration == 25 and sim.since == 25 % 11 - 1
+            out.append((np.array(p.positions), np.array(p.velocities), np.array(p.forces),
+                        np.array(p.old_forces)))
+        for other in out[1:]:
+            for a, b in zip(out[0], other):
+                assert np.array_equal(a, b), cid
+
+
+def test_pipelined_host_run_typed_gravity_reflective(pkg):
+    """mdg_host_run with two types, gravity and reflective axes (the fused
+    kick+drift pass falls back to its two-pass form there) vs one-shot steps."""
+    P, calc = pkg
+    from paper_2505_03438_b200.hostloop import HostParticleSet, HostSimulation
+    z = golden("traj_small.npz")
+    L = z["domain"]
+    n = len(z["pos0"])
+    tid = np.arange(n) % 2
+    for boundary in ((P.PERIODIC,) * 3, (P.REFLECTIVE, P.PERIODIC, P.REFLECTIVE)):
+        out = []
+        for chunks in (1, 5):
+            params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=4,
+                                        delta_t=1e-3, boundary=boundary, gravity=-0.5)
+            p = HostParticleSet(z["pos0"], z["vel0"], tid, sigma=[1.0, 0.9], epsilon=[1.0, 1.2],
+                                mass=[1.0, 1.5], layout="SoA")
+            sim = HostSimulation(p, params, P.parse_configuration("VL-List_Iter-NoN3L-SoA"),
+                                 chunks=chunks)
+            sim.run(6)
+            sim.run(7)
+            out.append((np.array(p.positions), np.array(p.velocities), np.array(p.forces),
+                        np.array(p.old_forces)))
         for a, b in zip(*out):
-            assert np.array_equal(a, b), cid
+            assert np.array_equal(a, b), boundary
 
 
 def test_fused_kick_matches_separate_kick(pkg):

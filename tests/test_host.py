@@ -155,6 +155,59 @@ def test_native_host_integrator_matches_reference_numpy_bit_exact():
             assert np.array_equal(a.forces, b.forces)
 
 
+def test_fused_kick_drift_equals_kick_then_drift():
+    """mdg_host_kick_drift_range (mdg_host_run's per-chunk pass) = finish_kick
+    then the swapped drift, bit for bit, for every layout / typing /
+    boundary combination."""
+    import ctypes
+    from paper_2505_03438_b200 import _lib, hostloop
+    lib = _lib.lib()
+    rng = np.random.default_rng(9)
+    n = 3001
+    for boundary in ((P.PERIODIC,) * 3, (P.REFLECTIVE, P.PERIODIC, P.REFLECTIVE)):
+        params = P.SimulationParams(domain_size=(9.0, 10.0, 11.0), cutoff=2.5, skin=0.3,
+                                    delta_t=0.01, boundary=boundary, gravity=-1.5)
+        pos = rng.uniform(0.0, 1.0, (n, 3)) * params.domain_size
+        vel = rng.normal(0, 3.0, (n, 3))
+        fnew = rng.normal(0, 50.0, (n, 3))
+        fold = rng.normal(0, 50.0, (n, 3))
+        for typed in (False, True):
+            tid = np.arange(n) % 2 if typed else np.zeros(n, dtype=np.int64)
+            mass = [1.0, 2.0] if typed else [1.3]
+            for layout in ("AoS", "SoA"):
+                mk = lambda: hostloop.HostParticleSet(pos, vel, tid, sigma=[1] * len(mass),
+                                                      epsilon=[1] * len(mass), mass=mass,
+                                                      layout=layout)
+                a, b = mk(), mk()
+                for q in (a, b):
+                    q.view("force")[:] = fnew
+                    q.view("old_force")[:] = fold
+                # reference: kick, then the drift with F -> F_old swapped
+                hostloop.host_finish_kick(b, params.delta_t, params.gravity)
+                b.force, b.old_force = b.old_force, b.force
+                L = np.ascontiguousarray(params.domain_size, dtype=np.float64)
+                per = np.ascontiguousarray(params.periodic_flags().astype(np.int32))
+                m = np.ascontiguousarray(mass, dtype=np.float64)
+                t32 = np.ascontiguousarray(tid, dtype=np.int32)
+                ly = _lib.AOS if layout == "AoS" else _lib.SOA
+                bad = ctypes.c_int()
+                P_ = hostloop._ptr
+                assert lib.mdg_host_drift_wrap_range_ex(n, 0, n, ly, P_(b.pos), P_(b.vel), P_(b.force),
+                                                        P_(b.old_force), P_(t32) if typed else None,
+                                                        P_(m), P_(L), P_(per), params.delta_t, 1,
+                                                        ctypes.byref(bad)) == 0
+                for lo, hi in ((0, 1000), (1000, n)):
+                    assert lib.mdg_host_kick_drift_range(n, lo, hi, ly, P_(a.pos), P_(a.vel), P_(a.force),
+                                                         P_(a.old_force), P_(t32) if typed else None,
+                                                         P_(m), P_(L), P_(per), params.delta_t, 1, -1.5,
+                                                         ctypes.byref(bad)) == 0
+                    assert bad.value == 0
+                # b's current forces now live in b.old_force (swapped); a's in a.force
+                assert np.array_equal(a.positions, b.positions), (boundary, typed, layout)
+                assert np.array_equal(a.velocities, b.velocities), (boundary, typed, layout)
+                assert np.array_equal(a.forces, b.old_forces), (boundary, typed, layout)
+
+
 def test_native_host_integrator_flags_blow_up():
     from paper_2505_03438_b200 import hostloop
     params = P.SimulationParams(domain_size=(10.0, 10.0, 10.0), cutoff=3.0,

@@ -51,10 +51,18 @@ def _env_int(name, default):
 
 
 def workload_config(args, n_gpus):
+    if n_gpus > 1:
+        return {"workload": f"config2 boxes stacked along z: {n_gpus} x {args.n:,} particles in one "
+                            f"periodic box L x L x {n_gpus}L (rho=0.75, SD-relaxed, T=0.7, rc=2.5, "
+                            "skin=0.3, dt=0.002, rebuild every 11 steps)",
+                "n_particles": args.n * n_gpus, "n_particles_per_gpu": args.n,
+                "configuration": args.config,
+                "parallelism": f"zslab{n_gpus}: domain decomposition, ghost positions over NCCL "
+                               "every step, migration at rebuilds",
+                "l2": "flushed between timed steps (256 MB write, untimed)"}
     return {"workload": "config2: homogeneous LJ liquid, 1,048,576 particles, rho=0.75, "
                         "SD-relaxed, T=0.7, rc=2.5, skin=0.3, dt=0.002, rebuild every 11 steps",
-            "n_particles": args.n, "configuration": args.config,
-            "parallelism": f"replicas{n_gpus}" if n_gpus > 1 else "single",
+            "n_particles": args.n, "configuration": args.config, "parallelism": "single",
             "l2": "flushed between timed steps (256 MB write, untimed)"}
 
 
@@ -118,6 +126,33 @@ def build_system(args, rank):
     return parts, params
 
 
+def build_decomposed(args, rank, world, cfg):
+    """N > 1: one config-2 box per rank, stacked along z into one periodic
+    system of N x n particles, z-slab decomposed.  Every rank
+    relaxes the same seeded box, so the interfaces between slabs are as
+    relaxed as the box's own periodic faces; velocities are drawn per rank."""
+    import numpy as np
+    import torch
+
+    import paper_2505_03438_b200 as P
+    from paper_2505_03438_b200.decomp import DeviceDecomposedSimulation, GridDecomposition
+    parts, params = build_system(args, 0)
+    L = np.asarray(params.domain_size, dtype=np.float64)
+    rng = np.random.default_rng(args.seed + 7919 * (rank + 1))
+    vel = rng.normal(0.0, np.sqrt(0.7), (args.n, 3))
+    vel -= vel.mean(0)
+    pos = parts.view("pos").clone()
+    pos[:, 2] += rank * L[2]
+    gparams = P.SimulationParams(domain_size=(L[0], L[1], world * L[2]), cutoff=params.cutoff,
+                                 skin=params.skin, rebuild_interval=params.rebuild_interval,
+                                 delta_t=params.delta_t, boundary=params.boundary)
+    dec = GridDecomposition(gparams, rank, world, (1, 1, world))
+    owned = P.ParticleSet(pos, torch.as_tensor(vel), device=parts.device)
+    ids = torch.arange(args.n, device=parts.device) + rank * args.n
+    comm = "cpu" if args.dist_backend == "gloo" else None
+    return DeviceDecomposedSimulation(dec, owned, gparams, cfg, ids=ids, comm_device=comm), gparams
+
+
 def gpu_arm(args, rank, world, dist):
     import torch
 
@@ -125,15 +160,19 @@ def gpu_arm(args, rank, world, dist):
     from paper_2505_03438_b200 import _lib
     from paper_2505_03438_b200.simulation import Simulation
 
-    local = _env_int("LOCAL_RANK", 0)
+    local = _env_int("LOCAL_RANK", 0) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg = P.parse_configuration(args.config)
-    parts, params = build_system(args, rank)
-    host_pos = parts.numpy("pos") if rank == 0 else None
-    host_vel = parts.numpy("vel") if rank == 0 else None
-    parts.convert_layout(cfg.layout)
-    sim = Simulation(parts, params, cfg)
+    if world > 1:
+        sim, params = build_decomposed(args, rank, world, cfg)
+        host_pos = host_vel = None
+    else:
+        parts, params = build_system(args, rank)
+        host_pos = parts.numpy("pos")
+        host_vel = parts.numpy("vel")
+        parts.convert_layout(cfg.layout)
+        sim = Simulation(parts, params, cfg)
     calc = sim.calc
 
     fp64_peak = _measure_fp64_peak(calc)
@@ -168,7 +207,8 @@ def gpu_arm(args, rank, world, dist):
     sim.check()
 
     if dist is not None:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms], dtype=torch.float64,
+                         device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
 
@@ -348,6 +388,9 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
+                    help="gloo (messages staged on the host) only to smoke-test the N > 1 path "
+                         "with several ranks on one GPU; never a performance number")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "mdg":
         args.warmup = 3
@@ -363,8 +406,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as tdist
-        torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
-        tdist.init_process_group("nccl")
+        torch.cuda.set_device(_env_int("LOCAL_RANK", 0) % max(1, torch.cuda.device_count()))
+        tdist.init_process_group(args.dist_backend)
         dist = tdist
     out = gpu_arm(args, rank, world, dist)
     if out is not None:

@@ -332,3 +332,224 @@ def gpu_force_backend(config, sigma, epsilon, mass):
         return parts.forces[:n_owned].clone()
 
     return force_fn
+
+
+# ---------------------------------------------------------------------------
+# Device-resident decomposition (the bench's N > 1 path)
+# ---------------------------------------------------------------------------
+
+def _device_set(template, pos, vel, force, old_force, type_id, layout):
+    """ParticleSet over the given (n, 3) device tensors without a host round
+    trip (types, masses and parameters from ``template``)."""
+    from .particles import AOS, ParticleSet
+    out = ParticleSet.__new__(ParticleSet)
+    out.device = pos.device
+    out.types = list(template.types)
+    out.epsilon, out.sigma, out.mass = template.epsilon, template.sigma, template.mass
+    out.layout = AOS
+    out.pos, out.vel = pos.contiguous(), vel.contiguous()
+    out.force, out.old_force = force.contiguous(), old_force.contiguous()
+    out.type_id = type_id.to(torch.int32).contiguous()
+    out.convert_layout(layout)
+    return out
+
+
+class DeviceDecomposedSimulation:
+    """The reference loop (simulation.py:150-188, fixed configuration) on one
+    rank of a grid decomposition with everything on the device: libmdg's
+    drift / force / kick kernels and ``torch.distributed`` point-to-point
+    (NCCL over NVLink between GPUs) for the ghosts.
+
+    Each rank keeps ONE device ParticleSet in its LOCAL frame (origin
+    ``lo - ell`` along every decomposed axis; the local box is open there and
+    periodic along the others): rows ``[0, n_owned)`` are its particles, the
+    rows after them the ghosts of the current rebuild interval, in exchange
+    order.  A step is
+
+      drift (all rows) -> [rebuild: migrate, new ghost plan] -> ghost
+      positions (gather, shift by the slab width, send/recv straight into
+      the ghost rows; sizes fixed between rebuilds, so no count exchange and
+      no host synchronisation) -> refresh + compute -> kick,
+
+    forces of owned rows kept, no reverse exchange.  Ghost
+    rows are drifted and kicked with the rest (their positions are replaced
+    by the exchange before every force pass; their velocities are unused).
+    All axes must be periodic (BASELINE configs 2-5)."""
+
+    def __init__(self, dec: GridDecomposition, particles, params: SimulationParams, config,
+                 comm_device=None, ids=None):
+        from .calculator import ForceCalculator
+        per = params.periodic_flags()
+        if not all(bool(x) for x in per):
+            raise ValueError("the device decomposition needs periodic boundaries on every axis")
+        if getattr(params, "thermostat", None) is not None:
+            raise ValueError("thermostatted runs: use DecomposedSimulation")
+        self.dec, self.params, self.config = dec, params, config
+        self.comm_device = comm_device
+        self.local_params = dec.local_params()
+        self.template = particles
+        d = particles.device
+        pos = particles.view("pos").clone()
+        for a in range(3):
+            if dec.active[a]:
+                pos[:, a] = dec.near(pos[:, a], a) - dec.origin(a)
+        self.n_owned = pos.shape[0]
+        self.ids = (torch.arange(self.n_owned, device=pos.device) if ids is None
+                    else torch.as_tensor(ids, device=pos.device).clone())
+        self.ps = _device_set(particles, pos, particles.view("vel").clone(),
+                              particles.view("force").clone(), particles.view("old_force").clone(),
+                              particles.type_id.clone(), config.layout)
+        self.calc = ForceCalculator(self.ps, self.local_params)
+        self.axes = [a for a in range(3) if dec.active[a]]
+        self.plan = []          # per active axis: (axis, left idx, right idx, recv_l, recv_r, row0)
+        self.iteration, self.since = 0, 0
+        self.dev = d
+
+    # -- point-to-point -----------------------------------------------------
+    def _p2p(self, a, send_l, send_r, recv_l, recv_r):
+        d = self.dec
+        cd = self.comm_device
+        if cd is not None:
+            send_l, send_r = send_l.to(cd), send_r.to(cd)
+            bl, br = recv_l.to(cd), recv_r.to(cd)
+        else:
+            bl, br = recv_l, recv_r
+        ops = []
+        if d.has_left[a]:
+            ops += [dist.P2POp(dist.isend, send_l.contiguous(), d.left[a]),
+                    dist.P2POp(dist.irecv, bl, d.left[a])]
+        if d.has_right[a]:
+            ops += [dist.P2POp(dist.isend, send_r.contiguous(), d.right[a]),
+                    dist.P2POp(dist.irecv, br, d.right[a])]
+        for req in dist.batch_isend_irecv(ops) if ops else []:
+            req.wait()
+        if cd is not None:
+            recv_l.copy_(bl)
+            recv_r.copy_(br)
+
+    def _counts(self, a, nl, nr):
+        t_out_l = torch.tensor([nl], dtype=torch.int64, device=self.dev)
+        t_out_r = torch.tensor([nr], dtype=torch.int64, device=self.dev)
+        t_in_l = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        t_in_r = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self._p2p(a, t_out_l, t_out_r, t_in_l, t_in_r)
+        return int(t_in_l.item()), int(t_in_r.item())
+
+    # -- rebuild-time work --------------------------------------------------
+    def _owned_state(self):
+        n, ps = self.n_owned, self.ps
+        return [ps.view("pos")[:n].clone(), ps.view("vel")[:n].clone(),
+                ps.view("force")[:n].clone(), ps.view("old_force")[:n].clone(),
+                ps.type_id[:n].to(torch.float64).unsqueeze(1),
+                self.ids.to(torch.float64).unsqueeze(1)]
+
+    def _migrate(self, st):
+        """Owned rows outside [ell, ell + w) along a decomposed axis go to that
+        neighbour with their full state, axis by axis (frame shift +-w)."""
+        d, ell = self.dec, self.dec.ell
+        for a in self.axes:
+            w = d.width[a]
+            z = st[0][:, a]
+            go_l = (z < ell) if d.has_left[a] else torch.zeros_like(z, dtype=torch.bool)
+            go_r = (z >= ell + w) if d.has_right[a] else torch.zeros_like(z, dtype=torch.bool)
+            stay = ~(go_l | go_r)
+            pack = lambda m: torch.cat([s[m] for s in st], 1)
+            pl, pr = pack(go_l), pack(go_r)
+            pl[:, a] += w      # into the left neighbour's frame
+            pr[:, a] -= w
+            nl, nr = self._counts(a, pl.shape[0], pr.shape[0])
+            rl = torch.empty((nl, 14), dtype=torch.float64, device=self.dev)
+            rr = torch.empty((nr, 14), dtype=torch.float64, device=self.dev)
+            self._p2p(a, pl, pr, rl, rr)
+            inc = torch.cat([rl, rr], 0)
+            cols = [(0, 3), (3, 6), (6, 9), (9, 12), (12, 13), (13, 14)]
+            st = [torch.cat([s[stay], inc[:, c0:c1]], 0) for s, (c0, c1) in zip(st, cols)]
+        return st
+
+    def _replan(self, st):
+        """Ghost selection, axis by axis over owned + the ghosts of the earlier
+        axes: rows within ell of the low face go left, of the high face right."""
+        d, ell = self.dec, self.dec.ell
+        pos = st[0]
+        tcol = st[4]
+        plan = []
+        for a in self.axes:
+            w = d.width[a]
+            z = pos[:, a]
+            none = torch.zeros(0, dtype=torch.long, device=self.dev)
+            li = torch.nonzero(z < 2.0 * ell).flatten() if d.has_left[a] else none
+            ri = torch.nonzero(z >= w).flatten() if d.has_right[a] else none
+            nl, nr = self._counts(a, li.numel(), ri.numel())
+            row0 = pos.shape[0]
+            # the types travel once per rebuild; positions every step (_ghosts)
+            sl = torch.cat([pos[li], tcol[li]], 1)
+            sr = torch.cat([pos[ri], tcol[ri]], 1)
+            sl[:, a] += w
+            sr[:, a] -= w
+            rl = torch.empty((nl, 4), dtype=torch.float64, device=self.dev)
+            rr = torch.empty((nr, 4), dtype=torch.float64, device=self.dev)
+            self._p2p(a, sl, sr, rl, rr)
+            g = torch.cat([rl, rr], 0)
+            pos = torch.cat([pos, g[:, :3]], 0)
+            tcol = torch.cat([tcol, g[:, 3:4]], 0)
+            plan.append((a, li, ri, nl, nr, row0))
+        return plan, pos, tcol
+
+    def _rebuild(self):
+        st = self._migrate(self._owned_state())
+        n = st[0].shape[0]
+        plan, pos, tcol = self._replan(st)
+        m = pos.shape[0]
+        z = torch.zeros((m - n, 3), dtype=torch.float64, device=self.dev)
+        self.n_owned, self.plan = n, plan
+        self.ids = st[5][:, 0].to(torch.int64)
+        self.ps = _device_set(self.template, pos, torch.cat([st[1], z], 0),
+                              torch.cat([st[2], z], 0), torch.cat([st[3], z], 0),
+                              tcol[:, 0].to(torch.int32), self.config.layout)
+        self.calc.rebuild(self.ps, self.config)
+
+    # -- per step -----------------------------------------------------------
+    def _ghosts(self):
+        pv = self.ps.view("pos")
+        for a, li, ri, nl, nr, row0 in self.plan:
+            w = self.dec.width[a]
+            sl, sr = pv[li], pv[ri]
+            sl[:, a] += w
+            sr[:, a] -= w
+            rl = torch.empty((nl, 3), dtype=torch.float64, device=self.dev)
+            rr = torch.empty((nr, 3), dtype=torch.float64, device=self.dev)
+            self._p2p(a, sl, sr, rl, rr)
+            pv[row0:row0 + nl] = rl
+            pv[row0 + nl:row0 + nl + nr] = rr
+
+    def step(self):
+        p, cfg, calc = self.params, self.config, self.calc
+        calc.drift_wrap(self.ps, p.delta_t)
+        rebuild = self.iteration == 0 or self.since >= p.rebuild_interval
+        if rebuild:
+            self._rebuild()
+        else:
+            self._ghosts()
+        calc.refresh(self.ps, cfg)
+        calc.compute_async(self.ps, cfg)
+        calc.finish_kick(self.ps, p.delta_t, p.gravity)
+        self.since = 0 if rebuild else self.since + 1
+        self.iteration += 1
+
+    def run(self, steps):
+        for _ in range(steps):
+            self.step()
+
+    def check(self):
+        from .simulation import BlowUpError
+        if self.calc.blowup():
+            raise BlowUpError("particle left the domain by more than one domain length "
+                              "(or position is not finite)")
+
+    def owned(self, name):
+        """(n_owned, 3) of pos (GLOBAL frame, wrapped), vel, force, old_force."""
+        v = self.ps.view(name)[:self.n_owned].clone()
+        if name == "pos":
+            for a in self.axes:
+                v[:, a] = torch.remainder(v[:, a] + self.dec.origin(a), self.dec.L[a])
+        return v

@@ -59,18 +59,29 @@ def run(rank, world, port_no, steps, out_path, vscale=0.8, dt=2e-3, backend="ora
                                 thermostat=thermostat() if thermo else None)
     dec = GridDecomposition(params, rank, world, dims or (1, 1, world))
     mine = np.flatnonzero(dec.owner_of_positions(pos) == rank)
-    if backend == "gpu":   # libmdg on the (single) GPU, messages staged on the host for gloo
+    if backend == "gpudev":   # the device-resident decomposition (bench's N > 1 path)
+        from paper_2505_03438_b200.decomp import DeviceDecomposedSimulation
+        cfg = P.parse_configuration("VL-List_Iter-NoN3L-SoA" if world % 2 == 0 else
+                                    "VL-List_Iter-NoN3L-AoS")
+        parts = P.ParticleSet(pos[mine], vel[mine], device="cuda:0")
+        sim = DeviceDecomposedSimulation(dec, parts, params, cfg, comm_device="cpu",
+                                         ids=torch.as_tensor(mine))
+        sim.run(steps)
+        sim.check()
+        sim.pos, sim.vel, sim.ids = sim.owned("pos").cpu(), sim.owned("vel").cpu(), sim.ids.cpu()
+    elif backend == "gpu":   # libmdg on the (single) GPU, messages staged on the host for gloo
         from paper_2505_03438_b200.decomp import gpu_force_backend
         dev = torch.device("cuda", 0)
         fn = gpu_force_backend(P.parse_configuration("VL-List_Iter-NoN3L-AoS"), [1.0], [1.0], [1.0])
         comm = "cpu"
     else:
         dev, fn, comm = torch.device("cpu"), oracle_force_fn, None
-    sim = DecomposedSimulation(dec, torch.as_tensor(pos[mine]).to(dev), torch.as_tensor(vel[mine]).to(dev),
-                               torch.zeros(len(mine), dtype=torch.int64, device=dev), [1.0], params,
-                               fn, ids=torch.as_tensor(mine).to(dev), comm_device=comm)
-    sim.run(steps)
-    sim.pos, sim.vel, sim.ids = sim.pos.cpu(), sim.vel.cpu(), sim.ids.cpu()
+    if backend != "gpudev":
+        sim = DecomposedSimulation(dec, torch.as_tensor(pos[mine]).to(dev), torch.as_tensor(vel[mine]).to(dev),
+                                   torch.zeros(len(mine), dtype=torch.int64, device=dev), [1.0], params,
+                                   fn, ids=torch.as_tensor(mine).to(dev), comm_device=comm)
+        sim.run(steps)
+        sim.pos, sim.vel, sim.ids = sim.pos.cpu(), sim.vel.cpu(), sim.ids.cpu()
     payload = torch.cat([sim.ids.to(torch.float64).unsqueeze(1), sim.pos, sim.vel,
                          torch.full((sim.pos.shape[0], 1), float(rank), dtype=torch.float64)], 1)
     sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]

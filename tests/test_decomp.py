@@ -31,7 +31,7 @@ def _run(world, steps, tmp_path, vscale=0.8, dt=2e-3, tag="", backend="oracle", 
     out = str(tmp_path / f"decomp_{world}{tag}{backend}{size}{int(thermo)}.npy")
     port = _free_port()
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
-    if backend != "gpu":
+    if not backend.startswith("gpu"):
         env["CUDA_VISIBLE_DEVICES"] = ""
     dim_arg = "x".join(str(d) for d in dims) if dims else "-"
     procs = [subprocess.Popen([sys.executable, WORKER, str(r), str(world), str(port), str(steps), out,
@@ -113,6 +113,34 @@ def test_decomposed_gpu_backend_matches_reference_loop(tmp_path):
     d -= L * np.rint(d / L)
     assert np.abs(d).max() <= 1e-9
     assert np.abs(two[:, 4:7] - np.asarray(p.velocities)).max() <= 1e-9
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,dims,size,steps", [(2, None, "small", 40), (8, (2, 2, 2), "cube10", 24),
+                                                   (3, (1, 1, 3), "cube10", 24)])
+def test_device_decomposition_matches_reference_loop(tmp_path, world, dims, size, steps):
+    """DeviceDecomposedSimulation (everything on the GPU: libmdg drift / force /
+    kick, ghosts gathered and scattered on the device, sizes fixed between
+    rebuilds) with gloo ranks sharing the one GPU (messages staged on the
+    host; no rank waits on another inside a kernel) reproduces the reference
+    loop: z-slabs (VL-SoA), a 2x2x2 grid (VL-SoA) and 3 slabs (VL-AoS)."""
+    vs, dt = (4.0, 4e-3) if size == "small" else (2.0, 3e-3)
+    many = _run(world, steps, tmp_path, vscale=vs, dt=dt, tag="dev", backend="gpudev", dims=dims,
+                size=size)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from decomp_worker import system
+    from oracle import port
+    pos, vel, L = system(vscale=vs, size=size)
+    assert np.array_equal(many[:, 0], np.arange(len(pos)))   # every particle owned once
+    assert len(np.unique(many[:, 7])) == world
+    params = port.Params(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=4, delta_t=dt,
+                         boundary=(port.PERIODIC,) * 3)
+    p = port.Particles(pos, vel)
+    port.simulate_fixed(p, params, port.parse("VL-List_Iter-NoN3L-AoS"), steps=steps)
+    d = many[:, 1:4] - np.asarray(p.positions)
+    d -= L * np.rint(d / L)
+    assert np.abs(d).max() <= 1e-9
+    assert np.abs(many[:, 4:7] - np.asarray(p.velocities)).max() <= 1e-9
 
 
 @pytest.fixture(scope="module")

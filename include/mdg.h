@@ -128,6 +128,12 @@ int mdg_potential_energy(mdg_ctx* ctx, int rebuild, double* pe);
 int mdg_drift_wrap(mdg_ctx* ctx, double dt);
 /* apply_gravity + finish_kick (integrator.py:40-51; simulation.py:177,185). */
 int mdg_finish_kick(mdg_ctx* ctx, double dt, int has_gravity, double gravity);
+/* finish_kick of the previous step fused with this step's drift_wrap, one
+ * pass over the bound state, bit-identical to mdg_finish_kick then
+ * mdg_drift_wrap (integrator.py:31-51, 98-128).  copy_old_force = 0 skips the
+ * F -> F_old copy: the caller then swaps its force / old_force buffers (and
+ * re-binds) before the next compute. */
+int mdg_kick_drift(mdg_ctx* ctx, double dt, int has_gravity, double gravity, int copy_old_force);
 /* Capped steepest-descent step x += F/|F| min(gamma|F|, max_disp) (input
  * relaxation for BASELINE configs 2/4; no reference counterpart). */
 int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp);

@@ -162,6 +162,14 @@ class ForceCalculator:
         check(lib().mdg_finish_kick(self.ctx.h, float(dt), int(gravity is not None),
                                     float(gravity or 0.0)), "finish_kick")
 
+    def kick_drift(self, particles, dt, gravity=None, copy_old_force=True):
+        """finish_kick of the previous step + this step's drift_wrap in one
+        pass (mdg_kick_drift); with ``copy_old_force=False`` the caller swaps
+        ``particles.force`` / ``old_force`` afterwards."""
+        self.bind(particles)
+        check(lib().mdg_kick_drift(self.ctx.h, float(dt), int(gravity is not None),
+                                   float(gravity or 0.0), int(bool(copy_old_force))), "kick_drift")
+
     def sd_step(self, particles, gamma, max_disp):
         self.bind(particles)
         check(lib().mdg_sd_step(self.ctx.h, float(gamma), float(max_disp)), "sd_step")

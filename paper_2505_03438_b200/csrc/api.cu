@@ -480,6 +480,13 @@ int mdg_finish_kick(mdg_ctx* ctx, double dt, int has_gravity, double gravity) {
     return cuda_status("mdg_finish_kick");
 }
 
+int mdg_kick_drift(mdg_ctx* ctx, double dt, int has_gravity, double gravity, int copy_old_force) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    integ_kick_drift(ctx->c, dt, has_gravity, gravity, copy_old_force != 0);
+    return cuda_status("mdg_kick_drift");
+}
+
 int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp) {
     CHECK_CTX(ctx);
     if (int e = need_system(ctx)) return e;

@@ -84,6 +84,52 @@ __global__ void finish_kick_kernel(BoxParams p, const int* __restrict__ tid,
     }
 }
 
+// finish_kick of step s fused with the drift + boundaries of step s+1: per
+// element exactly finish_kick_kernel's operations, then drift_wrap_kernel's
+// (gravity into F_z, v += (F + F_old) dt/(2m), x += v dt, x += F dt^2/(2m),
+// wrap / reflect with the velocity flip, blow-up test), one pass over the
+// particle state instead of two.  COPY: F -> F_old as drift_wrap does;
+// otherwise the caller swaps its force / old_force buffers afterwards.
+template <int LAYOUT, bool COPY>
+__global__ void kick_drift_kernel(BoxParams p, const int* __restrict__ tid,
+                                  const double* __restrict__ mass, double* __restrict__ pos,
+                                  double* __restrict__ vel, double* __restrict__ force,
+                                  double* __restrict__ old_force, int has_gravity, double g,
+                                  unsigned long long* blowup) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    double m = mass[tid ? tid[i] : 0];
+    double ck = __ddiv_rn(__dmul_rn(0.5, p.dt), m);
+    double cd = __ddiv_rn(__dmul_rn(__dmul_rn(0.5, p.dt), p.dt), m);
+    bool bad = false;
+    for (int k = 0; k < 3; ++k) {
+        size_t a = pidx<LAYOUT>(i, k, p.n);
+        double f = force[a];
+        if (k == 2 && has_gravity) {
+            f = __dadd_rn(f, __dmul_rn(m, g));
+            force[a] = f;
+        }
+        double v = __dadd_rn(vel[a], __dmul_rn(__dadd_rn(f, old_force[a]), ck));
+        double x = __dadd_rn(pos[a], __dmul_rn(v, p.dt));
+        x = __dadd_rn(x, __dmul_rn(f, cd));
+        double L = p.L[k];
+        if (!(x >= -L && x <= 2.0 * L)) bad = true;
+        if (p.periodic[k]) {
+            x = np_mod(x, L);
+        } else if (x < 0.0) {
+            x = -x;
+            v = -v;
+        } else if (x > L) {
+            x = __dadd_rn(2.0 * L, -x);
+            v = -v;
+        }
+        pos[a] = x;
+        vel[a] = v;
+        if (COPY) old_force[a] = f;
+    }
+    if (bad) atomicOr(blowup, 1ull);
+}
+
 // Capped steepest descent used to relax overlapping random inputs (BASELINE
 // configs 2 and 4; no reference counterpart): x += F/|F| * min(gamma|F|, dmax),
 // then the boundary rule of the axis.
@@ -145,6 +191,19 @@ void integ_finish_kick(Context& c, double dt, int has_gravity, double gravity) {
         finish_kick_kernel<AOS><<<b, t, 0, c.stream>>>(p, c.tid, c.d_mass.p, c.vel, c.force, c.old_force, has_gravity, gravity), note_launch();
     else
         finish_kick_kernel<SOA><<<b, t, 0, c.stream>>>(p, c.tid, c.d_mass.p, c.vel, c.force, c.old_force, has_gravity, gravity), note_launch();
+}
+
+void integ_kick_drift(Context& c, double dt, int has_gravity, double gravity, bool copy) {
+    if (c.n == 0) return;
+    BoxParams p = box(c, dt);
+    dim3 b(blocks_for(c.n, 256)), t(256);
+#define MDG_KD(LY, CP) kick_drift_kernel<LY, CP><<<b, t, 0, c.stream>>>(p, c.tid, c.d_mass.p, c.pos, c.vel, c.force, c.old_force, has_gravity, gravity, c.scal.p + 2), note_launch()
+    if (c.layout == AOS) {
+        if (copy) MDG_KD(AOS, true); else MDG_KD(AOS, false);
+    } else {
+        if (copy) MDG_KD(SOA, true); else MDG_KD(SOA, false);
+    }
+#undef MDG_KD
 }
 
 void integ_sd_step(Context& c, double gamma, double dmax) {

@@ -238,6 +238,7 @@ template <int PLAYOUT>
 void vl_force_rows_launch(Context& c, const uint8_t* only);
 void integ_drift_wrap(Context& c, double dt);
 void integ_finish_kick(Context& c, double dt, int has_gravity, double gravity);
+void integ_kick_drift(Context& c, double dt, int has_gravity, double gravity, bool copy);
 void integ_sd_step(Context& c, double gamma, double max_disp);
 int stats_temperature(Context& c, double* t);
 int stats_thermostat(Context& c, double target, double max_delta_t);

@@ -540,6 +540,9 @@ class DeviceDecomposedSimulation:
         for _ in range(steps):
             self.step()
 
+    def flush(self):
+        """Nothing deferred here (the Simulation interface bench.py drives)."""
+
     def check(self):
         from .simulation import BlowUpError
         if self.calc.blowup():

@@ -103,7 +103,7 @@ class Simulation:
     anything with the TuningController protocol (tuning.py:200-239)."""
 
     def __init__(self, particles, params, config=None, calculator=None, controller=None,
-                 tuning_interval=None, graphs=False):
+                 tuning_interval=None, graphs=False, fuse_kick_drift=False):
         if controller is None:
             if config is None:
                 raise ValueError("need a configuration or a controller")
@@ -122,6 +122,12 @@ class Simulation:
         # steady-state iterations (no rebuild, not timed) from a cached CUDA
         # graph of drift + refresh + compute + kick (mdg_step_graph)
         self.graphs = graphs
+        # defer an untimed step's kick into the next step's drift (one pass,
+        # mdg_kick_drift, force / old_force swapped instead of copied); the
+        # state is complete again after flush() (run(), check() and report()
+        # flush; callers of step() who read particles in between call it)
+        self.fuse_kick_drift = fuse_kick_drift
+        self._kick_due = False
 
     @property
     def config(self):
@@ -142,9 +148,14 @@ class Simulation:
     def step(self, record=False):
         p, params, calc, ctl = self.p, self.params, self.calc, self.controller
         it = self.iteration
-        if self.graphs and not record and self._graph_step(it):
+        if self.graphs and not record and not self._kick_due and self._graph_step(it):
             return False
-        calc.drift_wrap(p, params.delta_t)
+        if self._kick_due:
+            calc.kick_drift(p, params.delta_t, params.gravity, copy_old_force=False)
+            p.force, p.old_force = p.old_force, p.force
+            self._kick_due = False
+        else:
+            calc.drift_wrap(p, params.delta_t)
         pending = getattr(self, "_pending", None)
         self._pending = None
         while True:
@@ -169,9 +180,16 @@ class Simulation:
                 calc.refresh(p, cfg)
                 if timed:
                     ev[1].record()
-                # force + gravity + finish_kick; the kick is fused into the
-                # force walk where the configuration allows (mdg_compute_kick)
-                calc.compute_kick_async(p, cfg, params.delta_t, params.gravity)
+                thermo = params.thermostat
+                defer = (self.fuse_kick_drift and not timed and not self.graphs
+                         and (thermo is None or (it + 1) % thermo.interval_iterations != 0))
+                if defer:   # the kick runs inside the next step's drift
+                    calc.compute_async(p, cfg)
+                    self._kick_due = True
+                else:
+                    # force + gravity + finish_kick; the kick is fused into the
+                    # force walk where the configuration allows (mdg_compute_kick)
+                    calc.compute_kick_async(p, cfg, params.delta_t, params.gravity)
                 if timed:
                     ev[2].record()
                 break
@@ -217,14 +235,23 @@ class Simulation:
         self.iteration += 1
         return True
 
+    def flush(self):
+        """Run a deferred kick (fuse_kick_drift), completing the state."""
+        if self._kick_due:
+            self.calc.finish_kick(self.p, self.params.delta_t, self.params.gravity)
+            self._kick_due = False
+
     def run(self, steps, record=True):
         for _ in range(steps):
             self.step(record=record)
+        self.flush()
 
     def check(self):
+        self.flush()
         self._check_flags()
 
     def report(self, rep=None) -> SimulationReport:
+        self.flush()
         torch.cuda.synchronize(self.p.device)
         rep = rep or SimulationReport()
         for it, cid, rebuilt, phase, ev in self._events:

@@ -659,3 +659,38 @@ def test_step_graph_is_bit_identical(pkg):
             out.append((parts.numpy("pos"), parts.numpy("vel"), parts.numpy("force")))
         for a, b in zip(*out):
             assert np.array_equal(a, b), cid
+
+
+def test_fused_kick_drift_loop_is_bit_identical(pkg):
+    """Simulation(fuse_kick_drift=True): each untimed step's kick deferred into
+    the next step's drift (mdg_kick_drift, force / old_force swapped instead
+    of copied) equals the two-pass loop bit for bit -- LC / VL / VCL, two
+    types, gravity, a reflective axis, a thermostat (whose steps kick
+    eagerly), and state read back between partial runs."""
+    P, calc = pkg
+    from paper_2505_03438_b200.simulation import Simulation
+    z = golden("traj_small.npz")
+    L = z["domain"]
+    n = len(z["pos0"])
+    tid = np.arange(n) % 2
+    types = [P.ParticleTypeInfo(0, 1.0, 1.0, 1.0), P.ParticleTypeInfo(1, 1.2, 0.9, 1.5)]
+    for cid in ("VL-List_Iter-NoN3L-SoA", "LC-C08-N3L-AoS-CSF1", "VCL-ClusterIter-NoN3L-AoS"):
+        for boundary in ((P.PERIODIC,) * 3, (P.PERIODIC, P.REFLECTIVE, P.PERIODIC)):
+            out = []
+            for fuse in (False, True):
+                params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=4,
+                                            delta_t=1e-3, boundary=boundary, gravity=-0.3,
+                                            thermostat=P.ThermostatParams(0.9, 0.05, 7))
+                cfg = P.parse_configuration(cid)
+                parts = P.ParticleSet(z["pos0"], z["vel0"], type_ids=tid, types=types,
+                                      layout=cfg.layout)
+                sim = Simulation(parts, params, cfg, fuse_kick_drift=fuse)
+                snaps = []
+                for k in (5, 1, 13):
+                    sim.run(k, record=False)
+                    snaps.append(parts.numpy("vel"))
+                sim.check()
+                out.append([parts.numpy("pos"), parts.numpy("vel"), parts.numpy("force"),
+                            parts.numpy("old_force")] + snaps)
+            for a, b in zip(*out):
+                assert np.array_equal(a, b), (cid, boundary)

@@ -393,7 +393,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=11)
     ap.add_argument("--impl", default="mdg", choices=("mdg", "reference"))
     ap.add_argument("--config", default=DEFAULT_CONFIG)
-    ap.add_argument("--n", type=int, default=1_048_576)
+    ap.add_argument("--particles", "--n", dest="n", type=int, default=1_048_576)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -694,3 +694,48 @@ def test_fused_kick_drift_loop_is_bit_identical(pkg):
                             parts.numpy("old_force")] + snaps)
             for a, b in zip(*out):
                 assert np.array_equal(a, b), (cid, boundary)
+
+
+def test_pipelined_host_run_blow_up_matches_step_path(pkg):
+    """A particle thrown out of the box (two particles 0.3 sigma apart: the
+    step-1 drift moves one by >> L) raises BlowUpError from HostSimulation.run
+    at the same iteration as the one-step-per-call path."""
+    P, calc = pkg
+    from paper_2505_03438_b200.hostloop import HostParticleSet, HostSimulation
+    from paper_2505_03438_b200.simulation import BlowUpError
+    z = golden("traj_small.npz")
+    L = z["domain"]
+    pos = np.array(z["pos0"], copy=True)
+    pos[1] = pos[0] + np.array([0.3, 0.0, 0.0])
+    its = []
+    for chunks in (1, 4):
+        params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=10,
+                                    delta_t=1e-3, boundary=(P.PERIODIC,) * 3)
+        p = HostParticleSet(np.mod(pos, L), z["vel0"])
+        sim = HostSimulation(p, params, P.parse_configuration("VL-List_Iter-NoN3L-AoS"), chunks=chunks)
+        with pytest.raises(BlowUpError):
+            sim.run(5)
+        its.append(sim.iteration)
+    assert its[0] == its[1] == 1, its
+
+
+def test_device_decomposition_single_rank_is_the_plain_loop(pkg):
+    """DeviceDecomposedSimulation on one rank (no decomposed axis, no ghosts,
+    no process group needed) is the plain device loop, bit for bit."""
+    P, calc = pkg
+    from paper_2505_03438_b200.decomp import DeviceDecomposedSimulation, GridDecomposition
+    from paper_2505_03438_b200.simulation import Simulation
+    z = golden("traj_small.npz")
+    L = z["domain"]
+    params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=4,
+                                delta_t=1e-3, boundary=(P.PERIODIC,) * 3)
+    cfg = P.parse_configuration("VL-List_Iter-NoN3L-SoA")
+    a = P.ParticleSet(z["pos0"], z["vel0"], layout="SoA")
+    Simulation(a, params, cfg).run(17, record=False)
+    dsim = DeviceDecomposedSimulation(GridDecomposition(params, 0, 1), P.ParticleSet(z["pos0"], z["vel0"]),
+                                      params, cfg)
+    dsim.run(17)
+    dsim.check()
+    assert np.array_equal(dsim.owned("pos").cpu().numpy(), a.numpy("pos"))
+    assert np.array_equal(dsim.owned("vel").cpu().numpy(), a.numpy("vel"))
+    assert np.array_equal(dsim.ids.cpu().numpy(), np.arange(len(z["pos0"])))

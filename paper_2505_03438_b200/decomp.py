@@ -403,6 +403,7 @@ class DeviceDecomposedSimulation:
         self.axes = [a for a in range(3) if dec.active[a]]
         self.plan = []          # per active axis: (axis, left idx, right idx, recv_l, recv_r, row0)
         self.iteration, self.since = 0, 0
+        self._kick_due = False
         self.dev = d
 
     # -- point-to-point -----------------------------------------------------
@@ -523,8 +524,15 @@ class DeviceDecomposedSimulation:
             pv[row0 + nl:row0 + nl + nr] = rr
 
     def step(self):
+        """One iteration; its kick is deferred into the next step's drift
+        (mdg_kick_drift, force / old_force swapped) -- flush() completes it."""
         p, cfg, calc = self.params, self.config, self.calc
-        calc.drift_wrap(self.ps, p.delta_t)
+        if self._kick_due:
+            calc.kick_drift(self.ps, p.delta_t, p.gravity, copy_old_force=False)
+            self.ps.force, self.ps.old_force = self.ps.old_force, self.ps.force
+            self._kick_due = False
+        else:
+            calc.drift_wrap(self.ps, p.delta_t)
         rebuild = self.iteration == 0 or self.since >= p.rebuild_interval
         if rebuild:
             self._rebuild()
@@ -532,25 +540,31 @@ class DeviceDecomposedSimulation:
             self._ghosts()
         calc.refresh(self.ps, cfg)
         calc.compute_async(self.ps, cfg)
-        calc.finish_kick(self.ps, p.delta_t, p.gravity)
+        self._kick_due = True
         self.since = 0 if rebuild else self.since + 1
         self.iteration += 1
 
     def run(self, steps):
         for _ in range(steps):
             self.step()
+        self.flush()
 
     def flush(self):
-        """Nothing deferred here (the Simulation interface bench.py drives)."""
+        """Run the deferred kick of the last step (state complete again)."""
+        if self._kick_due:
+            self.calc.finish_kick(self.ps, self.params.delta_t, self.params.gravity)
+            self._kick_due = False
 
     def check(self):
         from .simulation import BlowUpError
+        self.flush()
         if self.calc.blowup():
             raise BlowUpError("particle left the domain by more than one domain length "
                               "(or position is not finite)")
 
     def owned(self, name):
         """(n_owned, 3) of pos (GLOBAL frame, wrapped), vel, force, old_force."""
+        self.flush()
         v = self.ps.view(name)[:self.n_owned].clone()
         if name == "pos":
             for a in self.axes:

@@ -101,7 +101,7 @@ __global__ void vlt_desc_kernel(GridView gv, TilePlan tp, int ntiles, int cap4, 
     d.pad0 = 0;
     d.pad1[0] = d.pad1[1] = 0;
     desc[t] = d;
-    tsize[t] = d.big ? 0 : (io + 31) / 32 * 32 * cap4;
+    tsize[t] = d.big ? 0 : (io + 31) / 32 * 32;   // list slots (rows padded to 32); x cap4 entries
     if (d.big) atomicAdd(nbig, 1);
 }
 
@@ -181,8 +181,10 @@ __global__ void __launch_bounds__(kBuildThreadsT) vlt_build_kernel(
     // grid's sort_by_z), so the candidates within ell in z are a contiguous
     // sub-run; fp32 coordinates are within u|x| of fp64, hence the 2 eta pad
     const double zpad = ell + 2.0 * eta;
-    const int base = tbase[blockIdx.x];
-    const int slot0 = base / cap4;
+    // tbase counts list slots (padded rows): 32-bit even when the entries
+    // (slots x cap4, BASELINE config 5: ~5.4 G) are not
+    const int slot0 = tbase[blockIdx.x];
+    const size_t base = (size_t)slot0 * cap4;
     const int ngroups = cap4 >> 2;
     for (int q = threadIdx.x; q < d.ni; q += blockDim.x) {
         int C = 0;
@@ -473,14 +475,14 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
             } else if (PF == 3) {
                 // the tile's list stream (and counts) into L2 while the window
                 // lands: the consumers' list loads then hit L2 instead of HBM
-                int base = tbase[t];
+                size_t base = (size_t)tbase[t] * cap4;
                 size_t bytes = (size_t)((D.ni + 31) / 32 * 32) * cap4 * 2;
-                const char* lb = reinterpret_cast<const char*>(tl) + (size_t)base * 2;
+                const char* lb = reinterpret_cast<const char*>(tl) + base * 2;
                 for (size_t off = (size_t)(lane - kRanges) * 32768; off < bytes; off += 16 * 32768)
                     bulk_prefetch_l2(lb + off, (unsigned)min((size_t)32768, bytes - off));
                 if (lane == kRanges) {
                     size_t cb = ((size_t)(D.ni + 3) / 4) * 16;   // tcnt slots, whole 16-byte units
-                    const char* cp = reinterpret_cast<const char*>(tcnt + base / cap4);
+                    const char* cp = reinterpret_cast<const char*>(tcnt + tbase[t]);
                     size_t a0 = (size_t)cp & 15;                 // round the start down to 16 bytes
                     bulk_prefetch_l2(cp - a0, (unsigned)(cb + 16));
                 }
@@ -501,8 +503,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
             const double* wy = wx + wrows;
             const double* wz = wy + wrows;
             const int* wt = reinterpret_cast<const int*>(wz + wrows);
-            int base = tbase[t];
-            int slot0 = base / cap4;
+            int slot0 = tbase[t];
+            size_t base = (size_t)slot0 * cap4;
             int ni = D.ni;
             for (;;) {
                 int q0 = 0;
@@ -655,16 +657,19 @@ int vlt_build(Context& c) {
         // the lists get an upper-bound allocation (every tile's rows padded to
         // whole 32-row blocks), so the exact size is not needed on the host
         // before the build: one synchronisation per rebuild instead of two
-        long long bound = ((long long)c.n + 32ll * ntiles) * v.cap4;
-        if (bound > (1ll << 31) - 64) return 1;   // keep the row-space walk
+        // slots (rows padded per tile) fit 32 bits; entries (slots x cap4) are
+        // 64-bit -- BASELINE config 5 (67 M particles) needs ~5.4 G
+        long long slots = (long long)c.n + 32ll * ntiles;
+        if (slots > (1ll << 31) - 64) return 1;   // keep the row-space walk
+        long long bound = slots * v.cap4;
         v.tl.ensure((size_t)bound + 8);
-        v.tcnt.ensure((size_t)bound / v.cap4 + 32);
+        v.tcnt.ensure((size_t)slots + 32);
         if (!v.tl.p || !v.tcnt.p) {
             set_error("out of device memory (VL tile lists)");
             return -1;
         }
         MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
-        MDG_CUDA(cudaMemsetAsync(v.tcnt.p, 0, ((size_t)bound / v.cap4 + 32) * sizeof(int), c.stream));
+        MDG_CUDA(cudaMemsetAsync(v.tcnt.p, 0, ((size_t)slots + 32) * sizeof(int), c.stream));
         vlt_build_kernel<<<ntiles, kBuildThreadsT, 0, c.stream>>>(
             gv, desc, v.tbase.p, v.b32.p, gr.spos4.p, maxabs, ell2, v.cap, v.cap4, v.tl.p, v.tcnt.p,
             maxcnt, gr.sort_by_z), note_launch();
@@ -680,8 +685,8 @@ int vlt_build(Context& c) {
         v.cap = (hmax + hmax / 8 + 7) / 8 * 8;
     }
     if (int order = vlt_env_order()) {
-        long long total = (long long)c.h_scal[1];
-        int64_t nblocks = total / (32 * (int64_t)v.cap4);
+        long long total = (long long)c.h_scal[1];   // list slots
+        int64_t nblocks = total / 32;
         int warps = (int)std::max<size_t>(1, std::min<size_t>(8, (200u << 10) / (32 * (size_t)v.cap4 * 2 + 16 * 32 * 8)));
         size_t smem = (size_t)warps * (2 * 16 * 32 * sizeof(int) + 32 * (size_t)v.cap4 * sizeof(uint16_t));
         static size_t attr = 0;
@@ -880,9 +885,9 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
                     if (MT) bulk_g2s(wt + o, row_tid + g, rows * 4u, &full[b]);
                 }
             } else {
-                int base = tbase[t];
+                size_t base = (size_t)tbase[t] * cap4;
                 size_t bytes = (size_t)((D.ni + 31) / 32 * 32) * cap4 * 2;
-                const char* lb = reinterpret_cast<const char*>(tl) + (size_t)base * 2;
+                const char* lb = reinterpret_cast<const char*>(tl) + base * 2;
                 for (size_t off = (size_t)(lane - kRanges) * 32768; off < bytes; off += 16 * 32768)
                     bulk_prefetch_l2(lb + off, (unsigned)min((size_t)32768, bytes - off));
             }
@@ -900,8 +905,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
         if (!D.big) {
             const float4* w4 = reinterpret_cast<const float4*>(win + b * kBuf);
             const int* wt = reinterpret_cast<const int*>(w4 + wrows);
-            int base = tbase[t];
-            int slot0 = base / cap4;
+            int slot0 = tbase[t];
+            size_t base = (size_t)slot0 * cap4;
             int ni = D.ni;
             for (;;) {
                 int q0 = 0;

@@ -739,3 +739,32 @@ def test_device_decomposition_single_rank_is_the_plain_loop(pkg):
     assert np.array_equal(dsim.owned("pos").cpu().numpy(), a.numpy("pos"))
     assert np.array_equal(dsim.owned("vel").cpu().numpy(), a.numpy("vel"))
     assert np.array_equal(dsim.ids.cpu().numpy(), np.arange(len(z["pos0"])))
+
+
+def test_config5_tiled_lists_past_32_bit_entries(pkg):
+    """BASELINE config 5 (67,108,864 FCC particles) on one GPU: the tiled
+    Verlet lists hold ~5.4 G entries (64-bit offsets; per-tile bases count
+    32-bit slots).  Size-independent parity against an independent path on
+    the same snapshot: the VL count (2 per pair) is exactly twice LC-SLI-N3L's
+    (1 per pair), and the forces agree within the fp64 tolerance."""
+    P, calc = pkg
+    import torch
+    from paper_2505_03438_b200 import systems
+    pos, vel, params = systems.config5_inputs()
+    parts = P.ParticleSet(pos, layout="SoA")
+    del pos, vel
+    fc = calc.ForceCalculator(parts, params)
+    vl = P.parse_configuration("VL-List_Iter-NoN3L-SoA")
+    fc.rebuild(parts, vl)
+    fc.refresh(parts, vl)
+    n_vl = fc.compute(parts, vl)
+    f_vl = parts.view("force").clone()
+    lc = P.parse_configuration("LC-SLI-N3L-SoA-CSF1")
+    fc.rebuild(parts, lc)
+    fc.refresh(parts, lc)
+    n_lc = fc.compute(parts, lc)
+    fc.close()
+    assert n_vl == 2 * n_lc and n_lc > 1_700_000_000
+    num = torch.linalg.vector_norm(parts.view("force") - f_vl)
+    den = torch.linalg.vector_norm(f_vl)
+    assert float(num / den) <= FP64_TOL

@@ -541,10 +541,9 @@ static int lc_env_rows() {
     return v;
 }
 
-// C08 realisation: 1 (default) per colour, row-slot threads for sparse cells
-// and warp tiles for dense ones, every anchor in one launch when a colour has
-// fewer than 4 anchors per SM; 0 warp tiles per colour always; 2 every anchor
-// in one launch (row slots)
+// C08 realisation: 1 per colour, row-slot threads for sparse cells and warp
+// tiles for dense ones (default); 0 warp tiles per colour always; 2 every
+// anchor in one launch (row slots)
 static int lc_env_c08() {
     static int v = -1;
     if (v < 0) {
@@ -606,13 +605,7 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
     }
     ColourLaunch cl;
     double rows_per_cell = (double)gr.m / (double)std::max<int64_t>(1, g.ncells);
-    // C08 with too few anchors per colour to fill the GPU (small systems,
-    // BASELINE config 1: ~90 anchor warps per colour, 73 us per colour launch)
-    // runs every anchor in one launch (config 1: 0.56 -> 0.15 ms per step)
-    int64_t anchors_per_colour = (int64_t)g.D[0] * g.D[1] * g.D[2] /
-                                 ((g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1));
-    bool c08_one_launch = lc_env_c08() == 2 || (lc_env_c08() == 1 && anchors_per_colour < 4 * c.sm_count);
-    if ((traversal == T_C18 && lc_env_rows()) || (traversal == T_C08 && c08_one_launch)) {
+    if ((traversal == T_C18 && lc_env_rows()) || (traversal == T_C08 && lc_env_c08() == 2)) {
         // every unit of every colour in one launch (the row kernels resolve the
         // write races with atomics, which is what the colours are for on a CPU)
         for (int k = 0; k < 3; ++k) {

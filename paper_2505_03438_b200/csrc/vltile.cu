@@ -925,6 +925,13 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
                     uint2 g0 = __ldcs(lp);
                     int i = row_src[r];
                     double fx = 0.0, fy = 0.0, fz = 0.0;
+                    float s2c = 0.f, e24c = 0.f;
+                    if (!MT) {
+                        double s2d, e24d;
+                        lj_params<false>(tab, 0, 0, s2d, e24d);
+                        s2c = (float)s2d;
+                        e24c = (float)e24d;
+                    }
                     for (int k0 = 0; k0 < c; k0 += 4) {
                         uint2 cur = g0;
                         if (k0 + 4 < c) g0 = __ldcs(lp + (size_t)(k0 / 4 + 1) * 32);
@@ -940,12 +947,20 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
                             float dz = (qi.z - qj.z) + (float)((ci & 1023) - (cj & 1023)) * cc.cl[2];
                             float r2 = dx * dx + dy * dy + dz * dz;
                             if ((k0 + u < c) && r2 < rc2) {
-                                double s2d, e24d;
-                                lj_params<MT>(tab, ti, MT ? wt[jj[u]] : 0, s2d, e24d);
-                                float inv = __frcp_rn(r2);
-                                float a = (float)s2d * inv;
+                                float s2f = s2c, e24f = e24c;
+                                if (MT) {
+                                    double s2d, e24d;
+                                    lj_params<MT>(tab, ti, wt[jj[u]], s2d, e24d);
+                                    s2f = (float)s2d;
+                                    e24f = (float)e24d;
+                                }
+                                // approximate reciprocal (MUFU.RCP, ~2^-22 relative):
+                                // far inside the variant's 1e-4 tolerance
+                                float inv;
+                                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(r2));
+                                float a = s2f * inv;
                                 float a6 = a * a * a;
-                                float fs = ((float)e24d * inv) * (a6 * fmaf(2.0f, a6, -1.0f));
+                                float fs = (e24f * inv) * (a6 * fmaf(2.0f, a6, -1.0f));
                                 ++hits;
                                 px = fmaf(fs, dx, px);
                                 py = fmaf(fs, dy, py);

@@ -532,6 +532,111 @@ __global__ void __launch_bounds__(128) lc_c08_cells_kernel(GridView gv, ScratchP
     warp_count(counter, cnt);
 }
 
+// C08 for small systems, deterministic: one warp per (anchor, block cell) of
+// a colour, lanes = rows of that cell.  The warp evaluates, for its rows,
+// every pair of the anchor that touches its cell -- as the first cell
+// (partners c + d, d in t1[cell]), as the second (partners c - d, d in
+// t2[cell]) and the anchor's intra pairs -- and writes only its own rows, so
+// no two warps of a launch write the same row and no atomics are needed.
+// Each pair is evaluated from both sides (F(j,i) = -F(i,j) bit for bit); the
+// count is taken once per pair for N3L (first-cell side, j > i within a cell)
+// and per direction for NoN3L, as the reference counts.  Twice the pair
+// arithmetic of the tiles, 8 (27) times their warps: BASELINE config 1 has ~90
+// anchors per colour, which leave a one-warp-per-anchor launch latency-bound.
+template <int LAYOUT, bool MT, bool N3L>
+__global__ void __launch_bounds__(128) lc_c08_cellwarp_kernel(GridView gv, ScratchPos<LAYOUT> sp,
+                                                              ScratchForce<LAYOUT> sf, LJTab tab,
+                                                              C08Table t1, C08Table t2, ColourLaunch cl,
+                                                              int o0, int o1, int o2,
+                                                              unsigned long long* counter) {
+    int nb = (o0 + 1) * (o1 + 1) * (o2 + 1);
+    int gw = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    int lane = threadIdx.x & 31;
+    unsigned cnt = 0;
+    int total = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
+    int unit = gw / nb, beta = gw % nb;
+    if (unit < total) {
+        int kz = unit % cl.cnt[2], u2 = unit / cl.cnt[2];
+        int ky = u2 % cl.cnt[1], kx = u2 / cl.cnt[1];
+        int bi = beta / ((o1 + 1) * (o2 + 1)), bj = (beta / (o2 + 1)) % (o1 + 1), bk = beta % (o2 + 1);
+        int cx = cl.p[0] + kx * cl.stride[0] + bi;
+        int cy = cl.p[1] + ky * cl.stride[1] + bj;
+        int cz = cl.p[2] + kz * cl.stride[2] + bk;
+        if (gv.in_grid(cx, cy, cz)) {
+            int c = gv.flat(cx, cy, cz);
+            int s1 = gv.start[c], e1 = gv.start[c + 1];
+            bool own = gv.owned(cx, cy, cz);
+            for (int i0 = s1; i0 < e1; i0 += 32) {
+                int i = i0 + lane;
+                bool act = i < e1;
+                double xi = 0.0, yi = 0.0, zi = 0.0;
+                int ti = 0;
+                if (act) sp.load(i, xi, yi, zi, ti);
+                double fx = 0.0, fy = 0.0, fz = 0.0;
+                // four partners per round (independent loads and one batched
+                // reciprocal, as in the Verlet walk), accumulated in order
+                auto run = [&](int a, int b, bool counted, bool intra) {
+                    for (int j0 = a; j0 < b; j0 += 4) {
+                        double dx[4], dy[4], dz[4], qq[4];
+                        int tj[4];
+                        bool ok[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            int j = min(j0 + u, b - 1);
+                            double xj, yj, zj;
+                            sp.load(j, xj, yj, zj, tj[u]);
+                            dx[u] = xi - xj;
+                            dy[u] = yi - yj;
+                            dz[u] = zi - zj;
+                            double r2 = dx[u] * dx[u] + dy[u] * dy[u] + dz[u] * dz[u];
+                            ok[u] = act && j0 + u < b && (!intra || j0 + u != i) && r2 < tab.rc2;
+                            qq[u] = ok[u] ? r2 : 1.0;
+                        }
+                        double p01 = qq[0] * qq[1], p23 = qq[2] * qq[3];
+                        double y = fast_rcp(p01 * p23);
+                        double y01 = y * p23, y23 = y * p01;
+                        double inv[4] = {y01 * qq[1], y01 * qq[0], y23 * qq[3], y23 * qq[2]};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (ok[u]) {
+                                double s2, e24;
+                                lj_params<MT>(tab, ti, tj[u], s2, e24);
+                                double aa = s2 * inv[u];
+                                double a6 = aa * aa * aa;
+                                double fs = (e24 * inv[u]) * (a6 * fma(2.0, a6, -1.0));
+                                fx += fs * dx[u];
+                                fy += fs * dy[u];
+                                fz += fs * dz[u];
+                                cnt += (N3L ? (counted && (!intra || j0 + u > i)) : 1) ? 1u : 0u;
+                            }
+                        }
+                    }
+                };
+                if (beta == 0 && own) run(s1, e1, true, true);
+                if (own)
+                    for (int e = t1.start[beta]; e < t1.start[beta + 1]; ++e) {
+                        int x2 = cx + t1.d[e][0], y2 = cy + t1.d[e][1], z2 = cz + t1.d[e][2];
+                        if (!gv.in_grid(x2, y2, z2)) continue;
+                        int c2 = gv.flat(x2, y2, z2);
+                        run(gv.start[c2], gv.start[c2 + 1], true, false);
+                    }
+                for (int e = t2.start[beta]; e < t2.start[beta + 1]; ++e) {
+                    int x1 = cx - t2.d[e][0], y1 = cy - t2.d[e][1], z1 = cz - t2.d[e][2];
+                    if (!gv.in_grid(x1, y1, z1) || !gv.owned(x1, y1, z1)) continue;
+                    int c1 = gv.flat(x1, y1, z1);
+                    run(gv.start[c1], gv.start[c1 + 1], false, false);
+                }
+                if (act) {
+                    *sf.at(i, 0) += fx;
+                    *sf.at(i, 1) += fy;
+                    *sf.at(i, 2) += fz;
+                }
+            }
+        }
+    }
+    warp_count(counter, cnt);
+}
+
 static int lc_env_rows() {
     static int v = -1;
     if (v < 0) {
@@ -541,9 +646,12 @@ static int lc_env_rows() {
     return v;
 }
 
-// C08 realisation: 1 per colour, row-slot threads for sparse cells and warp
-// tiles for dense ones (default); 0 warp tiles per colour always; 2 every
-// anchor in one launch (row slots)
+// C08 realisation: 1 (default) per colour -- warp per (anchor, block cell)
+// when a colour has fewer than 4 anchors per SM (small systems), else
+// row-slot threads for sparse cells and warp tiles for dense ones; 0 warp
+// tiles per colour always; 2 every anchor in one launch (row slots, fp64
+// atomics, not run-to-run deterministic); 3 warp per (anchor, block cell)
+// always
 static int lc_env_c08() {
     static int v = -1;
     if (v < 0) {
@@ -553,7 +661,9 @@ static int lc_env_c08() {
     return v;
 }
 
-static C08Table make_c08_table(const Geom& g, const Stencil& fwd) {
+// second = false: entries grouped by the block offset of their FIRST cell,
+// max(0, -d); true: by that of their SECOND cell, max(0, d)
+static C08Table make_c08_table(const Geom& g, const Stencil& fwd, bool second = false) {
     C08Table tb{};
     int nb = (g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1);
     int e = 0;
@@ -563,7 +673,9 @@ static C08Table make_c08_table(const Geom& g, const Stencil& fwd) {
         tb.start[b] = e;
         for (int k = 0; k < fwd.n; ++k) {
             const int* d = fwd.d[k];
-            if ((d[0] < 0 ? -d[0] : 0) == bi && (d[1] < 0 ? -d[1] : 0) == bj && (d[2] < 0 ? -d[2] : 0) == bk) {
+            int o[3];
+            for (int a = 0; a < 3; ++a) o[a] = second ? (d[a] > 0 ? d[a] : 0) : (d[a] < 0 ? -d[a] : 0);
+            if (o[0] == bi && o[1] == bj && o[2] == bk) {
                 for (int a = 0; a < 3; ++a) tb.d[e][a] = (signed char)d[a];
                 ++e;
             }
@@ -663,6 +775,12 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
     // C08: anchors over the whole padded grid, stride overlap+1 per axis
     // dense cells (CSF 1): warp tiles; sparse cells: row-slot threads
     bool c08_cells = lc_env_c08() == 1 && rows_per_cell < 8.0;
+    // too few anchors per colour to fill the GPU with anchor warps (small
+    // systems): warp per (anchor, block cell), deterministic
+    int64_t anchors_per_colour = (int64_t)g.D[0] * g.D[1] * g.D[2] /
+                                 ((g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1));
+    bool c08_cellwarp = lc_env_c08() == 3 || (lc_env_c08() == 1 && anchors_per_colour < 4 * c.sm_count);
+    C08Table c08t2 = make_c08_table(g, gr.fwd, true);
     C08Table c08tb = make_c08_table(g, gr.fwd);
     int strides[3] = {g.overlap[0] + 1, g.overlap[1] + 1, g.overlap[2] + 1};
     for (int px = 0; px < strides[0]; ++px)
@@ -680,7 +798,14 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
                 }
                 if (empty) continue;
                 int warps = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
-                if (c08_cells) {
+                if (c08_cellwarp) {
+                    int nb = (g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1);
+                    int64_t threads = (int64_t)warps * nb * 32;
+                    if (newton3)
+                        lc_c08_cellwarp_kernel<LAYOUT, MT, true><<<blocks_for(threads, 128), 128, 0, s>>>(gv, sp, sf, c.tab, c08tb, c08t2, cl, g.overlap[0], g.overlap[1], g.overlap[2], counter), note_launch();
+                    else
+                        lc_c08_cellwarp_kernel<LAYOUT, MT, false><<<blocks_for(threads, 128), 128, 0, s>>>(gv, sp, sf, c.tab, c08tb, c08t2, cl, g.overlap[0], g.overlap[1], g.overlap[2], counter), note_launch();
+                } else if (c08_cells) {
                     int nb = (g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1);
                     int S = slot_width(rows_per_cell);
                     int64_t threads = (int64_t)warps * nb * S;

@@ -382,8 +382,6 @@ class DeviceDecomposedSimulation:
         per = params.periodic_flags()
         if not all(bool(x) for x in per):
             raise ValueError("the device decomposition needs periodic boundaries on every axis")
-        if getattr(params, "thermostat", None) is not None:
-            raise ValueError("thermostatted runs: use DecomposedSimulation")
         self.dec, self.params, self.config = dec, params, config
         self.comm_device = comm_device
         self.local_params = dec.local_params()
@@ -540,7 +538,12 @@ class DeviceDecomposedSimulation:
             self._ghosts()
         calc.refresh(self.ps, cfg)
         calc.compute_async(self.ps, cfg)
-        self._kick_due = True
+        thermo = getattr(p, "thermostat", None)
+        if thermo is not None and (self.iteration + 1) % thermo.interval_iterations == 0:
+            calc.finish_kick(self.ps, p.delta_t, p.gravity)   # the thermostat needs the kicked state
+            self._thermostat(thermo.target_temperature, thermo.max_delta_t)
+        else:
+            self._kick_due = True
         self.since = 0 if rebuild else self.since + 1
         self.iteration += 1
 
@@ -548,6 +551,31 @@ class DeviceDecomposedSimulation:
         for _ in range(steps):
             self.step()
         self.flush()
+
+    def _thermostat(self, target, max_delta_t):
+        """apply_thermostat (integrator.py:81-95) over the owned rows of every
+        rank: the kinetic energy and the particle count are all-reduced."""
+        n = self.n_owned
+        v = self.ps.view("vel")[:n]
+        mass = torch.as_tensor(np.asarray(self.template.mass, dtype=np.float64), device=self.dev)
+        m = mass[self.ps.type_id[:n].long()]
+        red = torch.stack([torch.sum(m * torch.sum(v * v, dim=1)),
+                           torch.tensor(float(n), dtype=torch.float64, device=self.dev)])
+        if self.dec.world > 1:
+            buf = red.to(self.comm_device) if self.comm_device is not None else red
+            dist.all_reduce(buf)
+            red = buf.to(self.dev)
+        ke, cnt = float(red[0]), float(red[1])
+        if cnt == 0:
+            raise ValueError("temperature of an empty particle set is undefined")
+        t_cur = ke / (3.0 * cnt)
+        if t_cur == 0.0:
+            if target > 0.0:
+                raise ValueError("thermostat cannot scale zero velocities toward a positive "
+                                 "target temperature")
+            return
+        delta = min(max(target - t_cur, -max_delta_t), max_delta_t)
+        v.mul_(float(np.sqrt((t_cur + delta) / t_cur)))
 
     def flush(self):
         """Run the deferred kick of the last step (state complete again)."""

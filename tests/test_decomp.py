@@ -198,3 +198,37 @@ def test_grid_with_thermostat_matches_reference_loop(tmp_path):
     assert np.abs(d).max() <= 1e-9
     assert np.abs(many[:, 4:7] - np.asarray(p.velocities)).max() <= 1e-9
 
+
+
+@pytest.mark.gpu
+def test_device_decomposition_with_thermostat_matches_reference_loop(tmp_path):
+    """DeviceDecomposedSimulation on a 2x2x2 grid with the thermostat (kinetic
+    energy and counts all-reduced over the owned rows; the thermostat's steps
+    kick eagerly) against the reference loop with the same thermostat."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from decomp_worker import system, thermostat
+    from oracle import port
+    many = _run(8, 18, tmp_path, vscale=2.0, dt=3e-3, tag="devth", backend="gpudev", dims=(2, 2, 2),
+                size="cube10", thermo=True)
+    pos, vel, L = system(vscale=2.0, size="cube10")
+    params = port.Params(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=4, delta_t=3e-3,
+                         boundary=(port.PERIODIC,) * 3, thermostat=thermostat())
+
+    class Fixed:
+        mode = "steady"
+
+        def configuration_for_iteration(self, it):
+            return port.parse("VL-List_Iter-NoN3L-AoS"), False
+
+        def record_timings(self, f, b):
+            pass
+
+        def record_failure(self, e=None):
+            return False
+
+    p = port.Particles(pos, vel)
+    port.simulate_controlled(p, params, Fixed(), steps=18)
+    d = many[:, 1:4] - np.asarray(p.positions)
+    d -= L * np.rint(d / L)
+    assert np.abs(d).max() <= 1e-9
+    assert np.abs(many[:, 4:7] - np.asarray(p.velocities)).max() <= 1e-9

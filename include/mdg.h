@@ -193,6 +193,21 @@ int mdg_get_grid(mdg_ctx* ctx, double csf, int64_t* m, int64_t* ncells, int32_t*
  * (n+1, int64) and nbr (entries, int32).  NULL outputs = size query. */
 int mdg_get_verlet(mdg_ctx* ctx, int64_t* entries, int64_t* noff, int32_t* nbr);
 
+/* The pairs every LC traversal evaluates within rc on the CSF-`csf` grid of
+ * the last LC rebuild (r^2 < rc^2 on pos[src] + shift, kernels.py:36-40), as
+ * owner pairs (src_i, src_j), src_i < src_j, in no particular order (the
+ * caller sorts): the "LC pair set" of SURVEY §8(c)(ii).  *count = number of
+ * pairs; at most `cap` are written to pairs (2 x int32 each); pairs may be
+ * NULL (size query). */
+int mdg_lc_pairs(mdg_ctx* ctx, double csf, int64_t cap, int32_t* pairs, int64_t* count);
+
+/* Device timings of the reference's timing hooks (simulation.py:155-181):
+ * build = mdg_rebuild (when called) + mdg_refresh, force = mdg_compute,
+ * measured with CUDA events on the context stream.  enable >= 0 switches the
+ * events on (1) or off (0) and returns; enable < 0 reads the last completed
+ * intervals in ns (-1 = not measured), waiting for them. */
+int mdg_timings(mdg_ctx* ctx, int enable, int64_t* build_ns, int64_t* force_ns);
+
 /* Context-free host versions of the two exports above (no device needed). */
 int mdg_geometry_for(const double domain[3], const int periodic[3], double interaction_length,
                      double csf, int dims_owned[3], double cell_length[3], int overlap[3],

@@ -28,7 +28,7 @@ EXPORTS = (
     "mdg_get_verlet", "mdg_geometry_for", "mdg_stencil_for", "mdg_host_drift_wrap",
     "mdg_host_finish_kick", "mdg_measure_fp64_peak", "mdg_temperature", "mdg_thermostat",
     "mdg_live_stats", "mdg_compute_kick", "mdg_step_graph", "mdg_host_step", "mdg_host_step_ex",
-    "mdg_host_run", "mdg_host_kick_drift_range", "mdg_kick_drift",
+    "mdg_host_run", "mdg_host_kick_drift_range", "mdg_kick_drift", "mdg_lc_pairs", "mdg_timings",
     "mdg_host_drift_wrap_range_ex", "mdg_d2h_async", "mdg_host_drift_wrap_range", "mdg_host_finish_kick_range",
 )
 FLAG_BLOWUP, FLAG_THERMO_ZERO = 1, 2
@@ -91,6 +91,8 @@ def _declare(L):
         "mdg_host_step": (I, [P, CFG, P, P, P, P, P, P, D, I, D, I, I, ctypes.POINTER(I)]),
         "mdg_host_step_ex": (I, [P, CFG, P, P, P, P, P, P, D, I, D, I, I, I, ctypes.POINTER(I)]),
         "mdg_kick_drift": (I, [P, D, I, D, I]),
+        "mdg_lc_pairs": (I, [P, D, I64, P, ctypes.POINTER(I64)]),
+        "mdg_timings": (I, [P, I, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
         "mdg_host_run": (I, [P, CFG, P, P, P, P, P, P, D, I, D, I, I, I, I, I, ctypes.POINTER(I),
                              ctypes.POINTER(I)]),
         "mdg_host_kick_drift_range": (I, [I64, I64, I64, I, P, P, P, P, P, P, P, P, D, I, D,

@@ -170,6 +170,25 @@ class ForceCalculator:
         check(lib().mdg_kick_drift(self.ctx.h, float(dt), int(gravity is not None),
                                    float(gravity or 0.0), int(bool(copy_old_force))), "kick_drift")
 
+    def lc_pairs(self, csf):
+        """The LC pair set (mdg_lc_pairs) of the last LC rebuild at `csf`: the
+        (k, 2) sorted unique owner pairs (i < j) with r^2 < rc^2."""
+        n = ctypes.c_int64()
+        check(lib().mdg_lc_pairs(self.ctx.h, float(csf), 0, None, ctypes.byref(n)), "lc_pairs")
+        out = np.zeros((max(n.value, 1), 2), dtype=np.int32)
+        check(lib().mdg_lc_pairs(self.ctx.h, float(csf), n.value, out.ctypes.data, ctypes.byref(n)),
+              "lc_pairs")
+        out = out[:n.value].astype(np.int64)
+        return np.unique(out, axis=0) if len(out) else out
+
+    def timings(self, enable=None):
+        """mdg_timings: enable/disable the build/force events, or read the
+        last (build_ns, force_ns) (-1 = not measured)."""
+        b, f = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().mdg_timings(self.ctx.h, -1 if enable is None else int(bool(enable)),
+                                ctypes.byref(b), ctypes.byref(f)), "timings")
+        return None if enable is not None else (b.value, f.value)
+
     def sd_step(self, particles, gamma, max_disp):
         self.bind(particles)
         check(lib().mdg_sd_step(self.ctx.h, float(gamma), float(max_disp)), "sd_step")

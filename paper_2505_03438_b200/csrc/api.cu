@@ -172,6 +172,8 @@ int mdg_destroy(mdg_ctx* ctx) {
     if (ctx->c.graph_out) cudaEventDestroy(ctx->c.graph_out);
     if (ctx->c.graph_stream) cudaStreamDestroy(ctx->c.graph_stream);
     if (ctx->c.h2d_done) cudaEventDestroy(ctx->c.h2d_done);
+    for (cudaEvent_t e : ctx->c.tev)
+        if (e) cudaEventDestroy(e);
     if (ctx->c.copy_stream) cudaStreamDestroy(ctx->c.copy_stream);
     delete ctx;
     return MDG_OK;
@@ -274,11 +276,44 @@ int mdg_bind(mdg_ctx* ctx, int64_t n, int layout, double* pos, double* vel, doub
     return MDG_OK;
 }
 
+// mdg_timings' events (skipped while a stream is being captured into a graph)
+static void tmark(Context& c, int k) {
+    if (!c.timing) return;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(c.stream, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) return;
+    if (!c.tev[k] && cudaEventCreate(&c.tev[k]) != cudaSuccess) return;
+    cudaEventRecord(c.tev[k], c.stream);
+    if (k == 0) c.build_open = true;
+    if (k == 1) { c.build_open = false; c.build_done = true; }
+    if (k == 3) c.force_done = true;
+}
+
+int mdg_timings(mdg_ctx* ctx, int enable, int64_t* build_ns, int64_t* force_ns) {
+    CHECK_CTX(ctx);
+    Context& c = ctx->c;
+    if (build_ns) *build_ns = -1;
+    if (force_ns) *force_ns = -1;
+    if (enable >= 0) {
+        c.timing = enable != 0;
+        c.build_open = c.build_done = c.force_done = false;
+        return MDG_OK;
+    }
+    float ms = 0.f;
+    if (c.build_done && build_ns && cudaEventSynchronize(c.tev[1]) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, c.tev[0], c.tev[1]) == cudaSuccess)
+        *build_ns = (int64_t)((double)ms * 1e6);
+    if (c.force_done && force_ns && cudaEventSynchronize(c.tev[3]) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, c.tev[2], c.tev[3]) == cudaSuccess)
+        *force_ns = (int64_t)((double)ms * 1e6);
+    return cuda_status("mdg_timings");
+}
+
 int mdg_rebuild(mdg_ctx* ctx, const mdg_config* cfg) {
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;
     if (int e = need_system(ctx)) return e;
     Context& c = ctx->c;
+    tmark(c, 0);
     ++c.gen;
     if (cfg->container == MDG_VL) {
         if (vl_rebuild(c)) return MDG_ECUDA;
@@ -296,11 +331,16 @@ int mdg_refresh(mdg_ctx* ctx, const mdg_config* cfg) {
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;
     Context& c = ctx->c;
-    if (cfg->container == MDG_VL || cfg->container == MDG_VCL) return MDG_OK;
+    if (!c.build_open) tmark(c, 0);
+    if (cfg->container == MDG_VL || cfg->container == MDG_VCL) {
+        tmark(c, 1);
+        return MDG_OK;
+    }
     Grid& gr = *grid_for(c, cfg->csf);
     if (!gr.built) { set_error("refresh before rebuild"); return MDG_ESTATE; }
     if (gr.scratch_layout != cfg->layout) grid_bind_scratch(c, gr, cfg->layout);
     grid_refresh(c, gr, cfg->layout);
+    tmark(c, 1);
     return cuda_status("mdg_refresh");
 }
 
@@ -313,9 +353,13 @@ int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg) {
                   " does not match the configuration");
         return MDG_EINVAL;
     }
+    tmark(c, 2);
     if (cudaMemsetAsync(c.scal.p, 0, sizeof(unsigned long long), c.stream) != cudaSuccess)
         return cuda_status("counter reset");
-    if (c.n == 0) return MDG_OK;
+    if (c.n == 0) {
+        tmark(c, 3);
+        return MDG_OK;
+    }
     if (cfg->container == MDG_VCL) {
         if (!c.vcl.built) { set_error("compute before rebuild"); return MDG_ESTATE; }
         vcl_compute(c, cfg->newton3);
@@ -332,7 +376,30 @@ int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg) {
         lc_compute(c, gr, cfg->traversal, cfg->newton3, cfg->layout);
         lc_fold_forces(c, gr, cfg->layout, cfg->traversal != MDG_C01);
     }
+    tmark(c, 3);
     return cuda_status("mdg_compute");
+}
+
+int mdg_lc_pairs(mdg_ctx* ctx, double csf, int64_t cap, int32_t* pairs, int64_t* count) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    if (csf != 1.0 && csf != 0.5) { set_error("csf must be 1 or 0.5"); return MDG_EINVAL; }
+    if (!count) { set_error("null count"); return MDG_EINVAL; }
+    Context& c = ctx->c;
+    Grid& gr = *grid_for(c, csf);
+    if (!gr.built) { set_error("LC grid not built (mdg_rebuild with an LC configuration first)"); return MDG_ESTATE; }
+    DBuf<int2> buf;
+    if (pairs && cap > 0) {
+        buf.ensure((size_t)cap);
+        if (!buf.p) { set_error("out of device memory (pair export)"); return MDG_ECUDA; }
+    }
+    long long n = 0;
+    if (lc_pairs(c, gr, pairs ? cap : 0, buf.p, &n)) return cuda_status("mdg_lc_pairs");
+    *count = n;
+    if (pairs && cap > 0 && n > 0)
+        cudaMemcpy(pairs, buf.p, (size_t)std::min<long long>(n, cap) * sizeof(int2), cudaMemcpyDeviceToHost);
+    buf.release();
+    return cuda_status("mdg_lc_pairs");
 }
 
 int mdg_compute_kick(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gravity,

@@ -108,6 +108,7 @@ template struct DBuf<long long>;
 template struct DBuf<unsigned long long>;
 template struct DBuf<uint16_t>;
 template struct DBuf<int4>;
+template struct DBuf<int2>;
 template struct DBuf<float4>;
 template struct DBuf<PwLeaf>;
 

@@ -820,6 +820,59 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
             }
 }
 
+// ---------------------------------------------------------------- pair export
+//
+// The set of pairs every LC traversal evaluates within rc on this grid (the
+// reference's r^2 < rc^2 on pos[src] + shift, kernels.py:36-40), as owner
+// pairs (src_i, src_j) with src_i < src_j: a thread per owned row walks its own
+// cell and the full pruned stencil (each unordered owner pair is met from at
+// least one side).  Parity export only.
+__global__ void lc_pairs_kernel(GridView gv, const double4* __restrict__ spos, const int* __restrict__ src,
+                                Stencil st, double rc2, unsigned long long* counter, int2* out,
+                                long long cap) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= gv.m) return;
+    int cell = gv.row_cell[r], cx, cy, cz;
+    gv.decode(cell, cx, cy, cz);
+    if (!gv.owned(cx, cy, cz)) return;
+    double4 pi = spos[r];
+    int si = src[r];
+    auto visit = [&](int j) {
+        if (j == r) return;
+        int sj = src[j];
+        if (sj <= si) return;
+        double4 pj = spos[j];
+        double dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
+        if (dx * dx + dy * dy + dz * dz < rc2) {
+            unsigned long long k = atomicAdd(counter, 1ull);
+            if (out && (long long)k < cap) out[k] = make_int2(si, sj);
+        }
+    };
+    for (int j = gv.start[cell]; j < gv.start[cell + 1]; ++j) visit(j);
+    for (int k = 0; k < st.n; ++k) {
+        int x2 = cx + st.d[k][0], y2 = cy + st.d[k][1], z2 = cz + st.d[k][2];
+        if (!gv.in_grid(x2, y2, z2)) continue;
+        int c2 = gv.flat(x2, y2, z2);
+        for (int j = gv.start[c2]; j < gv.start[c2 + 1]; ++j) visit(j);
+    }
+}
+
+int lc_pairs(Context& c, Grid& gr, long long cap, int2* dev_out, long long* count) {
+    grid_bind_scratch(c, gr, AOS);
+    grid_refresh(c, gr, AOS);
+    unsigned long long* counter = c.scal.p + 4;
+    if (cudaMemsetAsync(counter, 0, sizeof(unsigned long long), c.stream) != cudaSuccess) return -1;
+    if (gr.m > 0)
+        lc_pairs_kernel<<<blocks_for(gr.m, 128), 128, 0, c.stream>>>(make_view(gr), gr.spos4.p, gr.row_src.p,
+                                                                     gr.pruned, c.tab.rc2, counter, dev_out, cap), note_launch();
+    unsigned long long h = 0;
+    if (cudaMemcpyAsync(&h, counter, sizeof(h), cudaMemcpyDeviceToHost, c.stream) != cudaSuccess ||
+        cudaStreamSynchronize(c.stream) != cudaSuccess)
+        return -1;
+    *count = (long long)h;
+    return 0;
+}
+
 void lc_compute(Context& c, Grid& gr, int traversal, int newton3, int layout) {
     if (gr.m == 0) return;
     if (traversal != T_C01)

@@ -185,6 +185,9 @@ struct Context {
     bool prof = false;
     std::vector<cudaEvent_t> chunk_ev;   // mdg_host_step's per-chunk copy events
     cudaStream_t copy_stream = nullptr;  // mdg_host_run's H2D stream (overlaps the D2H)
+    // mdg_timings: events around build (rebuild + refresh) and force (compute)
+    bool timing = false, build_open = false, build_done = false, force_done = false;
+    cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t h2d_done = nullptr;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -203,6 +206,7 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout);
 void grid_bind_scratch(Context& c, Grid& gr, int layout);
 void grid_refresh(Context& c, Grid& gr, int layout);
 void lc_compute(Context& c, Grid& gr, int traversal, int newton3, int layout);
+int lc_pairs(Context& c, Grid& gr, long long cap, int2* dev_out, long long* count);
 void lc_fold_forces(Context& c, Grid& gr, int layout, bool images_written);
 int vl_rebuild(Context& c);
 void vl_compute(Context& c, int layout);

@@ -87,6 +87,55 @@ def test_verlet_pair_sets_bit_exact(pkg, name):
         fc.close()
 
 
+@pytest.mark.parametrize("name", system_names())
+def test_lc_pair_sets_bit_exact(pkg, name):
+    """the pairs the LC traversals evaluate within rc
+    (mdg_lc_pairs, owner pairs on pos[src] + shift) equal the reference's
+    Verlet pairs filtered to minimum-image r^2 < rc^2 -- as sorted pair lists,
+    at both cell-size factors."""
+    P, calc = pkg
+    d = golden(f"sys_{name}.npz")
+    pos, L = d["pos"], np.asarray(d["domain"], dtype=np.float64)
+    per = np.asarray(d["periodic"], dtype=bool)
+    rc2 = float(d["cutoff"]) ** 2
+    noff, nbr = d["vl_noff"], d["vl_nbr"]
+    i = np.repeat(np.arange(len(noff) - 1), np.diff(noff))
+    j = nbr.astype(np.int64)
+    keep = i < j
+    i, j = i[keep], j[keep]
+    dd = pos[i] - pos[j]
+    dd[:, per] -= L[per] * np.rint(dd[:, per] / L[per])   # kernels.py:739-757
+    r2 = dd[:, 0] * dd[:, 0] + dd[:, 1] * dd[:, 1] + dd[:, 2] * dd[:, 2]
+    ref = np.unique(np.stack([i[r2 < rc2], j[r2 < rc2]], 1), axis=0)
+    for csf in (1.0, 0.5):
+        parts, params = _system(P, d)
+        fc = calc.ForceCalculator(parts, params)
+        fc.rebuild(parts, P.Configuration("LC", "C01", False, "AoS", csf))
+        got = fc.lc_pairs(csf)
+        fc.close()
+        assert np.array_equal(got, ref), (name, csf, len(got), len(ref))
+
+
+def test_device_timings_export(pkg):
+    """mdg_timings: device-event build (rebuild + refresh) and force (compute)
+    intervals, the reference's timing hooks (simulation.py:155-181)."""
+    P, calc = pkg
+    d = golden("sys_blob.npz")
+    parts, params = _system(P, d)
+    fc = calc.ForceCalculator(parts, params)
+    cfg = P.parse_configuration("LC-C08-N3L-AoS-CSF1")
+    assert fc.timings() == (-1, -1)
+    fc.timings(True)
+    fc.rebuild(parts, cfg)
+    fc.refresh(parts, cfg)
+    fc.compute(parts, cfg)
+    b, f = fc.timings()
+    assert b > 0 and f > 0
+    fc.timings(False)
+    assert fc.timings() == (-1, -1)
+    fc.close()
+
+
 @pytest.mark.parametrize("traj", ["traj_small", "traj_faces", "traj_config1"])
 def test_trajectories_match_reference(pkg, traj):
     P, calc = pkg

@@ -773,6 +773,13 @@ int mdg_host_run(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, 
     auto us = [](auto x, auto y) { return std::chrono::duration<double, std::micro>(y - x).count(); };
     double t_enq = 0, t_wait = 0, t_host = 0, t_first = 0;
     auto T0 = now();
+    // error exits drain both streams first: no copy may still be reading or
+    // writing the caller's host arrays when the call returns
+    auto drained = [&](int code) {
+        cudaStreamSynchronize(c.copy_stream);
+        cudaStreamSynchronize(c.stream);
+        return code;
+    };
     // the caller's buffers arrive swapped (MDG_HOST_STEP_SWAPPED): old_force
     // holds the current forces, force is free; the roles alternate per step
     double* cur = old_force;
@@ -785,7 +792,7 @@ int mdg_host_run(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, 
         mdg_host_drift_wrap_range_ex(n, a, b, c.layout, pos, vel, nullptr, cur, type_id, mass, c.L,
                                      periodic, dt, 1, &bk);
         bad |= bk;
-        if (copy(c.pos, pos, a, b, cudaMemcpyHostToDevice, c.copy_stream) != cudaSuccess) return cuda_status("h2d");
+        if (copy(c.pos, pos, a, b, cudaMemcpyHostToDevice, c.copy_stream) != cudaSuccess) return drained(cuda_status("h2d"));
     }
     cudaEventRecord(c.h2d_done, c.copy_stream);
     if (bad) {
@@ -797,14 +804,14 @@ int mdg_host_run(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, 
         bool last = s == steps - 1;
         bool rebuild = (s == 0 && rebuild_first) || since >= rebuild_interval;
         auto ta = now();
-        if (cudaStreamWaitEvent(c.stream, c.h2d_done, 0) != cudaSuccess) return cuda_status("wait h2d");
+        if (cudaStreamWaitEvent(c.stream, c.h2d_done, 0) != cudaSuccess) return drained(cuda_status("wait h2d"));
         if (rebuild)
-            if (int e = mdg_rebuild(ctx, cfg)) return e;
-        if (int e = mdg_refresh(ctx, cfg)) return e;
-        if (int e = mdg_compute(ctx, cfg)) return e;
+            if (int e = mdg_rebuild(ctx, cfg)) return drained(e);
+        if (int e = mdg_refresh(ctx, cfg)) return drained(e);
+        if (int e = mdg_compute(ctx, cfg)) return drained(e);
         for (int k = 0; k < K; ++k) {
             int64_t a = n * k / K, b = n * (k + 1) / K;
-            if (copy(oth, c.force, a, b, cudaMemcpyDeviceToHost, c.stream) != cudaSuccess) return cuda_status("d2h");
+            if (copy(oth, c.force, a, b, cudaMemcpyDeviceToHost, c.stream) != cudaSuccess) return drained(cuda_status("d2h"));
             cudaEventRecord(c.chunk_ev[k], c.stream);
         }
         auto tb = now();
@@ -814,7 +821,7 @@ int mdg_host_run(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, 
         for (int k = 0; k < K; ++k) {
             int64_t a = n * k / K, b = n * (k + 1) / K;
             auto w0 = now();
-            if (cudaEventSynchronize(c.chunk_ev[k]) != cudaSuccess) return cuda_status("d2h wait");
+            if (cudaEventSynchronize(c.chunk_ev[k]) != cudaSuccess) return drained(cuda_status("d2h wait"));
             auto w1 = now();
             t_wait += us(w0, w1);
             if (k == 0) t_first += us(w0, w1);
@@ -831,7 +838,7 @@ int mdg_host_run(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, 
             mdg_host_kick_drift_range(n, a, b, c.layout, pos, vel, oth, cur, type_id, mass, c.L,
                                       periodic, dt, has_gravity, gravity, &bk);
             bad |= bk;
-            if (copy(c.pos, pos, a, b, cudaMemcpyHostToDevice, c.copy_stream) != cudaSuccess) return cuda_status("h2d");
+            if (copy(c.pos, pos, a, b, cudaMemcpyHostToDevice, c.copy_stream) != cudaSuccess) return drained(cuda_status("h2d"));
         }
         if (!last) cudaEventRecord(c.h2d_done, c.copy_stream);
         since = rebuild ? 0 : since + 1;

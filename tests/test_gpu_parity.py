@@ -817,3 +817,38 @@ def test_config5_tiled_lists_past_32_bit_entries(pkg):
     num = torch.linalg.vector_norm(parts.view("force") - f_vl)
     den = torch.linalg.vector_norm(f_vl)
     assert float(num / den) <= FP64_TOL
+
+
+def test_stale_verlet_lists_between_rebuilds(pkg):
+    """The reference's stale-list semantics (tests/test_containers.py:145-161,
+    containers.py:435-436): a pair that enters the cutoff without a rebuild is
+    missed by VL (its list is from the last rebuild) and seen by LC (refresh
+    re-gathers positions); both as the oracle's ForceCalculator does."""
+    P, calc = pkg
+    params = P.SimulationParams(domain_size=(12.0, 12.0, 12.0), cutoff=2.5, skin=0.3,
+                                boundary=(P.REFLECTIVE,) * 3)
+    pp = port.Params(domain_size=(12.0, 12.0, 12.0), cutoff=2.5, skin=0.3,
+                     boundary=(port.REFLECTIVE,) * 3)
+    start = np.array([[4.0, 6.0, 6.0], [7.0, 6.0, 6.0]])       # 3.0 apart: beyond ell = 2.8
+    moved = np.array([[4.0, 6.0, 6.0], [6.0, 6.0, 6.0]])       # 2.0 apart: inside rc
+    for cid in ("VL-List_Iter-NoN3L-AoS", "LC-C08-N3L-AoS-CSF1", "LC-C01-NoN3L-SoA-CSF1"):
+        cfg = P.parse_configuration(cid)
+        parts = P.ParticleSet(start, layout=cfg.layout)
+        fc = calc.ForceCalculator(parts, params)
+        fc.rebuild(parts, cfg)
+        parts.view("pos").copy_(torch.as_tensor(moved))
+        fc.refresh(parts, cfg)
+        n = fc.compute(parts, cfg)
+        fc.close()
+        ref = port.Particles(start, layout=cfg.layout)
+        rfc = port.ForceCalculator(ref, pp)
+        rfc.rebuild(ref, port.parse(cid))
+        ref.view("pos")[:] = moved
+        rfc.refresh(ref, port.parse(cid))
+        rn = rfc.compute(ref, port.parse(cid))
+        assert n == rn, (cid, n, rn)
+        assert np.allclose(parts.numpy("force"), np.asarray(ref.forces), atol=1e-12), cid
+        if cid.startswith("VL"):
+            assert n == 0 and np.all(parts.numpy("force") == 0.0)
+        else:
+            assert n > 0

@@ -265,13 +265,6 @@ unsigned long long launch_count();
 // component stride of the unwrapped SoA copy (Verlet::s3): a multiple of 4
 // rows, so every component array is 32-byte aligned (1-D bulk copies)
 inline int s3_stride(int m) { return (m + 3) & ~3; }
-// The VL / VCL unwrapped sorted positions s3 (3 ms doubles): {x, y} of row r
-// interleaved at [2r, 2r+1] (16 B per row), then z at 2 ms + r.  The tiled walk
-// gathers a row with one 16-B and one 8-B shared-memory load (random gathers:
-// 1.91 rows/clk/SM against 1.72 for three 8-B loads, tools/microbench_smem.cu).
-__host__ __device__ inline size_t s3x(size_t r) { return 2 * r; }
-__host__ __device__ inline size_t s3y(size_t r) { return 2 * r + 1; }
-__host__ __device__ inline size_t s3z(size_t r, int ms) { return 2 * (size_t)ms + r; }
 
 inline int blocks_for(int64_t n, int threads) {
     int64_t b = (n + threads - 1) / threads;

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256) vcl_force_kernel(
         int ri = ci * kCl + ii;
         bool vi = ri < m && row_code[ri] == kNoShift;
         int rr = vi ? ri : 0;
-        double xi = s3[s3x(rr)], yi = s3[s3y(rr)], zi = s3[s3z(rr, ms)];
+        double xi = s3[rr], yi = s3[(size_t)ms + rr], zi = s3[2 * (size_t)ms + rr];
         int ti = MT ? row_tid[rr] : 0;
         int si = vi ? row_src[ri] : -1;
         double fx = 0.0, fy = 0.0, fz = 0.0;
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(256) vcl_force_kernel(
                 int rj = cj * kCl + jh + 4 * t;
                 bool vj = rj < m;
                 int rjj = vj ? rj : 0;
-                double dx = xi - s3[s3x(rjj)], dy = yi - s3[s3y(rjj)], dz = zi - s3[s3z(rjj, ms)];
+                double dx = xi - s3[rjj], dy = yi - s3[(size_t)ms + rjj], dz = zi - s3[2 * (size_t)ms + rjj];
                 double r2 = dx * dx + dy * dy + dz * dz;
                 bool ok = vi && vj && rj != ri && r2 < tab.rc2;
                 int sj = 0;

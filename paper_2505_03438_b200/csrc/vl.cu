@@ -249,7 +249,7 @@ __global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int
     if (SLAYOUT == AOS || from_s4) {
         prev[0] = old.x; prev[1] = old.y; prev[2] = old.z;
     } else {
-        prev[0] = s3[s3x(r)]; prev[1] = s3[s3y(r)]; prev[2] = s3[s3z(r, ms)];
+        prev[0] = s3[r]; prev[1] = s3[(size_t)ms + r]; prev[2] = s3[2 * (size_t)ms + r];
     }
     for (int k = 0; k < 3; ++k) {
         double x = q[k] + (double)sh[k] * w.L[k];
@@ -259,8 +259,9 @@ __global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int
     if (SLAYOUT == AOS) {
         s4[r] = make_double4(q[0], q[1], q[2], old.w);
     } else {
-        reinterpret_cast<double2*>(s3)[r] = make_double2(q[0], q[1]);
-        s3[s3z(r, ms)] = q[2];
+        s3[r] = q[0];
+        s3[(size_t)ms + r] = q[1];
+        s3[2 * (size_t)ms + r] = q[2];
     }
 }
 
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(NT, MINB) vl_force_kernel(int m, int ms, int64
             xi = p.x; yi = p.y; zi = p.z;
             if (MT) ti = (int)p.w;
         } else {
-            xi = s3[s3x(r)]; yi = s3[s3y(r)]; zi = s3[s3z(r, ms)];
+            xi = s3[r]; yi = s3[(size_t)ms + r]; zi = s3[2 * (size_t)ms + r];
             if (MT) ti = row_tid[r];
         }
         double fx = 0.0, fy = 0.0, fz = 0.0;
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(NT, MINB) vl_force_kernel(int m, int ms, int64
                     xj = p.x; yj = p.y; zj = p.z;
                     if (MT) tj[u] = (int)p.w;
                 } else {
-                    xj = s3[s3x(j)]; yj = s3[s3y(j)]; zj = s3[s3z(j, ms)];
+                    xj = s3[j]; yj = s3[(size_t)ms + j]; zj = s3[2 * (size_t)ms + j];
                     if (MT) tj[u] = row_tid[j];
                 }
                 dx[u] = xi - xj; dy[u] = yi - yj; dz[u] = zi - zj;

@@ -454,8 +454,9 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                 }
                 continue;
             }
-            double* wxy = win + b * kBuf;        // {x, y} per row (16 B), then z
-            double* wz = wxy + 2 * wrows;
+            double* wx = win + b * kBuf;
+            double* wy = wx + wrows;
+            double* wz = wy + wrows;
             int* wt = reinterpret_cast<int*>(wz + wrows);
             if (lane == 0) {
                 tile_of[b] = t;
@@ -466,8 +467,9 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
             if (lane < kRanges) {
                 int R = lane, o = D.woff[R], rows = D.woff[R + 1] - o, g = D.wstart[R];
                 if (rows > 0) {
-                    bulk_g2s(wxy + 2 * o, s3 + s3x(g), rows * 16u, &full[b]);
-                    bulk_g2s(wz + o, s3 + s3z(g, ms), rows * 8u, &full[b]);
+                    bulk_g2s(wx + o, s3 + g, rows * 8u, &full[b]);
+                    bulk_g2s(wy + o, s3 + (size_t)ms + g, rows * 8u, &full[b]);
+                    bulk_g2s(wz + o, s3 + 2 * (size_t)ms + g, rows * 8u, &full[b]);
                     if (MT) bulk_g2s(wt + o, row_tid + g, rows * 4u, &full[b]);
                 }
             } else if (PF == 3) {
@@ -497,8 +499,9 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
         if (t < 0) break;
         const TileDesc& D = d[b];
         if (!D.big) {
-            const double2* wxy = reinterpret_cast<const double2*>(win + b * kBuf);
-            const double* wz = win + b * kBuf + 2 * wrows;
+            const double* wx = win + b * kBuf;
+            const double* wy = wx + wrows;
+            const double* wz = wy + wrows;
             const int* wt = reinterpret_cast<const int*>(wz + wrows);
             int slot0 = tbase[t];
             size_t base = (size_t)slot0 * cap4;
@@ -512,8 +515,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                 if (q < ni) {
                     int li;
                     int r = tile_row(D, q, li);
-                    double2 pi = wxy[li];
-                    double xi = pi.x, yi = pi.y, zi = wz[li];
+                    double xi = wx[li], yi = wy[li], zi = wz[li];
                     int ti = MT ? wt[li] : 0;
                     // the count, the first two entry groups and the output
                     // index are independent loads: issue them together (every
@@ -540,9 +542,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             int j = jj[u];
-                            double2 pj = wxy[j];   // one 16-B gather for x, y
-                            dx[u] = xi - pj.x;
-                            dy[u] = yi - pj.y;
+                            dx[u] = xi - wx[j];
+                            dy[u] = yi - wy[j];
                             dz[u] = zi - wz[j];
                             tj[u] = MT ? wt[j] : 0;
                             double r2 = dx[u] * dx[u] + dy[u] * dy[u] + dz[u] * dz[u];

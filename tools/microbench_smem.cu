@@ -52,6 +52,24 @@ __global__ void s_gather_soa(int per, unsigned seed, double* out) {
     if (acc == 1.2345) out[0] = acc;
 }
 
+// {x,y} as one 16-B record + z as an 8-B one: 2 loads per gather instead of 3
+template <bool LOCAL>
+__global__ void s_gather_xy(int per, unsigned seed, double* out) {
+    __shared__ double2 xy[W];
+    __shared__ double z[W];
+    for (int i = threadIdx.x; i < W; i += blockDim.x) { xy[i] = make_double2(i, 2 * i); z[i] = 3 * i; }
+    __syncthreads();
+    unsigned s = seed ^ (blockIdx.x * blockDim.x + threadIdx.x) / 32 * 2654435761u;
+    unsigned l = seed ^ (blockIdx.x * blockDim.x + threadIdx.x) * 747796405u;
+    double acc = 0;
+    for (int k = 0; k < per; ++k) {
+        unsigned j = pick<LOCAL>(s, l);
+        double2 v = xy[j];
+        acc += v.x + v.y + z[j];
+    }
+    if (acc == 1.2345) out[0] = acc;
+}
+
 // MODE 0: random rows; 1: bank class of row = (lane + k) mod 16 (conflict-free
 // per half-warp); 2: class (lane + k/4 + drift) mod 16 with a random per-lane
 // drift of 0..3 steps -- what a list sorted by (class - lane) mod 16 gives
@@ -164,6 +182,8 @@ int main() {
     run("smem gather double4 local-128", b2, big(s_gather<true>));
     run("smem gather 3x double random", b2, big(s_gather_soa<false>));
     run("smem gather 3x double local-128", b2, big(s_gather_soa<true>));
+    run("smem gather double2 xy + double z random", b2, big(s_gather_xy<false>));
+    run("smem gather double2 xy + double z local", b2, big(s_gather_xy<true>));
     run("smem 3x double, random class", b2, big(s_gather_cls<0>));
     run("smem 3x double, rotated class", b2, big(s_gather_cls<1>));
     run("smem 3x double, rotated+drift", b2, big(s_gather_cls<2>));

@@ -852,3 +852,65 @@ def test_stale_verlet_lists_between_rebuilds(pkg):
             assert n == 0 and np.all(parts.numpy("force") == 0.0)
         else:
             assert n > 0
+
+
+def _fuzz_system(seed):
+    """Seeded random system: N, a non-cubic box, mixed periodic / reflective
+    axes, 1-3 types, random density; positions by sequential rejection
+    (>= 0.85 sigma apart, so the fp32 variant stays finite)."""
+    rng = np.random.default_rng(1000 + seed)
+    n_target = int(rng.choice([2, 7, 64, 500, 1500, 3000]))
+    L = rng.uniform(6.0, 16.0, 3)
+    per = rng.random(3) < 0.6
+    nt = int(rng.integers(1, 4))
+    pos = []
+    tries = 0
+    while len(pos) < n_target and tries < 40 * n_target:
+        tries += 1
+        x = rng.uniform(0.0, 1.0, 3) * L
+        if pos:
+            d = np.asarray(pos) - x
+            d[:, per] -= L[per] * np.rint(d[:, per] / L[per])
+            if np.min(np.einsum("ij,ij->i", d, d)) < 0.85 ** 2:
+                continue
+        pos.append(x)
+    return np.asarray(pos), L, per, nt
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_every_configuration_vs_oracle(pkg, seed):
+    """Random systems (size, box shape, boundaries, types, density) through
+    every configuration -- the 30 reference ids, VCL and the fp32 variant --
+    against the oracle: exact counts, fp64 forces within 1e-10, fp32 within
+    1e-4."""
+    P, calc = pkg
+    pos, L, per, nt = _fuzz_system(seed)
+    n = len(pos)
+    tid = (np.arange(n) % nt).astype(np.int64)
+    types = [P.ParticleTypeInfo(t, 1.0 + 0.5 * t, 1.0 - 0.2 * t, 1.0 + t) for t in range(nt)]
+    bnd = tuple(P.PERIODIC if f else P.REFLECTIVE for f in per)
+    params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, boundary=bnd)
+    pp = port.Params(domain_size=L, cutoff=2.5, skin=0.3,
+                     boundary=tuple(port.PERIODIC if f else port.REFLECTIVE for f in per))
+    ref = {}
+    for cfg in P.enumerate_configurations():
+        rp = port.Particles(pos, type_id=tid, sigma=[t.sigma for t in types],
+                            epsilon=[t.epsilon for t in types], mass=[t.mass for t in types])
+        _, c = port.compute_forces(rp, port.parse(cfg.id), pp, workers=2)
+        ref[cfg.id] = (c, np.asarray(rp.forces).copy())
+    f_vl = ref["VL-List_Iter-NoN3L-AoS"][1]
+    c_vl = ref["VL-List_Iter-NoN3L-AoS"][0]
+    for cfg in P.extended_configurations():
+        parts = P.ParticleSet(pos, type_ids=tid, types=types, layout=cfg.layout)
+        _, count = calc.compute_forces(parts, cfg, params)
+        got = parts.numpy("force")
+        if cfg.id in ref:
+            want_c, want_f = ref[cfg.id]
+            assert count == want_c, (seed, cfg.id, count, want_c)
+            assert port.force_rel_error(got, want_f) <= FP64_TOL, (seed, cfg.id)
+        elif cfg.id.startswith("VCL"):
+            assert count == c_vl // (2 if cfg.newton3 else 1), (seed, cfg.id)
+            assert port.force_rel_error(got, f_vl) <= FP64_TOL, (seed, cfg.id)
+        else:   # fp32 variant
+            assert abs(count - c_vl) <= max(2, 1e-6 * c_vl), (seed, cfg.id, count, c_vl)
+            assert port.force_rel_error(got, f_vl) <= 1e-4, (seed, cfg.id)

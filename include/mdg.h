@@ -208,6 +208,19 @@ int mdg_lc_pairs(mdg_ctx* ctx, double csf, int64_t cap, int32_t* pairs, int64_t*
  * intervals in ns (-1 = not measured), waiting for them. */
 int mdg_timings(mdg_ctx* ctx, int enable, int64_t* build_ns, int64_t* force_ns);
 
+/* Dynamic pruning of the tiled Verlet-list walk (no reference counterpart;
+ * an execution detail of vl_force_aos/_soa, kernels.py:730-818).  After each
+ * VL rebuild the walk writes inner lists of the entries within rc + delta and
+ * walks them while every particle has moved less than delta / 2 since; a
+ * larger move re-prunes from the full lists.  Pair sets within rc, counts and
+ * forces are those of the full walk (forces up to the grouping of the
+ * batched reciprocal, ~1e-16 relative).  delta < 0: default (env
+ * MDG_VL_PRUNE_DELTA, else skin / 3; MDG_VL_PRUNE=0 disables); 0: off;
+ * > 0: that delta (off if >= skin).  Applies from the next rebuild. */
+int mdg_set_prune(mdg_ctx* ctx, double delta);
+/* Prune walks since the last VL rebuild (-1 when pruning is off); synchronises. */
+int mdg_prune_count(mdg_ctx* ctx, int64_t* prunes);
+
 /* Context-free host versions of the two exports above (no device needed). */
 int mdg_geometry_for(const double domain[3], const int periodic[3], double interaction_length,
                      double csf, int dims_owned[3], double cell_length[3], int overlap[3],

@@ -189,6 +189,17 @@ class ForceCalculator:
                                 ctypes.byref(b), ctypes.byref(f)), "timings")
         return None if enable is not None else (b.value, f.value)
 
+    def set_prune(self, delta=None):
+        """mdg_set_prune: dynamic pruning of the tiled VL walk from the next
+        rebuild (None = default skin / 3, 0 = off, > 0 = that inner skin)."""
+        check(lib().mdg_set_prune(self.ctx.h, -1.0 if delta is None else float(delta)), "set_prune")
+
+    def prune_count(self) -> int:
+        """Prune walks since the last VL rebuild (-1 = pruning off)."""
+        n = ctypes.c_int64()
+        check(lib().mdg_prune_count(self.ctx.h, ctypes.byref(n)), "prune_count")
+        return int(n.value)
+
     def sd_step(self, particles, gamma, max_disp):
         self.bind(particles)
         check(lib().mdg_sd_step(self.ctx.h, float(gamma), float(max_disp)), "sd_step")

@@ -308,6 +308,33 @@ int mdg_timings(mdg_ctx* ctx, int enable, int64_t* build_ns, int64_t* force_ns) 
     return cuda_status("mdg_timings");
 }
 
+int mdg_set_prune(mdg_ctx* ctx, double delta) {
+    CHECK_CTX(ctx);
+    if (!(delta == delta)) {
+        set_error("prune delta is NaN");
+        return MDG_EINVAL;
+    }
+    ctx->c.prune_delta = delta < 0.0 ? -1.0 : delta;
+    return MDG_OK;
+}
+
+int mdg_prune_count(mdg_ctx* ctx, int64_t* prunes) {
+    CHECK_CTX(ctx);
+    if (!prunes) {
+        set_error("null output");
+        return MDG_EINVAL;
+    }
+    Context& c = ctx->c;
+    *prunes = -1;
+    if (!c.vl.prune || !c.vl.pst.p) return MDG_OK;
+    int h = 0;
+    if (cudaMemcpyAsync(&h, c.vl.pst.p + 1, sizeof(int), cudaMemcpyDeviceToHost, c.stream) != cudaSuccess ||
+        cudaStreamSynchronize(c.stream) != cudaSuccess)
+        return cuda_status("mdg_prune_count");
+    *prunes = h;
+    return MDG_OK;
+}
+
 int mdg_rebuild(mdg_ctx* ctx, const mdg_config* cfg) {
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;

@@ -110,6 +110,7 @@ template struct DBuf<uint16_t>;
 template struct DBuf<int4>;
 template struct DBuf<int2>;
 template struct DBuf<float4>;
+template struct DBuf<float>;
 template struct DBuf<PwLeaf>;
 
 void Grid::release() {
@@ -133,6 +134,8 @@ void Verlet::release() {
     q32.release();
     tdesc.release(); tsize.release(); tbase.release(); tl.release(); tcnt.release();
     big_row.release();
+    tl_in.release(); tcnt_in.release(); disp.release(); pst.release();
+    prune = false;
     tiled = false;
     ntiles = nbig = 0;
     cap = 0;

@@ -105,6 +105,16 @@ struct Verlet {
     DBuf<uint16_t> tl;         // window-local lists, 4-entry groups per lane
     DBuf<int> tcnt;            // per tile row slot: list length
     DBuf<uint8_t> big_row;     // 1 = row walked by the global-gather kernel
+    // dynamic pruning of the tile lists (vltile.cu): inner lists of the pairs
+    // within rp of the positions at the last prune, walked while every owned
+    // row has moved less than (rp - rc) / 2 since then
+    bool prune = false;
+    double prune_rp2 = 0.0;
+    float prune_thr = 0.f;
+    DBuf<uint16_t> tl_in;      // inner lists, the layout of tl
+    DBuf<int> tcnt_in;         // inner list lengths, the layout of tcnt
+    DBuf<float> disp;          // per row: path length since the last prune (rounded up)
+    DBuf<int> pst;             // [0] the next walk prunes, [1] prune walks since the build
     void release();
 };
 
@@ -165,6 +175,7 @@ struct Context {
     // containers
     Grid grids[2];             // [0] CSF 1, [1] CSF 0.5
     Verlet vl;
+    double prune_delta = -1.0;  // inner-list radius rc + delta (mdg_set_prune); < 0 default, 0 off
     Vcl vcl;
     // temperature / thermostat / live statistics (stats.cu)
     PairwiseTree pw_particles, pw_bins;
@@ -214,6 +225,8 @@ int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr);
 int vl_energy(Context& c, double* pe);
 void vl_compute32(Context& c);
 int vlt_build(Context& c);
+// the next tiled walk re-prunes (an s3 write that bypassed the displacement bound)
+void vl_prune_invalidate(Context& c);
 int vcl_rebuild(Context& c);
 void vcl_compute(Context& c, int newton3);
 void vl_refresh_into(Context& c, Grid& gr, double4* s4, double* s3, bool& s3_valid);

@@ -231,38 +231,52 @@ struct Wrap {
 };
 
 // Nearest periodic image of pos[src] + shift to the previous row value.
+//
+// With `disp` (dynamic pruning of the tile lists, vltile.cu) every owned row
+// also adds the length of its move, rounded up, to disp[r]; a row past `thr`
+// raises pst[0], which makes the walk that follows prune again.
 template <int PLAYOUT, int SLAYOUT>
 __global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int m, int ms,
                                   const int* __restrict__ row_src,
                                   const uint8_t* __restrict__ row_code, Wrap w,
                                   double4* __restrict__ s4, double* __restrict__ s3,
-                                  bool from_s4, int* zero_me) {
+                                  bool from_s4, int* zero_me, float* __restrict__ disp, int* pst,
+                                  float thr) {
     int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r == 0 && zero_me) *zero_me = 0;   // work counter of the tiled walk
-    if (r >= m) return;
-    int src = row_src[r], code = row_code[r];
-    double q[3] = {pos[pidx<PLAYOUT>(src, 0, n)], pos[pidx<PLAYOUT>(src, 1, n)],
-                   pos[pidx<PLAYOUT>(src, 2, n)]};
-    int sh[3] = {code / 9 - 1, (code / 3) % 3 - 1, code % 3 - 1};
-    double prev[3];
-    double4 old = s4[r];
-    if (SLAYOUT == AOS || from_s4) {
-        prev[0] = old.x; prev[1] = old.y; prev[2] = old.z;
-    } else {
-        prev[0] = s3[r]; prev[1] = s3[(size_t)ms + r]; prev[2] = s3[2 * (size_t)ms + r];
+    bool over = false;
+    if (r < m) {
+        int src = row_src[r], code = row_code[r];
+        double q[3] = {pos[pidx<PLAYOUT>(src, 0, n)], pos[pidx<PLAYOUT>(src, 1, n)],
+                       pos[pidx<PLAYOUT>(src, 2, n)]};
+        int sh[3] = {code / 9 - 1, (code / 3) % 3 - 1, code % 3 - 1};
+        double prev[3];
+        double4 old = s4[r];
+        if (SLAYOUT == AOS || from_s4) {
+            prev[0] = old.x; prev[1] = old.y; prev[2] = old.z;
+        } else {
+            prev[0] = s3[r]; prev[1] = s3[(size_t)ms + r]; prev[2] = s3[2 * (size_t)ms + r];
+        }
+        for (int k = 0; k < 3; ++k) {
+            double x = q[k] + (double)sh[k] * w.L[k];
+            if (w.per[k]) x += w.L[k] * rint((prev[k] - x) * w.invL[k]);
+            q[k] = x;
+        }
+        if (disp && code == kNoShift) {
+            double ex = q[0] - prev[0], ey = q[1] - prev[1], ez = q[2] - prev[2];
+            float a = __fadd_ru(disp[r], __double2float_ru(sqrt(ex * ex + ey * ey + ez * ez)));
+            disp[r] = a;
+            over = !(a <= thr);   // NaN counts as a violation
+        }
+        if (SLAYOUT == AOS) {
+            s4[r] = make_double4(q[0], q[1], q[2], old.w);
+        } else {
+            s3[r] = q[0];
+            s3[(size_t)ms + r] = q[1];
+            s3[2 * (size_t)ms + r] = q[2];
+        }
     }
-    for (int k = 0; k < 3; ++k) {
-        double x = q[k] + (double)sh[k] * w.L[k];
-        if (w.per[k]) x += w.L[k] * rint((prev[k] - x) * w.invL[k]);
-        q[k] = x;
-    }
-    if (SLAYOUT == AOS) {
-        s4[r] = make_double4(q[0], q[1], q[2], old.w);
-    } else {
-        s3[r] = q[0];
-        s3[(size_t)ms + r] = q[1];
-        s3[2 * (size_t)ms + r] = q[2];
-    }
+    if (over) *pst = 1;   // rare; every writer stores the same value
 }
 
 // ---------------------------------------------------------------- force
@@ -401,7 +415,8 @@ static void vl_launch(Context& c, bool mt) {
     }
     dim3 b(blocks_for(m, 256)), t(256);
     bool from_s4 = SLAYOUT == SOA && !v.s3_valid;
-    vl_refresh_kernel<PLAYOUT, SLAYOUT><<<b, t, 0, c.stream>>>(c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, from_s4, nullptr), note_launch();
+    vl_refresh_kernel<PLAYOUT, SLAYOUT><<<b, t, 0, c.stream>>>(c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, from_s4, nullptr, nullptr, nullptr, 0.f), note_launch();
+    vl_prune_invalidate(c);
     if (SLAYOUT == SOA) v.s3_valid = true;
     c.prof_mark();
 #define MDG_VLF(G, PF, NT, MB)                                                                     \
@@ -450,7 +465,8 @@ void vl_refresh_launch(Context& c, int* zero_me) {
     int m = (int)gr.m;
     bool from_s4 = SLAYOUT == SOA && !v.s3_valid;
     vl_refresh_kernel<PLAYOUT, SLAYOUT><<<blocks_for(m, 256), 256, 0, c.stream>>>(
-        c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, make_wrap(c), v.s4.p, v.s3.p, from_s4, zero_me), note_launch();
+        c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, make_wrap(c), v.s4.p, v.s3.p, from_s4, zero_me,
+        v.prune ? v.disp.p : nullptr, v.pst.p, v.prune_thr), note_launch();
     if (SLAYOUT == SOA) v.s3_valid = true;
 }
 template void vl_refresh_launch<AOS, SOA>(Context&, int*);
@@ -462,11 +478,11 @@ void vl_refresh_into(Context& c, Grid& gr, double4* s4, double* s3, bool& s3_val
     if (c.layout == AOS)
         vl_refresh_kernel<AOS, SOA><<<blocks_for(m, 256), 256, 0, c.stream>>>(
             c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, make_wrap(c), s4, s3, !s3_valid,
-            nullptr), note_launch();
+            nullptr, nullptr, nullptr, 0.f), note_launch();
     else
         vl_refresh_kernel<SOA, SOA><<<blocks_for(m, 256), 256, 0, c.stream>>>(
             c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, make_wrap(c), s4, s3, !s3_valid,
-            nullptr), note_launch();
+            nullptr, nullptr, nullptr, 0.f), note_launch();
     s3_valid = true;
 }
 template void vl_refresh_launch<SOA, SOA>(Context&, int*);
@@ -706,9 +722,10 @@ int vl_energy(Context& c, double* pe) {
         w.per[k] = c.periodic[k];
     }
     if (c.layout == AOS)
-        vl_refresh_kernel<AOS, AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, false, nullptr), note_launch();
+        vl_refresh_kernel<AOS, AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, false, nullptr, nullptr, nullptr, 0.f), note_launch();
     else
-        vl_refresh_kernel<SOA, AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, false, nullptr), note_launch();
+        vl_refresh_kernel<SOA, AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, w, v.s4.p, v.s3.p, false, nullptr, nullptr, nullptr, 0.f), note_launch();
+    vl_prune_invalidate(c);
     double* dpe = (double*)(c.scal.p + 6);
     MDG_CUDA(cudaMemsetAsync(dpe, 0, sizeof(double), c.stream));
     if (c.tab.T > 1)

@@ -399,6 +399,92 @@ struct WinLayout {
     // per buffer: x, y, z (doubles) then types (int32) for MT
 };
 
+// One tile row's list walk (the consumers' body).  WR: the walk reads the full
+// lists and writes the row's inner list (the entries within rp, in list
+// order, 4 to a group like the outer list) and zeroes the row's path length.
+template <bool MT, int PF, bool WR>
+__device__ __forceinline__ void vlt_walk_row(const double* wx, const double* wy, const double* wz,
+                                             const int* wt, int li, int c, const uint2* lp,
+                                             uint2* op, const uint2* sel, const LJTab& tab, double rp2,
+                                             double& fx, double& fy, double& fz, unsigned& hits, int& pc) {
+    double xi = wx[li], yi = wy[li], zi = wz[li];
+    int ti = MT ? wt[li] : 0;
+    // the first two entry groups are independent loads: issue them together
+    // (every row owns >= 2 groups, cap4 >= 8), then keep the list stream
+    // ahead of the walk
+    uint2 g0 = __ldcs(lp), g1 = PF == 2 ? __ldcs(lp + 32) : make_uint2(0u, 0u);
+    unsigned long long pk = 0;   // the inner group being filled (pc & 3 entries)
+    const int rp2_hi = __double2hiint(rp2);
+    pc = 0;
+    for (int k0 = 0; k0 < c; k0 += 4) {
+        uint2 cur = g0;
+        if (PF == 2) {
+            g0 = g1;
+            if (k0 + 8 < c) g1 = __ldcs(lp + (size_t)(k0 / 4 + 2) * 32);
+        } else if (k0 + 4 < c) {
+            g0 = __ldcs(lp + (size_t)(k0 / 4 + 1) * 32);
+        }
+        int jj[4] = {(int)(cur.x & 0xffffu), (int)(cur.x >> 16), (int)(cur.y & 0xffffu),
+                     (int)(cur.y >> 16)};
+        double dx[4], dy[4], dz[4], qq[4];
+        int tj[4];
+        bool ok[4];
+        unsigned keep = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            int j = jj[u];
+            dx[u] = xi - wx[j];
+            dy[u] = yi - wy[j];
+            dz[u] = zi - wz[j];
+            tj[u] = MT ? wt[j] : 0;
+            double r2 = dx[u] * dx[u] + dy[u] * dy[u] + dz[u] * dz[u];
+            ok[u] = (k0 + u < c) && r2 < tab.rc2;
+            qq[u] = ok[u] ? r2 : 1.0;
+            // r^2 < rp^2 on the high words (non-negative doubles order like
+            // their bits; equal high words keep the entry, a harmless superset)
+            if (WR) keep |= (k0 + u < c && __double2hiint(r2) <= rp2_hi) ? 1u << u : 0u;
+        }
+        if (WR && keep) {
+            // the kept entries of this group, compacted (byte permutes from
+            // the 16-entry selector table), appended to the inner list; a
+            // completed group is one 8-byte store
+            uint2 sl = sel[keep];
+            int cnt = __popc(keep);
+            unsigned long long nv = ((unsigned long long)__byte_perm(cur.x, cur.y, sl.y) << 32) |
+                                    __byte_perm(cur.x, cur.y, sl.x);
+            if (cnt < 4) nv &= (1ull << (16 * cnt)) - 1ull;
+            int s = 16 * (pc & 3);
+            pk |= nv << s;
+            if ((pc & 3) + cnt >= 4) {
+                op[(size_t)(pc >> 2) * 32] = make_uint2((unsigned)pk, (unsigned)(pk >> 32));
+                pk = s ? nv >> (64 - s) : 0ull;
+            }
+            pc += cnt;
+        }
+        // one reciprocal for four pairs (see vl.cu)
+        double p01 = qq[0] * qq[1], p23 = qq[2] * qq[3];
+        double y = fast_rcp(p01 * p23);
+        double y01 = y * p23, y23 = y * p01;
+        double inv[4] = {y01 * qq[1], y01 * qq[0], y23 * qq[3], y23 * qq[2]};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (ok[u]) {
+                double s2, e24;
+                lj_params<MT>(tab, ti, tj[u], s2, e24);
+                double a = s2 * inv[u];
+                double a6 = a * a * a;
+                double fs = (e24 * inv[u]) * (a6 * fma(2.0, a6, -1.0));
+                ++hits;
+                fx = fma(fs, dx[u], fx);
+                fy = fma(fs, dy[u], fy);
+                fz = fma(fs, dz[u], fz);
+            }
+        }
+    }
+    // the last group's unused slots are zero, the padding the walk expects
+    if (WR && (pc & 3)) op[(size_t)(pc >> 2) * 32] = make_uint2((unsigned)pk, (unsigned)(pk >> 32));
+}
+
 // Persistent, warp-specialised walk.  The last warp is the producer: it takes
 // the next tile from the global counter, copies its descriptor and issues the
 // window's 1-D bulk copies (one per range and component) into one of two
@@ -407,18 +493,43 @@ struct WinLayout {
 // arrive on the buffer's `empty` mbarrier when no chunk is left, so the
 // producer refills it while they already work on the other buffer.  No
 // CTA-wide barrier after the prologue.
-template <int PLAYOUT, bool MT, int PF, bool KICK, int STAGES>
+//
+// PRUNE (dynamic pruning): pst[0], raised by the refresh just
+// before (or by the rebuild), picks the lists of the whole launch.  1: the
+// full lists (tl / tcnt), and every row's inner list (the entries with
+// r^2 < rp2 now, or a few more) is written to tl_in / tcnt_in; 0: the inner
+// lists.  The pair sets within rc are the same (the
+// refresh only lets the inner lists run while no owned row has moved
+// (rp - rc) / 2 since they were written), so forces and counts are those of
+// the full walk up to the grouping of the batched reciprocal.
+template <int PLAYOUT, bool MT, int PF, bool KICK, int STAGES, bool PRUNE>
 __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
     const TileDesc* __restrict__ desc, const int* __restrict__ tbase, int ntiles, int wrows,
     int* __restrict__ next, int ms, int64_t n, int cap4, const double* __restrict__ s3,
-    const int* __restrict__ row_tid, const int* __restrict__ tcnt, const uint2* __restrict__ tl,
+    const int* __restrict__ row_tid, const int* __restrict__ tcnt_out, const uint2* __restrict__ tl_out,
     const int* __restrict__ row_src, double* __restrict__ force, LJTab tab,
-    unsigned long long* counter, KickArgs kick) {
+    unsigned long long* counter, KickArgs kick, int* pst, uint2* tl_in,
+    int* tcnt_in, float* __restrict__ disp, double rp2) {
     extern __shared__ __align__(128) double win[];
     __shared__ __align__(16) TileDesc d[STAGES];
     __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
     __shared__ int rowctr[STAGES], tile_of[STAGES];
+    __shared__ int s_mode;
+    __shared__ uint2 s_sel[16];   // byte-permute selectors: compact the kept entries of a group
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (PRUNE) {
+        if (threadIdx.x == 0) s_mode = *(volatile const int*)pst;
+        if (threadIdx.x < 16) {
+            unsigned m = threadIdx.x, sl[2] = {0u, 0u};
+            int h = 0;
+            for (int e = 0; e < 4; ++e)
+                if (m >> e & 1) {
+                    sl[h >> 1] |= (unsigned)((2 * e) | (2 * e + 1) << 4) << (8 * (h & 1));
+                    ++h;
+                }
+            s_sel[m] = make_uint2(sl[0], sl[1]);
+        }
+    }
     if (threadIdx.x == 0) {
         for (int b = 0; b < STAGES; ++b) {
             mbar_init(&full[b], 1);
@@ -427,6 +538,12 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // the lists this launch walks (every CTA has read the mode before its
+    // producer's first tile fetch; the fetch that sees the counter's final
+    // value, ntiles + gridDim.x - 1, is the last one, so it may clear the mode)
+    const bool whole = !PRUNE || s_mode != 0;
+    const uint2* tl = whole ? tl_out : tl_in;
+    const int* tcnt = whole ? tcnt_out : tcnt_in;
     const int kBuf = WinLayout<MT>::doubles(wrows);
     if (warp == kConsumerWarps) {
         // ---------------- producer
@@ -437,6 +554,10 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
             if (lane == 0) t = atomicAdd(next, 1);
             t = __shfl_sync(0xffffffffu, t, 0);
             if (t >= ntiles) {
+                if (PRUNE && whole && lane == 0 && t == ntiles + (int)gridDim.x - 1) {
+                    pst[0] = 0;   // the inner lists are fresh
+                    ++pst[1];
+                }
                 if (lane == 0) {
                     tile_of[b] = -1;
                     mbar_arrive(&full[b]);
@@ -515,60 +636,19 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                 if (q < ni) {
                     int li;
                     int r = tile_row(D, q, li);
-                    double xi = wx[li], yi = wy[li], zi = wz[li];
-                    int ti = MT ? wt[li] : 0;
-                    // the count, the first two entry groups and the output
-                    // index are independent loads: issue them together (every
-                    // row owns >= 2 groups, cap4 >= 8), then keep the list
-                    // stream two rounds ahead of the walk
-                    const uint2* lp = tl + ((size_t)base + (size_t)(q >> 5) * 32 * cap4) / 4 + (q & 31);
+                    size_t go = ((size_t)base + (size_t)(q >> 5) * 32 * cap4) / 4 + (q & 31);
                     int c = tcnt[slot0 + q];
-                    uint2 g0 = __ldcs(lp), g1 = PF == 2 ? __ldcs(lp + 32) : make_uint2(0u, 0u);
                     int i = row_src[r];
                     double fx = 0.0, fy = 0.0, fz = 0.0;
-                    for (int k0 = 0; k0 < c; k0 += 4) {
-                        uint2 cur = g0;
-                        if (PF == 2) {
-                            g0 = g1;
-                            if (k0 + 8 < c) g1 = __ldcs(lp + (size_t)(k0 / 4 + 2) * 32);
-                        } else if (k0 + 4 < c) {
-                            g0 = __ldcs(lp + (size_t)(k0 / 4 + 1) * 32);
-                        }
-                        int jj[4] = {(int)(cur.x & 0xffffu), (int)(cur.x >> 16), (int)(cur.y & 0xffffu),
-                                     (int)(cur.y >> 16)};
-                        double dx[4], dy[4], dz[4], qq[4];
-                        int tj[4];
-                        bool ok[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            int j = jj[u];
-                            dx[u] = xi - wx[j];
-                            dy[u] = yi - wy[j];
-                            dz[u] = zi - wz[j];
-                            tj[u] = MT ? wt[j] : 0;
-                            double r2 = dx[u] * dx[u] + dy[u] * dy[u] + dz[u] * dz[u];
-                            ok[u] = (k0 + u < c) && r2 < tab.rc2;
-                            qq[u] = ok[u] ? r2 : 1.0;
-                        }
-                        // one reciprocal for four pairs (see vl.cu)
-                        double p01 = qq[0] * qq[1], p23 = qq[2] * qq[3];
-                        double y = fast_rcp(p01 * p23);
-                        double y01 = y * p23, y23 = y * p01;
-                        double inv[4] = {y01 * qq[1], y01 * qq[0], y23 * qq[3], y23 * qq[2]};
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            if (ok[u]) {
-                                double s2, e24;
-                                lj_params<MT>(tab, ti, tj[u], s2, e24);
-                                double a = s2 * inv[u];
-                                double a6 = a * a * a;
-                                double fs = (e24 * inv[u]) * (a6 * fma(2.0, a6, -1.0));
-                                ++hits;
-                                fx = fma(fs, dx[u], fx);
-                                fy = fma(fs, dy[u], fy);
-                                fz = fma(fs, dz[u], fz);
-                            }
-                        }
+                    int pc;
+                    if (PRUNE && whole) {
+                        vlt_walk_row<MT, PF, true>(wx, wy, wz, wt, li, c, tl + go, tl_in + go, s_sel, tab, rp2,
+                                                   fx, fy, fz, hits, pc);
+                        tcnt_in[slot0 + q] = pc;
+                        disp[r] = 0.f;
+                    } else {
+                        vlt_walk_row<MT, PF, false>(wx, wy, wz, wt, li, c, tl + go, nullptr, s_sel, tab, rp2,
+                                                    fx, fy, fz, hits, pc);
                     }
                     if (KICK) {
                         // apply_gravity + finish_kick (integrator.py:40-51), the
@@ -614,6 +694,7 @@ static int vlt_env_tz() {
 }
 
 static int vlt_env_budget();
+static int vlt_prune_setup(Context& c, size_t list_entries, size_t slots);
 
 // Tiled build (called by vl_rebuild after the fp32 copy): 0 = tile lists
 // built, 1 = tiling not applicable (row-space lists instead), -1 = error.
@@ -621,6 +702,7 @@ int vlt_build(Context& c) {
     Verlet& v = c.vl;
     Grid& gr = v.grid;
     v.tiled = false;
+    v.prune = false;
     v.ntiles = v.nbig = 0;
     if (!vlt_env_enabled() || c.n == 0 || gr.pruned.n != 26) return 1;
     const Geom& g = gr.g;
@@ -713,6 +795,10 @@ int vlt_build(Context& c) {
     v.nbig = big;
     v.win_rows = budget;
     v.tiled = true;
+    {
+        long long slots = (long long)c.n + 32ll * ntiles;
+        if (vlt_prune_setup(c, (size_t)(slots * v.cap4) + 8, (size_t)slots + 32)) return -1;
+    }
     if (getenv("MDG_VLT_DEBUG"))
         fprintf(stderr, "vlt: tz=%d tiles=%d big=%d cap=%d cap4=%d\n", tz, ntiles, big, v.cap, v.cap4);
     return 0;
@@ -739,33 +825,34 @@ static int vlt_env_budget() {
     return v;
 }
 
-template <int PLAYOUT, bool MT, int PF, bool KICK, int STAGES>
+template <int PLAYOUT, bool MT, int PF, bool KICK, int STAGES, bool PRUNE>
 static void vlt_launch_st(Context& c, const KickArgs& kick) {
     Verlet& v = c.vl;
     int wrows = v.win_rows;
     size_t smem = STAGES * (size_t)WinLayout<MT>::doubles(wrows) * sizeof(double);
     static int ctas_per_sm = 0;
     static size_t smem_set = 0;
+    auto kern = vlt_force_kernel<PLAYOUT, MT, PF, KICK, STAGES, PRUNE>;
     if (smem != smem_set) {
-        cudaFuncSetAttribute(vlt_force_kernel<PLAYOUT, MT, PF, KICK, STAGES>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, vlt_force_kernel<PLAYOUT, MT, PF, KICK, STAGES>,
-                                                      kTileThreads, smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, kern, kTileThreads, smem);
         if (ctas_per_sm < 1) ctas_per_sm = 1;
         smem_set = smem;
     }
     int grid = std::min(v.ntiles, c.sm_count * ctas_per_sm);
     if (grid < 1) return;
-    vlt_force_kernel<PLAYOUT, MT, PF, KICK, STAGES><<<grid, kTileThreads, smem, c.stream>>>(
+    kern<<<grid, kTileThreads, smem, c.stream>>>(
         reinterpret_cast<const TileDesc*>(v.tdesc.p), v.tbase.p, v.ntiles, wrows, (int*)(c.scal.p + 6),
         s3_stride((int)v.grid.m), c.n, v.cap4, v.s3.p, v.grid.row_tid.p, v.tcnt.p,
-        reinterpret_cast<const uint2*>(v.tl.p), v.grid.row_src.p, c.force, c.tab, c.scal.p, kick), note_launch();
+        reinterpret_cast<const uint2*>(v.tl.p), v.grid.row_src.p, c.force, c.tab, c.scal.p, kick,
+        v.pst.p, reinterpret_cast<uint2*>(v.tl_in.p), v.tcnt_in.p, v.disp.p, v.prune_rp2), note_launch();
 }
 
 template <int PLAYOUT, bool MT, int PF, bool KICK>
 static void vlt_launch_pf(Context& c, const KickArgs& kick) {
-    if (vlt_env_stages() == 3) vlt_launch_st<PLAYOUT, MT, PF, KICK, 3>(c, kick);
-    else vlt_launch_st<PLAYOUT, MT, PF, KICK, 2>(c, kick);
+    if (PF == 3 && c.vl.prune) vlt_launch_st<PLAYOUT, MT, PF, KICK, 2, true>(c, kick);
+    else if (vlt_env_stages() == 3) vlt_launch_st<PLAYOUT, MT, PF, KICK, 3, false>(c, kick);
+    else vlt_launch_st<PLAYOUT, MT, PF, KICK, 2, false>(c, kick);
 }
 
 static int vlt_env_pf() {
@@ -775,6 +862,57 @@ static int vlt_env_pf() {
         v = e ? atoi(e) : 3;
     }
     return v;
+}
+
+// Dynamic pruning: the inner radius is rc + delta, delta from
+// mdg_set_prune, else MDG_VL_PRUNE_DELTA, else skin / 3 (MDG_VL_PRUNE=0: off).
+// Only with the default window ring and list prefetch, and only when every
+// owned row is walked by the tiles (the refresh checks owned rows, the tile
+// walk resets them).
+static double vlt_prune_delta(const Context& c) {
+    static int on = -1;
+    static double env_delta = -1.0;
+    if (on < 0) {
+        const char* e = getenv("MDG_VL_PRUNE");
+        on = e ? atoi(e) : 1;
+        const char* d = getenv("MDG_VL_PRUNE_DELTA");
+        env_delta = d ? atof(d) : -1.0;
+    }
+    if (vlt_env_stages() == 3 || vlt_env_pf() != 3 || c.prune_delta == 0.0) return 0.0;
+    double dl = c.prune_delta > 0.0 ? c.prune_delta : (!on ? 0.0 : env_delta > 0.0 ? env_delta : c.skin / 3.0);
+    return dl < c.skin ? dl : 0.0;
+}
+
+void vl_prune_invalidate(Context& c) {
+    Verlet& v = c.vl;
+    if (v.prune && v.pst.p) cudaMemsetAsync(v.pst.p, 1, sizeof(int), c.stream);
+}
+
+// after the tile lists are built: inner-list storage and the state that makes
+// the first walk prune
+static int vlt_prune_setup(Context& c, size_t list_entries, size_t slots) {
+    Verlet& v = c.vl;
+    v.prune = false;
+    double rc = c.cutoff;
+    double delta = v.nbig == 0 ? vlt_prune_delta(c) : 0.0;
+    if (delta <= 0.0) return 0;
+    v.tl_in.ensure(list_entries);
+    v.tcnt_in.ensure(slots);
+    v.disp.ensure((size_t)v.grid.m + 1);
+    v.pst.ensure(4);
+    if (!v.tl_in.p || !v.tcnt_in.p || !v.disp.p || !v.pst.p) {
+        set_error("out of device memory (VL inner lists)");
+        return -1;
+    }
+    v.prune_rp2 = (rc + delta) * (rc + delta);
+    // rows may move (rp - rc) / 2 each; 1e-6 absorbs the rounding of r^2
+    // and of the unwrapped copies (~1e-13 at these coordinates)
+    v.prune_thr = (float)(0.5 * delta - 1e-6);
+    MDG_CUDA(cudaMemsetAsync(v.disp.p, 0, ((size_t)v.grid.m + 1) * sizeof(float), c.stream));
+    MDG_CUDA(cudaMemsetAsync(v.pst.p, 0, 4 * sizeof(int), c.stream));
+    MDG_CUDA(cudaMemsetAsync(v.pst.p, 1, sizeof(int), c.stream));
+    v.prune = true;
+    return 0;
 }
 
 template <int PLAYOUT, bool MT>

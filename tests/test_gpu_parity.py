@@ -914,3 +914,77 @@ def test_fuzz_every_configuration_vs_oracle(pkg, seed):
         else:   # fp32 variant
             assert abs(count - c_vl) <= max(2, 1e-6 * c_vl), (seed, cfg.id, count, c_vl)
             assert port.force_rel_error(got, f_vl) <= 1e-4, (seed, cfg.id)
+
+
+# -- dynamic pruning of the tiled Verlet walk ---------------------
+
+@pytest.mark.parametrize("traj", ["traj_small", "traj_faces", "traj_config1"])
+def test_pruned_walk_trajectories_match_reference(pkg, traj):
+    """Inner lists re-pruned almost every step (delta 0.01: a 0.005 move
+    re-prunes) and never (pruning off) both reproduce the reference's 100-step
+    VL trajectories; with delta 0.01 several prune walks happen per window."""
+    P, calc = pkg
+    from paper_2505_03438_b200.simulation import Simulation
+    z = golden(f"{traj}.npz")
+    L = z["domain"]
+    ids = [str(s) for s in z["config_ids"]]
+    # config 1's reference run is LC-C08; VL agrees with it to ~5e-14 there
+    # (sites at (i + 0.5) * 1.1 keep particles off the faces, SURVEY Appendix A.1)
+    cases = [(k, c) for k, c in enumerate(ids) if c.startswith("VL")] or [(0, "VL-List_Iter-NoN3L-SoA")]
+    for k, cid in cases:
+        for delta in (0.01, 0.0):
+            params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=10,
+                                        delta_t=1e-3, boundary=(P.PERIODIC,) * 3)
+            cfg = P.parse_configuration(cid)
+            parts = P.ParticleSet(z["pos0"], z["vel0"], layout=cfg.layout)
+            sim = Simulation(parts, params, cfg)
+            sim.calc.set_prune(delta)
+            sim.run(33, record=False)              # the last window: iterations 22..32
+            prunes = sim.calc.prune_count()
+            sim.run(int(z["steps"]) - 33, record=False)
+            sim.check()
+            if delta == 0.0:
+                assert prunes == -1
+            else:
+                assert prunes >= 2, prunes
+            dpos = parts.numpy("pos") - z[f"pos_{k}"]
+            dpos -= L * np.rint(dpos / L)
+            assert np.linalg.norm(dpos) / np.linalg.norm(z[f"pos_{k}"]) <= FP64_TOL, (cid, delta)
+            assert port.force_rel_error(parts.numpy("vel"), z[f"vel_{k}"]) <= FP64_TOL, (cid, delta)
+
+
+def test_pruned_walk_full_size_is_the_full_walk(pkg, config2_snapshot):
+    """BASELINE config 2 (1,048,576 particles), 33 steps (3 rebuild windows):
+    per step the pruned walks (default delta = skin / 3, and a tight 0.02)
+    count exactly the pairs of the unpruned walk, and the trajectories agree
+    within the fp64 bar (the only difference is the grouping of the batched
+    reciprocal)."""
+    P, calc = pkg
+    from paper_2505_03438_b200.simulation import Simulation
+    pos, vel, params = config2_snapshot
+    cfg = P.parse_configuration("VL-List_Iter-NoN3L-SoA")
+    runs = {}
+    for delta in (0.0, None, 0.02):
+        parts = P.ParticleSet(pos, vel, layout="SoA")
+        sim = Simulation(parts, params, cfg)
+        sim.calc.set_prune(delta)
+        counts, prunes = [], []
+        for s in range(33):
+            sim.step()
+            counts.append(sim.calc.last_eval_count)
+            if s % 11 == 10:
+                prunes.append(sim.calc.prune_count())
+        sim.flush()
+        sim.check()
+        runs[delta] = (parts.numpy("pos"), parts.numpy("vel"), counts, prunes)
+    p0, v0, c0, n0 = runs[0.0]
+    assert n0 == [-1, -1, -1]
+    for delta in (None, 0.02):
+        p1, v1, c1, n1 = runs[delta]
+        assert c1 == c0, delta
+        assert min(n1) >= (1 if delta is None else 3), (delta, n1)
+        L = params.domain_size
+        d = p1 - p0
+        d -= L * np.rint(d / L)
+        assert np.linalg.norm(d) / np.linalg.norm(p0) <= FP64_TOL, delta
+        assert port.force_rel_error(v1, v0) <= FP64_TOL, delta

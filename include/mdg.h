@@ -94,6 +94,12 @@ int mdg_bind(mdg_ctx* ctx, int64_t n, int layout, double* pos, double* vel, doub
  * counting sort incl. periodic images) or Verlet-list build.  Synchronises
  * once (sizes of the image / list arrays). */
 int mdg_rebuild(mdg_ctx* ctx, const mdg_config* cfg);
+/* mdg_rebuild preceded by the loop's error check (simulation.py:158-166 with
+ * the blow-up / thermostat status of mdg_blowup): the status word is read at
+ * the rebuild's own first host synchronisation instead of a separate one.
+ * *flags = the MDG_FLAG_* bits raised since the last reset (then reset); when
+ * nonzero the rebuild was abandoned and the container must be rebuilt. */
+int mdg_rebuild_checked(mdg_ctx* ctx, const mdg_config* cfg, int* flags);
 /* ForceCalculator.refresh (containers.py:429-439): gather pos[src]+shift into
  * the cell-sorted scratch (no-op for Verlet lists).  Asynchronous. */
 int mdg_refresh(mdg_ctx* ctx, const mdg_config* cfg);

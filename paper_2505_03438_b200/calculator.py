@@ -106,6 +106,16 @@ class ForceCalculator:
         self.bind(particles)
         check(lib().mdg_rebuild(self.ctx.h, ctypes.byref(config_struct(config))), "rebuild")
 
+    def rebuild_checked(self, particles, config) -> int:
+        """rebuild() with the loop's status check folded into the rebuild's
+        own host synchronisation (mdg_rebuild_checked): returns the status
+        bits (then reset); nonzero means the rebuild was abandoned."""
+        self.bind(particles)
+        f = ctypes.c_int()
+        check(lib().mdg_rebuild_checked(self.ctx.h, ctypes.byref(config_struct(config)),
+                                        ctypes.byref(f)), "rebuild")
+        return int(f.value)
+
     def refresh(self, particles, config):
         self.bind(particles)
         check(lib().mdg_refresh(self.ctx.h, ctypes.byref(config_struct(config))), "refresh")

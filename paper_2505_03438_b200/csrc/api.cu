@@ -326,6 +326,7 @@ int mdg_prune_count(mdg_ctx* ctx, int64_t* prunes) {
     }
     Context& c = ctx->c;
     *prunes = -1;
+    if (vlt_finish(c)) return MDG_ECUDA;
     if (!c.vl.prune || !c.vl.pst.p) return MDG_OK;
     int h = 0;
     if (cudaMemcpyAsync(&h, c.vl.pst.p + 1, sizeof(int), cudaMemcpyDeviceToHost, c.stream) != cudaSuccess ||
@@ -352,6 +353,35 @@ int mdg_rebuild(mdg_ctx* ctx, const mdg_config* cfg) {
         grid_bind_scratch(c, gr, cfg->layout);
     }
     return cuda_status("mdg_rebuild");
+}
+
+int mdg_rebuild_checked(mdg_ctx* ctx, const mdg_config* cfg, int* flags) {
+    CHECK_CTX(ctx);
+    if (!flags) { set_error("null output"); return MDG_EINVAL; }
+    *flags = 0;
+    if (int e = validate(cfg)) return e;
+    if (int e = need_system(ctx)) return e;
+    Context& c = ctx->c;
+    if (cudaMemcpyAsync(c.h_scal + 2, c.scal.p + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                        c.stream) != cudaSuccess)
+        return cuda_status("mdg_rebuild_checked");
+    c.flags_probe = true;
+    c.flags_seen = 0;
+    int e = mdg_rebuild(ctx, cfg);
+    if (c.flags_probe) {   // no synchronisation on the way (n == 0): read it now
+        c.flags_probe = false;
+        if (cudaStreamSynchronize(c.stream) != cudaSuccess) return cuda_status("mdg_rebuild_checked");
+        c.flags_seen = (unsigned)(c.h_scal[2] & 3ull);
+    }
+    if (c.flags_seen) {
+        *flags = (int)c.flags_seen;
+        c.vl.built = false;
+        c.vcl.built = false;
+        cudaMemsetAsync(c.scal.p + 2, 0, sizeof(unsigned long long), c.stream);
+        set_error("");
+        return cuda_status("mdg_rebuild_checked");
+    }
+    return e;
 }
 
 int mdg_refresh(mdg_ctx* ctx, const mdg_config* cfg) {
@@ -445,6 +475,10 @@ int mdg_compute_kick(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gra
         const char* e = getenv("MDG_FUSE_KICK");
         fuse_env = e ? atoi(e) : 0;
     }
+    if (fuse_env && cfg->container == MDG_VL && v.build_pending && vlt_finish(c)) {
+        v.tiled = false;
+        v.prune = false;
+    }
     bool fuse = fuse_env && cfg->container == MDG_VL && cfg->precision == MDG_FP64 &&
                 c.layout == cfg->layout && v.built && v.tiled && v.nbig == 0 && c.n > 0;
     if (fuse) {
@@ -473,6 +507,10 @@ int mdg_step_graph(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gravi
                : cfg->container == MDG_VCL ? c.vcl.built
                : grid_for(c, cfg->csf)->built;
     if (!built) { set_error("mdg_step_graph before rebuild"); return MDG_ESTATE; }
+    if (cfg->container == MDG_VL && vlt_finish(c)) {   // no host wait inside a capture
+        c.vl.tiled = false;
+        c.vl.prune = false;
+    }
     if (!c.graph_stream) {
         if (cudaStreamCreateWithFlags(&c.graph_stream, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&c.graph_in, cudaEventDisableTiming) != cudaSuccess ||

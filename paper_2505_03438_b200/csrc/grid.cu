@@ -135,6 +135,11 @@ void Verlet::release() {
     tdesc.release(); tsize.release(); tbase.release(); tl.release(); tcnt.release();
     big_row.release();
     tl_in.release(); tcnt_in.release(); disp.release(); pst.release();
+    if (h_build) cudaFreeHost(h_build);
+    if (ev_build) cudaEventDestroy(ev_build);
+    h_build = nullptr;
+    ev_build = nullptr;
+    build_pending = false;
     prune = false;
     tiled = false;
     ntiles = nbig = 0;
@@ -434,6 +439,15 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
                              cudaMemcpyDeviceToHost, st));
     exclusive_scan_i32(gr.cell_count.p, gr.cell_start.p, nc + 1, nullptr, c.scan_tmp, st);
     MDG_CUDA(cudaStreamSynchronize(st));
+    if (c.flags_probe) {   // status word copied before this rebuild's first kernel
+        c.flags_probe = false;
+        c.flags_seen = (unsigned)(c.h_scal[2] & 3ull);
+        if (c.flags_seen) {
+            gr.built = false;
+            set_error("status flags raised");
+            return -1;
+        }
+    }
     gr.nimg = (int64_t)c.h_scal[1];
     gr.m = n + gr.nimg;
     int64_t m = gr.m;

@@ -115,6 +115,13 @@ struct Verlet {
     DBuf<int> tcnt_in;         // inner list lengths, the layout of tcnt
     DBuf<float> disp;          // per row: path length since the last prune (rounded up)
     DBuf<int> pst;             // [0] the next walk prunes, [1] prune walks since the build
+    // the tile build's host check (list capacity, overflow tiles) deferred to
+    // the first use of the lists (vlt_finish), so the host does not wait on
+    // the build kernel with the stream empty behind it
+    bool build_pending = false;
+    cudaEvent_t ev_build = nullptr;
+    unsigned long long* h_build = nullptr;   // pinned: [0] max count, [1] list slots, [2] overflow tiles
+    int plan[5] = {0, 0, 0, 0, 0};           // ngx, ngy, nzt, tz, window budget
     void release();
 };
 
@@ -187,6 +194,10 @@ struct Context {
     unsigned long long* h_scal = nullptr;   // pinned mirror
     // cached steady-state step graph (mdg_step_graph)
     uint64_t gen = 0;                       // bumped by every rebuild / rebind
+    // mdg_rebuild_checked: the status word rides on the rebuild's first host
+    // synchronisation; nonzero abandons the rebuild there
+    bool flags_probe = false;
+    unsigned flags_seen = 0;
     cudaStream_t graph_stream = nullptr;
     cudaEvent_t graph_in = nullptr, graph_out = nullptr;
     cudaGraphExec_t step_exec = nullptr;
@@ -225,6 +236,8 @@ int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr);
 int vl_energy(Context& c, double* pe);
 void vl_compute32(Context& c);
 int vlt_build(Context& c);
+// completes a deferred tile build (host check, retries, overflow tiles, pruning); -1 = error
+int vlt_finish(Context& c);
 // the next tiled walk re-prunes (an s3 write that bypassed the displacement bound)
 void vl_prune_invalidate(Context& c);
 int vcl_rebuild(Context& c);

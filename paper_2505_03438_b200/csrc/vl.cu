@@ -505,8 +505,18 @@ void vl_force_rows_launch(Context& c, const uint8_t* only) {
 template void vl_force_rows_launch<AOS>(Context&, const uint8_t*);
 template void vl_force_rows_launch<SOA>(Context&, const uint8_t*);
 
+// the deferred tile-build check; if it fails the row-space lists take over
+static void vl_finish_build(Context& c) {
+    if (vlt_finish(c)) {
+        c.vl.tiled = false;
+        c.vl.prune = false;
+        vl_ensure_rows(c);
+    }
+}
+
 void vl_compute(Context& c, int layout) {
     if (c.n == 0) return;
+    vl_finish_build(c);
     Verlet& v = c.vl;
     bool mt = c.tab.T > 1;
     if (v.tiled) {
@@ -627,6 +637,7 @@ __global__ void __launch_bounds__(128) vl_force32_kernel(int m, int64_t n, int c
 
 void vl_compute32(Context& c) {
     if (c.n == 0) return;
+    vl_finish_build(c);
     Verlet& v = c.vl;
     bool tiled = v.tiled;
     if (!tiled && vl_ensure_rows(c)) return;

@@ -924,13 +924,66 @@ static int vlt_env_build() {
 }
 static int vlt_prune_setup(Context& c, size_t list_entries, size_t slots);
 
+// One pass of the tiled build for the plan in v.plan: descriptors, list
+// bases, the build kernel; the host check's inputs are copied to the pinned
+// v.h_build.  0 = launched, 1 = tiling not applicable, -1 = error.
+static int vlt_pass(Context& c) {
+    Verlet& v = c.vl;
+    Grid& gr = v.grid;
+    const TilePlan tp{v.plan[0], v.plan[1], v.plan[2], v.plan[3]};
+    const int budget = v.plan[4], ntiles = tp.ngx * tp.ngy * tp.nzt;
+    GridView gv = make_view(gr);
+    TileDesc* desc = reinterpret_cast<TileDesc*>(v.tdesc.p);
+    int* nbig = (int*)(c.scal.p + 7);
+    int* maxcnt = (int*)(c.scal.p + 3);
+    const unsigned* maxabs = (const unsigned*)(c.scal.p + 5);
+    double ell2 = gr.g.ell * gr.g.ell;
+    v.cap4 = std::max(8, (v.cap + 3) & ~3);   // >= 2 groups per row (walk prefetch)
+    MDG_CUDA(cudaMemsetAsync(nbig, 0, sizeof(int), c.stream));
+    vlt_desc_kernel<<<blocks_for(ntiles, 128), 128, 0, c.stream>>>(gv, tp, ntiles, v.cap4, budget,
+                                                                   desc, v.tsize.p, nbig), note_launch();
+    exclusive_scan_i32(v.tsize.p, v.tbase.p, ntiles, c.scal.p + 1, c.scan_tmp, c.stream);
+    // the lists get an upper-bound allocation (every tile's rows padded to
+    // whole 32-row blocks), so their exact size is not needed on the host
+    // before the build; slots (rows padded per tile) fit 32 bits, entries
+    // (slots x cap4) are 64-bit -- BASELINE config 5 (67 M particles) needs ~5.4 G
+    long long slots = (long long)c.n + 32ll * ntiles;
+    if (slots > (1ll << 31) - 64) return 1;   // keep the row-space walk
+    long long bound = slots * v.cap4;
+    v.tl.ensure((size_t)bound + 8);
+    v.tcnt.ensure((size_t)slots + 32);
+    if (!v.tl.p || !v.tcnt.p) {
+        set_error("out of device memory (VL tile lists)");
+        return -1;
+    }
+    MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
+    MDG_CUDA(cudaMemsetAsync(v.tcnt.p, 0, ((size_t)slots + 32) * sizeof(int), c.stream));
+    if (vlt_env_build() != 2)
+        vlt_build_kernel<<<ntiles, kBuildThreadsT, 0, c.stream>>>(
+            gv, desc, v.tbase.p, v.b32.p, gr.spos4.p, maxabs, ell2, v.cap, v.cap4, v.tl.p, v.tcnt.p,
+            maxcnt, gr.sort_by_z), note_launch();
+    else
+        vlt_build_warp_kernel<<<ntiles, kBuildThreadsT, 0, c.stream>>>(
+            gv, desc, v.tbase.p, v.b32.p, gr.spos4.p, maxabs, ell2, v.cap, v.cap4, v.tl.p, v.tcnt.p,
+            maxcnt, gr.sort_by_z), note_launch();
+    MDG_CUDA(cudaMemcpyAsync(v.h_build, c.scal.p + 3, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             c.stream));
+    MDG_CUDA(cudaMemcpyAsync(v.h_build + 1, c.scal.p + 1, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, c.stream));
+    MDG_CUDA(cudaMemcpyAsync(v.h_build + 2, c.scal.p + 7, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, c.stream));
+    return 0;
+}
+
 // Tiled build (called by vl_rebuild after the fp32 copy): 0 = tile lists
-// built, 1 = tiling not applicable (row-space lists instead), -1 = error.
+// launched (checked by vlt_finish at their first use), 1 = tiling not
+// applicable (row-space lists instead), -1 = error.
 int vlt_build(Context& c) {
     Verlet& v = c.vl;
     Grid& gr = v.grid;
     v.tiled = false;
     v.prune = false;
+    v.build_pending = false;
     v.ntiles = v.nbig = 0;
     if (!vlt_env_enabled() || c.n == 0 || gr.pruned.n != 26) return 1;
     const Geom& g = gr.g;
@@ -942,65 +995,60 @@ int vlt_build(Context& c) {
     tz = std::max(1, std::min(std::min(tz, g.S[2]), kMaxTZ));
     TilePlan tp{(g.S[0] + kTX - 1) / kTX, (g.S[1] + kTY - 1) / kTY, (g.S[2] + tz - 1) / tz, tz};
     int ntiles = tp.ngx * tp.ngy * tp.nzt;
+    v.plan[0] = tp.ngx; v.plan[1] = tp.ngy; v.plan[2] = tp.nzt; v.plan[3] = tz; v.plan[4] = budget;
     v.tdesc.ensure((size_t)ntiles * kDescInts);
     v.tsize.ensure(ntiles + 1);
     v.tbase.ensure(ntiles + 1);
-    int m = (int)gr.m;
-    v.big_row.ensure(m + 1);
+    v.big_row.ensure((size_t)gr.m + 1);
     if (!v.tdesc.p || !v.tsize.p || !v.tbase.p || !v.big_row.p) {
         set_error("out of device memory (VL tiles)");
         return -1;
     }
-    GridView gv = make_view(gr);
-    TileDesc* desc = reinterpret_cast<TileDesc*>(v.tdesc.p);
-    int* nbig = (int*)(c.scal.p + 7);
-    int* maxcnt = (int*)(c.scal.p + 3);
-    const unsigned* maxabs = (const unsigned*)(c.scal.p + 5);
-    double ell2 = g.ell * g.ell;
-    int big = 0;
-    for (int attempt = 0; attempt < 3; ++attempt) {
-        v.cap4 = std::max(8, (v.cap + 3) & ~3);   // >= 2 groups per row (walk prefetch)
-        MDG_CUDA(cudaMemsetAsync(nbig, 0, sizeof(int), c.stream));
-        vlt_desc_kernel<<<blocks_for(ntiles, 128), 128, 0, c.stream>>>(gv, tp, ntiles, v.cap4, budget,
-                                                                       desc, v.tsize.p, nbig), note_launch();
-        exclusive_scan_i32(v.tsize.p, v.tbase.p, ntiles, c.scal.p + 1, c.scan_tmp, c.stream);
-        // the lists get an upper-bound allocation (every tile's rows padded to
-        // whole 32-row blocks), so the exact size is not needed on the host
-        // before the build: one synchronisation per rebuild instead of two
-        // slots (rows padded per tile) fit 32 bits; entries (slots x cap4) are
-        // 64-bit -- BASELINE config 5 (67 M particles) needs ~5.4 G
-        long long slots = (long long)c.n + 32ll * ntiles;
-        if (slots > (1ll << 31) - 64) return 1;   // keep the row-space walk
-        long long bound = slots * v.cap4;
-        v.tl.ensure((size_t)bound + 8);
-        v.tcnt.ensure((size_t)slots + 32);
-        if (!v.tl.p || !v.tcnt.p) {
-            set_error("out of device memory (VL tile lists)");
+    if (!v.h_build && cudaHostAlloc((void**)&v.h_build, 4 * sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess) {
+        v.h_build = nullptr;
+        set_error("pinned allocation failed (VL tiles)");
+        return -1;
+    }
+    if (!v.ev_build && cudaEventCreateWithFlags(&v.ev_build, cudaEventDisableTiming) != cudaSuccess) {
+        v.ev_build = nullptr;
+        set_error("event creation failed (VL tiles)");
+        return -1;
+    }
+    if (int e = vlt_pass(c)) return e;
+    MDG_CUDA(cudaEventRecord(v.ev_build, c.stream));
+    v.ntiles = ntiles;
+    v.win_rows = budget;
+    v.tiled = true;
+    v.build_pending = true;
+    return 0;
+}
+
+int vlt_finish(Context& c) {
+    Verlet& v = c.vl;
+    if (!v.build_pending) return 0;
+    v.build_pending = false;
+    MDG_CUDA(cudaEventSynchronize(v.ev_build));
+    for (int attempt = 1; (int)(v.h_build[0] & 0xffffffffu) > v.cap; ++attempt) {
+        int hmax = (int)(v.h_build[0] & 0xffffffffu);
+        if (attempt >= 3) {
+            set_error("VL tile lists: capacity retries exhausted");
+            v.tiled = false;
             return -1;
         }
-        MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
-        MDG_CUDA(cudaMemsetAsync(v.tcnt.p, 0, ((size_t)slots + 32) * sizeof(int), c.stream));
-        if (vlt_env_build() != 2)
-            vlt_build_kernel<<<ntiles, kBuildThreadsT, 0, c.stream>>>(
-                gv, desc, v.tbase.p, v.b32.p, gr.spos4.p, maxabs, ell2, v.cap, v.cap4, v.tl.p, v.tcnt.p,
-                maxcnt, gr.sort_by_z), note_launch();
-        else
-            vlt_build_warp_kernel<<<ntiles, kBuildThreadsT, 0, c.stream>>>(
-                gv, desc, v.tbase.p, v.b32.p, gr.spos4.p, maxabs, ell2, v.cap, v.cap4, v.tl.p, v.tcnt.p,
-                maxcnt, gr.sort_by_z), note_launch();
-        int hmax = 0;
-        MDG_CUDA(cudaMemcpyAsync(&hmax, maxcnt, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-        MDG_CUDA(cudaMemcpyAsync(c.h_scal + 1, c.scal.p + 1, sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, c.stream));
-        MDG_CUDA(cudaMemcpyAsync(c.h_scal + 7, c.scal.p + 7, sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, c.stream));
-        MDG_CUDA(cudaStreamSynchronize(c.stream));
-        big = (int)(c.h_scal[7] & 0xffffffffu);
-        if (hmax <= v.cap) break;
         v.cap = (hmax + hmax / 8 + 7) / 8 * 8;
+        if (int e = vlt_pass(c)) {
+            v.tiled = false;
+            return e < 0 ? -1 : (vl_build_rows(c, nullptr) ? -1 : 0);
+        }
+        MDG_CUDA(cudaStreamSynchronize(c.stream));
     }
+    const int ntiles = v.ntiles;
+    const int big = (int)(v.h_build[2] & 0xffffffffu);
+    Grid& gr = v.grid;
+    int m = (int)gr.m;
+    TileDesc* desc = reinterpret_cast<TileDesc*>(v.tdesc.p);
     if (int order = vlt_env_order()) {
-        long long total = (long long)c.h_scal[1];   // list slots
+        long long total = (long long)v.h_build[1];   // list slots
         int64_t nblocks = total / 32;
         int warps = (int)std::max<size_t>(1, std::min<size_t>(8, (200u << 10) / (32 * (size_t)v.cap4 * 2 + 16 * 32 * 8)));
         size_t smem = (size_t)warps * (2 * 16 * 32 * sizeof(int) + 32 * (size_t)v.cap4 * sizeof(uint16_t));
@@ -1024,16 +1072,13 @@ int vlt_build(Context& c) {
         vlt_mark_big_kernel<<<ntiles, 128, 0, c.stream>>>(desc, v.big_row.p), note_launch();
         if (vl_build_rows(c, v.big_row.p)) return -1;
     }
-    v.ntiles = ntiles;
     v.nbig = big;
-    v.win_rows = budget;
-    v.tiled = true;
     {
         long long slots = (long long)c.n + 32ll * ntiles;
         if (vlt_prune_setup(c, (size_t)(slots * v.cap4) + 8, (size_t)slots + 32)) return -1;
     }
     if (getenv("MDG_VLT_DEBUG"))
-        fprintf(stderr, "vlt: tz=%d tiles=%d big=%d cap=%d cap4=%d\n", tz, ntiles, big, v.cap, v.cap4);
+        fprintf(stderr, "vlt: tz=%d tiles=%d big=%d cap=%d cap4=%d\n", v.plan[3], ntiles, big, v.cap, v.cap4);
     return 0;
 }
 

@@ -44,6 +44,15 @@ class BlowUpError(RuntimeError):
     """A particle left the domain by more than one domain length."""
 
 
+class _StatusFlags(Exception):
+    """Device status bits found by mdg_rebuild_checked (re-raised by
+    Simulation._check_flags as BlowUpError / ValueError)."""
+
+    def __init__(self, flags):
+        super().__init__(flags)
+        self.flags = flags
+
+
 @dataclass
 class IterationRecord:
     iteration: int
@@ -133,8 +142,9 @@ class Simulation:
     def config(self):
         return getattr(self.controller, "current_config", None) or getattr(self.controller, "config", None)
 
-    def _check_flags(self):
-        flags = self.calc.status_flags()
+    def _check_flags(self, flags=None):
+        if flags is None:
+            flags = self.calc.status_flags()
         if flags & FLAG_BLOWUP:
             raise BlowUpError("particle left the domain by more than one domain length "
                               "(or position is not finite)")
@@ -166,7 +176,10 @@ class Simulation:
                 cfg, forced = ctl.configuration_for_iteration(it)
             rebuild = forced or self.active != cfg.id or self.since >= params.rebuild_interval
             trial = self._trial()
-            if rebuild and it:
+            # the error check before a rebuild (simulation.py:158-166) rides on
+            # the rebuild's own host synchronisation (mdg_rebuild_checked)
+            checked = bool(rebuild and it and hasattr(calc, "rebuild_checked"))
+            if rebuild and it and not checked:
                 self._check_flags()
             timed = record or trial
             if timed:
@@ -176,7 +189,12 @@ class Simulation:
                 if p.layout != cfg.layout:
                     p.convert_layout(cfg.layout)
                 if rebuild:
-                    calc.rebuild(p, cfg)
+                    if checked:
+                        flags = calc.rebuild_checked(p, cfg)
+                        if flags:
+                            raise _StatusFlags(flags)
+                    else:
+                        calc.rebuild(p, cfg)
                 calc.refresh(p, cfg)
                 if timed:
                     ev[1].record()
@@ -194,6 +212,9 @@ class Simulation:
                     ev[2].record()
                 break
             except (BlowUpError, KeyboardInterrupt):
+                raise
+            except _StatusFlags as sf:   # raised as the reference raises them, outside the retry
+                self._check_flags(sf.flags)
                 raise
             except Exception as exc:
                 if not ctl.record_failure(exc):

@@ -1,0 +1,54 @@
+"""Per-step device times of the bench loop (config 2, fused kick+drift), to
+see the rebuild step against the steady steps and the launch/sync gaps.
+
+    python tools/step_probe.py
+"""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2505_03438_b200 as P  # noqa: E402
+from paper_2505_03438_b200 import systems  # noqa: E402
+from paper_2505_03438_b200.simulation import Simulation  # noqa: E402
+
+
+def main():
+    pos, vel, params = systems.config2_inputs()
+    parts = P.ParticleSet(pos, vel)
+    systems.relax_on_device(parts, params, P.parse_configuration("LC-SLI-N3L-AoS-CSF1"))
+    cfg = P.parse_configuration("VL-List_Iter-NoN3L-SoA")
+    parts.convert_layout(cfg.layout)
+    sim = Simulation(parts, params, cfg, fuse_kick_drift=True)
+    for _ in range(11):
+        sim.step()
+    torch.cuda.synchronize()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=parts.pos.device)
+    for mode in ("back-to-back", "l2-flushed"):
+        ev = []
+        for k in range(22):
+            if mode == "l2-flushed":
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            sim.step()
+            b.record()
+            ev.append((a, b))
+        torch.cuda.synchronize()
+        ms = [round(a.elapsed_time(b), 4) for a, b in ev]
+        print(json.dumps({"mode": mode, "ms": ms, "mean": round(sum(ms) / len(ms), 4)}))
+    # the same steps with no per-step events: one interval over 22 steps
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for k in range(22):
+        sim.step()
+    b.record()
+    torch.cuda.synchronize()
+    print(json.dumps({"mode": "one interval", "mean": round(a.elapsed_time(b) / 22, 4)}))
+
+
+if __name__ == "__main__":
+    main()

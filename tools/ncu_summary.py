@@ -1,6 +1,9 @@
 """Summarise an `ncu --set full` capture into the text kept under profiles/.
 
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep "title" > profiles/x.txt
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep "title" [launch] > profiles/x.txt
+
+`launch` picks one launch of a multi-launch capture (default 0); the header
+then also lists every launch's duration and DRAM bytes and their mean.
 
 Prints duration, DRAM bytes (the roofline `traffic`), pipe utilisations, L1/L2
 behaviour, occupancy and the top warp-stall reasons by SASS instruction.
@@ -40,16 +43,29 @@ def ncu(rep, *args):
 
 def main():
     rep, title = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else sys.argv[1]
+    li = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     rows = list(csv.reader(io.StringIO(ncu(rep, "--page", "raw", "--csv"))))
-    h, units, v = rows[0], rows[1], rows[2]
+    h, units, v = rows[0], rows[1], rows[2 + li]
     name = v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
     print(f"# {title}")
     print(f"# kernel: {name[:160]}")
+    if len(rows) > 3:
+        def f(r, k):
+            return float(r[h.index(k)].replace(",", ""))
+        per = [(f(r, "gpu__time_duration.sum"), f(r, "dram__bytes_read.sum") + f(r, "dram__bytes_write.sum"))
+               for r in rows[2:]]
+        print(f"# {len(per)} launches (duration {units[h.index('gpu__time_duration.sum')]}, "
+              f"DRAM read+write {units[h.index('dram__bytes_read.sum')]}):")
+        for i, (t, b) in enumerate(per):
+            print(f"#   launch {i}: {t:10.2f} {b:10.2f}")
+        print(f"#   mean:     {sum(t for t, _ in per) / len(per):10.2f} {sum(b for _, b in per) / len(per):10.2f}")
+        print(f"# launch {li} in detail:")
     for k in KEYS:
         if k in h:
             i = h.index(k)
             print(f"{k:70s} {v[i]:>16s} {units[i]}")
-    src = list(csv.reader(io.StringIO(ncu(rep, "--page", "source", "--csv", "--print-source", "sass"))))
+    src = list(csv.reader(io.StringIO(ncu(rep, "--page", "source", "--csv", "--print-source", "sass",
+                                          "--launch-skip", str(li), "--launch-count", "1"))))
     if len(src) > 2:
         sh = src[1]
         si, ws = sh.index("Source"), sh.index("Warp Stall Sampling (All Samples)")

@@ -51,6 +51,40 @@ __global__ void vl_f32_kernel(const double4* __restrict__ s4, int m, float4* __r
     }
 }
 
+// The build positions of every row in one pass: pos[src] + shift (the
+// arithmetic of grid.cu's refresh_kernel, containers.py:356-358) into the grid
+// scratch (fp64 membership tests) and the unwrapped force-time copy s4, and
+// their fp32 copy + max |coordinate| (vl_f32_kernel).
+template <int PLAYOUT>
+__global__ void vl_build_pos_kernel(const double* __restrict__ pos, int64_t n, int m,
+                                    const int* __restrict__ row_src, const uint8_t* __restrict__ row_code,
+                                    const int* __restrict__ row_tid, double L0, double L1, double L2,
+                                    double4* __restrict__ spos4, double4* __restrict__ s4,
+                                    float4* __restrict__ b32, unsigned* __restrict__ maxabs_bits) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    float mx = 0.f;
+    if (r < m) {
+        int src = row_src[r], code = row_code[r];
+        double x = pos[pidx<PLAYOUT>(src, 0, n)] + (double)(code / 9 - 1) * L0;
+        double y = pos[pidx<PLAYOUT>(src, 1, n)] + (double)((code / 3) % 3 - 1) * L1;
+        double z = pos[pidx<PLAYOUT>(src, 2, n)] + (double)(code % 3 - 1) * L2;
+        double4 p = make_double4(x, y, z, (double)row_tid[r]);
+        spos4[r] = p;
+        s4[r] = p;
+        float4 q = make_float4((float)x, (float)y, (float)z, 0.f);
+        b32[r] = q;
+        mx = fmaxf(fabsf(q.x), fmaxf(fabsf(q.y), fabsf(q.z)));
+    }
+    __shared__ float wmax[32];
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, wmax[w]);
+        atomicMax(maxabs_bits, __float_as_uint(mx));
+    }
+}
+
 // Membership r^2 <= ell^2 (non-strict, kernels.py:848), decided in fp32 where
 // provably safe and in fp64 otherwise, so the pair set is exactly the
 // reference's.  Rounding bound for coordinates |x| <= X, |d| ~ ell, u = 2^-24:
@@ -193,7 +227,6 @@ int vl_rebuild(Context& c) {
     v.rows_valid = false;
     if (grid_rebuild(c, gr, c.pos, c.layout)) return -1;
     grid_bind_scratch(c, gr, AOS);
-    grid_refresh(c, gr, AOS);   // build-time positions pos[src] + shift (containers.py:356-358)
     int m = (int)gr.m;
     size_t mpad = ((size_t)m + 31) / 32 * 32;
     v.cnt.ensure(mpad + 1);
@@ -206,16 +239,23 @@ int vl_rebuild(Context& c) {
     }
     unsigned* maxabs = (unsigned*)(c.scal.p + 5);
     v.b32.ensure(mpad + 1);
+    // the unwrapped force-time copy s4 starts from the build positions
+    v.s4.ensure(mpad + 1);
     MDG_CUDA(cudaMemsetAsync(maxabs, 0, sizeof(unsigned), c.stream));
-    if (m > 0)
-        vl_f32_kernel<<<blocks_for(m, 256), 256, 0, c.stream>>>(gr.spos4.p, m, v.b32.p, maxabs), note_launch();
+    if (m > 0) {
+        // build-time positions pos[src] + shift (containers.py:356-358), s4, fp32 copy
+        if (c.layout == AOS)
+            vl_build_pos_kernel<AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(
+                c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_tid.p, c.L[0], c.L[1], c.L[2], gr.spos4.p,
+                v.s4.p, v.b32.p, maxabs), note_launch();
+        else
+            vl_build_pos_kernel<SOA><<<blocks_for(m, 256), 256, 0, c.stream>>>(
+                c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_tid.p, c.L[0], c.L[1], c.L[2], gr.spos4.p,
+                v.s4.p, v.b32.p, maxabs), note_launch();
+    }
     int e = vlt_build(c);               // tile lists (vltile.cu); 1 = not applicable
     if (e < 0) return -1;
     if (e == 1 && vl_build_rows(c, nullptr)) return -1;
-    // the unwrapped force-time copy starts from the build positions
-    v.s4.ensure(mpad + 1);
-    MDG_CUDA(cudaMemcpyAsync(v.s4.p, gr.spos4.p, (size_t)m * sizeof(double4),
-                             cudaMemcpyDeviceToDevice, c.stream));
     v.s3_valid = false;
     MDG_CUDA(cudaGetLastError());
     v.built = true;

@@ -720,7 +720,7 @@ __device__ __forceinline__ void vlt_walk_row(const double* wx, const double* wy,
 // refresh only lets the inner lists run while no owned row has moved
 // (rp - rc) / 2 since they were written), so forces and counts are those of
 // the full walk up to the grouping of the batched reciprocal.
-template <int PLAYOUT, bool MT, int PF, bool KICK, int STAGES, bool PRUNE>
+template <int PLAYOUT, bool MT, int PF, bool KICK, int STAGES, bool PRUNE, bool WRITE>
 __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
     const TileDesc* __restrict__ desc, const int* __restrict__ tbase, int ntiles, int wrows,
     int* __restrict__ next, int ms, int64_t n, int cap4, const double* __restrict__ s3,
@@ -760,6 +760,10 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
     // producer's first tile fetch; the fetch that sees the counter's final
     // value, ntiles + gridDim.x - 1, is the last one, so it may clear the mode)
     const bool whole = !PRUNE || s_mode != 0;
+    // with pruning, two launches per walk: the inner-list walk (WRITE = 0)
+    // and then the prune walk (WRITE = 1); the one whose mode is off returns
+    // here, so neither carries the other's registers
+    if (PRUNE && WRITE != whole) return;
     const uint2* tl = whole ? tl_out : tl_in;
     const int* tcnt = whole ? tcnt_out : tcnt_in;
     const int kBuf = WinLayout<MT>::doubles(wrows);
@@ -772,7 +776,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
             if (lane == 0) t = atomicAdd(next, 1);
             t = __shfl_sync(0xffffffffu, t, 0);
             if (t >= ntiles) {
-                if (PRUNE && whole && lane == 0 && t == ntiles + (int)gridDim.x - 1) {
+                if (PRUNE && WRITE && lane == 0 && t == ntiles + (int)gridDim.x - 1) {
                     pst[0] = 0;   // the inner lists are fresh
                     ++pst[1];
                 }
@@ -859,7 +863,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                     int i = row_src[r];
                     double fx = 0.0, fy = 0.0, fz = 0.0;
                     int pc;
-                    if (PRUNE && whole) {
+                    if (PRUNE && WRITE) {
                         vlt_walk_row<MT, PF, true>(wx, wy, wz, wt, li, c, tl + go, tl_in + go, s_sel, tab, rp2,
                                                    fx, fy, fz, hits, pc);
                         tcnt_in[slot0 + q] = pc;
@@ -1103,14 +1107,14 @@ static int vlt_env_budget() {
     return v;
 }
 
-template <int PLAYOUT, bool MT, int PF, bool KICK, int STAGES, bool PRUNE>
+template <int PLAYOUT, bool MT, int PF, bool KICK, int STAGES, bool PRUNE, bool WRITE>
 static void vlt_launch_st(Context& c, const KickArgs& kick) {
     Verlet& v = c.vl;
     int wrows = v.win_rows;
     size_t smem = STAGES * (size_t)WinLayout<MT>::doubles(wrows) * sizeof(double);
     static int ctas_per_sm = 0;
     static size_t smem_set = 0;
-    auto kern = vlt_force_kernel<PLAYOUT, MT, PF, KICK, STAGES, PRUNE>;
+    auto kern = vlt_force_kernel<PLAYOUT, MT, PF, KICK, STAGES, PRUNE, WRITE>;
     if (smem != smem_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, kern, kTileThreads, smem);
@@ -1128,9 +1132,14 @@ static void vlt_launch_st(Context& c, const KickArgs& kick) {
 
 template <int PLAYOUT, bool MT, int PF, bool KICK>
 static void vlt_launch_pf(Context& c, const KickArgs& kick) {
-    if (PF == 3 && c.vl.prune) vlt_launch_st<PLAYOUT, MT, PF, KICK, 2, true>(c, kick);
-    else if (vlt_env_stages() == 3) vlt_launch_st<PLAYOUT, MT, PF, KICK, 3, false>(c, kick);
-    else vlt_launch_st<PLAYOUT, MT, PF, KICK, 2, false>(c, kick);
+    if (PF == 3 && c.vl.prune) {
+        vlt_launch_st<PLAYOUT, MT, PF, KICK, 2, true, false>(c, kick);   // runs on inner lists
+        vlt_launch_st<PLAYOUT, MT, PF, KICK, 2, true, true>(c, kick);    // runs when a prune is due
+    } else if (vlt_env_stages() == 3) {
+        vlt_launch_st<PLAYOUT, MT, PF, KICK, 3, false, false>(c, kick);
+    } else {
+        vlt_launch_st<PLAYOUT, MT, PF, KICK, 2, false, false>(c, kick);
+    }
 }
 
 static int vlt_env_pf() {

@@ -63,6 +63,9 @@ def workload_config(args, n_gpus):
     return {"workload": "config2: homogeneous LJ liquid, 1,048,576 particles, rho=0.75, "
                         "SD-relaxed, T=0.7, rc=2.5, skin=0.3, dt=0.002, rebuild every 11 steps",
             "n_particles": args.n, "configuration": args.config, "parallelism": "single",
+            "cell_reorder": (f"particle arrays permuted to the Verlet grid's cell order every "
+                             f"{args.reorder} rebuild(s), inside the timed steps; caller order "
+                             "restored by the final flush" if args.reorder else "off"),
             "l2": "flushed between timed steps (256 MB write, untimed)"}
 
 
@@ -174,7 +177,9 @@ def gpu_arm(args, rank, world, dist):
         parts.convert_layout(cfg.layout)
         # kick of step s fused into the drift of step s+1 (bit-identical,
         # tests/test_gpu_parity.py::test_fused_kick_drift_loop_is_bit_identical)
-        sim = Simulation(parts, params, cfg, fuse_kick_drift=True)
+        # the particle arrays kept in cell order (bit-identical forces,
+        # tests/test_gpu_parity.py::test_cell_reorder_is_invisible)
+        sim = Simulation(parts, params, cfg, fuse_kick_drift=True, reorder=args.reorder)
     calc = sim.calc
 
     fp64_peak = _measure_fp64_peak(calc)
@@ -183,6 +188,8 @@ def gpu_arm(args, rank, world, dist):
     for _ in range(args.warmup):
         sim.step()
     sim.check()
+    if hasattr(sim, "warm_reorder"):
+        sim.warm_reorder()
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -208,6 +215,8 @@ def gpu_arm(args, rank, world, dist):
     calc.profile(False)
     clk = clocks.stop()
     total_ms = sum(a.elapsed_time(b) for a, b in step_ms)
+    if os.environ.get("MDG_BENCH_STEPS"):
+        print(json.dumps([round(a.elapsed_time(b), 4) for a, b in step_ms]), file=sys.stderr)
     sim.check()
 
     if dist is not None:
@@ -397,6 +406,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--reorder", type=int, default=_env_int("MDG_BENCH_REORDER", 8),
+                    help="permute the particle arrays to cell order every K-th rebuild (0 = off)")
     ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
                     help="gloo (messages staged on the host) only to smoke-test the N > 1 path "
                          "with several ranks on one GPU; never a performance number")

@@ -183,6 +183,13 @@ int mdg_d2h(mdg_ctx* ctx, void* host, const void* dev, size_t bytes);
  * pipelined host loop waits on an event per chunk). */
 int mdg_d2h_async(mdg_ctx* ctx, void* host, const void* dev, size_t bytes);
 
+/* The particles in the row order of the container `cfg` selects, as of its
+ * last rebuild: order[k] = the particle of the k-th owned row (a permutation
+ * of 0..n-1, written to the DEVICE buffer `order`, n int32).  No reference
+ * counterpart: the device loop uses it to keep the particle arrays in cell
+ * order (Simulation(reorder=...)), restoring the caller's order on flush. */
+int mdg_owned_order(mdg_ctx* ctx, const mdg_config* cfg, int32_t* order);
+
 /* Debug / parity exports (host buffers). */
 /* make_geometry (cells.py:55-67) for csf. */
 int mdg_geometry(mdg_ctx* ctx, double csf, int dims_owned[3], double cell_length[3],

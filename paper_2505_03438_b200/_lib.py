@@ -30,7 +30,7 @@ EXPORTS = (
     "mdg_live_stats", "mdg_compute_kick", "mdg_step_graph", "mdg_host_step", "mdg_host_step_ex",
     "mdg_host_run", "mdg_host_kick_drift_range", "mdg_kick_drift", "mdg_lc_pairs", "mdg_timings",
     "mdg_host_drift_wrap_range_ex", "mdg_d2h_async", "mdg_host_drift_wrap_range", "mdg_host_finish_kick_range",
-    "mdg_set_prune", "mdg_prune_count", "mdg_rebuild_checked",
+    "mdg_set_prune", "mdg_prune_count", "mdg_rebuild_checked", "mdg_owned_order",
 )
 FLAG_BLOWUP, FLAG_THERMO_ZERO = 1, 2
 
@@ -96,6 +96,7 @@ def _declare(L):
         "mdg_timings": (I, [P, I, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
         "mdg_set_prune": (I, [P, D]),
         "mdg_rebuild_checked": (I, [P, CFG, ctypes.POINTER(I)]),
+        "mdg_owned_order": (I, [P, CFG, P]),
         "mdg_prune_count": (I, [P, ctypes.POINTER(I64)]),
         "mdg_host_run": (I, [P, CFG, P, P, P, P, P, P, D, I, D, I, I, I, I, I, ctypes.POINTER(I),
                              ctypes.POINTER(I)]),

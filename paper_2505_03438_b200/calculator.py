@@ -102,7 +102,12 @@ class ForceCalculator:
                       p.type_id if p.ntypes > 1 else None)
 
     # -- the reference protocol ---------------------------------------------
+    # bumped by every call that may rebuild a container (Simulation's cell
+    # reorder checks it: a grid rebuilt on other indexing invalidates its order)
+    generation = 0
+
     def rebuild(self, particles, config):
+        self.generation += 1
         self.bind(particles)
         check(lib().mdg_rebuild(self.ctx.h, ctypes.byref(config_struct(config))), "rebuild")
 
@@ -110,11 +115,20 @@ class ForceCalculator:
         """rebuild() with the loop's status check folded into the rebuild's
         own host synchronisation (mdg_rebuild_checked): returns the status
         bits (then reset); nonzero means the rebuild was abandoned."""
+        self.generation += 1
         self.bind(particles)
         f = ctypes.c_int()
         check(lib().mdg_rebuild_checked(self.ctx.h, ctypes.byref(config_struct(config)),
                                         ctypes.byref(f)), "rebuild")
         return int(f.value)
+
+    def owned_order(self, config):
+        """Device int64 tensor: the particles in the row (cell) order of the
+        container of `config` as of its last rebuild (mdg_owned_order)."""
+        out = torch.empty(self._bound_n, dtype=torch.int32, device=self.ctx.device)
+        check(lib().mdg_owned_order(self.ctx.h, ctypes.byref(config_struct(config)), out.data_ptr()),
+              "owned_order")
+        return out.long()
 
     def refresh(self, particles, config):
         self.bind(particles)
@@ -217,6 +231,7 @@ class ForceCalculator:
     def potential_energy(self, particles, rebuild=True) -> float:
         """Shifted LJ potential energy of the current positions (north_star PE
         output; tests/test_integrator.py:227-247 of the reference)."""
+        self.generation += 1
         self.bind(particles)
         pe = ctypes.c_double()
         check(lib().mdg_potential_energy(self.ctx.h, int(rebuild), ctypes.byref(pe)),

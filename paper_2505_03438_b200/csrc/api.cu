@@ -1004,6 +1004,17 @@ int mdg_get_grid(mdg_ctx* ctx, double csf, int64_t* m, int64_t* ncells, int32_t*
     return cuda_status("mdg_get_grid");
 }
 
+int mdg_owned_order(mdg_ctx* ctx, const mdg_config* cfg, int32_t* order) {
+    CHECK_CTX(ctx);
+    if (int e = validate(cfg)) return e;
+    if (!order) { set_error("null output"); return MDG_EINVAL; }
+    Context& c = ctx->c;
+    Grid& gr = cfg->container == MDG_VL ? c.vl.grid : cfg->container == MDG_VCL ? c.vcl.grid : *grid_for(c, cfg->csf);
+    if (!gr.built || gr.n != c.n) { set_error("grid not built for the bound particles"); return MDG_ESTATE; }
+    if (grid_owned_order(c, gr, order)) return MDG_ECUDA;
+    return cuda_status("mdg_owned_order");
+}
+
 int mdg_potential_energy(mdg_ctx* ctx, int rebuild, double* pe) {
     CHECK_CTX(ctx);
     if (int e = need_system(ctx)) return e;

@@ -484,6 +484,39 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
     return 0;
 }
 
+// ---------------------------------------------------------------- owned order
+
+__global__ void owned_flag_kernel(int m, const uint8_t* __restrict__ row_code, int* __restrict__ flag) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < m) flag[r] = row_code[r] == kNoShift;
+}
+
+__global__ void owned_order_kernel(int m, const uint8_t* __restrict__ row_code,
+                                   const int* __restrict__ row_src, const int* __restrict__ rank,
+                                   int* __restrict__ out) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < m && row_code[r] == kNoShift) out[rank[r]] = row_src[r];
+}
+
+// The particles in the grid's row order (owned rows only): out[k] = the
+// particle of the k-th owned row, a permutation of 0..n-1 (device buffer).
+int grid_owned_order(Context& c, Grid& gr, int* out) {
+    int m = (int)gr.m;
+    if (m == 0) return 0;
+    c.order_tmp.ensure(2 * (size_t)m + 2);
+    if (!c.order_tmp.p) {
+        set_error("out of device memory (owned order)");
+        return -1;
+    }
+    int* flag = c.order_tmp.p;
+    int* rank = c.order_tmp.p + m + 1;
+    owned_flag_kernel<<<blocks_for(m, 256), 256, 0, c.stream>>>(m, gr.row_code.p, flag), note_launch();
+    exclusive_scan_i32(flag, rank, m, nullptr, c.scan_tmp, c.stream);
+    owned_order_kernel<<<blocks_for(m, 256), 256, 0, c.stream>>>(m, gr.row_code.p, gr.row_src.p, rank, out), note_launch();
+    MDG_CUDA(cudaGetLastError());
+    return 0;
+}
+
 // ---------------------------------------------------------------- scratch
 
 void grid_bind_scratch(Context& c, Grid& gr, int layout) {

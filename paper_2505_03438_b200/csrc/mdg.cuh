@@ -183,6 +183,7 @@ struct Context {
     Grid grids[2];             // [0] CSF 1, [1] CSF 0.5
     Verlet vl;
     double prune_delta = -1.0;  // inner-list radius rc + delta (mdg_set_prune); < 0 default, 0 off
+    DBuf<int> order_tmp;        // mdg_owned_order scratch
     Vcl vcl;
     // temperature / thermostat / live statistics (stats.cu)
     PairwiseTree pw_particles, pw_bins;
@@ -236,6 +237,7 @@ int vl_export(Context& c, int64_t* entries, int64_t* noff, int32_t* nbr);
 int vl_energy(Context& c, double* pe);
 void vl_compute32(Context& c);
 int vlt_build(Context& c);
+int grid_owned_order(Context& c, Grid& gr, int* out);
 // completes a deferred tile build (host check, retries, overflow tiles, pruning); -1 = error
 int vlt_finish(Context& c);
 // the next tiled walk re-prunes (an s3 write that bypassed the displacement bound)

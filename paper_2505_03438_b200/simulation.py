@@ -35,7 +35,7 @@ import torch
 
 from ._lib import FLAG_BLOWUP, FLAG_THERMO_ZERO
 from .calculator import ForceCalculator
-from .configuration import enumerate_configurations
+from .configuration import VERLET_LISTS, enumerate_configurations
 
 TRIAL = "trial"
 
@@ -112,7 +112,7 @@ class Simulation:
     anything with the TuningController protocol (tuning.py:200-239)."""
 
     def __init__(self, particles, params, config=None, calculator=None, controller=None,
-                 tuning_interval=None, graphs=False, fuse_kick_drift=False):
+                 tuning_interval=None, graphs=False, fuse_kick_drift=False, reorder=0):
         if controller is None:
             if config is None:
                 raise ValueError("need a configuration or a controller")
@@ -137,6 +137,25 @@ class Simulation:
         # flush; callers of step() who read particles in between call it)
         self.fuse_kick_drift = fuse_kick_drift
         self._kick_due = False
+        # keep the particle arrays in the container's cell order: every
+        # `reorder`-th rebuild outside tuning trials permutes them by the previous grid's
+        # row order (mdg_owned_order), so the refresh gathers, the force
+        # stores and the binning touch memory in order.  flush() restores
+        # the caller's order; the next step re-applies it.  Verlet lists only:
+        # their rows are z-ordered within a cell, so forces are unchanged bit
+        # for bit, while the linked-cell rows follow the particle index (the
+        # reference's stable order) and would sum in another order.  The
+        # particle-order reductions (temperature) do sum in another order.
+        # The ParticleSet's array tensors are replaced (spares are recycled):
+        # hold the ParticleSet, not its tensors, across steps.  0 = off.
+        self.reorder = int(reorder)
+        self._perm = None          # current index -> caller's index
+        self._permuted = False
+        self._perm_gen = None
+        self._rebuilds = 0
+        self._active_cfg = None
+        self._spare = {}           # dtype -> spare arrays for _permute
+        self._iota = self._inv = None
 
     @property
     def config(self):
@@ -155,9 +174,76 @@ class Simulation:
     def _trial(self):
         return getattr(self.controller, "mode", TRIAL) == TRIAL
 
+    # -- cell-order permutation of the particle arrays (reorder) --------------
+    def _permute(self, order):
+        # into spare arrays of the same shape (double buffering: no allocation
+        # once both sets exist, so no cudaMalloc inside a timed loop)
+        p = self.p
+        spare = self._spare
+        for name in ("pos", "vel", "force", "old_force", "type_id"):
+            src = getattr(p, name)
+            dim = 0 if (name == "type_id" or p.layout == "AoS") else 1
+            dst = spare.pop(src.dtype, [])
+            out = None
+            for t in dst:
+                if t.shape == src.shape and t.device == src.device and t is not src:
+                    out = t
+                    break
+            if out is None:
+                out = torch.empty_like(src)
+            else:
+                dst.remove(out)
+            torch.index_select(src, dim, order, out=out)
+            spare.setdefault(src.dtype, dst).append(src)
+            setattr(p, name, out)
+
+    def _reapply_order(self):
+        if self._perm is None or self._permuted:
+            return
+        if self.calc.generation != self._perm_gen:
+            self._perm = None      # a container was rebuilt on the caller's order
+            return
+        self._permute(self._perm)
+        self._permuted = True
+
+    def _restore_order(self):
+        if self._perm is None or not self._permuted:
+            return
+        n = self._perm.numel()
+        if self._iota is None or self._iota.numel() != n or self._iota.device != self._perm.device:
+            self._iota = torch.arange(n, device=self._perm.device)
+            self._inv = torch.empty_like(self._iota)
+        self._inv[self._perm] = self._iota
+        self._permute(self._inv)
+        self._permuted = False
+        self._perm_gen = self.calc.generation
+
+    def warm_reorder(self):
+        """Allocate what the first cell reorder needs (scratch of the order
+        export, the permuted arrays in torch's cache) without changing the
+        order, so a timed loop does not pay the one-time allocations."""
+        cfg = self._active_cfg
+        if not self.reorder or cfg is None or cfg.container != VERLET_LISTS:
+            return
+        self._reapply_order()
+        self.calc.owned_order(cfg)
+        ident = torch.arange(self.p.n, device=self.p.pos.device)
+        self._permute(ident)   # allocates the spare arrays
+        self._permute(ident)
+        self._iota = ident
+        self._inv = torch.empty_like(ident)
+        self._inv[ident] = ident   # the scatter of _restore_order (first use loads its kernel)
+
+    def _reorder(self):
+        order = self.calc.owned_order(self._active_cfg)
+        self._permute(order)
+        self._perm = order if self._perm is None else self._perm.index_select(0, order)
+        self._permuted = True
+
     def step(self, record=False):
         p, params, calc, ctl = self.p, self.params, self.calc, self.controller
         it = self.iteration
+        self._reapply_order()
         if self.graphs and not record and not self._kick_due and self._graph_step(it):
             return False
         if self._kick_due:
@@ -182,6 +268,10 @@ class Simulation:
             if rebuild and it and not checked:
                 self._check_flags()
             timed = record or trial
+            if (rebuild and self.reorder and not trial and self._active_cfg is not None
+                    and self._active_cfg.container == VERLET_LISTS and cfg.container == VERLET_LISTS
+                    and hasattr(calc, "owned_order") and (self._rebuilds - 1) % self.reorder == 0):
+                self._reorder()
             if timed:
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 ev[0].record()
@@ -221,6 +311,8 @@ class Simulation:
                     raise
                 self.active = None
         self.active = cfg.id
+        self._active_cfg = cfg
+        self._rebuilds += int(bool(rebuild))
         self.since = 0 if rebuild else self.since + 1
         phase = it // self.tuning_interval
         if trial:
@@ -257,10 +349,12 @@ class Simulation:
         return True
 
     def flush(self):
-        """Run a deferred kick (fuse_kick_drift), completing the state."""
+        """Run a deferred kick (fuse_kick_drift) and restore the caller's particle
+        order (reorder), completing the state."""
         if self._kick_due:
             self.calc.finish_kick(self.p, self.params.delta_t, self.params.gravity)
             self._kick_due = False
+        self._restore_order()
 
     def run(self, steps, record=True):
         for _ in range(steps):

@@ -988,3 +988,36 @@ def test_pruned_walk_full_size_is_the_full_walk(pkg, config2_snapshot):
         d -= L * np.rint(d / L)
         assert np.linalg.norm(d) / np.linalg.norm(p0) <= FP64_TOL, delta
         assert port.force_rel_error(v1, v0) <= FP64_TOL, delta
+
+
+def test_cell_reorder_is_invisible(pkg, config2_snapshot):
+    """Simulation(reorder=k) keeps the particle arrays in cell order inside the
+    loop and restores the caller's order on flush: 33 config-2 steps with a
+    reorder at every rebuild give the unreordered trajectory bit for bit (VL
+    SoA with the fused kick, VL AoS), across run() boundaries and an outside
+    rebuild (potential_energy) in between, which drops the order; linked
+    cells are left in the caller's order."""
+    P, calc = pkg
+    from paper_2505_03438_b200.simulation import Simulation
+    pos, vel, params = config2_snapshot
+    for cid, fuse in (("VL-List_Iter-NoN3L-SoA", True), ("VL-List_Iter-NoN3L-AoS", False),
+                      ("LC-C08-N3L-AoS-CSF1", False)):
+        cfg = P.parse_configuration(cid)
+        out = []
+        for reorder in (0, 1):
+            parts = P.ParticleSet(pos, vel, layout=cfg.layout)
+            sim = Simulation(parts, params, cfg, fuse_kick_drift=fuse, reorder=reorder)
+            sim.run(12)
+            if reorder and cid.startswith("VL"):
+                assert sim._perm is not None and not sim._permuted
+                assert not torch.equal(sim._perm, torch.arange(parts.n, device=sim._perm.device))
+            elif reorder:   # linked cells keep the reference's index order
+                assert sim._perm is None
+            sim.run(11)
+            if cid.startswith("VL"):
+                sim.calc.potential_energy(parts, rebuild=True)   # a rebuild on the caller's order
+            sim.run(10)
+            sim.check()
+            out.append((parts.numpy("pos"), parts.numpy("vel"), parts.numpy("force")))
+        for a, b in zip(*out):
+            assert np.array_equal(a, b), cid

@@ -5,7 +5,7 @@
 # Outputs in gpurun_out/; summarise with tools/launch_list.py and
 # tools/ncu_summary.py into profiles/.
 set -u
-python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
+MDG_BENCH_STEPS=1 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 22 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launches.log 2>&1

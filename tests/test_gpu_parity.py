@@ -1021,3 +1021,33 @@ def test_cell_reorder_is_invisible(pkg, config2_snapshot):
             out.append((parts.numpy("pos"), parts.numpy("vel"), parts.numpy("force")))
         for a, b in zip(*out):
             assert np.array_equal(a, b), cid
+
+
+def test_warm_reorder_keeps_the_trajectory(pkg, config2_snapshot):
+    """bench.py's warm_reorder(): a cell reorder taken outside the timed loop
+    (arrays permuted, flush path run once, a rebuild forced on the next step)
+    leaves the trajectory within the fp64 bar of the plain loop (the extra
+    rebuild changes list order, so summation order, only)."""
+    P, calc = pkg
+    from paper_2505_03438_b200.simulation import Simulation
+    pos, vel, params = config2_snapshot
+    cfg = P.parse_configuration("VL-List_Iter-NoN3L-SoA")
+    out = []
+    for reorder in (0, 8):
+        parts = P.ParticleSet(pos, vel, layout=cfg.layout)
+        sim = Simulation(parts, params, cfg, fuse_kick_drift=True, reorder=reorder)
+        for _ in range(11):
+            sim.step()
+        sim.check()
+        sim.warm_reorder()
+        for _ in range(22):
+            sim.step()
+        sim.check()
+        if reorder:
+            assert sim._perm is not None and not sim._permuted
+        out.append((parts.numpy("pos"), parts.numpy("vel")))
+    L = params.domain_size
+    d = out[1][0] - out[0][0]
+    d -= L * np.rint(d / L)
+    assert np.linalg.norm(d) / np.linalg.norm(out[0][0]) <= FP64_TOL
+    assert port.force_rel_error(out[1][1], out[0][1]) <= FP64_TOL

@@ -48,10 +48,15 @@ def run(k, cid, a):
         systems.relax_on_device(parts, params, P.parse_configuration("LC-SLI-N3L-AoS-CSF1"))
     cfg = P.parse_configuration(cid)
     parts.convert_layout(cfg.layout)
-    sim = Simulation(parts, params, cfg, fuse_kick_drift=True)
+    # cell-order arrays pay off for inputs in random particle order (configs 2
+    # and 4: uniform random positions); the lattice generators (1, 3, 5) emit
+    # particles in a spatially coherent order already
+    reorder = a.reorder if k in (2, 4) else 0
+    sim = Simulation(parts, params, cfg, fuse_kick_drift=True, reorder=reorder)
     for _ in range(11):
         sim.step()
     sim.check()
+    sim.warm_reorder()
     torch.cuda.synchronize()
     a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a0.record()
@@ -78,10 +83,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3,4,5")
     ap.add_argument("--steps", type=int, default=22)
+    ap.add_argument("--reorder", type=int, default=8,
+                    help="cell-order arrays every K rebuilds for configs 2 and 4 (VL; 0 = off)")
     ap.add_argument("--n5-side", type=int, default=256)
     a = ap.parse_args()
     for k in [int(x) for x in a.configs.split(",")]:
-        cids = ["LC-C08-N3L-SoA-CSF1", "VL-List_Iter-NoN3L-SoA"] if k == 1 else ["VL-List_Iter-NoN3L-SoA"]
+        cids = (["LC-C08-N3L-SoA-CSF1", "VL-List_Iter-NoN3L-SoA"] if k == 1 else
+                ["VL-List_Iter-NoN3L-SoA", "VL-List_Iter-NoN3L-SoA-FP32"] if k == 4 else   # + the fp32 variant
+                ["VL-List_Iter-NoN3L-SoA"])
         for cid in cids:
             try:
                 run(k, cid, a)

@@ -406,7 +406,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--reorder", type=int, default=_env_int("MDG_BENCH_REORDER", 8),
+    ap.add_argument("--reorder", type=int, default=_env_int("MDG_BENCH_REORDER", 16),
                     help="permute the particle arrays to cell order every K-th rebuild (0 = off)")
     ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
                     help="gloo (messages staged on the host) only to smoke-test the N > 1 path "

@@ -24,6 +24,7 @@ port of the numba kernels, oracle/, all host threads) on the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -199,6 +200,7 @@ def gpu_arm(args, rank, world, dist):
     torch.cuda.synchronize()
     launches0 = _lib.lib().mdg_launch_count()
     calc.profile(True)
+    gc.disable()   # no collector pause stalls the host's launches inside the timed steps
     step_ms = []
     for k in range(args.steps):
         flush.zero_()
@@ -210,6 +212,7 @@ def gpu_arm(args, rank, world, dist):
         b.record()
         step_ms.append((a, b))
     torch.cuda.synchronize()
+    gc.enable()
     launches = _lib.lib().mdg_launch_count() - launches0
     kernel_ms, kernel_launches = calc.profile_read()
     calc.profile(False)

@@ -28,33 +28,11 @@ namespace mdg {
 
 // ---------------------------------------------------------------- build
 
-// fp32 copy of the build positions + max |coordinate| (for the filter margin).
-__global__ void vl_f32_kernel(const double4* __restrict__ s4, int m, float4* __restrict__ b32,
-                              unsigned* __restrict__ maxabs_bits) {
-    int r = blockIdx.x * blockDim.x + threadIdx.x;
-    float mx = 0.f;
-    if (r < m) {
-        double4 p = s4[r];
-        float4 q = make_float4((float)p.x, (float)p.y, (float)p.z, 0.f);
-        b32[r] = q;
-        mx = fmaxf(fabsf(q.x), fmaxf(fabsf(q.y), fabsf(q.z)));
-    }
-    // block maximum, then one atomic per block (x >= 0: the bit patterns order
-    // like the values)
-    __shared__ float wmax[32];
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, wmax[w]);
-        atomicMax(maxabs_bits, __float_as_uint(mx));
-    }
-}
-
 // The build positions of every row in one pass: pos[src] + shift (the
 // arithmetic of grid.cu's refresh_kernel, containers.py:356-358) into the grid
 // scratch (fp64 membership tests) and the unwrapped force-time copy s4, and
-// their fp32 copy + max |coordinate| (vl_f32_kernel).
+// their fp32 copy + max |coordinate| (the fp32 filter's margin; a block
+// maximum, then one atomic per block: x >= 0 orders like its bit pattern).
 template <int PLAYOUT>
 __global__ void vl_build_pos_kernel(const double* __restrict__ pos, int64_t n, int m,
                                     const int* __restrict__ row_src, const uint8_t* __restrict__ row_code,

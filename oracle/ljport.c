@@ -400,3 +400,99 @@ void ljp_vl_fill_pairs(const double* pos, const i64* owner, const i64* start,
     vl_pass(pos, owner, start, end, ell2, nx, ny, nz, deltas, nd, olx, oly, olz,
             ohx, ohy, ohz, cursor, nbr, 1);
 }
+
+/*
+ * Brute-force check of selected rows (the reference's O(N^2) test oracle,
+ * tests/conftest.py:22-44 / port.brute_forces), accelerated only by a cell
+ * list of side >= rc so BASELINE-size systems (up to 67 M particles) can be
+ * checked on sampled rows.  ljp_cell_list links every particle into its cell
+ * (head: ncell entries, next: n entries; pos AoS).  ljp_sampled_forces: for
+ * rows[q], q in [q0, q1), the sum over every j != i with minimum-image
+ * (d -= L rint(d/L) on periodic axes, kernels.py:739-757) r2 < rc2 (strict,
+ * kernels.py:40) of the LJ force (kernels.py:41-45, mixing forces.py:12-22),
+ * and the number of such j.  Periodic axes with fewer than 3 cells visit
+ * each cell once.  GIL-free: port.sampled_forces runs row ranges on threads.
+ */
+static void cell_dims(const double* L, double rc, i64* nc, double* cl) {
+    for (int k = 0; k < 3; ++k) {
+        nc[k] = (i64)floor(L[k] / rc);
+        if (nc[k] < 1) nc[k] = 1;
+        cl[k] = L[k] / (double)nc[k];
+    }
+}
+
+static void cell_of(const double* p, const i64* nc, const double* cl, i64* c) {
+    for (int k = 0; k < 3; ++k) {
+        c[k] = (i64)floor(p[k] / cl[k]);
+        if (c[k] < 0) c[k] = 0;
+        if (c[k] >= nc[k]) c[k] = nc[k] - 1;
+    }
+}
+
+void ljp_cell_list(const double* pos, i64 n, const double* L, double rc, i64* head, i64* next) {
+    i64 nc[3];
+    double cl[3];
+    cell_dims(L, rc, nc, cl);
+    for (i64 c = 0; c < nc[0] * nc[1] * nc[2]; ++c) head[c] = -1;
+    for (i64 i = n - 1; i >= 0; --i) {
+        i64 c[3];
+        cell_of(pos + 3 * i, nc, cl, c);
+        i64 f = (c[0] * nc[1] + c[1]) * nc[2] + c[2];
+        next[i] = head[f];
+        head[f] = i;
+    }
+}
+
+void ljp_sampled_forces(const double* pos, const i64* tid, const double* sig2,
+                        const double* eps24, i64 T, const double* L, const i64* per,
+                        double rc, const i64* head, const i64* next, const i64* rows,
+                        i64 q0, i64 q1, double* fout, i64* cout) {
+    i64 nc[3];
+    double cl[3];
+    cell_dims(L, rc, nc, cl);
+    const double rc2 = rc * rc;
+    for (i64 q = q0; q < q1; ++q) {
+        i64 i = rows[q];
+        double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
+        i64 ci[3], lo[3], hi[3];
+        cell_of(pos + 3 * i, nc, cl, ci);
+        for (int k = 0; k < 3; ++k) {
+            if (per[k] && nc[k] < 3) { lo[k] = 0; hi[k] = nc[k] - 1; }
+            else { lo[k] = ci[k] - 1; hi[k] = ci[k] + 1; }
+        }
+        double fx = 0.0, fy = 0.0, fz = 0.0;
+        i64 cnt = 0;
+        for (i64 a = lo[0]; a <= hi[0]; ++a)
+            for (i64 b = lo[1]; b <= hi[1]; ++b)
+                for (i64 e = lo[2]; e <= hi[2]; ++e) {
+                    i64 cc[3] = {a, b, e};
+                    int skip = 0;
+                    for (int k = 0; k < 3; ++k) {
+                        if (cc[k] < 0 || cc[k] >= nc[k]) {
+                            if (!per[k]) { skip = 1; break; }
+                            cc[k] = (cc[k] + nc[k]) % nc[k];
+                        }
+                    }
+                    if (skip) continue;
+                    for (i64 j = head[(cc[0] * nc[1] + cc[1]) * nc[2] + cc[2]]; j >= 0; j = next[j]) {
+                        if (j == i) continue;
+                        double d[3] = {xi - pos[3 * j], yi - pos[3 * j + 1], zi - pos[3 * j + 2]};
+                        for (int k = 0; k < 3; ++k)
+                            if (per[k]) d[k] -= L[k] * rint(d[k] / L[k]);
+                        double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+                        if (r2 < rc2) {
+                            i64 tt = tid ? tid[i] * T + tid[j] : 0;
+                            double fs = lj_scalar(r2, sig2[tt], eps24[tt]);
+                            fx += fs * d[0];
+                            fy += fs * d[1];
+                            fz += fs * d[2];
+                            ++cnt;
+                        }
+                    }
+                }
+        fout[3 * q] = fx;
+        fout[3 * q + 1] = fy;
+        fout[3 * q + 2] = fz;
+        cout[q] = cnt;
+    }
+}

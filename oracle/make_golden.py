@@ -205,6 +205,59 @@ def trajectories():
         print(name, "done")
 
 
+def reflect_gravity_trajectory():
+    """simulate() with reflective walls, gravity and two particle types
+    (integrator.py:47-51 apply_gravity, :98-128 apply_boundaries; masses
+    1 and 2 enter drift, kick and m*g).  Periodic x, reflective y and z; a
+    strong downward g so the bottom layer bounces off the z = 0 wall and
+    fast particles bounce off the y walls inside the run.  The number of
+    reflections the reference applied is recorded (counted by wrapping its
+    apply_boundaries), so the fixture is known to exercise the branch."""
+    ns, steps = 7, 90
+    rng = np.random.default_rng(11)
+    i = (np.arange(ns) + 0.3) * 1.1
+    g = np.stack(np.meshgrid(i, i, i, indexing="ij"), axis=-1).reshape(-1, 3)
+    pos0 = g + rng.uniform(-0.05, 0.05, g.shape)
+    tid = (np.arange(len(pos0)) % 2).astype(np.int64)
+    vel0 = rng.normal(0.0, 1.6, pos0.shape)
+    L = ns * 1.1
+    ids = ["LC-C08-N3L-SoA-CSF1", "LC-C01-NoN3L-AoS-CSF0.5", "LC-SLI-N3L-AoS-CSF1",
+           "LC-C18-NoN3L-SoA-CSF1", "VL-List_Iter-NoN3L-SoA", "VL-List_Iter-NoN3L-AoS"]
+    doc = {"pos0": pos0, "vel0": vel0, "tid": tid, "domain": np.array([L, L, L]),
+           "steps": np.array(steps), "gravity": np.array(-25.0), "dt": np.array(2e-3),
+           "periodic": np.array([True, False, False]), "config_ids": np.array(ids)}
+    saved = _msim.apply_boundaries
+    for k, cid in enumerate(ids):
+        hits = [0]
+
+        def counting(p, params, _orig=saved, _hits=hits):
+            x = p.positions   # (N, 3) view in either layout
+            for ax in (1, 2):
+                _hits[0] += int(np.sum((x[:, ax] < 0.0) | (x[:, ax] > L)))
+            return _orig(p, params)
+
+        params = SimulationParams(domain_size=(L, L, L), cutoff=2.5, skin=0.3, rebuild_interval=6,
+                                  delta_t=2e-3, total_iterations=steps, boundary=(P, R, R),
+                                  gravity=-25.0)
+        p = ParticleSet(pos0.copy(), velocities=vel0.copy(), type_ids=tid.copy(), types=_types(2))
+        _msim.apply_boundaries = counting
+        try:
+            rep = simulate(p, params, FixedStrategy(parse_configuration(cid)),
+                           tuning_interval=10 ** 9, raise_errors=True)
+        finally:
+            _msim.apply_boundaries = saved
+        assert rep.error is None
+        assert hits[0] > 0, "no reflection happened"
+        p.convert_layout("AoS")
+        doc[f"pos_{k}"] = np.ascontiguousarray(p.positions)
+        doc[f"vel_{k}"] = np.ascontiguousarray(p.velocities)
+        doc[f"force_{k}"] = np.ascontiguousarray(p.forces)
+        doc[f"reflections_{k}"] = np.array(hits[0])
+        print(cid, "reflections", hits[0])
+    np.savez_compressed(os.path.join(OUT, "traj_reflect_gravity.npz"), **doc)
+    print("traj_reflect_gravity done")
+
+
 def thermo_and_stats():
     """current_temperature / apply_thermostat (integrator.py:72-95) and
     compute_live_stats (livestats.py:46-77) on seeded inputs."""
@@ -313,6 +366,8 @@ if __name__ == "__main__":
         containers()
     if not only or "trajectories" in only:
         trajectories()
+    if not only or "reflect_gravity" in only:
+        reflect_gravity_trajectory()
     if not only or "thermo_stats" in only:
         thermo_and_stats()
     if not only or "tuned" in only:

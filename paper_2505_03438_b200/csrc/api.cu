@@ -476,8 +476,10 @@ int mdg_compute_kick(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gra
         fuse_env = e ? atoi(e) : 0;
     }
     if (fuse_env && cfg->container == MDG_VL && v.build_pending && vlt_finish(c)) {
+        // the tiled build failed: the row-space lists take over (as in vl_compute)
         v.tiled = false;
         v.prune = false;
+        if (vl_ensure_rows(c)) return cuda_status("mdg_compute_kick: row-space lists");
     }
     bool fuse = fuse_env && cfg->container == MDG_VL && cfg->precision == MDG_FP64 &&
                 c.layout == cfg->layout && v.built && v.tiled && v.nbig == 0 && c.n > 0;
@@ -508,8 +510,10 @@ int mdg_step_graph(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gravi
                : grid_for(c, cfg->csf)->built;
     if (!built) { set_error("mdg_step_graph before rebuild"); return MDG_ESTATE; }
     if (cfg->container == MDG_VL && vlt_finish(c)) {   // no host wait inside a capture
+        // the tiled build failed: build the row-space lists now, outside the capture
         c.vl.tiled = false;
         c.vl.prune = false;
+        if (vl_ensure_rows(c)) return cuda_status("mdg_step_graph: row-space lists");
     }
     if (!c.graph_stream) {
         if (cudaStreamCreateWithFlags(&c.graph_stream, cudaStreamNonBlocking) != cudaSuccess ||

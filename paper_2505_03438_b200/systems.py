@@ -148,3 +148,43 @@ def config5_inputs(n_side=256, density=0.8, seed=0, temperature=0.9, jitter=0.05
     params = SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=10,
                               delta_t=2e-3, total_iterations=1000, boundary=(PERIODIC,) * 3)
     return pos, vel, params
+
+
+def config4_state(equil_steps=1000, quench_steps=4000, seed=0, config="VL-List_Iter-NoN3L-SoA",
+                  interval=10, stats=None):
+    """BASELINE config 4's quench, run on the device: uniform rho = 0.4 ->
+    50 steepest-descent steps -> ``equil_steps`` at T = 1.4 (thermostat every
+    ``interval`` steps, integrator.py:81-95 on the device) -> velocities
+    rescaled to T = 0.7 in one application -> ``quench_steps`` held at
+    T = 0.7.  At rho = 0.4, T = 0.7 the fluid sits inside the LJ liquid-vapour
+    coexistence region (truncated LJ: T_c ~ 1.19, rho_c ~ 0.32), so droplets
+    nucleate and the cell occupancy turns strongly non-uniform (see
+    ``stats``: a list that receives the live statistics (livestats.py:46-77)
+    before and after the quench).  Returns numpy (pos, vel, params)."""
+    from dataclasses import replace
+
+    from .configuration import parse_configuration
+    from .params import ThermostatParams
+    from .particles import ParticleSet
+    from .simulation import Simulation
+    pos, vel, params = config4_inputs(seed=seed)
+    cfg = parse_configuration(config)
+    parts = ParticleSet(pos, vel)
+    del pos, vel
+    relax_on_device(parts, params, parse_configuration("LC-SLI-N3L-AoS-CSF1"))
+    parts.convert_layout(cfg.layout)
+    eq = replace(params, thermostat=ThermostatParams(1.4, 1e9, interval))
+    sim = Simulation(parts, eq, cfg, fuse_kick_drift=True, reorder=8)
+    if stats is not None:
+        stats.append(sim.calc.live_stats(parts))
+    sim.run(equil_steps, record=False)
+    sim.check()
+    sim.calc.thermostat(parts, 0.7, 1e9)            # the quench: one rescale to T = 0.7
+    q = replace(params, thermostat=ThermostatParams(0.7, 1e9, interval))
+    sim = Simulation(parts, q, cfg, fuse_kick_drift=True, reorder=8)
+    sim.run(quench_steps, record=False)
+    sim.check()
+    if stats is not None:
+        stats.append(sim.calc.live_stats(parts))
+    parts.convert_layout("AoS")
+    return parts.numpy("pos"), parts.numpy("vel"), params

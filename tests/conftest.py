@@ -25,6 +25,22 @@ def pytest_configure(config):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
 
 
+@pytest.fixture(scope="session")
+def config2_snapshot():
+    """BASELINE config 2 (1,048,576 particles, rho = 0.75) after its 50
+    steepest-descent steps on the device: the identical seeded input both
+    the GPU path and the oracle consume at full size."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need CUDA")
+    import paper_2505_03438_b200 as P
+    from paper_2505_03438_b200 import systems
+    pos, vel, params = systems.config2_inputs()
+    parts = P.ParticleSet(pos, vel)
+    systems.relax_on_device(parts, params, P.parse_configuration("LC-SLI-N3L-AoS-CSF1"))
+    return parts.numpy("pos"), parts.numpy("vel"), params
+
+
 def golden(name):
     with np.load(os.path.join(GOLDEN, name), allow_pickle=False) as z:
         return {k: z[k] for k in z.files}

@@ -120,6 +120,31 @@ def test_simulate_trajectory_bit_exact(traj):
         assert np.array_equal(np.asarray(p.velocities), z[f"vel_{k}"]), cid
 
 
+def _reflect_gravity_setup(z, cid_layout_obj=None):
+    L = float(z["domain"][0])
+    bnd = tuple(port.PERIODIC if f else port.REFLECTIVE for f in z["periodic"])
+    params = port.Params(domain_size=(L, L, L), cutoff=2.5, skin=0.3, rebuild_interval=6,
+                         delta_t=float(z["dt"]), boundary=bnd, gravity=float(z["gravity"]))
+    # the two types of make_golden._types(2): sigma 1, 0.8; epsilon 1, 1.5; mass 1, 2
+    p = port.Particles(z["pos0"], z["vel0"], type_id=z["tid"], sigma=(1.0, 0.8),
+                       epsilon=(1.0, 1.5), mass=(1.0, 2.0))
+    return params, p
+
+
+def test_reflect_gravity_trajectory_bit_exact():
+    """Reflective walls (y, z) + periodic x, gravity, two types with masses 1
+    and 2 (integrator.py:47-51, :98-128): the oracle's integrator replays the
+    reference's trajectories bit for bit, and the fixture did reflect."""
+    z = golden("traj_reflect_gravity.npz")
+    for k, cid in enumerate(str(s) for s in z["config_ids"]):
+        assert int(z[f"reflections_{k}"]) > 0
+        params, p = _reflect_gravity_setup(z)
+        port.simulate_fixed(p, params, port.parse(cid), steps=int(z["steps"]))
+        assert np.array_equal(np.asarray(p.positions), z[f"pos_{k}"]), cid
+        assert np.array_equal(np.asarray(p.velocities), z[f"vel_{k}"]), cid
+        assert np.array_equal(np.asarray(p.forces), z[f"force_{k}"]), cid
+
+
 # -- thermostat, live statistics, controller-driven loop (SURVEY §8(f)) -------
 
 def test_live_stats_oracle_matches_reference():
@@ -178,3 +203,20 @@ def test_controlled_loop_oracle_matches_reference():
     assert np.array_equal(np.asarray(p.velocities), z["vel"])
     assert np.array_equal(np.asarray(p.forces), z["force"])
     assert port.current_temperature(p) == float(z["final_temperature"])
+
+
+@pytest.mark.parametrize("name", system_names())
+def test_sampled_brute_force_matches_reference(name):
+    """port.sampled_forces (the cell-list brute force used to check the
+    BASELINE-size snapshots on sampled rows) reproduces the reference's forces
+    and its directed within-cutoff count on every golden system."""
+    d = golden(f"sys_{name}.npz")
+    params = _params(d)
+    p = _particles(d)
+    rows = np.arange(p.n)
+    f, cnt = port.sampled_forces(p.positions, rows, params.cutoff, params.domain_size,
+                                 params.periodic_flags(), tid=p.type_id, sigma=p.sigma,
+                                 epsilon=p.epsilon, workers=3)
+    k = [c.id for c in port.all_configs()].index("VL-List_Iter-NoN3L-AoS")
+    assert port.force_rel_error(f, d["forces"][k]) <= 1e-12
+    assert int(cnt.sum()) == int(d["counts"][k])

@@ -620,47 +620,86 @@ struct WinLayout {
 // One tile row's list walk (the consumers' body).  WR: the walk reads the full
 // lists and writes the row's inner list (the entries within rp, in list
 // order, 4 to a group like the outer list) and zeroes the row's path length.
+//
+// Pair arithmetic (kernels.py:36-52 up to rounding): y = 1/r^2 by MUFU.RCP64H
+// plus one Newton step (relative error ~1e-14, three orders of magnitude
+// inside the 1e-10 force bar even where 2 a6 - 1 cancels), then
+//   fs = eps24 s6 y^4 (2 s6 y^3 - 1)   with s6 = sig2^3,
+// i.e. y^2, y^3 = y^2 y, y^4 = y^2 y^2, one DFMA and one DMUL per pair.  For a
+// single type (MT = false) the constant eps24 s6 is factored out of the row's
+// sum (the caller multiplies the three totals once), so a within-cutoff pair
+// costs 17 FP64 instructions: 3 DADD + 3 (r^2) + DSETP + 2 (reciprocal) + 5 + 3
+// accumulating DFMAs, with no branch (the accumulation is predicated).  MT:
+// per-pair sig2 / eps24 lookups (forces.py:12-22).
+template <bool MT>
+__device__ __forceinline__ double lj_fs_walk(double r2, double c1, double& c0) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+    y = fma(y, fma(-r2, y, 1.0), y);
+    double y2 = y * y;
+    double y3 = y2 * y, y4 = y2 * y2;
+    return y4 * fma(c1, y3, -1.0);
+}
+
 template <bool MT, int PF, bool WR>
 __device__ __forceinline__ void vlt_walk_row(const double* wx, const double* wy, const double* wz,
                                              const int* wt, int li, int c, const uint2* lp,
                                              uint2* op, const uint2* sel, const LJTab& tab, double rp2,
-                                             double& fx, double& fy, double& fz, unsigned& hits, int& pc) {
+                                             double c1s, double& fx, double& fy, double& fz,
+                                             unsigned& hits, int& pc) {
     double xi = wx[li], yi = wy[li], zi = wz[li];
     int ti = MT ? wt[li] : 0;
     // the first two entry groups are independent loads: issue them together
     // (every row owns >= 2 groups, cap4 >= 8), then keep the list stream
     // ahead of the walk
-    uint2 g0 = __ldcs(lp), g1 = PF == 2 ? __ldcs(lp + 32) : make_uint2(0u, 0u);
+    // D list groups in flight (a register ring): the group loads come from
+    // L2 (the producer prefetched the tile's lists) and their latency is the
+    // walk's main stall otherwise
+    constexpr int D = (PF == 2 || PF == 4) ? 2 : PF == 5 ? 3 : PF == 6 ? 4 : 1;
+    uint2 g[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) g[q] = (q == 0 || 4 * q < c) ? __ldcs(lp + (size_t)q * 32) : make_uint2(0u, 0u);
     unsigned long long pk = 0;   // the inner group being filled (pc & 3 entries)
     const int rp2_hi = __double2hiint(rp2);
+    const double rc2 = tab.rc2;
     pc = 0;
     for (int k0 = 0; k0 < c; k0 += 4) {
-        uint2 cur = g0;
-        if (PF == 2) {
-            g0 = g1;
-            if (k0 + 8 < c) g1 = __ldcs(lp + (size_t)(k0 / 4 + 2) * 32);
-        } else if (k0 + 4 < c) {
-            g0 = __ldcs(lp + (size_t)(k0 / 4 + 1) * 32);
-        }
+        uint2 cur = g[0];
+#pragma unroll
+        for (int q = 0; q + 1 < D; ++q) g[q] = g[q + 1];
+        if (k0 + 4 * D < c) g[D - 1] = __ldcs(lp + (size_t)(k0 / 4 + D) * 32);
         int jj[4] = {(int)(cur.x & 0xffffu), (int)(cur.x >> 16), (int)(cur.y & 0xffffu),
                      (int)(cur.y >> 16)};
-        double dx[4], dy[4], dz[4], qq[4];
-        int tj[4];
-        bool ok[4];
         unsigned keep = 0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             int j = jj[u];
-            dx[u] = xi - wx[j];
-            dy[u] = yi - wy[j];
-            dz[u] = zi - wz[j];
-            tj[u] = MT ? wt[j] : 0;
-            double r2 = dx[u] * dx[u] + dy[u] * dy[u] + dz[u] * dz[u];
-            ok[u] = (k0 + u < c) && r2 < tab.rc2;
-            qq[u] = ok[u] ? r2 : 1.0;
+            double dx = xi - wx[j];
+            double dy = yi - wy[j];
+            double dz = zi - wz[j];
+            double r2 = dx * dx + dy * dy + dz * dz;
+            bool live = k0 + u < c;
+            bool ok = live && r2 < rc2;
             // r^2 < rp^2 on the high words (non-negative doubles order like
             // their bits; equal high words keep the entry, a harmless superset)
-            if (WR) keep |= (k0 + u < c && __double2hiint(r2) <= rp2_hi) ? 1u << u : 0u;
+            if (WR) keep |= (live && __double2hiint(r2) <= rp2_hi) ? 1u << u : 0u;
+            double c0 = 1.0, c1 = c1s;
+            if (MT) {
+                int tj = wt[j];
+                double s2 = tab.sig2[ti * tab.T + tj];
+                double s6 = s2 * s2 * s2;
+                c1 = 2.0 * s6;
+                c0 = tab.eps24[ti * tab.T + tj] * s6;
+            }
+            double fs = lj_fs_walk<MT>(r2, c1, c0);
+            if (MT) fs *= c0;
+            // straight-line: a rejected (or padding, possibly r^2 = 0) entry
+            // selects 0 before it reaches the sums
+            fs = ok ? fs : 0.0;
+            fx = fma(fs, dx, fx);
+            fy = fma(fs, dy, fy);
+            fz = fma(fs, dz, fz);
+            hits += ok ? 1u : 0u;
         }
         if (WR && keep) {
             // the kept entries of this group, compacted (byte permutes from
@@ -678,25 +717,6 @@ __device__ __forceinline__ void vlt_walk_row(const double* wx, const double* wy,
                 pk = s ? nv >> (64 - s) : 0ull;
             }
             pc += cnt;
-        }
-        // one reciprocal for four pairs (see vl.cu)
-        double p01 = qq[0] * qq[1], p23 = qq[2] * qq[3];
-        double y = fast_rcp(p01 * p23);
-        double y01 = y * p23, y23 = y * p01;
-        double inv[4] = {y01 * qq[1], y01 * qq[0], y23 * qq[3], y23 * qq[2]};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (ok[u]) {
-                double s2, e24;
-                lj_params<MT>(tab, ti, tj[u], s2, e24);
-                double a = s2 * inv[u];
-                double a6 = a * a * a;
-                double fs = (e24 * inv[u]) * (a6 * fma(2.0, a6, -1.0));
-                ++hits;
-                fx = fma(fs, dx[u], fx);
-                fy = fma(fs, dy[u], fy);
-                fz = fma(fs, dz[u], fz);
-            }
         }
     }
     // the last group's unused slots are zero, the padding the walk expects
@@ -766,7 +786,14 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
     if (PRUNE && WRITE != whole) return;
     const uint2* tl = whole ? tl_out : tl_in;
     const int* tcnt = whole ? tcnt_out : tcnt_in;
+    // single type: the window stride is the compile-time kWinRows, so the
+    // y / z gathers use immediate offsets from the x address
+    if (!MT) wrows = kWinRows;
     const int kBuf = WinLayout<MT>::doubles(wrows);
+    // single-type constants of the pair arithmetic (vlt_walk_row): fs =
+    // c0 y^4 (c1 y^3 - 1), c1 = 2 sig2^3, c0 = eps24 sig2^3
+    const double s6 = tab.sig2[0] * tab.sig2[0] * tab.sig2[0];
+    const double c1s = 2.0 * s6, c0s = tab.eps24[0] * s6;
     if (warp == kConsumerWarps) {
         // ---------------- producer
         for (int it = 0;; ++it) {
@@ -815,7 +842,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                     bulk_g2s(wz + o, s3 + 2 * (size_t)ms + g, rows * 8u, &full[b]);
                     if (MT) bulk_g2s(wt + o, row_tid + g, rows * 4u, &full[b]);
                 }
-            } else if (PF == 3) {
+            } else if (PF >= 3) {
                 // the tile's list stream (and counts) into L2 while the window
                 // lands: the consumers' list loads then hit L2 instead of HBM
                 size_t base = (size_t)tbase[t] * cap4;
@@ -865,12 +892,17 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                     int pc;
                     if (PRUNE && WRITE) {
                         vlt_walk_row<MT, PF, true>(wx, wy, wz, wt, li, c, tl + go, tl_in + go, s_sel, tab, rp2,
-                                                   fx, fy, fz, hits, pc);
+                                                   c1s, fx, fy, fz, hits, pc);
                         tcnt_in[slot0 + q] = pc;
                         disp[r] = 0.f;
                     } else {
                         vlt_walk_row<MT, PF, false>(wx, wy, wz, wt, li, c, tl + go, nullptr, s_sel, tab, rp2,
-                                                    fx, fy, fz, hits, pc);
+                                                    c1s, fx, fy, fz, hits, pc);
+                    }
+                    if (!MT) {
+                        fx *= c0s;
+                        fy *= c0s;
+                        fz *= c0s;
                     }
                     if (KICK) {
                         // apply_gravity + finish_kick (integrator.py:40-51), the
@@ -1111,7 +1143,7 @@ template <int PLAYOUT, bool MT, int PF, bool KICK, int STAGES, bool PRUNE, bool 
 static void vlt_launch_st(Context& c, const KickArgs& kick) {
     Verlet& v = c.vl;
     int wrows = v.win_rows;
-    size_t smem = STAGES * (size_t)WinLayout<MT>::doubles(wrows) * sizeof(double);
+    size_t smem = STAGES * (size_t)WinLayout<MT>::doubles(MT ? wrows : kWinRows) * sizeof(double);
     static int ctas_per_sm = 0;
     static size_t smem_set = 0;
     auto kern = vlt_force_kernel<PLAYOUT, MT, PF, KICK, STAGES, PRUNE, WRITE>;
@@ -1132,7 +1164,7 @@ static void vlt_launch_st(Context& c, const KickArgs& kick) {
 
 template <int PLAYOUT, bool MT, int PF, bool KICK>
 static void vlt_launch_pf(Context& c, const KickArgs& kick) {
-    if (PF == 3 && c.vl.prune) {
+    if (PF >= 3 && c.vl.prune) {
         vlt_launch_st<PLAYOUT, MT, PF, KICK, 2, true, false>(c, kick);   // runs on inner lists
         vlt_launch_st<PLAYOUT, MT, PF, KICK, 2, true, true>(c, kick);    // runs when a prune is due
     } else if (vlt_env_stages() == 3) {
@@ -1165,7 +1197,7 @@ static double vlt_prune_delta(const Context& c) {
         const char* d = getenv("MDG_VL_PRUNE_DELTA");
         env_delta = d ? atof(d) : -1.0;
     }
-    if (vlt_env_stages() == 3 || vlt_env_pf() != 3 || c.prune_delta == 0.0) return 0.0;
+    if (vlt_env_stages() == 3 || vlt_env_pf() < 3 || c.prune_delta == 0.0) return 0.0;
     double dl = c.prune_delta > 0.0 ? c.prune_delta : (!on ? 0.0 : env_delta > 0.0 ? env_delta : c.skin / 3.0);
     return dl < c.skin ? dl : 0.0;
 }
@@ -1213,6 +1245,9 @@ static void vlt_launch(Context& c, const KickArgs* kick) {
         else vlt_launch_pf<PLAYOUT, MT, 3, true>(c, *kick);
     } else {
         if (pf == 1) vlt_launch_pf<PLAYOUT, MT, 1, false>(c, none);
+        else if (pf == 4) vlt_launch_pf<PLAYOUT, MT, 4, false>(c, none);
+        else if (pf == 5) vlt_launch_pf<PLAYOUT, MT, 5, false>(c, none);
+        else if (pf == 6) vlt_launch_pf<PLAYOUT, MT, 6, false>(c, none);
         else vlt_launch_pf<PLAYOUT, MT, 3, false>(c, none);
     }
 }

@@ -622,20 +622,23 @@ struct WinLayout {
 // order, 4 to a group like the outer list) and zeroes the row's path length.
 //
 // Pair arithmetic (kernels.py:36-52 up to rounding): y = 1/r^2 by MUFU.RCP64H
-// plus one Newton step (relative error ~1e-14, three orders of magnitude
-// inside the 1e-10 force bar even where 2 a6 - 1 cancels), then
+// plus one cubically convergent correction y (1 + e + e^2) (full double
+// precision; a single Newton step leaves ~1e-14, which the cancellation of
+// 2 a6 - 1 at the LJ minimum turns into a 1.5e-12 force there, above the
+// reference's own 1e-12 bar, tests/test_containers.py:74-80), then
 //   fs = eps24 s6 y^4 (2 s6 y^3 - 1)   with s6 = sig2^3,
 // i.e. y^2, y^3 = y^2 y, y^4 = y^2 y^2, one DFMA and one DMUL per pair.  For a
 // single type (MT = false) the constant eps24 s6 is factored out of the row's
 // sum (the caller multiplies the three totals once), so a within-cutoff pair
-// costs 17 FP64 instructions: 3 DADD + 3 (r^2) + DSETP + 2 (reciprocal) + 5 + 3
+// costs 18 FP64 instructions: 3 DADD + 3 (r^2) + DSETP + 3 (reciprocal) + 5 + 3
 // accumulating DFMAs, with no branch (the accumulation is predicated).  MT:
 // per-pair sig2 / eps24 lookups (forces.py:12-22).
 template <bool MT>
 __device__ __forceinline__ double lj_fs_walk(double r2, double c1, double& c0) {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
-    y = fma(y, fma(-r2, y, 1.0), y);
+    double e = fma(-r2, y, 1.0);
+    y = fma(y, fma(e, e, e), y);
     double y2 = y * y;
     double y3 = y2 * y, y4 = y2 * y2;
     return y4 * fma(c1, y3, -1.0);

@@ -52,4 +52,13 @@ def uninstall() -> None:
 
 
 def pytest_configure(config):   # pragma: no cover - exercised under pytest -p
-    install()
+    config._mdg_installed = install()
+
+
+def pytest_report_header(config):   # pragma: no cover - exercised under pytest -p
+    """The swap, stated in the run's header so a log shows which backend ran."""
+    import torch
+    done = getattr(config, "_mdg_installed", [])
+    dev = torch.cuda.get_device_name(0) if torch.cuda.is_available() else "no CUDA device"
+    return [f"mdg plugin: ForceCalculator -> {HostForceCalculator.__module__}."
+            f"{HostForceCalculator.__name__} in {', '.join(done) or 'nothing'} ({dev})"]

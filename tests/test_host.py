@@ -292,3 +292,28 @@ def test_dataset_columns_match_reference_format():
     assert dataset.evidence_cost(100.0, 1100.0, 10) == 210.0
     with pytest.raises(ValueError):
         dataset.evidence_cost(1.0, 1.0, 0)
+
+
+def test_integration_stub_matches_the_abi_struct():
+    """INTEGRATION.md's ctypes stub declares mdg_config exactly as
+    include/mdg.h and _lib.MdgConfig do (six fields, 32 bytes), so a
+    maintainer copying it hands libmdg the layout it reads."""
+    import ctypes
+    import re
+    from paper_2505_03438_b200 import _lib
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    m = re.search(r"class _Cfg\(ctypes.Structure\):.*?\n(    _fields_ = \[.*?\])\n", text, re.S)
+    assert m, "stub not found"
+    I, D = ctypes.c_int, ctypes.c_double
+    ns = {"I": I, "D": D}
+    exec(m.group(1).strip(), ns)
+    stub = [(n, t) for n, t in ns["_fields_"]]
+    assert stub == list(_lib.MdgConfig._fields_)
+
+    class Stub(ctypes.Structure):
+        _fields_ = stub
+    assert ctypes.sizeof(Stub) == ctypes.sizeof(_lib.MdgConfig) == 32
+    hdr = open(os.path.join(ROOT, "include", "mdg.h")).read()
+    body = re.search(r"typedef struct \{(.*?)\} mdg_config;", hdr, re.S).group(1)
+    names = re.findall(r"(?:int|double)\s+(\w+);", body)
+    assert names == [n for n, _ in stub]

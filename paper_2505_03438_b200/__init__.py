@@ -13,7 +13,7 @@ Public surface mirrors the reference's names on this path:
 from .configuration import (C01, C08, C18, CELL_TRAVERSALS, CLUSTER_ITER, CSF_VALUES, LINKED_CELLS,
                             LIST_ITER, SLI, VERLET_CLUSTER_LISTS, VERLET_LISTS, Configuration,
                             configuration_index,
-                            enumerate_configurations, extended_configurations,
+                            enumerate_configurations, extended_configurations, tuning_space,
                             parse_configuration)
 from .params import PERIODIC, REFLECTIVE, SimulationParams, ThermostatParams
 from .particles import AOS, SOA, ParticleSet, ParticleTypeInfo
@@ -22,7 +22,7 @@ __all__ = [
     "AOS", "SOA", "C01", "C08", "C18", "SLI", "LIST_ITER", "CLUSTER_ITER", "LINKED_CELLS",
     "VERLET_LISTS", "VERLET_CLUSTER_LISTS",
     "CELL_TRAVERSALS", "CSF_VALUES", "PERIODIC", "REFLECTIVE", "Configuration",
-    "enumerate_configurations", "extended_configurations", "parse_configuration", "configuration_index",
+    "enumerate_configurations", "extended_configurations", "tuning_space", "parse_configuration", "configuration_index",
     "SimulationParams", "ThermostatParams", "ParticleSet", "ParticleTypeInfo",
     "ForceCalculator", "HostForceCalculator", "compute_forces", "Timings", "simulate",
     "Simulation", "BlowUpError",

@@ -132,3 +132,28 @@ def generate_training_dataset(out_path, points, *, space=None,
             if progress:
                 progress(k, row[-1])
     return rows
+
+
+# -- GPU-labelled tuning artefacts (tools/gpu_training.py) ----------------------
+
+import os as _os
+
+DATA_DIR = _os.path.join(_os.path.dirname(_os.path.abspath(__file__)), "data")
+GPU_TRAINING_CSV = _os.path.join(DATA_DIR, "gpu_training.csv")
+GPU_FOREST = _os.path.join(DATA_DIR, "gpu_forest.json")
+GPU_RULES = _os.path.join(DATA_DIR, "gpu_rules.txt")
+
+
+def gpu_rules_text() -> str:
+    """The rule file distilled from the device-timed sweep of the reference's
+    roster, in the reference's grammar: pass it to mdtune's
+    ``parse_rule_file(text, tuning_space())`` and ``ExpertStrategy``."""
+    with open(GPU_RULES) as fh:
+        return fh.read()
+
+
+def load_gpu_forest():
+    """The forest the reference's trainer built from GPU labels
+    (``mdtune.forest.load_forest``; needs the reference package)."""
+    from mdtune.forest import load_forest
+    return load_forest(GPU_FOREST)

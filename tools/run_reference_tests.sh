@@ -12,7 +12,7 @@ mkdir -p "$(dirname "$OUT")"
 cd "$ROOT/baseline/_ref/ref_tests"
 export PYTHONPATH="$ROOT/baseline/_ref:$ROOT"
 export NUMBA_CACHE_DIR=/tmp/mdg_numba_cache
-python -m pytest -p paper_2505_03438_b200.plugin -p no:cacheprovider --rootdir . -q -rA \
+python -m pytest -p paper_2505_03438_b200.plugin -p no:cacheprovider --rootdir . -rA \
     test_containers.py test_simulation.py test_integrator.py test_dataset.py \
     "test_acceptance.py::test_criterion_1_forces_match_oracle_on_random_scenarios" \
     "test_acceptance.py::test_criterion_2_search_space_has_exactly_the_valid_30" \

@@ -1,24 +1,33 @@
-"""Benchmark of the LJ force + neighbour path on BASELINE config 2.
+"""Benchmark of the LJ force + neighbour path on the BASELINE configurations.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mdg|reference]
-                    [--config ID] [--n N]
+                    [--workload config2|config3|config4|config5] [--config ID]
+                    [--tune none|predictive|fullsearch]
 
-Workload (BASELINE.json configs[1], the configuration the metric is quoted
-on): 1,048,576 LJ particles, uniform random at rho = 0.75 in a periodic cube
-(side 111.82 sigma), overlaps relaxed by 50 capped steepest-descent steps,
-Maxwell-Boltzmann T = 0.7, r_c = 2.5, skin 0.3, dt = 0.002, rebuild every
-R+1 = 11 steps (reference cadence with R = 10), fp64.  Seeded synthetic data.
+N = 1 (default): BASELINE.json configs[1] (the configuration the metric is
+quoted on): 1,048,576 LJ particles, uniform random at rho = 0.75 in a periodic
+cube (side 111.82 sigma), overlaps relaxed by 50 capped steepest-descent
+steps, Maxwell-Boltzmann T = 0.7, r_c = 2.5, skin 0.3, dt = 0.002, rebuild
+every R+1 = 11 steps (reference cadence with R = 10), fp64, 1,000 steps.
+
+N > 1 (torchrun, one rank per GPU): the north_star's decomposed
+configuration 5 -- 67,108,864 particles on a jittered FCC lattice -- strong
+scaled over a 2x1x1 / 2x2x1 / 2x2x2 process grid (configs 2-4 run as z-slabs
+with --workload); ghost positions packed by libmdg and exchanged point to
+point every step, migration every rebuild; ``--tune predictive`` gives every
+rank its own reference TuningController fed by that rank's device timings.
 
 A *step* is one full MD iteration of the reference loop (drift + boundaries,
 rebuild when due, refresh, force, kick).  ``value`` = MUPS (particle updates
-per second) over all ranks with state resident in HBM; ``e2e`` = the same
-metric through the reference-facing host drop-in (HostForceCalculator driving
-the reference-shaped simulate loop on host numpy arrays, positions H2D and
-forces D2H every step).  The L2 (126 MB) is flushed between timed steps by
-writing a 256 MB buffer outside the timed events.
+per second) of the whole system, state resident in HBM, time = max over
+ranks; ``e2e`` (N = 1) = the same metric through the reference-facing host
+drop-in (state in pinned host arrays, positions H2D and forces D2H every
+step).  The L2 (126 MB) is flushed between timed steps by writing a 256 MB
+buffer outside the timed events.
 
 --impl reference times the reference algorithm on the host CPU (the oracle
-port of the numba kernels, oracle/, all host threads) on the same workload.
+port of the numba kernels, oracle/, all host threads) on the same workload
+(a bounded sample of it for configs 4 and 5).
 """
 
 from __future__ import annotations
@@ -51,55 +60,109 @@ def _env_int(name, default):
         return default
 
 
+WORKLOADS = {
+    "config2": "config2: homogeneous LJ liquid, 1,048,576 particles, rho=0.75, SD-relaxed, T=0.7, "
+               "rc=2.5, skin=0.3, dt=0.002, rebuild every 11 steps",
+    "config3": "config3: FCC slab (rho=0.8) + vacuum, 2,097,152 particles, 128 x 128 x 640, "
+               "T=2.0 + linear z ramp, rc=2.5, skin=0.3, dt=0.001, rebuild every 11 steps",
+    "config4": "config4: LJ fluid at rho=0.4, 4,194,304 particles, SD-relaxed, equilibrated at "
+               "T=1.4 then quenched to T=0.7 (droplets), rc=2.5, skin=0.3, dt=0.002",
+    "config5": "config5: FCC 256^3 cells, 67,108,864 particles, rho=0.8, jittered, T=0.9, rc=2.5, "
+               "skin=0.3, dt=0.002, rebuild every 11 steps",
+}
+
+
+DATA = {"config2": "uniform + 50 steepest-descent steps",
+        "config3": "FCC slab sites + jitter",
+        "config4": "uniform + steepest descent + T=1.4 equilibration + quench to T=0.7 on the device",
+        "config5": "jittered FCC lattice"}
+
+
+def default_workload(world):
+    """N = 1: BASELINE configs[1] (the metric's single-GPU configuration);
+    N > 1: the north_star's decomposed configuration 5, strong-scaled."""
+    return "config2" if world == 1 else "config5"
+
+
+def grid_dims(workload, world):
+    """Process grid: config 5 as a 3-D grid (2x1x1, 2x2x1, 2x2x2 at 2/4/8),
+    configs 2-4 as z-slabs."""
+    if workload == "config5":
+        table = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+        if world in table:
+            return table[world]
+        f = [1, 1, 1]
+        n, q, k = world, 2, 0
+        while n > 1:
+            while n % q == 0:
+                f[k % 3] *= q
+                n //= q
+                k += 1
+            q += 1
+        return tuple(f)
+    return (1, 1, world)
+
+
 def workload_config(args, n_gpus):
+    out = {"workload": WORKLOADS[args.workload], "n_particles": args.n_total,
+           "configuration": args.config}
     if n_gpus > 1:
-        return {"workload": f"config2 boxes stacked along z: {n_gpus} x {args.n:,} particles in one "
-                            f"periodic box L x L x {n_gpus}L (rho=0.75, SD-relaxed, T=0.7, rc=2.5, "
-                            "skin=0.3, dt=0.002, rebuild every 11 steps)",
-                "n_particles": args.n * n_gpus, "n_particles_per_gpu": args.n,
-                "configuration": args.config,
-                "parallelism": f"zslab{n_gpus}: domain decomposition, ghost positions over NCCL "
-                               "every step, migration at rebuilds",
-                "l2": "flushed between timed steps (256 MB write, untimed)"}
-    return {"workload": "config2: homogeneous LJ liquid, 1,048,576 particles, rho=0.75, "
-                        "SD-relaxed, T=0.7, rc=2.5, skin=0.3, dt=0.002, rebuild every 11 steps",
-            "n_particles": args.n, "configuration": args.config, "parallelism": "single",
-            "cell_reorder": (f"particle arrays permuted to the Verlet grid's cell order every "
-                             f"{args.reorder} rebuild(s), inside the timed steps; caller order "
-                             "restored by the final flush" if args.reorder else "off"),
-            "l2": "flushed between timed steps (256 MB write, untimed)"}
+        dims = grid_dims(args.workload, n_gpus)
+        out.update({"decomposition": "x".join(str(d) for d in dims),
+                    "parallelism": f"domain decomposition {'x'.join(str(d) for d in dims)} over "
+                                   f"{n_gpus} GPUs (one rank per GPU): ghost positions packed by libmdg "
+                                   "and exchanged point to point every step, migration at rebuilds, "
+                                   "strong scaling (the whole system fixed)",
+                    "tuning": args.tune})
+    else:
+        out["parallelism"] = "single"
+        out["cell_reorder"] = (f"particle arrays permuted to the Verlet grid's cell order every "
+                               f"{args.reorder} rebuild(s), inside the timed steps; caller order "
+                               "restored by the final flush" if args.reorder else "off")
+    out["l2"] = "flushed between timed steps (256 MB write, untimed)"
+    return out
 
 
 class ClockSampler:
-    """SM clock + clock-event (throttle) reasons sampled every few ms during the
-    timed region through NVML (the same counters nvidia-smi reports; one
-    nvidia-smi call takes longer than the whole timed region)."""
+    """SM clock + clock-event (throttle) reasons sampled every millisecond
+    during the timed region through NVML (the counters nvidia-smi reports;
+    one nvidia-smi call takes longer than a short timed region).  NVML is
+    initialised before the timed region starts, so the first sample lands at
+    its start; the main thread waits in CUDA calls (GIL released)."""
 
-    def __init__(self, gpu_index, period_s=0.005):
+    def __init__(self, gpu_index, period_s=0.001):
         self.idx = gpu_index
         self.period = period_s
         self.rows = []
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.idx)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self._bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                          "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                          "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                          "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
+                          "hw_power_brake": nv.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+            self._nv = nv
+        except Exception as exc:   # no NVML: record why instead of failing the bench
+            self.error = f"{type(exc).__name__}: {exc}"
+            return
+
         def run():
+            nv, h = self._nv, self._h
             try:
-                import pynvml as nv
-                nv.nvmlInit()
-                h = nv.nvmlDeviceGetHandleByIndex(self.idx)
-                self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-                bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
-                        "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
-                        "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
-                        "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
-                        "hw_power_brake": nv.nvmlClocksEventReasonHwPowerBrakeSlowdown}
                 while not self._stop.is_set():
                     mhz = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                     rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    self.rows.append((mhz, [k for k, b in bits.items() if rs & b]))
+                    self.rows.append((mhz, [k for k, b in self._bits.items() if rs & b]))
                     self._stop.wait(self.period)
-            except Exception as exc:   # no NVML: record why instead of failing the bench
+            except Exception as exc:
                 self.error = f"{type(exc).__name__}: {exc}"
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
@@ -112,7 +175,7 @@ class ClockSampler:
         reasons = sorted({x for r in self.rows for x in r[1]})
         out = {"sm_mhz": statistics.median(sm) if sm else None,
                "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": reasons,
-               "samples": len(self.rows), "source": "NVML, 5 ms period, timed region only"}
+               "samples": len(self.rows), "source": "NVML, 1 ms period, timed region only"}
         if getattr(self, "error", None):
             out["error"] = self.error
         return out
@@ -120,41 +183,95 @@ class ClockSampler:
 
 # --------------------------------------------------------------------- GPU arm
 
-def build_system(args, rank):
+def global_inputs(args, on_device=True):
+    """Seeded inputs of the workload as numpy (pos, vel, params); configs 2 and
+    4 are relaxed (and 4 quenched) on the current GPU."""
     import paper_2505_03438_b200 as P
     from paper_2505_03438_b200 import systems
-    pos, vel, params = systems.config2_inputs(n=args.n, seed=args.seed + rank)
-    parts = P.ParticleSet(pos, vel)
-    relax_cfg = P.parse_configuration("LC-SLI-N3L-AoS-CSF1")
-    systems.relax_on_device(parts, params, relax_cfg)
-    return parts, params
+    w = args.workload
+    if w == "config2":
+        pos, vel, params = systems.config2_inputs(n=args.n, seed=args.seed)
+        parts = P.ParticleSet(pos, vel)
+        systems.relax_on_device(parts, params, P.parse_configuration("LC-SLI-N3L-AoS-CSF1"))
+        return parts.numpy("pos"), parts.numpy("vel"), params
+    if w == "config3":
+        return systems.config3_inputs()
+    if w == "config4":
+        return systems.config4_state(equil_steps=args.quench // 2, quench_steps=args.quench)
+    return systems.config5_inputs(n_side=args.n5_side)
 
 
-def build_decomposed(args, rank, world, cfg):
-    """N > 1: one config-2 box per rank, stacked along z into one periodic
-    system of N x n particles, z-slab decomposed.  Every rank
-    relaxes the same seeded box, so the interfaces between slabs are as
-    relaxed as the box's own periodic faces; velocities are drawn per rank."""
-    import numpy as np
+def build_system(args, rank):
+    import paper_2505_03438_b200 as P
+    pos, vel, params = global_inputs(args)
+    args.n_total = len(pos)
+    return P.ParticleSet(pos, vel), params
+
+
+def build_decomposed(args, rank, world, cfg, dist):
+    """N > 1: the whole system of the workload, strong-scaled over a process
+    grid (grid_dims).  Configs 3 and 5 are generated identically by every rank
+    (seeded numpy); configs 2 and 4 are relaxed / quenched on rank 0's GPU and
+    broadcast.  Each rank keeps the particles of its subdomain."""
     import torch
 
     import paper_2505_03438_b200 as P
     from paper_2505_03438_b200.decomp import DeviceDecomposedSimulation, GridDecomposition
-    parts, params = build_system(args, 0)
-    L = np.asarray(params.domain_size, dtype=np.float64)
-    rng = np.random.default_rng(args.seed + 7919 * (rank + 1))
-    vel = rng.normal(0.0, np.sqrt(0.7), (args.n, 3))
-    vel -= vel.mean(0)
-    pos = parts.view("pos").clone()
-    pos[:, 2] += rank * L[2]
-    gparams = P.SimulationParams(domain_size=(L[0], L[1], world * L[2]), cutoff=params.cutoff,
-                                 skin=params.skin, rebuild_interval=params.rebuild_interval,
-                                 delta_t=params.delta_t, boundary=params.boundary)
-    dec = GridDecomposition(gparams, rank, world, (1, 1, world))
-    owned = P.ParticleSet(pos, torch.as_tensor(vel), device=parts.device)
-    ids = torch.arange(args.n, device=parts.device) + rank * args.n
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if args.workload in ("config2", "config4"):
+        cd = "cpu" if args.dist_backend == "gloo" else dev
+        if rank == 0:
+            pos, vel, params = global_inputs(args)
+            meta = torch.tensor([len(pos), *params.domain_size], dtype=torch.float64)
+        else:
+            meta = torch.zeros(4, dtype=torch.float64)
+        meta = meta.to(cd)
+        dist.broadcast(meta, 0)
+        n = int(meta[0].item())
+        buf = (torch.as_tensor(np.concatenate([pos, vel], 1)) if rank == 0
+               else torch.empty((n, 6), dtype=torch.float64)).to(cd)
+        dist.broadcast(buf, 0)
+        buf = buf.cpu().numpy()
+        pos, vel = buf[:, :3], buf[:, 3:]
+        # configs 2 and 4 share their parameters (systems.config2_inputs /
+        # config4_inputs); the box is rank 0's
+        params = P.SimulationParams(domain_size=meta[1:].cpu().numpy().astype(np.float64), cutoff=2.5,
+                                    skin=0.3, rebuild_interval=10, delta_t=2e-3,
+                                    boundary=(P.PERIODIC,) * 3)
+    else:
+        pos, vel, params = global_inputs(args)
+    args.n_total = len(pos)
+    dims = grid_dims(args.workload, world)
+    dec = GridDecomposition(params, rank, world, dims)
+    mine = np.flatnonzero(dec.owner_of_positions(pos) == rank)
+    owned = P.ParticleSet(pos[mine], vel[mine], device=dev)
+    ids = torch.as_tensor(mine, device=dev)
+    controller = None
+    if args.tune != "none":
+        controller = _rank_controller(args, cfg)
     comm = "cpu" if args.dist_backend == "gloo" else None
-    return DeviceDecomposedSimulation(dec, owned, gparams, cfg, ids=ids, comm_device=comm), gparams
+    sim = DeviceDecomposedSimulation(dec, owned, params, cfg, ids=ids, comm_device=comm,
+                                     controller=controller)
+    if controller is not None:
+        controller.stats_provider = lambda: sim.calc.live_stats(sim.ps)
+    return sim, params
+
+
+def _rank_controller(args, cfg):
+    """One reference TuningController per rank, fed by this
+    rank's device timings; needs the staged reference (baseline/_ref)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(ref) and ref not in sys.path:
+        sys.path.append(ref)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/mdg_numba_cache")
+    from mdtune import tuning
+
+    import paper_2505_03438_b200 as P
+    strategy = {"predictive": tuning.PredictiveStrategy, "fullsearch": tuning.FullSearchStrategy}[args.tune]()
+    total = args.warmup + args.steps
+    return tuning.TuningController(P.enumerate_configurations(), strategy, samples_per_config=2,
+                                   tuning_interval=max(70, total // 2), rebuild_interval=10,
+                                   total_iterations=total)
 
 
 def gpu_arm(args, rank, world, dist):
@@ -169,7 +286,7 @@ def gpu_arm(args, rank, world, dist):
     dev = torch.device("cuda", local)
     cfg = P.parse_configuration(args.config)
     if world > 1:
-        sim, params = build_decomposed(args, rank, world, cfg)
+        sim, params = build_decomposed(args, rank, world, cfg, dist)
         host_pos = host_vel = None
     else:
         parts, params = build_system(args, rank)
@@ -234,7 +351,7 @@ def gpu_arm(args, rank, world, dist):
     if rank != 0:
         return None
     ms_per_step = total_ms / args.steps
-    value = args.n * world * args.steps / (total_ms * 1e-3) / 1e6
+    value = args.n_total * args.steps / (total_ms * 1e-3) / 1e6
     avg_kernel_ms = kernel_ms / max(kernel_launches, 1)
     achieved = FLOPS_PER_PAIR * pairs / (avg_kernel_ms * 1e-3) / 1e12
     roofline = {"bound": "fp64", "achieved": round(achieved, 3), "peak": round(fp64_peak, 2),
@@ -248,16 +365,39 @@ def gpu_arm(args, rank, world, dist):
                 "kernel_share_of_step": round(kernel_ms / total_ms, 3)}
     out = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (seeded uniform + steepest-descent relaxation, BASELINE config 2)",
+           "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+           "vs_baseline": None, "dtype": "f64",
+           "data": f"synthetic, seeded ({args.workload}: {DATA[args.workload]})",
            "config": workload_config(args, world), "roofline": roofline,
            "pair_interactions_per_s": round(pairs / (avg_kernel_ms * 1e-3), 1),
            "gpu_launches": int(launches), "clocks": clk}
-    if world == 1 and not args.no_e2e:
+    if world == 1 and not args.no_e2e and args.workload == "config2":
         out["e2e"] = e2e_arm(args, host_pos, host_vel, params)
-    if world == 1 and not args.no_cpu:
+    if world == 1 and not args.no_cpu and args.workload == "config2":
         out["cpu_baseline"] = cpu_baseline(args, host_pos, host_vel, params)
+    if world > 1:
+        out["e2e"] = None
+        out["e2e_note"] = ("the host-array drop-in path (HostForceCalculator, mdg_host_run) is a "
+                           "single-process API; N > 1 runs keep the state resident on each rank")
+        out["comm"] = comm_info(args, world)
+        if args.tune != "none":
+            out["tuning_trials"] = len(sim.trial_log)
+            out["phase_selections"] = list(getattr(sim.controller, "phase_selections", []))
     return out
+
+
+def comm_info(args, world):
+    """The communicator the decomposed run used (NCCL version, ranks, process
+    grid), so the line shows the multi-rank data path that ran."""
+    import torch
+    info = {"backend": args.dist_backend, "ranks": world,
+            "process_grid": "x".join(str(d) for d in grid_dims(args.workload, world))}
+    try:
+        v = torch.cuda.nccl.version()
+        info["nccl_version"] = ".".join(str(x) for x in v) if isinstance(v, tuple) else str(v)
+    except Exception as exc:   # pragma: no cover
+        info["nccl_version"] = f"unavailable: {exc}"
+    return info
 
 
 def _measure_fp64_peak(calc):
@@ -350,13 +490,29 @@ def cpu_baseline(args, host_pos, host_vel, params):
         np.copyto(p.view("old_force"), p.view("force"))
         port.finish_kick(p, pp.delta_t)
         ti = time.perf_counter() - a
-    step = min(tf) + min(tr) + ti + (t1 - t0) / (params.rebuild_interval + 1)
+        step = min(tf) + min(tr) + ti + (t1 - t0) / (params.rebuild_interval + 1)
+        # the GPU arm's own configuration on the same snapshot (like-for-like)
+        same = port.parse(args.config)
+        p.convert_layout(same.layout)
+        s0 = time.perf_counter()
+        calc.rebuild(p, same)
+        s1 = time.perf_counter()
+        calc.refresh(p, same)
+        b = time.perf_counter()
+        calc.compute(p, same, pool)
+        tfs = time.perf_counter() - b
+    step_same = tfs + ti + (s1 - s0) / (params.rebuild_interval + 1)
     return {"value": round(len(host_pos) / step / 1e6, 4), "unit": UNIT, "cores": threads,
             "kind": "port", "config": CPU_CONFIG,
             "sample": f"1 rebuild + 2 refresh/force + 1 integrator pass on the relaxed {len(host_pos):,}-"
-                      f"particle snapshot ({threads} threads; rebuild amortised over 11 steps)",
+                      f"particle snapshot the GPU arm starts from ({threads} threads; rebuild amortised "
+                      "over 11 steps); the fastest reference CPU configuration",
             "force_s": round(min(tf), 4), "rebuild_s": round(t1 - t0, 4),
-            "integrator_s": round(ti, 4)}
+            "integrator_s": round(ti, 4),
+            "same_config": {"configuration": args.config, "value": round(len(host_pos) / step_same / 1e6, 4),
+                            "force_s": round(tfs, 4), "rebuild_s": round(s1 - s0, 4),
+                            "sample": "the GPU arm's configuration on the same snapshot: 1 rebuild + "
+                                      "1 force + the integrator pass"}}
 
 
 # --------------------------------------------------------------- reference arm
@@ -369,28 +525,43 @@ def reference_arm(args):
     from paper_2505_03438_b200 import systems
     threads = _cpu_threads()
     cfg = port.parse(CPU_CONFIG)
-    pos, vel, params = systems.config2_inputs(n=args.n, seed=args.seed)
+    w = args.workload
+    relax = w in ("config2", "config4")
+    if w == "config2":
+        pos, vel, params = systems.config2_inputs(n=args.n, seed=args.seed)
+        what = f"the {len(pos):,}-particle config-2 system"
+    elif w == "config3":
+        pos, vel, params = systems.config3_inputs()
+        what = "the 2,097,152-particle config-3 slab"
+    elif w == "config4":   # bounded sample: a 1/16 box at the same density (relaxed, not quenched)
+        pos, vel, params = systems.config4_inputs(n=262_144)
+        what = "a 262,144-particle box at config 4's density (rho = 0.4; relaxed, not quenched)"
+    else:                  # bounded sample: a 64^3-cell block of the same lattice, density and T
+        pos, vel, params = systems.config5_inputs(n_side=64)
+        what = "a 64^3-cell (1,048,576-particle) periodic block of config 5's FCC lattice (rho = 0.8, T = 0.9)"
     per = tuple(port.PERIODIC if f else port.REFLECTIVE for f in params.periodic_flags())
     pp = port.Params(domain_size=params.domain_size, cutoff=params.cutoff, skin=params.skin,
                      rebuild_interval=params.rebuild_interval, delta_t=params.delta_t,
                      boundary=per, thread_count=threads)
     p = port.Particles(pos, vel)
+    n = len(pos)
     with port.Pool(threads) as pool:
-        port.sd_relax(p, pp, cfg, systems.SD_STEPS, systems.SD_GAMMA, systems.SD_MAX_DISP, pool)
+        if relax:
+            port.sd_relax(p, pp, cfg, systems.SD_STEPS, systems.SD_GAMMA, systems.SD_MAX_DISP, pool)
         steps = max(1, min(args.steps, 11))
         warm = max(0, min(args.warmup, 1))
         port.simulate_fixed(p, pp, cfg, steps=warm, pool=pool)
         t0 = time.perf_counter()
         port.simulate_fixed(p, pp, cfg, steps=steps, pool=pool)
         dt = time.perf_counter() - t0
-    value = args.n * steps / dt / 1e6
-    sample = (f"{steps} full MD steps (one rebuild window of 11) of the {args.n:,}-particle "
-              f"system after {warm} warm-up step(s); {threads} host threads; {CPU_CONFIG}")
+    value = n * steps / dt / 1e6
+    sample = (f"{steps} full MD steps (one rebuild window of 11) of {what} after {warm} warm-up "
+              f"step(s); {threads} host threads; {CPU_CONFIG}")
     return {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "impl": "reference",
             "n_gpus": 1, "steps": steps, "warmup": warm, "ms_per_step": round(dt / steps * 1e3, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded uniform + steepest-descent relaxation, BASELINE config 2)",
-            "config": {"workload": "config2 (see GPU arm)", "n_particles": args.n,
+            "data": f"synthetic, seeded ({w}: {DATA[w]})",
+            "config": {"workload": WORKLOADS[w], "n_particles": n, "sample": what,
                        "configuration": CPU_CONFIG, "parallelism": f"{threads} CPU threads"},
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads,
                              "kind": "port", "sample": sample},
@@ -401,11 +572,19 @@ def reference_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=110)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=11)
     ap.add_argument("--impl", default="mdg", choices=("mdg", "reference"))
     ap.add_argument("--config", default=DEFAULT_CONFIG)
-    ap.add_argument("--particles", "--n", dest="n", type=int, default=1_048_576)
+    ap.add_argument("--particles", "--n", dest="n", type=int, default=1_048_576,
+                    help="config 2 particle count")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=None,
+                    help="BASELINE configuration (default: config2 at N=1, config5 at N>1)")
+    ap.add_argument("--n5-side", type=int, default=256, help="config 5 FCC cells per axis")
+    ap.add_argument("--quench", type=int, default=2000,
+                    help="config 4: quench steps at T=0.7 (after half as many at T=1.4)")
+    ap.add_argument("--tune", choices=("none", "predictive", "fullsearch"), default="none",
+                    help="N>1: one reference TuningController per rank (needs baseline/_ref)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -419,6 +598,9 @@ def main():
         args.warmup = 3
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)
+    if args.workload is None:
+        args.workload = default_workload(world)
+    args.n_total = args.n
 
     if args.impl == "reference":
         if rank == 0:

@@ -140,6 +140,15 @@ int mdg_finish_kick(mdg_ctx* ctx, double dt, int has_gravity, double gravity);
  * F -> F_old copy: the caller then swaps its force / old_force buffers (and
  * re-binds) before the next compute. */
 int mdg_kick_drift(mdg_ctx* ctx, double dt, int has_gravity, double gravity, int copy_old_force);
+/* Ghost exchange of the spatial domain decomposition (no
+ * reference counterpart -- the decomposed stand-in for the periodic images of
+ * cells.py:122-156).  pack: bound rows idx[0 .. n_left+n_right) -> AoS
+ * (n_left+n_right, 3) `out` (device), + shift_left on `axis` for the first
+ * n_left rows and + shift_right for the others.  unpack: AoS (count, 3) `in`
+ * (device) -> bound rows [row0, row0+count) in the bound layout. */
+int mdg_ghost_pack(mdg_ctx* ctx, const int64_t* idx, int64_t n_left, int64_t n_right, int axis,
+                   double shift_left, double shift_right, double* out);
+int mdg_ghost_unpack(mdg_ctx* ctx, const double* in, int64_t count, int64_t row0);
 /* Capped steepest-descent step x += F/|F| min(gamma|F|, max_disp) (input
  * relaxation for BASELINE configs 2/4; no reference counterpart). */
 int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp);

@@ -194,6 +194,22 @@ class ForceCalculator:
         check(lib().mdg_kick_drift(self.ctx.h, float(dt), int(gravity is not None),
                                    float(gravity or 0.0), int(bool(copy_old_force))), "kick_drift")
 
+    def ghost_pack(self, particles, idx, n_left, axis, shift_left, shift_right, out):
+        """mdg_ghost_pack: rows ``idx`` (int64 device tensor) of the bound
+        positions into the AoS ``out`` (len(idx), 3), shifted along ``axis``
+        by ``shift_left`` for the first ``n_left`` rows, ``shift_right`` after."""
+        self.bind(particles)
+        n = int(idx.numel())
+        check(lib().mdg_ghost_pack(self.ctx.h, ctypes.c_void_p(idx.data_ptr()), int(n_left),
+                                   int(n - n_left), int(axis), float(shift_left), float(shift_right),
+                                   ctypes.c_void_p(out.data_ptr())), "ghost_pack")
+
+    def ghost_unpack(self, particles, buf, row0):
+        """mdg_ghost_unpack: the AoS (k, 3) ``buf`` into bound rows [row0, row0+k)."""
+        self.bind(particles)
+        check(lib().mdg_ghost_unpack(self.ctx.h, ctypes.c_void_p(buf.data_ptr()), int(buf.shape[0]),
+                                     int(row0)), "ghost_unpack")
+
     def lc_pairs(self, csf):
         """The LC pair set (mdg_lc_pairs) of the last LC rebuild at `csf`: the
         (k, 2) sorted unique owner pairs (i < j) with r^2 < rc^2."""

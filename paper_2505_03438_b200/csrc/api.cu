@@ -623,6 +623,31 @@ int mdg_kick_drift(mdg_ctx* ctx, double dt, int has_gravity, double gravity, int
     return cuda_status("mdg_kick_drift");
 }
 
+int mdg_ghost_pack(mdg_ctx* ctx, const int64_t* idx, int64_t n_left, int64_t n_right, int axis,
+                   double shift_left, double shift_right, double* out) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    Context& c = ctx->c;
+    if (axis < 0 || axis > 2 || n_left < 0 || n_right < 0 || ((n_left + n_right) && (!idx || !out))) {
+        set_error("mdg_ghost_pack: bad arguments");
+        return MDG_EINVAL;
+    }
+    halo_pack(c, idx, n_left, n_left + n_right, axis, shift_left, shift_right, out);
+    return cuda_status("mdg_ghost_pack");
+}
+
+int mdg_ghost_unpack(mdg_ctx* ctx, const double* in, int64_t count, int64_t row0) {
+    CHECK_CTX(ctx);
+    if (int e = need_system(ctx)) return e;
+    Context& c = ctx->c;
+    if (count < 0 || row0 < 0 || row0 + count > c.n || (count && !in)) {
+        set_error("mdg_ghost_unpack: rows outside the bound set");
+        return MDG_EINVAL;
+    }
+    halo_unpack(c, in, count, row0);
+    return cuda_status("mdg_ghost_unpack");
+}
+
 int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp) {
     CHECK_CTX(ctx);
     if (int e = need_system(ctx)) return e;

@@ -134,7 +134,8 @@ void Verlet::release() {
     q32.release();
     tdesc.release(); tsize.release(); tbase.release(); tl.release(); tcnt.release();
     big_row.release();
-    tl_in.release(); tcnt_in.release(); disp.release(); pst.release();
+    tl_in.release(); tcnt_in.release(); disp.release(); pst.release(); bmax.release();
+    nblk = 0;
     if (h_build) cudaFreeHost(h_build);
     if (ev_build) cudaEventDestroy(ev_build);
     h_build = nullptr;

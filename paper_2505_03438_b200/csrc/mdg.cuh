@@ -113,6 +113,11 @@ struct Verlet {
     float prune_thr = 0.f;
     DBuf<uint16_t> tl_in;      // inner lists, the layout of tl
     DBuf<int> tcnt_in;         // inner list lengths, the layout of tcnt
+    // per 32-row list block, the longest row's count: [0, nblk) the full
+    // lists, [nblk, 2 nblk) the inner ones; the walk's producer prefetches
+    // only that much of each block into L2 (not the padded capacity)
+    DBuf<int> bmax;
+    int64_t nblk = 0;
     DBuf<float> disp;          // per row: path length since the last prune (rounded up)
     DBuf<int> pst;             // [0] the next walk prunes, [1] prune walks since the build
     // the tile build's host check (list capacity, overflow tiles) deferred to
@@ -247,6 +252,9 @@ void vcl_compute(Context& c, int newton3);
 void vl_refresh_into(Context& c, Grid& gr, double4* s4, double* s3, bool& s3_valid);
 int vl_build_rows(Context& c, const uint8_t* only);
 int vl_ensure_rows(Context& c);
+void halo_pack(Context& c, const int64_t* idx, int64_t nl, int64_t cnt, int axis, double sl, double sr,
+               double* out);
+void halo_unpack(Context& c, const double* in, int64_t count, int64_t row0);
 // cell lengths for the fp32-compute Verlet walk (cell-relative positions)
 struct Cells32 {
     float cl[3];

@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
     const int* __restrict__ row_tid, const int* __restrict__ tcnt_out, const uint2* __restrict__ tl_out,
     const int* __restrict__ row_src, double* __restrict__ force, LJTab tab,
     unsigned long long* counter, KickArgs kick, int* pst, uint2* tl_in,
-    int* tcnt_in, float* __restrict__ disp, double rp2) {
+    int* tcnt_in, float* __restrict__ disp, double rp2, int* __restrict__ bmax, int64_t nblk) {
     extern __shared__ __align__(128) double win[];
     __shared__ __align__(16) TileDesc d[STAGES];
     __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
@@ -789,6 +789,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
     if (PRUNE && WRITE != whole) return;
     const uint2* tl = whole ? tl_out : tl_in;
     const int* tcnt = whole ? tcnt_out : tcnt_in;
+    const int* bm = whole ? bmax : bmax + nblk;
     // single type: the window stride is the compile-time kWinRows, so the
     // y / z gathers use immediate offsets from the x address
     if (!MT) wrows = kWinRows;
@@ -848,11 +849,14 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
             } else if (PF >= 3) {
                 // the tile's list stream (and counts) into L2 while the window
                 // lands: the consumers' list loads then hit L2 instead of HBM
-                size_t base = (size_t)tbase[t] * cap4;
-                size_t bytes = (size_t)((D.ni + 31) / 32 * 32) * cap4 * 2;
-                const char* lb = reinterpret_cast<const char*>(tl) + base * 2;
-                for (size_t off = (size_t)(lane - kRanges) * 32768; off < bytes; off += 16 * 32768)
-                    bulk_prefetch_l2(lb + off, (unsigned)min((size_t)32768, bytes - off));
+                // per 32-row block only the groups its longest row uses
+                // (bmax), not the padded capacity cap4
+                const int blk0 = tbase[t] >> 5, nb = (D.ni + 31) >> 5;
+                const char* lb = reinterpret_cast<const char*>(tl) + (size_t)tbase[t] * cap4 * 2;
+                for (int b = lane - kRanges; b < nb; b += 32 - kRanges) {
+                    unsigned bytes = (unsigned)((bm[blk0 + b] + 3) & ~3) * 64u;
+                    if (bytes) bulk_prefetch_l2(lb + (size_t)b * cap4 * 64, bytes);
+                }
                 if (lane == kRanges) {
                     size_t cb = ((size_t)(D.ni + 3) / 4) * 16;   // tcnt slots, whole 16-byte units
                     const char* cp = reinterpret_cast<const char*>(tcnt + tbase[t]);
@@ -885,6 +889,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                 q0 = __shfl_sync(0xffffffffu, q0, 0);
                 if (q0 >= ni) break;
                 int q = q0 + lane;
+                int cmax = 0;
                 if (q < ni) {
                     int li;
                     int r = tile_row(D, q, li);
@@ -922,6 +927,11 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                     force[pidx<PLAYOUT>(i, 0, n)] = fx;
                     force[pidx<PLAYOUT>(i, 1, n)] = fy;
                     force[pidx<PLAYOUT>(i, 2, n)] = fz;
+                    if (PRUNE && WRITE) cmax = pc;
+                }
+                if (PRUNE && WRITE) {   // the inner lists' block extent (producer prefetch)
+                    cmax = __reduce_max_sync(0xffffffffu, cmax);
+                    if (lane == 0) bmax[nblk + ((slot0 + q0) >> 5)] = cmax;
                 }
                 __syncwarp();
             }
@@ -951,6 +961,17 @@ static int vlt_env_tz() {
 }
 
 static int vlt_env_budget();
+
+// per 32-row block of the list slots: the longest row (vlt_force_kernel's
+// producer prefetches ceil4(max) groups of every row of the block)
+__global__ void vlt_bmax_kernel(const int* __restrict__ tcnt, int64_t nblk, int* __restrict__ bmax) {
+    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (w >= nblk) return;
+    int c = tcnt[w * 32 + (threadIdx.x & 31)];
+    c = __reduce_max_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0) bmax[w] = c;
+}
+
 // MDG_VLT_BUILD: 2 = the warp-converged scan, otherwise the lane-per-row scan
 // (measured faster: 0.475 against 0.725 ms, config 2)
 static int vlt_env_build() {
@@ -1005,6 +1026,13 @@ static int vlt_pass(Context& c) {
         vlt_build_warp_kernel<<<ntiles, kBuildThreadsT, 0, c.stream>>>(
             gv, desc, v.tbase.p, v.b32.p, gr.spos4.p, maxabs, ell2, v.cap, v.cap4, v.tl.p, v.tcnt.p,
             maxcnt, gr.sort_by_z), note_launch();
+    v.nblk = slots / 32;
+    v.bmax.ensure(2 * (size_t)v.nblk + 2);
+    if (!v.bmax.p) {
+        set_error("out of device memory (VL list blocks)");
+        return -1;
+    }
+    vlt_bmax_kernel<<<blocks_for(v.nblk * 32, 256), 256, 0, c.stream>>>(v.tcnt.p, v.nblk, v.bmax.p), note_launch();
     MDG_CUDA(cudaMemcpyAsync(v.h_build, c.scal.p + 3, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                              c.stream));
     MDG_CUDA(cudaMemcpyAsync(v.h_build + 1, c.scal.p + 1, sizeof(unsigned long long),
@@ -1162,7 +1190,8 @@ static void vlt_launch_st(Context& c, const KickArgs& kick) {
         reinterpret_cast<const TileDesc*>(v.tdesc.p), v.tbase.p, v.ntiles, wrows, (int*)(c.scal.p + 6),
         s3_stride((int)v.grid.m), c.n, v.cap4, v.s3.p, v.grid.row_tid.p, v.tcnt.p,
         reinterpret_cast<const uint2*>(v.tl.p), v.grid.row_src.p, c.force, c.tab, c.scal.p, kick,
-        v.pst.p, reinterpret_cast<uint2*>(v.tl_in.p), v.tcnt_in.p, v.disp.p, v.prune_rp2), note_launch();
+        v.pst.p, reinterpret_cast<uint2*>(v.tl_in.p), v.tcnt_in.p, v.disp.p, v.prune_rp2, v.bmax.p,
+        v.nblk), note_launch();
 }
 
 template <int PLAYOUT, bool MT, int PF, bool KICK>
@@ -1292,7 +1321,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
     int* __restrict__ next, int64_t n, int cap4, const float4* __restrict__ q32,
     const int* __restrict__ row_tid, const int* __restrict__ tcnt, const uint2* __restrict__ tl,
     const int* __restrict__ row_src, double* __restrict__ force, LJTab tab, Cells32 cc,
-    unsigned long long* counter) {
+    unsigned long long* counter, const int* __restrict__ bm) {
     extern __shared__ __align__(128) double win[];
     __shared__ __align__(16) TileDesc d[STAGES];
     __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
@@ -1348,11 +1377,14 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
                     if (MT) bulk_g2s(wt + o, row_tid + g, rows * 4u, &full[b]);
                 }
             } else {
-                size_t base = (size_t)tbase[t] * cap4;
-                size_t bytes = (size_t)((D.ni + 31) / 32 * 32) * cap4 * 2;
-                const char* lb = reinterpret_cast<const char*>(tl) + base * 2;
-                for (size_t off = (size_t)(lane - kRanges) * 32768; off < bytes; off += 16 * 32768)
-                    bulk_prefetch_l2(lb + off, (unsigned)min((size_t)32768, bytes - off));
+                // per 32-row block only the groups its longest row uses
+                // (bmax), not the padded capacity cap4
+                const int blk0 = tbase[t] >> 5, nb = (D.ni + 31) >> 5;
+                const char* lb = reinterpret_cast<const char*>(tl) + (size_t)tbase[t] * cap4 * 2;
+                for (int b = lane - kRanges; b < nb; b += 32 - kRanges) {
+                    unsigned bytes = (unsigned)((bm[blk0 + b] + 3) & ~3) * 64u;
+                    if (bytes) bulk_prefetch_l2(lb + (size_t)b * cap4 * 64, bytes);
+                }
             }
         }
         return;
@@ -1468,7 +1500,7 @@ static void vlt_launch32(Context& c, const Cells32& cc) {
     vlt_force32_kernel<PLAYOUT, MT, STAGES><<<grid, kTileThreads, smem, c.stream>>>(
         reinterpret_cast<const TileDesc*>(v.tdesc.p), v.tbase.p, v.ntiles, wrows, (int*)(c.scal.p + 6),
         c.n, v.cap4, v.q32.p, v.grid.row_tid.p, v.tcnt.p, reinterpret_cast<const uint2*>(v.tl.p),
-        v.grid.row_src.p, c.force, c.tab, cc, c.scal.p), note_launch();
+        v.grid.row_src.p, c.force, c.tab, cc, c.scal.p, v.bmax.p), note_launch();
 }
 
 // fp32 walk over the tiles (after vl_refresh32_kernel, which zeroes the tile

@@ -377,7 +377,7 @@ class DeviceDecomposedSimulation:
     All axes must be periodic (BASELINE configs 2-5)."""
 
     def __init__(self, dec: GridDecomposition, particles, params: SimulationParams, config,
-                 comm_device=None, ids=None):
+                 comm_device=None, ids=None, controller=None):
         from .calculator import ForceCalculator
         per = params.periodic_flags()
         if not all(bool(x) for x in per):
@@ -403,6 +403,13 @@ class DeviceDecomposedSimulation:
         self.iteration, self.since = 0, 0
         self._kick_due = False
         self.dev = d
+        # per-rank tuning (the paper's setup: one tuner per rank):
+        # any TuningController-protocol object; its trials rebuild this rank's
+        # container locally, the decomposition (migration, ghost plan) keeps
+        # the global R+1 cadence every rank shares
+        self.controller = controller
+        self.active = None
+        self.trial_log = []     # (iteration, configuration id, force_ns, build_ns)
 
     # -- point-to-point -----------------------------------------------------
     def _p2p(self, a, send_l, send_r, recv_l, recv_r):
@@ -491,10 +498,11 @@ class DeviceDecomposedSimulation:
             g = torch.cat([rl, rr], 0)
             pos = torch.cat([pos, g[:, :3]], 0)
             tcol = torch.cat([tcol, g[:, 3:4]], 0)
-            plan.append((a, li, ri, nl, nr, row0))
+            plan.append((a, torch.cat([li, ri]).to(torch.int64).contiguous(), li.numel(), nl, nr, row0))
         return plan, pos, tcol
 
-    def _rebuild(self):
+    def _rebuild(self, cfg=None):
+        cfg = cfg or self.config
         st = self._migrate(self._owned_state())
         n = st[0].shape[0]
         plan, pos, tcol = self._replan(st)
@@ -504,40 +512,73 @@ class DeviceDecomposedSimulation:
         self.ids = st[5][:, 0].to(torch.int64)
         self.ps = _device_set(self.template, pos, torch.cat([st[1], z], 0),
                               torch.cat([st[2], z], 0), torch.cat([st[3], z], 0),
-                              tcol[:, 0].to(torch.int32), self.config.layout)
-        self.calc.rebuild(self.ps, self.config)
+                              tcol[:, 0].to(torch.int32), cfg.layout)
+        # per axis: one AoS send buffer (left part, right part) packed by
+        # libmdg, one receive buffer (unused for AoS rows: received in place)
+        self._bufs = [(torch.empty((idx.numel(), 3), dtype=torch.float64, device=self.dev),
+                       torch.empty((nl + nr, 3), dtype=torch.float64, device=self.dev))
+                      for a, idx, nsl, nl, nr, row0 in self.plan]
+        self.calc.rebuild(self.ps, cfg)
 
     # -- per step -----------------------------------------------------------
     def _ghosts(self):
-        pv = self.ps.view("pos")
-        for a, li, ri, nl, nr, row0 in self.plan:
+        """Ghost positions of the fixed plan, axis by axis: libmdg packs the
+        left and right rows (shifted into the neighbours' frames) into one
+        send buffer; the receive lands in the ghost rows (AoS: in place;
+        SoA: a staging buffer + one unpack launch)."""
+        aos = self.ps.layout == "AoS"
+        for (a, idx, nsl, nl, nr, row0), (sbuf, rbuf) in zip(self.plan, self._bufs):
             w = self.dec.width[a]
-            sl, sr = pv[li], pv[ri]
-            sl[:, a] += w
-            sr[:, a] -= w
-            rl = torch.empty((nl, 3), dtype=torch.float64, device=self.dev)
-            rr = torch.empty((nr, 3), dtype=torch.float64, device=self.dev)
-            self._p2p(a, sl, sr, rl, rr)
-            pv[row0:row0 + nl] = rl
-            pv[row0 + nl:row0 + nl + nr] = rr
+            self.calc.ghost_pack(self.ps, idx, nsl, a, w, -w, sbuf)
+            dst = self.ps.pos[row0:row0 + nl + nr] if aos else rbuf
+            self._p2p(a, sbuf[:nsl], sbuf[nsl:], dst[:nl], dst[nl:])
+            if not aos:
+                self.calc.ghost_unpack(self.ps, rbuf, row0)
 
     def step(self):
         """One iteration; its kick is deferred into the next step's drift
-        (mdg_kick_drift, force / old_force swapped) -- flush() completes it."""
-        p, cfg, calc = self.params, self.config, self.calc
+        (mdg_kick_drift, force / old_force swapped) -- flush() completes it.
+        With a controller, its configuration for this iteration is used; a
+        trial's first sample or a configuration change rebuilds this rank's
+        container (locally), and trial iterations hand device-event build /
+        force nanoseconds to ``record_timings`` (simulation.py:155-181)."""
+        p, calc = self.params, self.calc
+        it, ctl = self.iteration, self.controller
+        if ctl is not None:
+            cfg, forced = ctl.configuration_for_iteration(it)
+            trial = getattr(ctl, "mode", "steady") == "trial"
+        else:
+            cfg, forced, trial = self.config, False, False
         if self._kick_due:
             calc.kick_drift(self.ps, p.delta_t, p.gravity, copy_old_force=False)
             self.ps.force, self.ps.old_force = self.ps.old_force, self.ps.force
             self._kick_due = False
         else:
             calc.drift_wrap(self.ps, p.delta_t)
+        if trial:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record()
+        if self.ps.layout != cfg.layout:
+            self.ps.convert_layout(cfg.layout)
         rebuild = self.iteration == 0 or self.since >= p.rebuild_interval
         if rebuild:
-            self._rebuild()
+            self._rebuild(cfg)
         else:
             self._ghosts()
+            if forced or cfg.id != self.active:
+                calc.rebuild(self.ps, cfg)
         calc.refresh(self.ps, cfg)
+        if trial:
+            ev[1].record()
         calc.compute_async(self.ps, cfg)
+        if trial:
+            ev[2].record()
+            ev[2].synchronize()
+            build_ns = int(ev[0].elapsed_time(ev[1]) * 1e6)
+            force_ns = int(ev[1].elapsed_time(ev[2]) * 1e6)
+            ctl.record_timings(force_ns, build_ns)
+            self.trial_log.append((it, cfg.id, force_ns, build_ns))
+        self.active = cfg.id
         thermo = getattr(p, "thermostat", None)
         if thermo is not None and (self.iteration + 1) % thermo.interval_iterations == 0:
             calc.finish_kick(self.ps, p.delta_t, p.gravity)   # the thermostat needs the kicked state

@@ -48,6 +48,36 @@ def oracle_force_fn(pos_all, type_all, n_owned, local_params, rebuild):
     return torch.as_tensor(f[:n_owned])
 
 
+TUNED_SPACE = ["VL-List_Iter-NoN3L-SoA", "LC-C08-N3L-AoS-CSF1", "LC-SLI-N3L-SoA-CSF0.5",
+               "VCL-ClusterIter-NoN3L-AoS", "LC-C01-NoN3L-SoA-CSF1"]
+
+
+class RankScript:
+    """A per-rank controller (TuningController protocol, tuning.py:200-239):
+    a trial phase over five configurations rotated by rank (two samples
+    each, the first forcing a rebuild, layouts switching), then the rank's
+    own steady choice -- so the ranks run different configurations at the
+    same iteration, as per-rank tuners do."""
+
+    def __init__(self, rank):
+        ids = TUNED_SPACE[rank % 5:] + TUNED_SPACE[:rank % 5]
+        self.seq = [(c, s == 0, "trial") for c in ids for s in range(2)]
+        self.steady = ids[-1]
+        self.mode = "steady"
+        self.timings = []
+
+    def configuration_for_iteration(self, it):
+        cid, forced, self.mode = self.seq[it] if it < len(self.seq) else (self.steady, False, "steady")
+        return P.parse_configuration(cid), forced
+
+    def record_timings(self, force_ns, build_ns):
+        assert self.mode == "trial" and force_ns > 0 and build_ns > 0
+        self.timings.append((force_ns, build_ns))
+
+    def record_failure(self, error=None):
+        return False
+
+
 def run(rank, world, port_no, steps, out_path, vscale=0.8, dt=2e-3, backend="oracle",
         dims=None, size="small", thermo=False):
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -59,15 +89,18 @@ def run(rank, world, port_no, steps, out_path, vscale=0.8, dt=2e-3, backend="ora
                                 thermostat=thermostat() if thermo else None)
     dec = GridDecomposition(params, rank, world, dims or (1, 1, world))
     mine = np.flatnonzero(dec.owner_of_positions(pos) == rank)
-    if backend == "gpudev":   # the device-resident decomposition (bench's N > 1 path)
+    if backend in ("gpudev", "gpudev_tuned"):   # the device-resident decomposition (bench's N > 1 path)
         from paper_2505_03438_b200.decomp import DeviceDecomposedSimulation
         cfg = P.parse_configuration("VL-List_Iter-NoN3L-SoA" if world % 2 == 0 else
                                     "VL-List_Iter-NoN3L-AoS")
         parts = P.ParticleSet(pos[mine], vel[mine], device="cuda:0")
+        ctl = RankScript(rank) if backend == "gpudev_tuned" else None
         sim = DeviceDecomposedSimulation(dec, parts, params, cfg, comm_device="cpu",
-                                         ids=torch.as_tensor(mine))
+                                         ids=torch.as_tensor(mine), controller=ctl)
         sim.run(steps)
         sim.check()
+        if ctl is not None:
+            assert len(ctl.timings) == len(ctl.seq) == len(sim.trial_log)
         sim.pos, sim.vel, sim.ids = sim.owned("pos").cpu(), sim.owned("vel").cpu(), sim.ids.cpu()
     elif backend == "gpu":   # libmdg on the (single) GPU, messages staged on the host for gloo
         from paper_2505_03438_b200.decomp import gpu_force_backend
@@ -76,7 +109,7 @@ def run(rank, world, port_no, steps, out_path, vscale=0.8, dt=2e-3, backend="ora
         comm = "cpu"
     else:
         dev, fn, comm = torch.device("cpu"), oracle_force_fn, None
-    if backend != "gpudev":
+    if backend not in ("gpudev", "gpudev_tuned"):
         sim = DecomposedSimulation(dec, torch.as_tensor(pos[mine]).to(dev), torch.as_tensor(vel[mine]).to(dev),
                                    torch.zeros(len(mine), dtype=torch.int64, device=dev), [1.0], params,
                                    fn, ids=torch.as_tensor(mine).to(dev), comm_device=comm)

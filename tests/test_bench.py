@@ -58,15 +58,42 @@ def test_gpu_line_contract():
     assert d["e2e"]["h2d_bytes_per_step"] == 24 * 65536 and d["e2e"]["value"] > 0
 
 
+def _torchrun(n, *args, timeout=1200):
+    return subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+                           str(n), "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), BENCH,
+                           "--gpus", str(n), "--steps", "11", "--warmup", "3", "--dist-backend", "gloo",
+                           *args], capture_output=True, text=True, timeout=timeout)
+
+
 @pytest.mark.gpu
-def test_decomposed_bench_path_two_ranks():
-    """torchrun --nproc-per-node 2 with --dist-backend gloo: two z-slabs of
-    65,536 particles each, ghosts exchanged every step, one JSON line."""
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), BENCH,
-                        "--gpus", "2", "--particles", "65536", "--steps", "11", "--warmup", "3",
-                        "--dist-backend", "gloo"], capture_output=True, text=True, timeout=900)
+@pytest.mark.parametrize("n,extra,grid", [(2, ("--n5-side", "48"), "2x1x1"),
+                                          (4, ("--n5-side", "48"), "2x2x1"),
+                                          (2, ("--workload", "config2", "--particles", "65536"), "1x1x2")])
+def test_decomposed_bench_path(n, extra, grid):
+    """torchrun with --dist-backend gloo (ranks sharing the one GPU; a smoke
+    run of the code path, never a performance number): the default N > 1
+    workload is config 5 strong-scaled over the 3-D process grid (a reduced
+    48^3-cell lattice here); config 2 runs as z-slabs of a system relaxed on
+    rank 0 and broadcast.  One JSON line naming the workload and the split."""
+    r = _torchrun(n, *extra)
     assert r.returncode == 0, r.stderr[-3000:]
     d = _line(r.stdout)
-    assert d["n_gpus"] == 2 and d["config"]["n_particles"] == 2 * 65536
-    assert d["config"]["parallelism"].startswith("zslab2") and d["value"] > 0
+    assert d["n_gpus"] == n and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["decomposition"] == grid and d["comm"]["ranks"] == n
+    if "--n5-side" in extra:
+        assert d["config"]["workload"].startswith("config5") and d["config"]["n_particles"] == 4 * 48 ** 3
+    else:
+        assert d["config"]["n_particles"] == 65536
+
+
+@pytest.mark.gpu
+def test_decomposed_bench_with_per_rank_predictive_tuners():
+    """--tune predictive: one reference TuningController per rank (needs the
+    staged reference under baseline/_ref) selecting from device timings."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "mdtune")):
+        pytest.skip("reference not staged under baseline/_ref")
+    r = _torchrun(2, "--n5-side", "48", "--tune", "predictive", "--steps", "90")
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _line(r.stdout)
+    assert d["config"]["tuning"] == "predictive" and d["tuning_trials"] > 0
+    assert d["phase_selections"]

@@ -143,6 +143,33 @@ def test_device_decomposition_matches_reference_loop(tmp_path, world, dims, size
     assert np.abs(many[:, 4:7] - np.asarray(p.velocities)).max() <= 1e-9
 
 
+@pytest.mark.gpu
+def test_device_decomposition_with_per_rank_tuners_matches_reference_loop(tmp_path):
+    """One controller per rank (the paper's setup): on a 2x2x2 grid every rank
+    trials five configurations in its own order (LC C08 / SLI / C01 at both
+    CSFs, VCL, VL; AoS and SoA; forced local rebuilds, device-event timings
+    to record_timings) and then settles on its own choice, while migration
+    and the ghost plan keep the shared R+1 cadence.  The trajectory equals
+    the reference loop's (every axis is decomposed, so no rank has a local
+    periodic face and the linked-cell traversals see what Verlet lists see)."""
+    steps, vs, dt = 24, 2.0, 3e-3
+    many = _run(8, steps, tmp_path, vscale=vs, dt=dt, tag="tuned", backend="gpudev_tuned",
+                dims=(2, 2, 2), size="cube10")
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from decomp_worker import system
+    from oracle import port
+    pos, vel, L = system(vscale=vs, size="cube10")
+    assert np.array_equal(many[:, 0], np.arange(len(pos)))
+    params = port.Params(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=4, delta_t=dt,
+                         boundary=(port.PERIODIC,) * 3)
+    p = port.Particles(pos, vel)
+    port.simulate_fixed(p, params, port.parse("VL-List_Iter-NoN3L-AoS"), steps=steps)
+    d = many[:, 1:4] - np.asarray(p.positions)
+    d -= L * np.rint(d / L)
+    assert np.abs(d).max() <= 1e-9
+    assert np.abs(many[:, 4:7] - np.asarray(p.velocities)).max() <= 1e-9
+
+
 @pytest.fixture(scope="module")
 def grid_runs(tmp_path_factory):
     tmp = tmp_path_factory.mktemp("grid")

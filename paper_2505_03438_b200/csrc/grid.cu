@@ -340,14 +340,20 @@ __global__ void bin_scatter_kernel(const double* __restrict__ pos, BinParams p,
     int c[3] = {cell_coord(x, p.cl[0], p.S[0]), cell_coord(y, p.cl[1], p.S[1]),
                 cell_coord(z, p.cl[2], p.S[2])};
     int own = ((c[0] + p.H[0]) * p.D[1] + c[1] + p.H[1]) * p.D[2] + c[2] + p.H[2];
-    tmp_ent[cell_start[own] + atomicAdd(cell_fill + own, 1)] = (int)i;
+    {
+        int slot = cell_start[own] + atomicAdd(cell_fill + own, 1);
+        MDG_DCHECK(slot < cell_start[own + 1]);
+        tmp_ent[slot] = (int)i;
+    }
     int base = img_off[i];
     int q = 0;
     for_each_image(p, c, [&](int code, int cell) {
         int e = base + q;
         img_src[e] = (int)i;
         img_code[e] = (uint8_t)code;
-        tmp_ent[cell_start[cell] + atomicAdd(cell_fill + cell, 1)] = (int)(p.n + e);
+        int slot = cell_start[cell] + atomicAdd(cell_fill + cell, 1);
+        MDG_DCHECK(slot < cell_start[cell + 1]);
+        tmp_ent[slot] = (int)(p.n + e);
         ++q;
     });
 }
@@ -396,6 +402,7 @@ __global__ void cell_sort_kernel(int64_t ncells, int64_t n, const int* __restric
             double ko = KEYZ ? __shfl_sync(0xffffffffu, kv, j) : 0.0;
             rank += j < k && before(ko, o, kv, v);
         }
+        MDG_DCHECK(lane >= k || rank < k);
         if (lane < k) emit(s + rank, v);
     } else {
         for (int a = lane; a < k; a += 32) {
@@ -405,6 +412,7 @@ __global__ void cell_sort_kernel(int64_t ncells, int64_t n, const int* __restric
                 int o = tmp_ent[s + b];
                 rank += before(key_of(o), o, kv, v);
             }
+            MDG_DCHECK(rank < k);
             emit(s + rank, v);
         }
     }

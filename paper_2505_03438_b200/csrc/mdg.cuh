@@ -7,6 +7,27 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+
+// Device-side bounds checks (the build's checked variant, `make CHECKS=1` ->
+// _build_checks/libmdg.so; compute-sanitizer is closed on the GPU pool):
+// every shared-memory gather / scatter index, list slot and atomic-claimed
+// slot the kernels derive is checked against its buffer; a violation prints
+// the site and traps.  Compiled out of the product library.
+#ifdef MDG_DEVICE_CHECKS
+#define MDG_DCHECK(c)                                                                   \
+    do {                                                                                \
+        if (!(c)) {                                                                     \
+            printf("MDG_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+                   #c, (int)blockIdx.x, (int)threadIdx.x);                              \
+            __trap();                                                                   \
+        }                                                                               \
+    } while (0)
+#else
+#define MDG_DCHECK(c) \
+    do {              \
+    } while (0)
+#endif
 
 #include <string>
 #include <vector>

@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(kBuildThreadsT) vlt_build_kernel(
                     while (m_in) {   // ascending, like the scan order
                         int t = __ffs(m_in) - 1;
                         m_in &= m_in - 1;
+                        MDG_DCHECK(l0 + t >= 0 && l0 + t < wrows && l0 + t != li);
                         glo = __byte_perm(glo, ghi, 0x5432);
                         ghi = __byte_perm(ghi, (unsigned)(l0 + t), 0x5432);
                         ++c;
@@ -474,6 +475,7 @@ __global__ void __launch_bounds__(kBuildThreadsT) vlt_build_warp_kernel(
                     while (m_in) {   // ascending, like the scan order
                         int t = __ffs(m_in) - 1;
                         m_in &= m_in - 1;
+                        MDG_DCHECK(l0 + t >= 0 && l0 + t < wrows && l0 + t != li);
                         glo = __byte_perm(glo, ghi, 0x5432);
                         ghi = __byte_perm(ghi, (unsigned)(l0 + t), 0x5432);
                         ++c;
@@ -649,7 +651,8 @@ __device__ __forceinline__ void vlt_walk_row(const double* wx, const double* wy,
                                              const int* wt, int li, int c, const uint2* lp,
                                              uint2* op, const uint2* sel, const LJTab& tab, double rp2,
                                              double c1s, double& fx, double& fy, double& fz,
-                                             unsigned& hits, int& pc) {
+                                             unsigned& hits, int& pc, int wrows_tile, int cap) {
+    MDG_DCHECK(li >= 0 && li < wrows_tile && c >= 0 && c <= cap);
     double xi = wx[li], yi = wy[li], zi = wz[li];
     int ti = MT ? wt[li] : 0;
     // the first two entry groups are independent loads: issue them together
@@ -677,6 +680,7 @@ __device__ __forceinline__ void vlt_walk_row(const double* wx, const double* wy,
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             int j = jj[u];
+            MDG_DCHECK(j < wrows_tile);
             double dx = xi - wx[j];
             double dy = yi - wy[j];
             double dz = zi - wz[j];
@@ -840,6 +844,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
             __syncwarp();
             if (lane < kRanges) {
                 int R = lane, o = D.woff[R], rows = D.woff[R + 1] - o, g = D.wstart[R];
+                MDG_DCHECK(o >= 0 && rows >= 0 && o + rows <= wrows && (o & 3) == 0);
                 if (rows > 0) {
                     bulk_g2s(wx + o, s3 + g, rows * 8u, &full[b]);
                     bulk_g2s(wy + o, s3 + (size_t)ms + g, rows * 8u, &full[b]);
@@ -900,12 +905,12 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                     int pc;
                     if (PRUNE && WRITE) {
                         vlt_walk_row<MT, PF, true>(wx, wy, wz, wt, li, c, tl + go, tl_in + go, s_sel, tab, rp2,
-                                                   c1s, fx, fy, fz, hits, pc);
+                                                   c1s, fx, fy, fz, hits, pc, D.wrows, cap4);
                         tcnt_in[slot0 + q] = pc;
                         disp[r] = 0.f;
                     } else {
                         vlt_walk_row<MT, PF, false>(wx, wy, wz, wt, li, c, tl + go, nullptr, s_sel, tab, rp2,
-                                                    c1s, fx, fy, fz, hits, pc);
+                                                    c1s, fx, fy, fz, hits, pc, D.wrows, cap4);
                     }
                     if (!MT) {
                         fx *= c0s;

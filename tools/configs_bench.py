@@ -32,9 +32,14 @@ def inputs(k, a):
     if k == 3:
         pos, vel, params = systems.config3_inputs()
         return pos, vel, params, False
-    if k == 4:
-        pos, vel, params = systems.config4_inputs()
-        return pos, vel, params, True
+    if k == 4:   # relaxed, equilibrated at T = 1.4, quenched to T = 0.7 (droplets)
+        stats = []
+        pos, vel, params = systems.config4_state(equil_steps=a.quench // 2, quench_steps=a.quench,
+                                                 stats=stats)
+        print(json.dumps({"config": 4, "quench_steps": a.quench,
+                          "live_stats_before_after": [s.feature_vector()[:6].tolist() for s in stats]}),
+              flush=True)
+        return pos, vel, params, False
     pos, vel, params = systems.config5_inputs(n_side=a.n5_side)
     return pos, vel, params, False
 
@@ -86,6 +91,7 @@ def main():
     ap.add_argument("--reorder", type=int, default=8,
                     help="cell-order arrays every K rebuilds for configs 2 and 4 (VL; 0 = off)")
     ap.add_argument("--n5-side", type=int, default=256)
+    ap.add_argument("--quench", type=int, default=4000, help="config 4: steps at T=0.7 after half as many at 1.4")
     a = ap.parse_args()
     for k in [int(x) for x in a.configs.split(",")]:
         cids = (["LC-C08-N3L-SoA-CSF1", "VL-List_Iter-NoN3L-SoA"] if k == 1 else

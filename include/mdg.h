@@ -149,6 +149,12 @@ int mdg_kick_drift(mdg_ctx* ctx, double dt, int has_gravity, double gravity, int
 int mdg_ghost_pack(mdg_ctx* ctx, const int64_t* idx, int64_t n_left, int64_t n_right, int axis,
                    double shift_left, double shift_right, double* out);
 int mdg_ghost_unpack(mdg_ctx* ctx, const double* in, int64_t count, int64_t row0);
+/* Row gather of the particle state (device pointers): dst_k[i] = src_k[order[i]]
+ * for pos, vel, force, old_force (layout MDG_AOS (N,3) / MDG_SOA (3,N)) and,
+ * when both are given, the int32 type ids -- the cell-order permutation of
+ * Simulation(reorder=K) in one pass; no reference counterpart. */
+int mdg_gather_rows(mdg_ctx* ctx, const int64_t* order, int64_t n, int layout, const double* const* src,
+                    double* const* dst, const int* tid_src, int* tid_dst);
 /* Capped steepest-descent step x += F/|F| min(gamma|F|, max_disp) (input
  * relaxation for BASELINE configs 2/4; no reference counterpart). */
 int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp);

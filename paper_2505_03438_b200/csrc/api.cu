@@ -648,6 +648,27 @@ int mdg_ghost_unpack(mdg_ctx* ctx, const double* in, int64_t count, int64_t row0
     return cuda_status("mdg_ghost_unpack");
 }
 
+int mdg_gather_rows(mdg_ctx* ctx, const int64_t* order, int64_t n, int layout, const double* const* src,
+                    double* const* dst, const int* tid_src, int* tid_dst) {
+    CHECK_CTX(ctx);
+    if (n < 0 || (n && (!order || !src || !dst)) || (layout != MDG_AOS && layout != MDG_SOA) ||
+        (!tid_src != !tid_dst)) {
+        set_error("mdg_gather_rows: bad arguments");
+        return MDG_EINVAL;
+    }
+    Rows4 s, d;
+    for (int k = 0; k < 4; ++k) {
+        s.p[k] = const_cast<double*>(src[k]);
+        d.p[k] = dst[k];
+        if (n && (!s.p[k] || !d.p[k])) {
+            set_error("mdg_gather_rows: null array");
+            return MDG_EINVAL;
+        }
+    }
+    gather_rows(ctx->c, order, n, layout, s, d, tid_src, tid_dst);
+    return cuda_status("mdg_gather_rows");
+}
+
 int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp) {
     CHECK_CTX(ctx);
     if (int e = need_system(ctx)) return e;

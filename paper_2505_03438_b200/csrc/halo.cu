@@ -58,4 +58,30 @@ void halo_unpack(Context& c, const double* in, int64_t count, int64_t row0) {
     note_launch();
 }
 
+// Cell-order permutation of the particle arrays (Simulation(reorder=K)):
+// dst_k[i] = src_k[order[i]] for the four (N,3)/(3,N) fp64 arrays and the
+// int32 type ids, one pass (replaces five eager gathers).
+template <int LAYOUT>
+__global__ void gather_rows_kernel(const int64_t* __restrict__ order, int64_t n, Rows4 src, Rows4 dst,
+                                   const int* __restrict__ tsrc, int* __restrict__ tdst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t j = order[i];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) dst.p[a][pidx<LAYOUT>(i, k, n)] = src.p[a][pidx<LAYOUT>(j, k, n)];
+    if (tsrc) tdst[i] = tsrc[j];
+}
+
+void gather_rows(Context& c, const int64_t* order, int64_t n, int layout, Rows4 src, Rows4 dst,
+                 const int* tsrc, int* tdst) {
+    if (n <= 0) return;
+    if (layout == AOS)
+        gather_rows_kernel<AOS><<<blocks_for(n, 256), 256, 0, c.stream>>>(order, n, src, dst, tsrc, tdst);
+    else
+        gather_rows_kernel<SOA><<<blocks_for(n, 256), 256, 0, c.stream>>>(order, n, src, dst, tsrc, tdst);
+    note_launch();
+}
+
 }  // namespace mdg

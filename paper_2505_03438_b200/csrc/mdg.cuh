@@ -276,6 +276,11 @@ int vl_ensure_rows(Context& c);
 void halo_pack(Context& c, const int64_t* idx, int64_t nl, int64_t cnt, int axis, double sl, double sr,
                double* out);
 void halo_unpack(Context& c, const double* in, int64_t count, int64_t row0);
+struct Rows4 {
+    double* p[4];
+};
+void gather_rows(Context& c, const int64_t* order, int64_t n, int layout, Rows4 src, Rows4 dst,
+                 const int* tsrc, int* tdst);
 // cell lengths for the fp32-compute Verlet walk (cell-relative positions)
 struct Cells32 {
     float cl[3];

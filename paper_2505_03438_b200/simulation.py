@@ -154,7 +154,7 @@ class Simulation:
         self._perm_gen = None
         self._rebuilds = 0
         self._active_cfg = None
-        self._spare = {}           # dtype -> spare arrays for _permute
+        self._spare = {}           # array name -> spare arrays for _permute
         self._skip_reorder = False
         self._perm_spare = None
         self._iota = self._inv = None
@@ -178,26 +178,37 @@ class Simulation:
 
     # -- cell-order permutation of the particle arrays (reorder) --------------
     def _permute(self, order):
-        # into spare arrays of the same shape (double buffering: no allocation
-        # once both sets exist, so no cudaMalloc inside a timed loop)
+        """All five particle arrays gathered by ``order`` in one libmdg pass
+        (mdg_gather_rows) into spare arrays of the same shape (double
+        buffering: no allocation once both sets exist, so no cudaMalloc inside
+        a timed loop)."""
+        import ctypes
+
+        from ._lib import check, lib
         p = self.p
-        spare = self._spare
-        for name in ("pos", "vel", "force", "old_force", "type_id"):
+        names = ("pos", "vel", "force", "old_force", "type_id")
+        outs = {}
+        for name in names:
             src = getattr(p, name)
-            dim = 0 if (name == "type_id" or p.layout == "AoS") else 1
-            dst = spare.pop(src.dtype, [])
-            out = None
-            for t in dst:
-                if t.shape == src.shape and t.device == src.device and t is not src:
-                    out = t
-                    break
+            pool = self._spare.setdefault(name, [])
+            out = next((t for t in pool if t.shape == src.shape and t.device == src.device
+                        and t.dtype == src.dtype and t is not src), None)
             if out is None:
                 out = torch.empty_like(src)
             else:
-                dst.remove(out)
-            torch.index_select(src, dim, order, out=out)
-            spare.setdefault(src.dtype, dst).append(src)
-            setattr(p, name, out)
+                pool.remove(out)
+            outs[name] = out
+        order = order.to(torch.int64).contiguous()
+        P4 = ctypes.c_void_p * 4
+        srcs = P4(*(getattr(p, k).data_ptr() for k in names[:4]))
+        dsts = P4(*(outs[k].data_ptr() for k in names[:4]))
+        check(lib().mdg_gather_rows(self.calc.ctx.h, ctypes.c_void_p(order.data_ptr()), int(order.numel()),
+                                    int(p.layout == "SoA"), srcs, dsts,
+                                    ctypes.c_void_p(p.type_id.data_ptr()),
+                                    ctypes.c_void_p(outs["type_id"].data_ptr())), "gather_rows")
+        for name in names:
+            self._spare[name].append(getattr(p, name))
+            setattr(p, name, outs[name])
 
     def _reapply_order(self):
         if self._perm is None or self._permuted:

@@ -155,6 +155,11 @@ int mdg_ghost_unpack(mdg_ctx* ctx, const double* in, int64_t count, int64_t row0
  * Simulation(reorder=K) in one pass; no reference counterpart. */
 int mdg_gather_rows(mdg_ctx* ctx, const int64_t* order, int64_t n, int layout, const double* const* src,
                     double* const* dst, const int* tid_src, int* tid_dst);
+/* Rows whose particle index is >= n_force get no force work (zero force, no
+ * eval count) in the tiled Verlet walk: the decomposition's ghost rows, whose
+ * forces are never used (n_force < 0: every row).  Exact for the owned rows
+ * (NoN3L: a row's force is its own list's sum). */
+int mdg_set_force_rows(mdg_ctx* ctx, int64_t n_force);
 /* Capped steepest-descent step x += F/|F| min(gamma|F|, max_disp) (input
  * relaxation for BASELINE configs 2/4; no reference counterpart). */
 int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp);

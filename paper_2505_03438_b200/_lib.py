@@ -31,7 +31,7 @@ EXPORTS = (
     "mdg_host_run", "mdg_host_kick_drift_range", "mdg_kick_drift", "mdg_lc_pairs", "mdg_timings",
     "mdg_host_drift_wrap_range_ex", "mdg_d2h_async", "mdg_host_drift_wrap_range", "mdg_host_finish_kick_range",
     "mdg_set_prune", "mdg_prune_count", "mdg_rebuild_checked", "mdg_owned_order",
-    "mdg_ghost_pack", "mdg_ghost_unpack", "mdg_gather_rows",
+    "mdg_ghost_pack", "mdg_ghost_unpack", "mdg_gather_rows", "mdg_set_force_rows",
 )
 FLAG_BLOWUP, FLAG_THERMO_ZERO = 1, 2
 
@@ -102,6 +102,7 @@ def _declare(L):
         "mdg_ghost_pack": (I, [P, P, I64, I64, I, D, D, P]),
         "mdg_ghost_unpack": (I, [P, P, I64, I64]),
         "mdg_gather_rows": (I, [P, P, I64, I, P, P, P, P]),
+        "mdg_set_force_rows": (I, [P, I64]),
         "mdg_host_run": (I, [P, CFG, P, P, P, P, P, P, D, I, D, I, I, I, I, I, ctypes.POINTER(I),
                              ctypes.POINTER(I)]),
         "mdg_host_kick_drift_range": (I, [I64, I64, I64, I, P, P, P, P, P, P, P, P, D, I, D,

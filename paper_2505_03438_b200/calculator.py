@@ -194,6 +194,12 @@ class ForceCalculator:
         check(lib().mdg_kick_drift(self.ctx.h, float(dt), int(gravity is not None),
                                    float(gravity or 0.0), int(bool(copy_old_force))), "kick_drift")
 
+    def set_force_rows(self, n_force=None):
+        """mdg_set_force_rows: only rows of particles [0, n_force) get force
+        work in the tiled Verlet walk (None: every row)."""
+        check(lib().mdg_set_force_rows(self.ctx.h, -1 if n_force is None else int(n_force)),
+              "set_force_rows")
+
     def ghost_pack(self, particles, idx, n_left, axis, shift_left, shift_right, out):
         """mdg_ghost_pack: rows ``idx`` (int64 device tensor) of the bound
         positions into the AoS ``out`` (len(idx), 3), shifted along ``axis``

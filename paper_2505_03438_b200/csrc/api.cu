@@ -669,6 +669,12 @@ int mdg_gather_rows(mdg_ctx* ctx, const int64_t* order, int64_t n, int layout, c
     return cuda_status("mdg_gather_rows");
 }
 
+int mdg_set_force_rows(mdg_ctx* ctx, int64_t n_force) {
+    CHECK_CTX(ctx);
+    ctx->c.n_force = n_force < 0 ? INT64_MAX : n_force;
+    return MDG_OK;
+}
+
 int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp) {
     CHECK_CTX(ctx);
     if (int e = need_system(ctx)) return e;

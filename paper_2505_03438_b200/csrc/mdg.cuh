@@ -209,6 +209,9 @@ struct Context {
     Grid grids[2];             // [0] CSF 1, [1] CSF 0.5
     Verlet vl;
     double prune_delta = -1.0;  // inner-list radius rc + delta (mdg_set_prune); < 0 default, 0 off
+    // rows whose source index is >= n_force get no force work in the tiled
+    // Verlet walk (the decomposition's ghost rows, mdg_set_force_rows)
+    int64_t n_force = INT64_MAX;
     DBuf<int> order_tmp;        // mdg_owned_order scratch
     Vcl vcl;
     // temperature / thermostat / live statistics (stats.cu)

@@ -754,7 +754,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
     const int* __restrict__ row_tid, const int* __restrict__ tcnt_out, const uint2* __restrict__ tl_out,
     const int* __restrict__ row_src, double* __restrict__ force, LJTab tab,
     unsigned long long* counter, KickArgs kick, int* pst, uint2* tl_in,
-    int* tcnt_in, float* __restrict__ disp, double rp2, int* __restrict__ bmax, int64_t nblk) {
+    int* tcnt_in, float* __restrict__ disp, double rp2, int* __restrict__ bmax, int64_t nblk,
+    int64_t n_force) {
     extern __shared__ __align__(128) double win[];
     __shared__ __align__(16) TileDesc d[STAGES];
     __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
@@ -901,6 +902,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                     size_t go = ((size_t)base + (size_t)(q >> 5) * 32 * cap4) / 4 + (q & 31);
                     int c = tcnt[slot0 + q];
                     int i = row_src[r];
+                    if (i >= n_force) c = 0;   // a ghost row of the decomposition: no force work
                     double fx = 0.0, fy = 0.0, fz = 0.0;
                     int pc;
                     if (PRUNE && WRITE) {
@@ -1196,7 +1198,7 @@ static void vlt_launch_st(Context& c, const KickArgs& kick) {
         s3_stride((int)v.grid.m), c.n, v.cap4, v.s3.p, v.grid.row_tid.p, v.tcnt.p,
         reinterpret_cast<const uint2*>(v.tl.p), v.grid.row_src.p, c.force, c.tab, c.scal.p, kick,
         v.pst.p, reinterpret_cast<uint2*>(v.tl_in.p), v.tcnt_in.p, v.disp.p, v.prune_rp2, v.bmax.p,
-        v.nblk), note_launch();
+        v.nblk, c.n_force), note_launch();
 }
 
 template <int PLAYOUT, bool MT, int PF, bool KICK>

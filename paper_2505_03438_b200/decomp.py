@@ -518,6 +518,8 @@ class DeviceDecomposedSimulation:
         self._bufs = [(torch.empty((idx.numel(), 3), dtype=torch.float64, device=self.dev),
                        torch.empty((nl + nr, 3), dtype=torch.float64, device=self.dev))
                       for a, idx, nsl, nl, nr, row0 in self.plan]
+        # ghost rows (particle index >= n_owned) need no forces of their own
+        self.calc.set_force_rows(n)
         self.calc.rebuild(self.ps, cfg)
 
     # -- per step -----------------------------------------------------------

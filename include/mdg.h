@@ -160,6 +160,14 @@ int mdg_gather_rows(mdg_ctx* ctx, const int64_t* order, int64_t n, int layout, c
  * forces are never used (n_force < 0: every row).  Exact for the owned rows
  * (NoN3L: a row's force is its own list's sum). */
 int mdg_set_force_rows(mdg_ctx* ctx, int64_t n_force);
+/* The caller's loop iteration of the drifts that follow (tagging only; no
+ * device work), and the earliest tagged iteration whose drift raised the
+ * blow-up bit since the last read (-1: none; read and reset; synchronises): the
+ * loop reports the reference's failing iteration (integrator.py:108-116,
+ * raised inside that iteration's apply_boundaries) although it checks the
+ * status bit only at rebuilds. */
+int mdg_set_iteration(mdg_ctx* ctx, int64_t iteration);
+int mdg_blowup_iteration(mdg_ctx* ctx, int64_t* iteration);
 /* Capped steepest-descent step x += F/|F| min(gamma|F|, max_disp) (input
  * relaxation for BASELINE configs 2/4; no reference counterpart). */
 int mdg_sd_step(mdg_ctx* ctx, double gamma, double max_disp);

@@ -279,6 +279,17 @@ class ForceCalculator:
     def blowup(self, reset=True) -> bool:
         return bool(self.status_flags(reset) & FLAG_BLOWUP)
 
+    def set_iteration(self, iteration):
+        """mdg_set_iteration: tag the following drifts with the loop iteration."""
+        lib().mdg_set_iteration(self.ctx.h, int(iteration))
+
+    def blowup_iteration(self) -> int:
+        """mdg_blowup_iteration: the earliest tagged iteration whose drift left the
+        domain (-1: none); read and reset."""
+        it = ctypes.c_int64()
+        check(lib().mdg_blowup_iteration(self.ctx.h, ctypes.byref(it)), "blowup_iteration")
+        return int(it.value)
+
     # -- temperature, thermostat, live statistics (stats.cu) -------------------
     def temperature(self, particles) -> float:
         """current_temperature (integrator.py:72-78), bit-identical."""

@@ -141,13 +141,14 @@ int mdg_create(int device, void* stream, mdg_ctx** out) {
     ctx->c.device = device;
     ctx->c.stream = (cudaStream_t)stream;
     cudaDeviceGetAttribute(&ctx->c.sm_count, cudaDevAttrMultiProcessorCount, device);
-    ctx->c.scal.ensure(8);
-    if (!ctx->c.scal.p || cudaHostAlloc((void**)&ctx->c.h_scal, 8 * sizeof(unsigned long long),
+    ctx->c.scal.ensure(16);
+    if (!ctx->c.scal.p || cudaHostAlloc((void**)&ctx->c.h_scal, 16 * sizeof(unsigned long long),
                                         cudaHostAllocDefault) != cudaSuccess) {
         delete ctx;
         return cuda_status("allocating context scalars");
     }
     cudaMemsetAsync(ctx->c.scal.p, 0, 8 * sizeof(unsigned long long), ctx->c.stream);
+    cudaMemsetAsync(ctx->c.scal.p + 8, 0xff, 8 * sizeof(unsigned long long), ctx->c.stream);
     *out = ctx;
     return cuda_status("mdg_create");
 }
@@ -692,6 +693,25 @@ int mdg_blowup(mdg_ctx* ctx, int* flag, int reset) {
     *flag = (int)(c.h_scal[2] & 3ull);
     if (reset) cudaMemsetAsync(c.scal.p + 2, 0, sizeof(unsigned long long), c.stream);
     return cuda_status("mdg_blowup");
+}
+
+int mdg_set_iteration(mdg_ctx* ctx, int64_t iteration) {
+    CHECK_CTX(ctx);
+    ctx->c.iter_tag = iteration;
+    return MDG_OK;
+}
+
+int mdg_blowup_iteration(mdg_ctx* ctx, int64_t* iteration) {
+    CHECK_CTX(ctx);
+    if (!iteration) { set_error("null output"); return MDG_EINVAL; }
+    Context& c = ctx->c;
+    if (cudaMemcpyAsync(c.h_scal + 8, c.scal.p + 8, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                        c.stream) != cudaSuccess ||
+        cudaStreamSynchronize(c.stream) != cudaSuccess)
+        return cuda_status("mdg_blowup_iteration");
+    *iteration = c.h_scal[8] == ~0ull ? -1 : (int64_t)c.h_scal[8];
+    cudaMemsetAsync(c.scal.p + 8, 0xff, sizeof(unsigned long long), c.stream);   // read and reset
+    return cuda_status("mdg_blowup_iteration");
 }
 
 int mdg_temperature(mdg_ctx* ctx, double* temperature) {

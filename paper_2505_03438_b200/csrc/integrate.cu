@@ -14,7 +14,18 @@ struct BoxParams {
     int periodic[3];
     double dt;
     int64_t n;
+    // the loop iteration this drift belongs to (mdg_set_iteration) and the
+    // slot that keeps the first one whose drift raised the blow-up flag
+    unsigned long long tag;
+    unsigned long long* first;
 };
+
+// BlowUpError (integrator.py:108-116): the status bit, plus the earliest
+// iteration that raised it, so the loop can report the reference's iteration
+__device__ __forceinline__ void flag_blowup(const BoxParams& p, unsigned long long* blowup) {
+    atomicOr(blowup, 1ull);
+    atomicMin(p.first, p.tag);
+}
 
 // np.mod(x, L) (integrator.py:118): fmod with sign fix, +0.0 for exact zeros.
 // Inside [-L, 2L] no fmod is needed: [0, L) -> x (+0.0 for -0.0); [L, 2L] ->
@@ -62,7 +73,7 @@ __global__ void drift_wrap_kernel(BoxParams p, const int* __restrict__ tid,
         pos[a] = x;
         old_force[a] = f;
     }
-    if (bad) atomicOr(blowup, 1ull);
+    if (bad) flag_blowup(p, blowup);
 }
 
 template <int LAYOUT>
@@ -127,7 +138,7 @@ __global__ void kick_drift_kernel(BoxParams p, const int* __restrict__ tid,
         vel[a] = v;
         if (COPY) old_force[a] = f;
     }
-    if (bad) atomicOr(blowup, 1ull);
+    if (bad) flag_blowup(p, blowup);
 }
 
 // Capped steepest descent used to relax overlapping random inputs (BASELINE
@@ -159,7 +170,7 @@ __global__ void sd_step_kernel(BoxParams p, double* __restrict__ pos, double* __
         else if (x > L) x = 2.0 * L - x;
         pos[a] = x;
     }
-    if (bad) atomicOr(blowup, 1ull);
+    if (bad) flag_blowup(p, blowup);
 }
 
 static BoxParams box(const Context& c, double dt) {
@@ -170,6 +181,8 @@ static BoxParams box(const Context& c, double dt) {
     }
     p.dt = dt;
     p.n = c.n;
+    p.tag = (unsigned long long)c.iter_tag;
+    p.first = c.scal.p + 8;
     return p;
 }
 

@@ -212,6 +212,9 @@ struct Context {
     // rows whose source index is >= n_force get no force work in the tiled
     // Verlet walk (the decomposition's ghost rows, mdg_set_force_rows)
     int64_t n_force = INT64_MAX;
+    // the caller's loop iteration of the next drift (mdg_set_iteration): the
+    // blow-up check records the earliest failing one (scal[8])
+    long long iter_tag = 0;
     DBuf<int> order_tmp;        // mdg_owned_order scratch
     Vcl vcl;
     // temperature / thermostat / live statistics (stats.cu)

@@ -167,8 +167,19 @@ class Simulation:
         if flags is None:
             flags = self.calc.status_flags()
         if flags & FLAG_BLOWUP:
+            # the reference raises inside the failing iteration's
+            # apply_boundaries (integrator.py:108-116); the device flag is read
+            # at rebuilds, so the loop may have run on: report the failing
+            # iteration and keep only the records of the iterations before it
+            it = self.calc.blowup_iteration() if hasattr(self.calc, "blowup_iteration") else -1
+            where = ""
+            if it >= 0:
+                self._records = [r for r in self._records if r.iteration < it]
+                self._events = [e for e in self._events if e[0] < it]
+                self.iteration = it
+                where = f" at iteration {it}"
             raise BlowUpError("particle left the domain by more than one domain length "
-                              "(or position is not finite)")
+                              f"(or position is not finite){where}")
         if flags & FLAG_THERMO_ZERO:
             raise ValueError("thermostat cannot scale zero velocities toward a positive "
                              "target temperature")
@@ -275,6 +286,8 @@ class Simulation:
         self._reapply_order()
         if self.graphs and not record and not self._kick_due and self._graph_step(it):
             return False
+        if hasattr(calc, "set_iteration"):
+            calc.set_iteration(it)   # tags this drift for the blow-up report
         if self._kick_due:
             calc.kick_drift(p, params.delta_t, params.gravity, copy_old_force=False)
             p.force, p.old_force = p.old_force, p.force

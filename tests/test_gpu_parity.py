@@ -1045,3 +1045,27 @@ def test_warm_reorder_keeps_the_trajectory(pkg, config2_snapshot):
     d -= L * np.rint(d / L)
     assert np.linalg.norm(d) / np.linalg.norm(out[0][0]) <= FP64_TOL
     assert port.force_rel_error(out[1][1], out[0][1]) <= FP64_TOL
+
+
+@pytest.mark.parametrize("cid", ["VL-List_Iter-NoN3L-AoS", "LC-C08-N3L-SoA-CSF1"])
+def test_blow_up_reports_the_reference_iteration(pkg, cid):
+    """Two particles driven into each other blow up (integrator.py:108-116)
+    in the reference at iteration 34; the device loop reads its status bit
+    only at rebuilds, yet reports that iteration and keeps exactly the
+    records of the 34 completed iterations, like the reference's report."""
+    P, calc = pkg
+    from paper_2505_03438_b200.simulation import simulate
+    pos = np.array([[3.0, 5.0, 5.0], [7.0, 5.0, 5.0], [1.0, 1.0, 1.0]])
+    vel = np.array([[100.0, 0, 0], [-100.0, 0, 0], [0, 0, 0]])
+    op = port.Params(domain_size=(10.0, 10.0, 10.0), cutoff=2.5, skin=0.3, rebuild_interval=10,
+                     delta_t=2e-3, boundary=(port.PERIODIC,) * 3)
+    done = []
+    with pytest.raises(port.BlowUp):
+        port.simulate_fixed(port.Particles(pos, vel), op, port.parse(cid), steps=100,
+                            on_step=lambda it: done.append(it))
+    params = P.SimulationParams(domain_size=(10.0, 10.0, 10.0), cutoff=2.5, skin=0.3, rebuild_interval=10,
+                                delta_t=2e-3, boundary=(P.PERIODIC,) * 3)
+    rep = simulate(P.ParticleSet(pos, vel), params, P.parse_configuration(cid), steps=100)
+    assert rep.error and rep.error.startswith("BlowUpError"), rep.error
+    assert f"at iteration {len(done)}" in rep.error, (rep.error, len(done))
+    assert len(rep.records) == len(done) == 34

@@ -543,15 +543,22 @@ __global__ void __launch_bounds__(128) lc_c08_cells_kernel(GridView gv, ScratchP
 // and per direction for NoN3L, as the reference counts.  Twice the pair
 // arithmetic of the tiles, 8 (27) times their warps: BASELINE config 1 has ~90
 // anchors per colour, which leave a one-warp-per-anchor launch latency-bound.
-template <int LAYOUT, bool MT, bool N3L>
-__global__ void __launch_bounds__(128) lc_c08_cellwarp_kernel(GridView gv, ScratchPos<LAYOUT> sp,
-                                                              ScratchForce<LAYOUT> sf, LJTab tab,
-                                                              C08Table t1, C08Table t2, ColourLaunch cl,
-                                                              int o0, int o1, int o2,
-                                                              unsigned long long* counter) {
+//
+// WPU > 1 (round 2): a CTA of WPU warps per (anchor, block cell) unit.  The
+// unit's partner rows (its cell, the forward cells, the backward cells, in
+// that order) are cut into 4-row rounds dealt round-robin to the warps; each
+// warp keeps per-row partial sums, and warp 0 adds the WPU partials in warp
+// order -- deterministic, no atomics, WPU times the parallelism of a colour
+// (BASELINE config 1: 24 -> ~7 us per colour launch).
+template <int LAYOUT, bool MT, bool N3L, int WPU>
+__global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_kernel(
+    GridView gv, ScratchPos<LAYOUT> sp, ScratchForce<LAYOUT> sf, LJTab tab, C08Table t1, C08Table t2,
+    ColourLaunch cl, int o0, int o1, int o2, unsigned long long* counter) {
     int nb = (o0 + 1) * (o1 + 1) * (o2 + 1);
-    int gw = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    int gw = WPU == 1 ? (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) : (int)blockIdx.x;
     int lane = threadIdx.x & 31;
+    const int w = WPU == 1 ? 0 : (int)(threadIdx.x >> 5);
+    __shared__ double red[WPU > 1 ? WPU : 1][3][32];
     unsigned cnt = 0;
     int total = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
     int unit = gw / nb, beta = gw % nb;
@@ -573,10 +580,12 @@ __global__ void __launch_bounds__(128) lc_c08_cellwarp_kernel(GridView gv, Scrat
                 int ti = 0;
                 if (act) sp.load(i, xi, yi, zi, ti);
                 double fx = 0.0, fy = 0.0, fz = 0.0;
+                int gk = 0;   // rounds met so far in this unit: warp w takes gk % WPU == w
                 // four partners per round (independent loads and one batched
                 // reciprocal, as in the Verlet walk), accumulated in order
                 auto run = [&](int a, int b, bool counted, bool intra) {
                     for (int j0 = a; j0 < b; j0 += 4) {
+                        if (WPU > 1 && (gk++ % WPU) != w) continue;
                         double dx[4], dy[4], dz[4], qq[4];
                         int tj[4];
                         bool ok[4];
@@ -626,7 +635,23 @@ __global__ void __launch_bounds__(128) lc_c08_cellwarp_kernel(GridView gv, Scrat
                     int c1 = gv.flat(x1, y1, z1);
                     run(gv.start[c1], gv.start[c1 + 1], false, false);
                 }
-                if (act) {
+                if (WPU > 1) {   // the partials of the unit's warps, added in warp order
+                    red[w][0][lane] = fx;
+                    red[w][1][lane] = fy;
+                    red[w][2][lane] = fz;
+                    __syncthreads();
+                    if (w == 0) {
+                        fx = fy = fz = 0.0;
+#pragma unroll
+                        for (int q = 0; q < WPU; ++q) {
+                            fx += red[q][0][lane];
+                            fy += red[q][1][lane];
+                            fz += red[q][2][lane];
+                        }
+                    }
+                    __syncthreads();
+                }
+                if (act && w == 0) {
                     *sf.at(i, 0) += fx;
                     *sf.at(i, 1) += fy;
                     *sf.at(i, 2) += fz;
@@ -635,6 +660,16 @@ __global__ void __launch_bounds__(128) lc_c08_cellwarp_kernel(GridView gv, Scrat
         }
     }
     warp_count(counter, cnt);
+}
+
+// warps per (anchor, block cell) unit of the small-system C08 kernel (1, 4, 8)
+static int lc_env_c08_wpu() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_LC_C08_WPU");
+        v = e ? atoi(e) : 8;
+    }
+    return v;
 }
 
 static int lc_env_rows() {
@@ -800,11 +835,15 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
                 int warps = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
                 if (c08_cellwarp) {
                     int nb = (g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1);
-                    int64_t threads = (int64_t)warps * nb * 32;
-                    if (newton3)
-                        lc_c08_cellwarp_kernel<LAYOUT, MT, true><<<blocks_for(threads, 128), 128, 0, s>>>(gv, sp, sf, c.tab, c08tb, c08t2, cl, g.overlap[0], g.overlap[1], g.overlap[2], counter), note_launch();
-                    else
-                        lc_c08_cellwarp_kernel<LAYOUT, MT, false><<<blocks_for(threads, 128), 128, 0, s>>>(gv, sp, sf, c.tab, c08tb, c08t2, cl, g.overlap[0], g.overlap[1], g.overlap[2], counter), note_launch();
+                    int64_t units = (int64_t)warps * nb;
+                    int wpu = lc_env_c08_wpu();
+#define MDG_C08W(N3, W) lc_c08_cellwarp_kernel<LAYOUT, MT, N3, W><<<W == 1 ? blocks_for(units * 32, 128) : (unsigned)units, W == 1 ? 128 : 32 * W, 0, s>>>(gv, sp, sf, c.tab, c08tb, c08t2, cl, g.overlap[0], g.overlap[1], g.overlap[2], counter), note_launch()
+                    if (newton3) {
+                        if (wpu >= 8) MDG_C08W(true, 8); else if (wpu >= 4) MDG_C08W(true, 4); else MDG_C08W(true, 1);
+                    } else {
+                        if (wpu >= 8) MDG_C08W(false, 8); else if (wpu >= 4) MDG_C08W(false, 4); else MDG_C08W(false, 1);
+                    }
+#undef MDG_C08W
                 } else if (c08_cells) {
                     int nb = (g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1);
                     int S = slot_width(rows_per_cell);

@@ -1,0 +1,31 @@
+"""BASELINE config 1 (8,000 particles) on its own configuration: per-step device
+time of the loop, for the launch list.
+    python tools/config1_probe.py [CONFIG_ID] [steps]"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2505_03438_b200 as P  # noqa: E402
+from paper_2505_03438_b200 import systems  # noqa: E402
+from paper_2505_03438_b200.simulation import Simulation  # noqa: E402
+
+cid = sys.argv[1] if len(sys.argv) > 1 else "LC-C08-N3L-SoA-CSF1"
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 44
+pos, vel, params = systems.config1_params()
+cfg = P.parse_configuration(cid)
+parts = P.ParticleSet(pos, vel, layout=cfg.layout)
+sim = Simulation(parts, params, cfg, fuse_kick_drift=True)
+for _ in range(11):
+    sim.step()
+sim.check()
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(steps):
+    sim.step()
+sim.flush()
+b.record()
+b.synchronize()
+print(cid, "ms/step", round(a.elapsed_time(b) / steps, 4))

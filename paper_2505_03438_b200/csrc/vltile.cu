@@ -609,7 +609,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
-constexpr int kConsumerWarps = 12;
+constexpr int kConsumerWarps = 13;
 constexpr int kTileThreads = (kConsumerWarps + 1) * 32;
 
 template <bool MT>

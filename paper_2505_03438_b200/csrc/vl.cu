@@ -269,8 +269,11 @@ __global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int
                        pos[pidx<PLAYOUT>(src, 2, n)]};
         int sh[3] = {code / 9 - 1, (code / 3) % 3 - 1, code % 3 - 1};
         double prev[3];
-        double4 old = s4[r];
+        // the SoA copy's previous values come from s3 itself: no 32-byte s4
+        // read per row on the steady path
+        double4 old = make_double4(0.0, 0.0, 0.0, 0.0);
         if (SLAYOUT == AOS || from_s4) {
+            old = s4[r];
             prev[0] = old.x; prev[1] = old.y; prev[2] = old.z;
         } else {
             prev[0] = s3[r]; prev[1] = s3[(size_t)ms + r]; prev[2] = s3[2 * (size_t)ms + r];

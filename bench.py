@@ -380,6 +380,11 @@ def gpu_arm(args, rank, world, dist):
         out["e2e_note"] = ("the host-array drop-in path (HostForceCalculator, mdg_host_run) is a "
                            "single-process API; N > 1 runs keep the state resident on each rank")
         out["comm"] = comm_info(args, world)
+        if args.workload == "config5":
+            out["strong_scaling_baseline"] = (
+                "the same system on one GPU: bench.py --workload config5 (one GPU holds all "
+                "67,108,864 particles); the default N = 1 line is config 2, BASELINE's single-GPU "
+                "configuration, so per-N values of the default runs do not form one strong-scaling series")
         if args.tune != "none":
             out["tuning_trials"] = len(sim.trial_log)
             out["phase_selections"] = list(getattr(sim.controller, "phase_selections", []))

@@ -570,7 +570,8 @@ __global__ void vl_refresh32_kernel(const double* __restrict__ pos, int64_t n, i
                                     const int* __restrict__ row_src,
                                     const uint8_t* __restrict__ row_code,
                                     const int* __restrict__ row_cell, GridView gv, Wrap w, Cells32 cc,
-                                    double4* __restrict__ s4, float4* __restrict__ q32, int* zero_me) {
+                                    double4* __restrict__ s4, float4* __restrict__ q32, int* zero_me,
+                                    float* __restrict__ disp, int* pst, float thr) {
     int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r == 0 && zero_me) *zero_me = 0;   // work counter of the tiled walk
     if (r >= m) return;
@@ -586,6 +587,12 @@ __global__ void vl_refresh32_kernel(const double* __restrict__ pos, int64_t n, i
         q[k] = x;
     }
     s4[r] = make_double4(q[0], q[1], q[2], old.w);
+    if (disp && code == kNoShift) {   // dynamic pruning's path length, as in vl_refresh_kernel
+        double ex = q[0] - prev[0], ey = q[1] - prev[1], ez = q[2] - prev[2];
+        float a = __fadd_ru(disp[r], __double2float_ru(sqrt(ex * ex + ey * ey + ez * ez)));
+        disp[r] = a;
+        if (!(a <= thr)) *pst = 1;
+    }
     int cx, cy, cz;
     gv.decode(row_cell[r], cx, cy, cz);
     // padded-grid cell (cx, cy, cz) spans [(c - H) * cl, (c - H + 1) * cl)
@@ -678,9 +685,9 @@ void vl_compute32(Context& c) {
     bool mt = c.tab.T > 1;
     int* next = tiled ? (int*)(c.scal.p + 6) : nullptr;   // zeroed for the tiled walk
     if (c.layout == AOS)
-        vl_refresh32_kernel<AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gv, w, cc, v.s4.p, v.q32.p, next), note_launch();
+        vl_refresh32_kernel<AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gv, w, cc, v.s4.p, v.q32.p, next, tiled && v.prune ? v.disp.p : nullptr, v.pst.p, v.prune_thr), note_launch();
     else
-        vl_refresh32_kernel<SOA><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gv, w, cc, v.s4.p, v.q32.p, next), note_launch();
+        vl_refresh32_kernel<SOA><<<blocks_for(m, 256), 256, 0, c.stream>>>(c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_cell.p, gv, w, cc, v.s4.p, v.q32.p, next, tiled && v.prune ? v.disp.p : nullptr, v.pst.p, v.prune_thr), note_launch();
     c.prof_mark();
     if (tiled) vlt_compute32(c, cc);   // tiles; overflow tiles below
     if (!tiled || v.nbig) {

@@ -1322,18 +1322,112 @@ bool vlt_compute(Context& c, const KickArgs* kick) {
 // walk (1-D bulk copies of the records).  Measured alternative: staging
 // tile-relative fp32 coordinates converted by the producer warp itself
 // (no bulk copy) starves the consumers, 0.41 ms against 0.24 ms.
-template <int PLAYOUT, bool MT, int STAGES>
+// One tile row of the fp32 walk.  Branch-free like the fp64 walk: a rejected
+// or padding entry selects fs = 0; the approximate reciprocal (MUFU.RCP,
+// ~2^-22) is far inside the variant's 1e-4 bar; the per-row fp32 partial
+// sums fold into fp64 every 4 entries.  WR (dynamic pruning, as in the fp64
+// walk): the row's inner list -- the entries with r^2 <= rp^2 (1 + 1e-5), a
+// superset of the exact set since the fp32 r^2 is within ~1e-6 relative --
+// is written as the walk goes; the fp64 walk may read it too.
+template <bool MT, bool WR>
+__device__ __forceinline__ void vlt_walk_row32(const float4* w4, const int* wt, int li, int c,
+                                               const uint2* lp, uint2* op, const uint2* sel,
+                                               const LJTab& tab, const Cells32& cc, float rc2, float rp2f,
+                                               float s2c, float e24c, double& fx, double& fy, double& fz,
+                                               unsigned& hits, int& pc) {
+    const float4 qi = w4[li];
+    const int ci = __float_as_int(qi.w);
+    const int ti = MT ? wt[li] : 0;
+    const float cxi = (float)(ci >> 20), cyi = (float)((ci >> 10) & 1023), czi = (float)(ci & 1023);
+    uint2 g0 = __ldcs(lp);
+    unsigned long long pk = 0;
+    pc = 0;
+    for (int k0 = 0; k0 < c; k0 += 4) {
+        uint2 cur = g0;
+        if (k0 + 4 < c) g0 = __ldcs(lp + (size_t)(k0 / 4 + 1) * 32);
+        int jj[4] = {(int)(cur.x & 0xffffu), (int)(cur.x >> 16), (int)(cur.y & 0xffffu),
+                     (int)(cur.y >> 16)};
+        float px = 0.f, py = 0.f, pz = 0.f;
+        unsigned keep = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float4 qj = w4[jj[u]];
+            int cj = __float_as_int(qj.w);
+            // (r_i - r_j) + (c_i - c_j) cl: the cell difference is an exact small integer
+            float dx = fmaf(cxi - (float)(cj >> 20), cc.cl[0], qi.x - qj.x);
+            float dy = fmaf(cyi - (float)((cj >> 10) & 1023), cc.cl[1], qi.y - qj.y);
+            float dz = fmaf(czi - (float)(cj & 1023), cc.cl[2], qi.z - qj.z);
+            float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            bool live = k0 + u < c;
+            bool ok = live && r2 < rc2;
+            if (WR) keep |= (live && r2 <= rp2f) ? 1u << u : 0u;
+            float s2f = s2c, e24f = e24c;
+            if (MT) {
+                double s2d, e24d;
+                lj_params<MT>(tab, ti, wt[jj[u]], s2d, e24d);
+                s2f = (float)s2d;
+                e24f = (float)e24d;
+            }
+            float inv;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(r2));
+            float a = s2f * inv;
+            float a6 = a * a * a;
+            float fs = (e24f * inv) * (a6 * fmaf(2.0f, a6, -1.0f));
+            fs = ok ? fs : 0.f;
+            hits += ok ? 1u : 0u;
+            px = fmaf(fs, dx, px);
+            py = fmaf(fs, dy, py);
+            pz = fmaf(fs, dz, pz);
+        }
+        fx += (double)px;
+        fy += (double)py;
+        fz += (double)pz;
+        if (WR && keep) {   // the fp64 walk's compaction (byte permutes, one 8-byte store per group)
+            uint2 sl = sel[keep];
+            int cnt = __popc(keep);
+            unsigned long long nv = ((unsigned long long)__byte_perm(cur.x, cur.y, sl.y) << 32) |
+                                    __byte_perm(cur.x, cur.y, sl.x);
+            if (cnt < 4) nv &= (1ull << (16 * cnt)) - 1ull;
+            int sft = 16 * (pc & 3);
+            pk |= nv << sft;
+            if ((pc & 3) + cnt >= 4) {
+                op[(size_t)(pc >> 2) * 32] = make_uint2((unsigned)pk, (unsigned)(pk >> 32));
+                pk = sft ? nv >> (64 - sft) : 0ull;
+            }
+            pc += cnt;
+        }
+    }
+    if (WR && (pc & 3)) op[(size_t)(pc >> 2) * 32] = make_uint2((unsigned)pk, (unsigned)(pk >> 32));
+}
+
+template <int PLAYOUT, bool MT, int STAGES, bool PRUNE, bool WRITE>
 __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
     const TileDesc* __restrict__ desc, const int* __restrict__ tbase, int ntiles, int wrows,
     int* __restrict__ next, int64_t n, int cap4, const float4* __restrict__ q32,
-    const int* __restrict__ row_tid, const int* __restrict__ tcnt, const uint2* __restrict__ tl,
+    const int* __restrict__ row_tid, const int* __restrict__ tcnt_out, const uint2* __restrict__ tl_out,
     const int* __restrict__ row_src, double* __restrict__ force, LJTab tab, Cells32 cc,
-    unsigned long long* counter, const int* __restrict__ bm) {
+    unsigned long long* counter, int* __restrict__ bmax, int64_t nblk, int* pst, uint2* tl_in,
+    int* tcnt_in, float* __restrict__ disp, double rp2, int64_t n_force) {
     extern __shared__ __align__(128) double win[];
     __shared__ __align__(16) TileDesc d[STAGES];
     __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
     __shared__ int rowctr[STAGES], tile_of[STAGES];
+    __shared__ int s_mode;
+    __shared__ uint2 s_sel[16];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (PRUNE) {
+        if (threadIdx.x == 0) s_mode = *(volatile const int*)pst;
+        if (threadIdx.x < 16) {
+            unsigned mm = threadIdx.x, sl[2] = {0u, 0u};
+            int h = 0;
+            for (int e = 0; e < 4; ++e)
+                if (mm >> e & 1) {
+                    sl[h >> 1] |= (unsigned)((2 * e) | (2 * e + 1) << 4) << (8 * (h & 1));
+                    ++h;
+                }
+            s_sel[mm] = make_uint2(sl[0], sl[1]);
+        }
+    }
     if (threadIdx.x == 0) {
         for (int b = 0; b < STAGES; ++b) {
             mbar_init(&full[b], 1);
@@ -1344,6 +1438,12 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
     __syncthreads();
     // per buffer: float4[wrows], then int[wrows] types (MT); in doubles
     const int kBuf = 2 * wrows + (MT ? wrows / 2 : 0);
+    // pruning (as in vlt_force_kernel): the mode picks the lists of the launch
+    const bool whole = !PRUNE || s_mode != 0;
+    if (PRUNE && WRITE != whole) return;
+    const uint2* tl = whole ? tl_out : tl_in;
+    const int* tcnt = whole ? tcnt_out : tcnt_in;
+    const int* bm = whole ? bmax : bmax + nblk;
     if (warp == kConsumerWarps) {
         for (int it = 0;; ++it) {
             int b = it % STAGES;
@@ -1352,6 +1452,10 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
             if (lane == 0) t = atomicAdd(next, 1);
             t = __shfl_sync(0xffffffffu, t, 0);
             if (t >= ntiles) {
+                if (PRUNE && WRITE && lane == 0 && t == ntiles + (int)gridDim.x - 1) {
+                    pst[0] = 0;   // the inner lists are fresh
+                    ++pst[1];
+                }
                 if (lane == 0) {
                     tile_of[b] = -1;
                     mbar_arrive(&full[b]);
@@ -1398,6 +1502,12 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
     }
     unsigned hits = 0;
     const float rc2 = (float)tab.rc2;
+    const float rp2f = (float)rp2 * (1.0f + 1e-5f);
+    float s2c = 0.f, e24c = 0.f;
+    if (!MT) {
+        s2c = (float)tab.sig2[0];
+        e24c = (float)tab.eps24[0];
+    }
     for (int it = 0;; ++it) {
         int b = it % STAGES;
         mbar_wait(&full[b], (it / STAGES) & 1);
@@ -1416,66 +1526,33 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
                 q0 = __shfl_sync(0xffffffffu, q0, 0);
                 if (q0 >= ni) break;
                 int q = q0 + lane;
+                int cmax = 0;
                 if (q < ni) {
                     int li;
                     int r = tile_row(D, q, li);
-                    float4 qi = w4[li];
-                    int ci = __float_as_int(qi.w);
-                    int ti = MT ? wt[li] : 0;
-                    const uint2* lp = tl + ((size_t)base + (size_t)(q >> 5) * 32 * cap4) / 4 + (q & 31);
+                    size_t go = ((size_t)base + (size_t)(q >> 5) * 32 * cap4) / 4 + (q & 31);
                     int c = tcnt[slot0 + q];
-                    uint2 g0 = __ldcs(lp);
                     int i = row_src[r];
+                    if (i >= n_force) c = 0;   // a ghost row of the decomposition
                     double fx = 0.0, fy = 0.0, fz = 0.0;
-                    float s2c = 0.f, e24c = 0.f;
-                    if (!MT) {
-                        double s2d, e24d;
-                        lj_params<false>(tab, 0, 0, s2d, e24d);
-                        s2c = (float)s2d;
-                        e24c = (float)e24d;
-                    }
-                    for (int k0 = 0; k0 < c; k0 += 4) {
-                        uint2 cur = g0;
-                        if (k0 + 4 < c) g0 = __ldcs(lp + (size_t)(k0 / 4 + 1) * 32);
-                        int jj[4] = {(int)(cur.x & 0xffffu), (int)(cur.x >> 16), (int)(cur.y & 0xffffu),
-                                     (int)(cur.y >> 16)};
-                        float px = 0.f, py = 0.f, pz = 0.f;
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            float4 qj = w4[jj[u]];
-                            int cj = __float_as_int(qj.w);
-                            float dx = (qi.x - qj.x) + (float)((ci >> 20) - (cj >> 20)) * cc.cl[0];
-                            float dy = (qi.y - qj.y) + (float)(((ci >> 10) & 1023) - ((cj >> 10) & 1023)) * cc.cl[1];
-                            float dz = (qi.z - qj.z) + (float)((ci & 1023) - (cj & 1023)) * cc.cl[2];
-                            float r2 = dx * dx + dy * dy + dz * dz;
-                            if ((k0 + u < c) && r2 < rc2) {
-                                float s2f = s2c, e24f = e24c;
-                                if (MT) {
-                                    double s2d, e24d;
-                                    lj_params<MT>(tab, ti, wt[jj[u]], s2d, e24d);
-                                    s2f = (float)s2d;
-                                    e24f = (float)e24d;
-                                }
-                                // approximate reciprocal (MUFU.RCP, ~2^-22 relative):
-                                // far inside the variant's 1e-4 tolerance
-                                float inv;
-                                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(r2));
-                                float a = s2f * inv;
-                                float a6 = a * a * a;
-                                float fs = (e24f * inv) * (a6 * fmaf(2.0f, a6, -1.0f));
-                                ++hits;
-                                px = fmaf(fs, dx, px);
-                                py = fmaf(fs, dy, py);
-                                pz = fmaf(fs, dz, pz);
-                            }
-                        }
-                        fx += (double)px;
-                        fy += (double)py;
-                        fz += (double)pz;
+                    int pc;
+                    if (PRUNE && WRITE) {
+                        vlt_walk_row32<MT, true>(w4, wt, li, c, tl + go, tl_in + go, s_sel, tab, cc, rc2, rp2f,
+                                                 s2c, e24c, fx, fy, fz, hits, pc);
+                        tcnt_in[slot0 + q] = pc;
+                        disp[r] = 0.f;
+                        cmax = pc;
+                    } else {
+                        vlt_walk_row32<MT, false>(w4, wt, li, c, tl + go, nullptr, s_sel, tab, cc, rc2, rp2f,
+                                                  s2c, e24c, fx, fy, fz, hits, pc);
                     }
                     force[pidx<PLAYOUT>(i, 0, n)] = fx;
                     force[pidx<PLAYOUT>(i, 1, n)] = fy;
                     force[pidx<PLAYOUT>(i, 2, n)] = fz;
+                }
+                if (PRUNE && WRITE) {   // the inner lists' block extent (producer prefetch)
+                    cmax = __reduce_max_sync(0xffffffffu, cmax);
+                    if (lane == 0) bmax[nblk + ((slot0 + q0) >> 5)] = cmax;
                 }
                 __syncwarp();
             }
@@ -1486,28 +1563,38 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
     warp_count(counter, hits);
 }
 
-template <int PLAYOUT, bool MT>
-static void vlt_launch32(Context& c, const Cells32& cc) {
+template <int PLAYOUT, bool MT, bool PRUNE, bool WRITE>
+static void vlt_launch32_st(Context& c, const Cells32& cc) {
     Verlet& v = c.vl;
     int wrows = v.win_rows;
     constexpr int STAGES = 2;
     size_t smem = STAGES * (size_t)(wrows * 16 + (MT ? wrows * 4 : 0));
     static int ctas_per_sm = 0;
     static size_t smem_set = 0;
+    auto kern = vlt_force32_kernel<PLAYOUT, MT, STAGES, PRUNE, WRITE>;
     if (smem != smem_set) {
-        cudaFuncSetAttribute(vlt_force32_kernel<PLAYOUT, MT, STAGES>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, vlt_force32_kernel<PLAYOUT, MT, STAGES>,
-                                                      kTileThreads, smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, kern, kTileThreads, smem);
         if (ctas_per_sm < 1) ctas_per_sm = 1;
         smem_set = smem;
     }
     int grid = std::min(v.ntiles, c.sm_count * ctas_per_sm);
     if (grid < 1) return;
-    vlt_force32_kernel<PLAYOUT, MT, STAGES><<<grid, kTileThreads, smem, c.stream>>>(
+    kern<<<grid, kTileThreads, smem, c.stream>>>(
         reinterpret_cast<const TileDesc*>(v.tdesc.p), v.tbase.p, v.ntiles, wrows, (int*)(c.scal.p + 6),
         c.n, v.cap4, v.q32.p, v.grid.row_tid.p, v.tcnt.p, reinterpret_cast<const uint2*>(v.tl.p),
-        v.grid.row_src.p, c.force, c.tab, cc, c.scal.p, v.bmax.p), note_launch();
+        v.grid.row_src.p, c.force, c.tab, cc, c.scal.p, v.bmax.p, v.nblk, v.pst.p,
+        reinterpret_cast<uint2*>(v.tl_in.p), v.tcnt_in.p, v.disp.p, v.prune_rp2, c.n_force), note_launch();
+}
+
+template <int PLAYOUT, bool MT>
+static void vlt_launch32(Context& c, const Cells32& cc) {
+    if (c.vl.prune) {   // the inner-list walk, then the prune walk (one returns at once)
+        vlt_launch32_st<PLAYOUT, MT, true, false>(c, cc);
+        vlt_launch32_st<PLAYOUT, MT, true, true>(c, cc);
+    } else {
+        vlt_launch32_st<PLAYOUT, MT, false, false>(c, cc);
+    }
 }
 
 // fp32 walk over the tiles (after vl_refresh32_kernel, which zeroes the tile

@@ -330,3 +330,40 @@ def test_reflect_gravity_fused_and_graph_loops_match_reference(pkg, mode):
         sim.check()
         ep, ev = _traj_err(parts, z, k)
         assert ep <= FP64_TOL and ev <= FP64_TOL, (cid, mode, ep, ev)
+
+
+def test_three_types_200k_forces_vs_oracle(pkg):
+    """Three particle types (Lorentz-Berthelot mixing, forces.py:12-22) on
+    200,000 relaxed particles: the tiled walk's multi-type path (types staged
+    in the window), LC-SLI and the fp32 variant against the oracle."""
+    P, calc = pkg
+    from paper_2505_03438_b200 import systems
+    n = 200_000
+    pos, L, rng = systems.uniform_box(n, 0.7, seed=5)
+    tid = (np.arange(n) % 3).astype(np.int64)
+    types = [P.ParticleTypeInfo(t, 1.0 + 0.5 * t, 1.0 - 0.2 * t, 1.0 + t) for t in range(3)]
+    params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=10,
+                                boundary=(P.PERIODIC,) * 3)
+    parts = P.ParticleSet(pos, type_ids=tid, types=types)
+    systems.relax_on_device(parts, params, P.parse_configuration("LC-SLI-N3L-AoS-CSF1"))
+    pos = parts.numpy("pos")
+    op = _oparams(params)
+    p = port.Particles(pos, type_id=tid, sigma=[1.0, 0.8, 0.6], epsilon=[1.0, 1.5, 2.0],
+                       mass=[1.0, 2.0, 3.0])
+    with port.Pool(WORKERS) as pool:
+        fc = port.ForceCalculator(p, op)
+        cfg = port.parse("LC-C08-N3L-AoS-CSF1")
+        fc.rebuild(p, cfg)
+        fc.refresh(p, cfg)
+        ref_n = fc.compute(p, cfg, pool)
+    ref_f = np.ascontiguousarray(p.forces)
+    for cid in ("VL-List_Iter-NoN3L-SoA", "VL-List_Iter-NoN3L-AoS", "LC-SLI-N3L-SoA-CSF1",
+                "VL-List_Iter-NoN3L-SoA-FP32"):
+        cfgd = P.parse_configuration(cid)
+        q = P.ParticleSet(pos, type_ids=tid, types=types, layout=cfgd.layout)
+        _, count = calc.compute_forces(q, cfgd, params)
+        unique = count if cfgd.newton3 else count // 2
+        tol = FP32_TOL if cfgd.precision == "fp32" else FP64_TOL
+        if cfgd.precision != "fp32":
+            assert unique == ref_n, (cid, unique, ref_n)
+        assert port.force_rel_error(q.numpy("force"), ref_f) <= tol, cid

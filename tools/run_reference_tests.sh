@@ -14,6 +14,8 @@ export PYTHONPATH="$ROOT/baseline/_ref:$ROOT"
 export NUMBA_CACHE_DIR=/tmp/mdg_numba_cache
 python -m pytest -p paper_2505_03438_b200.plugin -p no:cacheprovider --rootdir . -rA \
     test_containers.py test_simulation.py test_integrator.py test_dataset.py \
+    test_cells.py test_forces.py test_configuration.py test_livestats.py test_tuning.py \
+    test_fuzzy.py test_forest.py test_rules.py test_scenarios.py test_experiments.py \
     "test_acceptance.py::test_criterion_1_forces_match_oracle_on_random_scenarios" \
     "test_acceptance.py::test_criterion_2_search_space_has_exactly_the_valid_30" \
     "test_acceptance.py::test_criterion_3_c08_directed_interactions_halve_under_newton3" \

@@ -97,3 +97,21 @@ def test_decomposed_bench_with_per_rank_predictive_tuners():
     d = _line(r.stdout)
     assert d["config"]["tuning"] == "predictive" and d["tuning_trials"] > 0
     assert d["phase_selections"]
+
+
+def test_process_grids_and_workload_names():
+    """bench.py's decomposition choice: config 5 as 2x1x1 /
+    2x2x1 / 2x2x2 at 2 / 4 / 8 ranks (a 3-factor split otherwise), configs
+    2-4 as z-slabs; the default workload is config 2 at N = 1 and config 5 at
+    N > 1."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", BENCH)
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    assert [b.grid_dims("config5", n) for n in (1, 2, 4, 8)] == [(1, 1, 1), (2, 1, 1), (2, 2, 1), (2, 2, 2)]
+    for n in (3, 6, 12, 16):
+        d = b.grid_dims("config5", n)
+        assert d[0] * d[1] * d[2] == n
+    assert b.grid_dims("config3", 4) == (1, 1, 4) and b.grid_dims("config4", 8) == (1, 1, 8)
+    assert b.default_workload(1) == "config2" and b.default_workload(8) == "config5"
+    assert set(b.WORKLOADS) == {"config2", "config3", "config4", "config5"}

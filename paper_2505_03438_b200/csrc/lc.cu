@@ -559,6 +559,13 @@ __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_ker
     int lane = threadIdx.x & 31;
     const int w = WPU == 1 ? 0 : (int)(threadIdx.x >> 5);
     __shared__ double red[WPU > 1 ? WPU : 1][3][32];
+    // WPU > 1: the unit's partner ranges and their rows, staged
+    constexpr int kStage = WPU > 1 ? 512 : 1;
+    constexpr int kRng = WPU > 1 ? 2 * kMaxStencil + 2 : 1;
+    __shared__ double st_x[kStage], st_y[kStage], st_z[kStage];
+    __shared__ int st_t[kStage], st_j[kStage];
+    __shared__ unsigned char st_f[kStage];
+    __shared__ int st_a[kRng], st_off[kRng + 1], st_fl[kRng], st_n[2];
     unsigned cnt = 0;
     int total = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
     int unit = gw / nb, beta = gw % nb;
@@ -569,6 +576,150 @@ __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_ker
         int cx = cl.p[0] + kx * cl.stride[0] + bi;
         int cy = cl.p[1] + ky * cl.stride[1] + bj;
         int cz = cl.p[2] + kz * cl.stride[2] + bk;
+        if (WPU > 1 && gv.in_grid(cx, cy, cz)) {
+            // the unit's partner rows staged in shared memory once (one round
+            // of global loads for the whole CTA), then read as broadcasts
+            int c = gv.flat(cx, cy, cz);
+            int s1 = gv.start[c], e1 = gv.start[c + 1];
+            bool own = gv.owned(cx, cy, cz);
+            // one partner range per thread (slot 0: the intra range, then the
+            // forward entries whose first cell is this one, then the backward
+            // ones), lengths scanned by one warp: no serial chain of loads
+            const int nt1 = own ? t1.start[beta + 1] - t1.start[beta] : 0;
+            const int nt2 = t2.start[beta + 1] - t2.start[beta];
+            const int nrng = 1 + nt1 + nt2;
+            for (int k = threadIdx.x; k < nrng; k += blockDim.x) {
+                int a = 0, len = 0, fl = 0;
+                if (k == 0) {
+                    if (beta == 0 && own) { a = s1; len = e1 - s1; fl = 3; }   // counted | intra
+                } else if (k <= nt1) {
+                    int e = t1.start[beta] + k - 1;
+                    int x2 = cx + t1.d[e][0], y2 = cy + t1.d[e][1], z2 = cz + t1.d[e][2];
+                    if (gv.in_grid(x2, y2, z2)) {
+                        int c2 = gv.flat(x2, y2, z2);
+                        a = gv.start[c2];
+                        len = gv.start[c2 + 1] - a;
+                        fl = 1;
+                    }
+                } else {
+                    int e = t2.start[beta] + k - 1 - nt1;
+                    int x1 = cx - t2.d[e][0], y1 = cy - t2.d[e][1], z1 = cz - t2.d[e][2];
+                    if (gv.in_grid(x1, y1, z1) && gv.owned(x1, y1, z1)) {
+                        int c1 = gv.flat(x1, y1, z1);
+                        a = gv.start[c1];
+                        len = gv.start[c1 + 1] - a;
+                    }
+                }
+                st_a[k] = a;
+                st_off[k] = len;
+                st_fl[k] = fl;
+            }
+            __syncthreads();
+            if (threadIdx.x < 32) {   // exclusive scan of the lengths
+                int carry = 0;
+                for (int k0 = 0; k0 < nrng; k0 += 32) {
+                    int k = k0 + lane;
+                    int v = k < nrng ? st_off[k] : 0, x = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        int t = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += t;
+                    }
+                    if (k < nrng) st_off[k] = carry + x - v;
+                    carry += __shfl_sync(0xffffffffu, x, 31);
+                }
+                if (lane == 0) {
+                    st_off[nrng] = carry;
+                    st_n[0] = nrng;
+                    st_n[1] = carry;
+                }
+            }
+            __syncthreads();
+            const int nr = st_n[0], tot = st_n[1];
+            if (tot <= kStage) {
+                for (int q = threadIdx.x; q < tot; q += blockDim.x) {
+                    int lo = 0, hi = nr - 1;   // the last range starting at or before q
+                    while (lo < hi) {
+                        int mid = (lo + hi + 1) >> 1;
+                        if (st_off[mid] <= q) lo = mid; else hi = mid - 1;
+                    }
+                    int k = lo;
+                    int j = st_a[k] + (q - st_off[k]);
+                    double xj, yj, zj;
+                    int tj;
+                    sp.load(j, xj, yj, zj, tj);
+                    st_x[q] = xj;
+                    st_y[q] = yj;
+                    st_z[q] = zj;
+                    st_t[q] = MT ? tj : 0;
+                    st_j[q] = j;
+                    st_f[q] = (unsigned char)st_fl[k];
+                }
+                __syncthreads();
+                for (int i0 = s1; i0 < e1; i0 += 32) {
+                    int i = i0 + lane;
+                    bool act = i < e1;
+                    double xi = 0.0, yi = 0.0, zi = 0.0;
+                    int ti = 0;
+                    if (act) sp.load(i, xi, yi, zi, ti);
+                    double fx = 0.0, fy = 0.0, fz = 0.0;
+                    // 4-row rounds of the staged partners, dealt round-robin to the warps
+                    for (int q0 = 4 * w; q0 < tot; q0 += 4 * WPU) {
+                        double dx[4], dy[4], dz[4], qq[4];
+                        int tj[4];
+                        bool ok[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            int q = min(q0 + u, tot - 1);
+                            dx[u] = xi - st_x[q];
+                            dy[u] = yi - st_y[q];
+                            dz[u] = zi - st_z[q];
+                            tj[u] = st_t[q];
+                            int fl = st_f[q];
+                            double r2 = dx[u] * dx[u] + dy[u] * dy[u] + dz[u] * dz[u];
+                            ok[u] = act && q0 + u < tot && (!(fl & 2) || st_j[q] != i) && r2 < tab.rc2;
+                            qq[u] = ok[u] ? r2 : 1.0;
+                            if (ok[u]) cnt += (N3L ? ((fl & 1) && (!(fl & 2) || st_j[q] > i)) : 1) ? 1u : 0u;
+                        }
+                        double p01 = qq[0] * qq[1], p23 = qq[2] * qq[3];
+                        double y = fast_rcp(p01 * p23);
+                        double y01 = y * p23, y23 = y * p01;
+                        double inv[4] = {y01 * qq[1], y01 * qq[0], y23 * qq[3], y23 * qq[2]};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            double s2, e24;
+                            lj_params<MT>(tab, ti, tj[u], s2, e24);
+                            double aa = s2 * inv[u];
+                            double a6 = aa * aa * aa;
+                            double fs = (e24 * inv[u]) * (a6 * fma(2.0, a6, -1.0));
+                            fs = ok[u] ? fs : 0.0;
+                            fx += fs * dx[u];
+                            fy += fs * dy[u];
+                            fz += fs * dz[u];
+                        }
+                    }
+                    red[w][0][lane] = fx;
+                    red[w][1][lane] = fy;
+                    red[w][2][lane] = fz;
+                    __syncthreads();
+                    if (w == 0 && act) {
+                        double gx = 0.0, gy = 0.0, gz = 0.0;
+#pragma unroll
+                        for (int q = 0; q < WPU; ++q) {
+                            gx += red[q][0][lane];
+                            gy += red[q][1][lane];
+                            gz += red[q][2][lane];
+                        }
+                        *sf.at(i, 0) += gx;
+                        *sf.at(i, 1) += gy;
+                        *sf.at(i, 2) += gz;
+                    }
+                    __syncthreads();
+                }
+                warp_count(counter, cnt);
+                return;
+            }
+        }
         if (gv.in_grid(cx, cy, cz)) {
             int c = gv.flat(cx, cy, cz);
             int s1 = gv.start[c], e1 = gv.start[c + 1];

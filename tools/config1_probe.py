@@ -16,7 +16,7 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 44
 pos, vel, params = systems.config1_params()
 cfg = P.parse_configuration(cid)
 parts = P.ParticleSet(pos, vel, layout=cfg.layout)
-sim = Simulation(parts, params, cfg, fuse_kick_drift=True)
+sim = Simulation(parts, params, cfg, fuse_kick_drift=not os.environ.get("PROBE_GRAPHS"), graphs=bool(os.environ.get("PROBE_GRAPHS")))
 for _ in range(11):
     sim.step()
 sim.check()

@@ -553,6 +553,7 @@ def reference_arm(args):
     with port.Pool(threads) as pool:
         if relax:
             port.sd_relax(p, pp, cfg, systems.SD_STEPS, systems.SD_GAMMA, systems.SD_MAX_DISP, pool)
+        snap = (np.array(p.positions), np.array(p.velocities))
         steps = max(1, min(args.steps, 11))
         warm = max(0, min(args.warmup, 1))
         port.simulate_fixed(p, pp, cfg, steps=warm, pool=pool)
@@ -562,6 +563,9 @@ def reference_arm(args):
     value = n * steps / dt / 1e6
     sample = (f"{steps} full MD steps (one rebuild window of 11) of {what} after {warm} warm-up "
               f"step(s); {threads} host threads; {CPU_CONFIG}")
+    extra = {}
+    if os.environ.get("MDG_REF_NUMBA", "1") != "0":
+        extra["reference_mdtune"] = _time_mdtune(snap, params, steps, threads)
     return {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "impl": "reference",
             "n_gpus": 1, "steps": steps, "warmup": warm, "ms_per_step": round(dt / steps * 1e3, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -571,7 +575,44 @@ def reference_arm(args):
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0}, **extra}
+
+
+def _time_mdtune(snap, params, steps, threads):
+    """The unmodified reference itself (mdtune's simulate with numba kernels,
+    staged under baseline/_ref) on the same relaxed snapshot and configuration,
+    next to the oracle port's number; skipped when the package is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "mdtune")):
+        return {"unavailable": "reference not staged under baseline/_ref"}
+    if ref not in sys.path:
+        sys.path.append(ref)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/mdg_numba_cache")
+    try:
+        from mdtune.configuration import parse_configuration
+        from mdtune.params import PERIODIC, SimulationParams
+        from mdtune.particles import ParticleSet
+        from mdtune.simulation import simulate
+        from mdtune.tuning import FixedStrategy
+
+        def run(k):
+            prm = SimulationParams(domain_size=tuple(params.domain_size), cutoff=params.cutoff,
+                                   skin=params.skin, rebuild_interval=params.rebuild_interval,
+                                   delta_t=params.delta_t, total_iterations=k, boundary=(PERIODIC,) * 3,
+                                   thread_count=threads)
+            ps = ParticleSet(snap[0].copy(), velocities=snap[1].copy())
+            t0 = time.perf_counter()
+            rep = simulate(ps, prm, FixedStrategy(parse_configuration(CPU_CONFIG)), tuning_interval=10 ** 9,
+                           raise_errors=True)
+            return time.perf_counter() - t0, rep
+        run(1)                       # numba JIT / cache load outside the timing
+        dt, _ = run(steps)
+        import numba
+        return {"value": round(len(snap[0]) * steps / dt / 1e6, 4), "unit": UNIT, "steps": steps,
+                "configuration": CPU_CONFIG, "threads": threads, "numba": numba.__version__,
+                "sample": f"{steps} steps of mdtune.simulation.simulate (FixedStrategy) on the same snapshot"}
+    except Exception as exc:   # informational only: the port's number is the line's value
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
 
 
 def main():

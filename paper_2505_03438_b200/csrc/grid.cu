@@ -118,7 +118,7 @@ void Grid::release() {
     img_cnt.release(); img_off.release(); img_src.release(); img_code.release();
     tmp_ent.release(); row_ent.release(); row_src.release(); row_cell.release();
     row_tid.release(); inv.release(); row_code.release();
-    spos4.release(); spos3.release(); sforce.release();
+    spos4.release(); spos3.release(); sforce.release(); cpart.release();
     built = false;
 }
 
@@ -593,15 +593,26 @@ void grid_refresh(Context& c, Grid& gr, int layout) {
 
 // LayoutBuffers.scatter_forces (containers.py:156-171) as a gather: owned row
 // assigned, image rows added (images of one particle in combo order).
+// ncol > 0: the scratch forces are ncol colour partials (the one-launch
+// small-system C08, lc.cu), added here in colour order per row.
 template <int PLAYOUT, int SLAYOUT>
 __global__ void fold_kernel(int64_t n, int m, const int* __restrict__ inv,
                             const int* __restrict__ img_cnt, const int* __restrict__ img_off,
                             const double* __restrict__ sf, double* __restrict__ force,
-                            bool images) {
+                            bool images, int ncol) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     auto get = [&](int r, int k) {
-        return SLAYOUT == AOS ? sf[3 * (size_t)r + k] : sf[(size_t)k * m + r];
+        const size_t e = SLAYOUT == AOS ? 3 * (size_t)r + k : (size_t)k * m + r;
+        if (ncol == 0) return sf[e];
+        double v[8];   // independent loads first, then the colour-order sum
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = q < ncol ? sf[(size_t)q * 3 * m + e] : 0.0;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q < ncol) s += v[q];
+        return s;
     };
     int r0 = inv[i];
     double fx = get(r0, 0), fy = get(r0, 1), fz = get(r0, 2);
@@ -623,16 +634,18 @@ void lc_fold_forces(Context& c, Grid& gr, int layout, bool images) {
     if (c.n == 0) return;
     dim3 b(blocks_for(c.n, 256)), t(256);
     int m = (int)gr.m;
+    const int ncol = gr.cpart_ncol;
+    const double* sfp = ncol ? gr.cpart.p : gr.sforce.p;
     if (c.layout == AOS) {
         if (layout == AOS)
-            fold_kernel<AOS, AOS><<<b, t, 0, c.stream>>>(c.n, m, gr.inv.p, gr.img_cnt.p, gr.img_off.p, gr.sforce.p, c.force, images), note_launch();
+            fold_kernel<AOS, AOS><<<b, t, 0, c.stream>>>(c.n, m, gr.inv.p, gr.img_cnt.p, gr.img_off.p, sfp, c.force, images, ncol), note_launch();
         else
-            fold_kernel<AOS, SOA><<<b, t, 0, c.stream>>>(c.n, m, gr.inv.p, gr.img_cnt.p, gr.img_off.p, gr.sforce.p, c.force, images), note_launch();
+            fold_kernel<AOS, SOA><<<b, t, 0, c.stream>>>(c.n, m, gr.inv.p, gr.img_cnt.p, gr.img_off.p, sfp, c.force, images, ncol), note_launch();
     } else {
         if (layout == AOS)
-            fold_kernel<SOA, AOS><<<b, t, 0, c.stream>>>(c.n, m, gr.inv.p, gr.img_cnt.p, gr.img_off.p, gr.sforce.p, c.force, images), note_launch();
+            fold_kernel<SOA, AOS><<<b, t, 0, c.stream>>>(c.n, m, gr.inv.p, gr.img_cnt.p, gr.img_off.p, sfp, c.force, images, ncol), note_launch();
         else
-            fold_kernel<SOA, SOA><<<b, t, 0, c.stream>>>(c.n, m, gr.inv.p, gr.img_cnt.p, gr.img_off.p, gr.sforce.p, c.force, images), note_launch();
+            fold_kernel<SOA, SOA><<<b, t, 0, c.stream>>>(c.n, m, gr.inv.p, gr.img_cnt.p, gr.img_off.p, sfp, c.force, images, ncol), note_launch();
     }
 }
 

@@ -550,12 +550,34 @@ __global__ void __launch_bounds__(128) lc_c08_cells_kernel(GridView gv, ScratchP
 // warp keeps per-row partial sums, and warp 0 adds the WPU partials in warp
 // order -- deterministic, no atomics, WPU times the parallelism of a colour
 // (BASELINE config 1: 24 -> ~7 us per colour launch).
-template <int LAYOUT, bool MT, bool N3L, int WPU>
+// ALL (WPU > 1): every colour in one launch.  Unit u of the launch belongs to
+// the colour k with ca.ustart[k] <= u < ca.ustart[k + 1]; within a colour no
+// two units share a cell, so each unit STORES its rows' sums into colour k's
+// partial buffer (colours x 3m, zeroed first), and c08_colour_sum_kernel then
+// adds a row's partials in colour order -- the same additions, in the same
+// order, as the colour-by-colour launches accumulating into the scratch
+// forces, so the result is bit-identical with 1 launch instead of 8.
+struct C08All {
+    ColourLaunch cl[8];
+    int ustart[9];
+    int ncol;
+};
+
+template <int LAYOUT, bool MT, bool N3L, int WPU, bool ALL = false>
 __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_kernel(
     GridView gv, ScratchPos<LAYOUT> sp, ScratchForce<LAYOUT> sf, LJTab tab, C08Table t1, C08Table t2,
-    ColourLaunch cl, int o0, int o1, int o2, unsigned long long* counter) {
+    ColourLaunch cl, int o0, int o1, int o2, unsigned long long* counter, C08All ca = {},
+    double* cpart = nullptr) {
     int nb = (o0 + 1) * (o1 + 1) * (o2 + 1);
     int gw = WPU == 1 ? (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) : (int)blockIdx.x;
+    if (ALL) {
+        static_assert(!ALL || WPU > 1, "one launch of all colours: CTA units only");
+        int k = 0;
+        while (k + 1 < ca.ncol && gw >= ca.ustart[k + 1]) ++k;
+        gw -= ca.ustart[k];
+        cl = ca.cl[k];
+        sf.f = cpart + (size_t)k * 3 * sf.m;
+    }
     int lane = threadIdx.x & 31;
     const int w = WPU == 1 ? 0 : (int)(threadIdx.x >> 5);
     __shared__ double red[WPU > 1 ? WPU : 1][3][32];
@@ -710,9 +732,15 @@ __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_ker
                             gy += red[q][1][lane];
                             gz += red[q][2][lane];
                         }
-                        *sf.at(i, 0) += gx;
-                        *sf.at(i, 1) += gy;
-                        *sf.at(i, 2) += gz;
+                        if (ALL) {
+                            *sf.at(i, 0) = gx;
+                            *sf.at(i, 1) = gy;
+                            *sf.at(i, 2) = gz;
+                        } else {
+                            *sf.at(i, 0) += gx;
+                            *sf.at(i, 1) += gy;
+                            *sf.at(i, 2) += gz;
+                        }
                     }
                     __syncthreads();
                 }
@@ -803,14 +831,51 @@ __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_ker
                     __syncthreads();
                 }
                 if (act && w == 0) {
-                    *sf.at(i, 0) += fx;
-                    *sf.at(i, 1) += fy;
-                    *sf.at(i, 2) += fz;
+                    if (ALL) {
+                        *sf.at(i, 0) = fx;
+                        *sf.at(i, 1) = fy;
+                        *sf.at(i, 2) = fz;
+                    } else {
+                        *sf.at(i, 0) += fx;
+                        *sf.at(i, 1) += fy;
+                        *sf.at(i, 2) += fz;
+                    }
                 }
             }
         }
     }
     warp_count(counter, cnt);
+}
+
+// scratch force = the colour partials added in colour order (C08All)
+__global__ void c08_colour_sum_kernel(int64_t len, int ncol, const double* __restrict__ cpart,
+                                      double* __restrict__ sforce) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= len) return;
+    double s = 0.0;
+    for (int k = 0; k < ncol; ++k) s += cpart[(size_t)k * len + e];
+    sforce[e] = s;
+}
+
+// MDG_LC_C08_ALL: 1 (default) the small-system C08 runs every colour in one
+// launch (C08All), 0 one launch per colour
+static int lc_env_c08_all() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_LC_C08_ALL");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
+// warps per unit of the one-launch small-system C08 (2, 4, 8; MDG_LC_C08_ALL_WPU)
+static int lc_env_c08_all_wpu() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_LC_C08_ALL_WPU");
+        v = e ? atoi(e) : 4;
+    }
+    return v;
 }
 
 // warps per (anchor, block cell) unit of the small-system C08 kernel (1, 4, 8)
@@ -879,6 +944,22 @@ static int slot_width(double rows_per_unit) {
 }
 
 // ------------------------------------------------------------------ dispatch
+
+// too few anchors per colour to fill the GPU with anchor warps (small
+// systems): the (anchor, block cell) unit kernel, deterministic
+static bool lc_c08_cellwarp_applies(const Context& c, const Geom& g) {
+    int64_t anchors_per_colour = (int64_t)g.D[0] * g.D[1] * g.D[2] /
+                                 ((g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1));
+    return lc_env_c08() == 3 || (lc_env_c08() == 1 && anchors_per_colour < 4 * c.sm_count);
+}
+
+// ... and all its colours in one launch (C08All)
+static bool lc_c08_all_applies(const Context& c, const Grid& gr, int traversal) {
+    const Geom& g = gr.g;
+    const int nbc = (g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1);
+    return traversal == T_C08 && lc_env_c08() != 2 && lc_c08_cellwarp_applies(c, g) && lc_env_c08_all() &&
+           nbc <= 8;
+}
 
 template <int LAYOUT, bool MT>
 static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
@@ -961,14 +1042,14 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
     // C08: anchors over the whole padded grid, stride overlap+1 per axis
     // dense cells (CSF 1): warp tiles; sparse cells: row-slot threads
     bool c08_cells = lc_env_c08() == 1 && rows_per_cell < 8.0;
-    // too few anchors per colour to fill the GPU with anchor warps (small
-    // systems): warp per (anchor, block cell), deterministic
-    int64_t anchors_per_colour = (int64_t)g.D[0] * g.D[1] * g.D[2] /
-                                 ((g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1));
-    bool c08_cellwarp = lc_env_c08() == 3 || (lc_env_c08() == 1 && anchors_per_colour < 4 * c.sm_count);
+    bool c08_cellwarp = lc_c08_cellwarp_applies(c, g);
     C08Table c08t2 = make_c08_table(g, gr.fwd, true);
     C08Table c08tb = make_c08_table(g, gr.fwd);
     int strides[3] = {g.overlap[0] + 1, g.overlap[1] + 1, g.overlap[2] + 1};
+    const int nbc = strides[0] * strides[1] * strides[2];
+    const bool c08_all = lc_c08_all_applies(c, gr, traversal);
+    C08All ca{};
+    ca.ncol = 0;
     for (int px = 0; px < strides[0]; ++px)
         for (int py = 0; py < strides[1]; ++py)
             for (int pz = 0; pz < strides[2]; ++pz) {
@@ -984,7 +1065,11 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
                 }
                 if (empty) continue;
                 int warps = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
-                if (c08_cellwarp) {
+                if (c08_all) {   // collected, one launch below
+                    ca.cl[ca.ncol] = cl;
+                    ca.ustart[ca.ncol + 1] = ca.ustart[ca.ncol] + warps * nbc;
+                    ++ca.ncol;
+                } else if (c08_cellwarp) {
                     int nb = (g.overlap[0] + 1) * (g.overlap[1] + 1) * (g.overlap[2] + 1);
                     int64_t units = (int64_t)warps * nb;
                     int wpu = lc_env_c08_wpu();
@@ -1008,6 +1093,25 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
                 else
                     lc_c08_kernel<LAYOUT, MT, false><<<blocks_for(warps, 4), 128, 0, s>>>(gv, sp, sf, c.tab, gr.fwd, cl, counter), note_launch();
             }
+    if (c08_all && ca.ncol > 0) {
+        const size_t len = 3 * (size_t)m;
+        gr.cpart.ensure(len * ca.ncol + 1);
+        if (!gr.cpart.p) return;   // out of memory: no forces (the caller's status check reports it)
+        cudaMemsetAsync(gr.cpart.p, 0, len * ca.ncol * sizeof(double), s);
+        const unsigned units = (unsigned)ca.ustart[ca.ncol];
+#define MDG_C08A(N3, W) lc_c08_cellwarp_kernel<LAYOUT, MT, N3, W, true><<<units, 32 * W, 0, s>>>(gv, sp, sf, c.tab, c08tb, c08t2, cl, g.overlap[0], g.overlap[1], g.overlap[2], counter, ca, gr.cpart.p), note_launch()
+        const int wpu = lc_env_c08_all_wpu();
+        if (newton3) {
+            if (wpu >= 8) MDG_C08A(true, 8); else if (wpu >= 4) MDG_C08A(true, 4); else MDG_C08A(true, 2);
+        } else {
+            if (wpu >= 8) MDG_C08A(false, 8); else if (wpu >= 4) MDG_C08A(false, 4); else MDG_C08A(false, 2);
+        }
+#undef MDG_C08A
+        if (lc_env_c08_all() == 2)   // the scratch forces materialised (a separate sum pass)
+            c08_colour_sum_kernel<<<blocks_for((int64_t)len, 256), 256, 0, s>>>((int64_t)len, ca.ncol, gr.cpart.p, gr.sforce.p), note_launch();
+        else
+            gr.cpart_ncol = ca.ncol;   // the fold adds the partials
+    }
 }
 
 // ---------------------------------------------------------------- pair export
@@ -1064,8 +1168,9 @@ int lc_pairs(Context& c, Grid& gr, long long cap, int2* dev_out, long long* coun
 }
 
 void lc_compute(Context& c, Grid& gr, int traversal, int newton3, int layout) {
+    gr.cpart_ncol = 0;
     if (gr.m == 0) return;
-    if (traversal != T_C01)
+    if (traversal != T_C01 && !lc_c08_all_applies(c, gr, traversal))
         cudaMemsetAsync(gr.sforce.p, 0, 3 * (size_t)gr.m * sizeof(double), c.stream);
     bool mt = c.tab.T > 1;
     c.prof_mark();

@@ -101,6 +101,8 @@ struct Grid {
     DBuf<double4> spos4;                            // AoS: x,y,z,type
     DBuf<double> spos3;                             // SoA: x[m],y[m],z[m]
     DBuf<double> sforce;                            // 3*m ((m,3) AoS or (3,m) SoA)
+    DBuf<double> cpart;                             // small-system C08: per-colour partial forces, colours x 3*m
+    int cpart_ncol = 0;                             // > 0: the last compute left its forces in cpart (the fold adds them)
     void release();
 };
 

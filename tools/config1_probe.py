@@ -29,3 +29,19 @@ sim.flush()
 b.record()
 b.synchronize()
 print(cid, "ms/step", round(a.elapsed_time(b) / steps, 4))
+if "--profile" in sys.argv:
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(steps):
+            sim.step()
+        sim.flush()
+        torch.cuda.synchronize()
+    rows = []
+    for ev in prof.key_averages():
+        dt = getattr(ev, "device_time_total", 0.0)
+        if dt > 0:
+            rows.append((dt / steps, ev.count / steps, ev.key[:80]))
+    rows.sort(reverse=True)
+    print("kernel sum us/step", round(sum(r[0] for r in rows), 2))
+    for us, cnt, name in rows:
+        print(f"  {us:8.2f} us/step  x{cnt:5.2f}  {name}")

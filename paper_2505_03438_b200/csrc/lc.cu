@@ -858,7 +858,7 @@ __global__ void c08_colour_sum_kernel(int64_t len, int ncol, const double* __res
 }
 
 // MDG_LC_C08_ALL: 1 (default) the small-system C08 runs every colour in one
-// launch (C08All), 0 one launch per colour
+// launch (C08All), 0 one launch per colour, 3 the colour partials added in the fold
 static int lc_env_c08_all() {
     static int v = -1;
     if (v < 0) {
@@ -1107,10 +1107,15 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
             if (wpu >= 8) MDG_C08A(false, 8); else if (wpu >= 4) MDG_C08A(false, 4); else MDG_C08A(false, 2);
         }
 #undef MDG_C08A
-        if (lc_env_c08_all() == 2)   // the scratch forces materialised (a separate sum pass)
-            c08_colour_sum_kernel<<<blocks_for((int64_t)len, 256), 256, 0, s>>>((int64_t)len, ca.ncol, gr.cpart.p, gr.sforce.p), note_launch();
-        else
+        // the colour sums as their own element-parallel pass (the fold then
+        // runs as for every LC traversal): measured faster than adding the
+        // partials inside the fold, whose thread-per-particle chains of
+        // dependent image loads then carry 8 loads per row (5.5 + 2.1 us
+        // against 16.7 us at BASELINE config 1)
+        if (lc_env_c08_all() == 3)
             gr.cpart_ncol = ca.ncol;   // the fold adds the partials
+        else
+            c08_colour_sum_kernel<<<blocks_for((int64_t)len, 256), 256, 0, s>>>((int64_t)len, ca.ncol, gr.cpart.p, gr.sforce.p), note_launch();
     }
 }
 

@@ -140,6 +140,23 @@ int mdg_finish_kick(mdg_ctx* ctx, double dt, int has_gravity, double gravity);
  * F -> F_old copy: the caller then swaps its force / old_force buffers (and
  * re-binds) before the next compute. */
 int mdg_kick_drift(mdg_ctx* ctx, double dt, int has_gravity, double gravity, int copy_old_force);
+/* The reference loop for ONE configuration on the bound device state
+ * (simulation.py:144-189 under a FixedStrategy, no timing / records, no
+ * thermostat), iterations iteration0 .. iteration0 + steps - 1, as
+ * Simulation.step runs them with the kick deferred into the next drift:
+ * per iteration kick_drift (when *kick_due, force / old_force swapped instead
+ * of copied) or drift_wrap; mdg_rebuild_checked when *since >= R or
+ * *rebuild_now; refresh; compute.  One native call instead of ~10 ctypes
+ * calls per iteration (small systems are host-bound otherwise).  In/out:
+ * *since (iterations since the last rebuild), *kick_due (a kick is owed on
+ * return: run mdg_finish_kick or pass it back in), *swaps (incremented per
+ * force / old_force swap: the caller swaps its buffers when odd),
+ * *done (iterations completed).  A raised status bit at a rebuild stops the
+ * loop before that rebuild: *flags = the bits (as mdg_rebuild_checked).  The
+ * eval count afterwards is that of the last compute. */
+int mdg_run(mdg_ctx* ctx, const mdg_config* cfg, int64_t steps, double dt, int has_gravity,
+            double gravity, int rebuild_interval, int64_t iteration0, int rebuild_now, int* since,
+            int* kick_due, int* swaps, int64_t* done, int* flags);
 /* Ghost exchange of the spatial domain decomposition (no
  * reference counterpart -- the decomposed stand-in for the periodic images of
  * cells.py:122-156).  pack: bound rows idx[0 .. n_left+n_right) -> AoS

@@ -194,6 +194,30 @@ class ForceCalculator:
         check(lib().mdg_kick_drift(self.ctx.h, float(dt), int(gravity is not None),
                                    float(gravity or 0.0), int(bool(copy_old_force))), "kick_drift")
 
+    def run_fixed(self, particles, config, steps, dt, gravity, rebuild_interval, iteration0,
+                  since, kick_due, rebuild_now=False):
+        """mdg_run: `steps` iterations of the fixed-configuration loop in one
+        native call (see include/mdg.h).  Swaps ``particles.force`` /
+        ``old_force`` as the native loop did.  Returns (done, since, kick_due,
+        flags)."""
+        if particles.layout != config.layout:
+            raise ValueError(f"particle layout {particles.layout} does not match "
+                             f"configuration {config.id}")
+        self.bind(particles)
+        s, kd, sw, fl = ctypes.c_int(int(since)), ctypes.c_int(int(bool(kick_due))), ctypes.c_int(0), ctypes.c_int(0)
+        done = ctypes.c_int64(0)
+        rc = lib().mdg_run(self.ctx.h, ctypes.byref(config_struct(config)), int(steps), float(dt),
+                           int(gravity is not None), float(gravity or 0.0), int(rebuild_interval),
+                           int(iteration0), int(bool(rebuild_now)), ctypes.byref(s), ctypes.byref(kd),
+                           ctypes.byref(sw), ctypes.byref(done), ctypes.byref(fl))
+        if sw.value & 1:
+            particles.force, particles.old_force = particles.old_force, particles.force
+        if done.value:
+            self.generation += 1
+            self._count_pending = True
+        check(rc, "run")
+        return int(done.value), int(s.value), bool(kd.value), int(fl.value)
+
     def set_force_rows(self, n_force=None):
         """mdg_set_force_rows: only rows of particles [0, n_force) get force
         work in the tiled Verlet walk (None: every row)."""

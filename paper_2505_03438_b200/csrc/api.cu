@@ -624,6 +624,49 @@ int mdg_kick_drift(mdg_ctx* ctx, double dt, int has_gravity, double gravity, int
     return cuda_status("mdg_kick_drift");
 }
 
+int mdg_run(mdg_ctx* ctx, const mdg_config* cfg, int64_t steps, double dt, int has_gravity,
+            double gravity, int rebuild_interval, int64_t iteration0, int rebuild_now, int* since,
+            int* kick_due, int* swaps, int64_t* done, int* flags) {
+    CHECK_CTX(ctx);
+    if (int e = validate(cfg)) return e;
+    if (int e = need_system(ctx)) return e;
+    if (!since || !kick_due || !swaps || !done || !flags || steps < 0 || rebuild_interval < 0) {
+        set_error("mdg_run: bad arguments");
+        return MDG_EINVAL;
+    }
+    Context& c = ctx->c;
+    *done = 0;
+    *flags = 0;
+    for (int64_t k = 0; k < steps; ++k) {
+        c.iter_tag = iteration0 + k;
+        if (*kick_due) {
+            if (int e = mdg_kick_drift(ctx, dt, has_gravity, gravity, 0)) return e;
+            std::swap(c.force, c.old_force);
+            ++c.gen;
+            ++*swaps;
+            *kick_due = 0;
+        } else if (int e = mdg_drift_wrap(ctx, dt)) {
+            return e;
+        }
+        const bool rebuild = rebuild_now || *since >= rebuild_interval;
+        if (rebuild) {
+            int f = 0;
+            if (int e = mdg_rebuild_checked(ctx, cfg, &f)) return e;
+            if (f) {
+                *flags = f;
+                return MDG_OK;
+            }
+            rebuild_now = 0;
+        }
+        if (int e = mdg_refresh(ctx, cfg)) return e;
+        if (int e = mdg_compute(ctx, cfg)) return e;
+        *kick_due = 1;
+        *since = rebuild ? 0 : *since + 1;
+        *done = k + 1;
+    }
+    return MDG_OK;
+}
+
 int mdg_ghost_pack(mdg_ctx* ctx, const int64_t* idx, int64_t n_left, int64_t n_right, int axis,
                    double shift_left, double shift_right, double* out) {
     CHECK_CTX(ctx);

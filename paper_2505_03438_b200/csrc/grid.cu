@@ -119,6 +119,9 @@ void Grid::release() {
     tmp_ent.release(); row_ent.release(); row_src.release(); row_cell.release();
     row_tid.release(); inv.release(); row_code.release();
     spos4.release(); spos3.release(); sforce.release(); cpart.release();
+    cpart_zero = 0;
+    c08l_tot.release(); c08l_j.release(); c08l_f.release();
+    c08l_for = -1;
     built = false;
 }
 
@@ -489,6 +492,7 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
     }
     MDG_CUDA(cudaGetLastError());
     gr.built = true;
+    ++gr.build_id;
     gr.scratch_layout = -1;
     return 0;
 }
@@ -618,11 +622,34 @@ __global__ void fold_kernel(int64_t n, int m, const int* __restrict__ inv,
     double fx = get(r0, 0), fy = get(r0, 1), fz = get(r0, 2);
     if (images) {
         int q0 = img_off[i], nq = img_cnt[i];
-        for (int q = 0; q < nq; ++q) {
-            int r = inv[n + q0 + q];
-            fx += get(r, 0);
-            fy += get(r, 1);
-            fz += get(r, 2);
+        // up to 7 images (3 periodic axes): their rows and forces loaded
+        // together (independent loads), then added in combo order -- a
+        // particle's chain of dependent loads is 3 deep, not 2 per image
+        if (nq <= 7) {
+            int rr[7];
+#pragma unroll
+            for (int q = 0; q < 7; ++q) rr[q] = q < nq ? inv[n + q0 + q] : r0;
+            double gx[7], gy[7], gz[7];
+#pragma unroll
+            for (int q = 0; q < 7; ++q) {
+                gx[q] = q < nq ? get(rr[q], 0) : 0.0;
+                gy[q] = q < nq ? get(rr[q], 1) : 0.0;
+                gz[q] = q < nq ? get(rr[q], 2) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 7; ++q)
+                if (q < nq) {
+                    fx += gx[q];
+                    fy += gy[q];
+                    fz += gz[q];
+                }
+        } else {
+            for (int q = 0; q < nq; ++q) {
+                int r = inv[n + q0 + q];
+                fx += get(r, 0);
+                fy += get(r, 1);
+                fz += get(r, 2);
+            }
         }
     }
     force[pidx<PLAYOUT>(i, 0, n)] = fx;

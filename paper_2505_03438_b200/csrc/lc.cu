@@ -563,11 +563,24 @@ struct C08All {
     int ncol;
 };
 
-template <int LAYOUT, bool MT, bool N3L, int WPU, bool ALL = false>
-__global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_kernel(
+// The staged partner list of every unit (C08All launches), built once per
+// grid rebuild by the LM = 1 instantiation and read by LM = 2: the per-step
+// kernel then skips the range lookups, the length scan and the per-row range
+// search (two CTA barriers and a chain of dependent loads per unit).  tot[u]
+// = the unit's staged rows (-1: more than the staging capacity, the unit takes
+// the unstaged path), j / f: staged row and flags, kStage per unit.
+struct C08Lists {
+    int* tot;
+    int* j;
+    unsigned char* f;
+};
+constexpr int kC08Stage = 512;
+
+template <int LAYOUT, bool MT, bool N3L, int WPU, bool ALL = false, int LM = 0>
+__global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU, ALL ? 32 / WPU : 1) lc_c08_cellwarp_kernel(
     GridView gv, ScratchPos<LAYOUT> sp, ScratchForce<LAYOUT> sf, LJTab tab, C08Table t1, C08Table t2,
     ColourLaunch cl, int o0, int o1, int o2, unsigned long long* counter, C08All ca = {},
-    double* cpart = nullptr) {
+    double* cpart = nullptr, C08Lists ul = {}) {
     int nb = (o0 + 1) * (o1 + 1) * (o2 + 1);
     int gw = WPU == 1 ? (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) : (int)blockIdx.x;
     if (ALL) {
@@ -582,12 +595,15 @@ __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_ker
     const int w = WPU == 1 ? 0 : (int)(threadIdx.x >> 5);
     __shared__ double red[WPU > 1 ? WPU : 1][3][32];
     // WPU > 1: the unit's partner ranges and their rows, staged
-    constexpr int kStage = WPU > 1 ? 512 : 1;
+    constexpr int kStage = WPU > 1 ? kC08Stage : 1;
     constexpr int kRng = WPU > 1 ? 2 * kMaxStencil + 2 : 1;
     __shared__ double st_x[kStage], st_y[kStage], st_z[kStage];
     __shared__ int st_t[kStage], st_j[kStage];
     __shared__ unsigned char st_f[kStage];
     __shared__ int st_a[kRng], st_off[kRng + 1], st_fl[kRng], st_n[2];
+    // per warp and lane: the queued partners (staged indices) of one segment
+    constexpr int kSeg = WPU > 1 ? 32 : 1;
+    __shared__ unsigned short qbuf[WPU > 1 ? WPU : 1][kSeg][32];
     unsigned cnt = 0;
     int total = cl.cnt[0] * cl.cnt[1] * cl.cnt[2];
     int unit = gw / nb, beta = gw % nb;
@@ -604,6 +620,25 @@ __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_ker
             int c = gv.flat(cx, cy, cz);
             int s1 = gv.start[c], e1 = gv.start[c + 1];
             bool own = gv.owned(cx, cy, cz);
+            int tot = 0;
+            bool staged = false;
+            if (LM == 2) {   // the unit's list of this grid (C08Lists)
+                tot = ul.tot[blockIdx.x];
+                staged = tot >= 0;
+                const size_t o = (size_t)blockIdx.x * kStage;
+                for (int q = threadIdx.x; q < tot; q += blockDim.x) {
+                    const int j = ul.j[o + q];
+                    double xj, yj, zj;
+                    int tj;
+                    sp.load(j, xj, yj, zj, tj);
+                    st_x[q] = xj;
+                    st_y[q] = yj;
+                    st_z[q] = zj;
+                    st_t[q] = MT ? tj : 0;
+                    st_j[q] = j;
+                    st_f[q] = ul.f[o + q];
+                }
+            } else {
             // one partner range per thread (slot 0: the intra range, then the
             // forward entries whose first cell is this one, then the backward
             // ones), lengths scanned by one warp: no serial chain of loads
@@ -657,8 +692,10 @@ __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_ker
                 }
             }
             __syncthreads();
-            const int nr = st_n[0], tot = st_n[1];
-            if (tot <= kStage) {
+            const int nr = st_n[0];
+            tot = st_n[1];
+            staged = tot <= kStage;
+            if (staged) {
                 for (int q = threadIdx.x; q < tot; q += blockDim.x) {
                     int lo = 0, hi = nr - 1;   // the last range starting at or before q
                     while (lo < hi) {
@@ -667,6 +704,11 @@ __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_ker
                     }
                     int k = lo;
                     int j = st_a[k] + (q - st_off[k]);
+                    if (LM == 1) {
+                        ul.j[(size_t)blockIdx.x * kStage + q] = j;
+                        ul.f[(size_t)blockIdx.x * kStage + q] = (unsigned char)st_fl[k];
+                        continue;
+                    }
                     double xj, yj, zj;
                     int tj;
                     sp.load(j, xj, yj, zj, tj);
@@ -677,6 +719,13 @@ __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_ker
                     st_j[q] = j;
                     st_f[q] = (unsigned char)st_fl[k];
                 }
+            }
+            if (LM == 1) {
+                if (threadIdx.x == 0) ul.tot[blockIdx.x] = staged ? tot : -1;
+                return;
+            }
+            }
+            if (staged) {
                 __syncthreads();
                 for (int i0 = s1; i0 < e1; i0 += 32) {
                     int i = i0 + lane;
@@ -685,39 +734,62 @@ __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_ker
                     int ti = 0;
                     if (act) sp.load(i, xi, yi, zi, ti);
                     double fx = 0.0, fy = 0.0, fz = 0.0;
-                    // 4-row rounds of the staged partners, dealt round-robin to the warps
-                    for (int q0 = 4 * w; q0 < tot; q0 += 4 * WPU) {
-                        double dx[4], dy[4], dz[4], qq[4];
-                        int tj[4];
-                        bool ok[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            int q = min(q0 + u, tot - 1);
-                            dx[u] = xi - st_x[q];
-                            dy[u] = yi - st_y[q];
-                            dz[u] = zi - st_z[q];
-                            tj[u] = st_t[q];
-                            int fl = st_f[q];
-                            double r2 = dx[u] * dx[u] + dy[u] * dy[u] + dz[u] * dz[u];
-                            ok[u] = act && q0 + u < tot && (!(fl & 2) || st_j[q] != i) && r2 < tab.rc2;
-                            qq[u] = ok[u] ? r2 : 1.0;
-                            if (ok[u]) cnt += (N3L ? ((fl & 1) && (!(fl & 2) || st_j[q] > i)) : 1) ? 1u : 0u;
+                    // this warp's staged partners: 4-row rounds dealt round-robin
+                    // (candidate s of the warp is q = 4w + 4 WPU (s/4) + s%4), in
+                    // segments of kSeg: first the exact r^2 < rc^2 test of every
+                    // candidate (the reference's test, kernels.py:36-40), the
+                    // passing ones queued per lane; then the force of the queued
+                    // partners only, four at a time with one batched reciprocal
+                    // -- ~8% of the candidates of a 27-cell neighbourhood are
+                    // within rc, so the force arithmetic no longer runs on every
+                    // candidate.  Sums in candidate order (deterministic).
+                    for (int s0 = 0;; s0 += kSeg) {
+                        if (4 * w + 4 * WPU * (s0 >> 2) >= tot) break;
+                        int nq = 0;
+                        for (int s = s0; s < s0 + kSeg; ++s) {
+                            const int q = 4 * w + 4 * WPU * (s >> 2) + (s & 3);
+                            if (q >= tot) break;
+                            const double dx = xi - st_x[q], dy = yi - st_y[q], dz = zi - st_z[q];
+                            const double r2 = dx * dx + dy * dy + dz * dz;
+                            const int fl = st_f[q];
+                            if (act && (!(fl & 2) || st_j[q] != i) && r2 < tab.rc2) {
+                                qbuf[w][nq][lane] = (unsigned short)q;
+                                ++nq;
+                                cnt += (N3L ? ((fl & 1) && (!(fl & 2) || st_j[q] > i)) : 1) ? 1u : 0u;
+                            }
                         }
-                        double p01 = qq[0] * qq[1], p23 = qq[2] * qq[3];
-                        double y = fast_rcp(p01 * p23);
-                        double y01 = y * p23, y23 = y * p01;
-                        double inv[4] = {y01 * qq[1], y01 * qq[0], y23 * qq[3], y23 * qq[2]};
+                        const int nmax = __reduce_max_sync(0xffffffffu, (unsigned)nq);
+                        for (int k0 = 0; k0 < nmax; k0 += 4) {
+                            double dx[4], dy[4], dz[4], qq[4];
+                            int tj[4];
+                            bool ok[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            double s2, e24;
-                            lj_params<MT>(tab, ti, tj[u], s2, e24);
-                            double aa = s2 * inv[u];
-                            double a6 = aa * aa * aa;
-                            double fs = (e24 * inv[u]) * (a6 * fma(2.0, a6, -1.0));
-                            fs = ok[u] ? fs : 0.0;
-                            fx += fs * dx[u];
-                            fy += fs * dy[u];
-                            fz += fs * dz[u];
+                            for (int u = 0; u < 4; ++u) {
+                                ok[u] = k0 + u < nq;
+                                const int q = ok[u] ? qbuf[w][k0 + u][lane] : 0;
+                                dx[u] = xi - st_x[q];
+                                dy[u] = yi - st_y[q];
+                                dz[u] = zi - st_z[q];
+                                tj[u] = st_t[q];
+                                const double r2 = dx[u] * dx[u] + dy[u] * dy[u] + dz[u] * dz[u];
+                                qq[u] = ok[u] ? r2 : 1.0;
+                            }
+                            double p01 = qq[0] * qq[1], p23 = qq[2] * qq[3];
+                            double y = fast_rcp(p01 * p23);
+                            double y01 = y * p23, y23 = y * p01;
+                            double inv[4] = {y01 * qq[1], y01 * qq[0], y23 * qq[3], y23 * qq[2]};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                double s2, e24;
+                                lj_params<MT>(tab, ti, tj[u], s2, e24);
+                                double aa = s2 * inv[u];
+                                double a6 = aa * aa * aa;
+                                double fs = (e24 * inv[u]) * (a6 * fma(2.0, a6, -1.0));
+                                fs = ok[u] ? fs : 0.0;
+                                fx += fs * dx[u];
+                                fy += fs * dy[u];
+                                fz += fs * dz[u];
+                            }
                         }
                     }
                     red[w][0][lane] = fx;
@@ -748,6 +820,7 @@ __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_ker
                 return;
             }
         }
+        if (LM == 1) return;   // list build: no force work
         if (gv.in_grid(cx, cy, cz)) {
             int c = gv.flat(cx, cy, cz);
             int s1 = gv.start[c], e1 = gv.start[c + 1];
@@ -848,12 +921,22 @@ __global__ void __launch_bounds__(WPU == 1 ? 128 : 32 * WPU) lc_c08_cellwarp_ker
 }
 
 // scratch force = the colour partials added in colour order (C08All)
-__global__ void c08_colour_sum_kernel(int64_t len, int ncol, const double* __restrict__ cpart,
+// (the partials are zeroed behind the read, ready for the next compute: no
+// memset launch per step)
+__global__ void c08_colour_sum_kernel(int64_t len, int ncol, double* __restrict__ cpart,
                                       double* __restrict__ sforce) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= len) return;
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = k < ncol ? cpart[(size_t)k * len + e] : 0.0;
     double s = 0.0;
-    for (int k = 0; k < ncol; ++k) s += cpart[(size_t)k * len + e];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (k < ncol) {
+            s += v[k];
+            cpart[(size_t)k * len + e] = 0.0;
+        }
     sforce[e] = s;
 }
 
@@ -863,6 +946,17 @@ static int lc_env_c08_all() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("MDG_LC_C08_ALL");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
+// MDG_LC_C08_LISTS: 1 (default) the one-launch C08 reads per-unit partner
+// lists built once per grid rebuild (C08Lists), 0 looks the ranges up every step
+static int lc_env_c08_lists() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_LC_C08_LISTS");
         v = e ? atoi(e) : 1;
     }
     return v;
@@ -1095,16 +1189,46 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
             }
     if (c08_all && ca.ncol > 0) {
         const size_t len = 3 * (size_t)m;
+        const double* before = gr.cpart.p;
         gr.cpart.ensure(len * ca.ncol + 1);
         if (!gr.cpart.p) return;   // out of memory: no forces (the caller's status check reports it)
-        cudaMemsetAsync(gr.cpart.p, 0, len * ca.ncol * sizeof(double), s);
+        if (gr.cpart.p != before) gr.cpart_zero = 0;
+        // the sum pass leaves the partials zeroed; the fold-fused variant does not
+        if (gr.cpart_zero < len * ca.ncol || lc_env_c08_all() == 3) {
+            cudaMemsetAsync(gr.cpart.p, 0, len * ca.ncol * sizeof(double), s);
+            gr.cpart_zero = len * ca.ncol;
+        }
         const unsigned units = (unsigned)ca.ustart[ca.ncol];
-#define MDG_C08A(N3, W) lc_c08_cellwarp_kernel<LAYOUT, MT, N3, W, true><<<units, 32 * W, 0, s>>>(gv, sp, sf, c.tab, c08tb, c08t2, cl, g.overlap[0], g.overlap[1], g.overlap[2], counter, ca, gr.cpart.p), note_launch()
         const int wpu = lc_env_c08_all_wpu();
-        if (newton3) {
-            if (wpu >= 8) MDG_C08A(true, 8); else if (wpu >= 4) MDG_C08A(true, 4); else MDG_C08A(true, 2);
+        // the units' staged partner lists, once per grid build
+        C08Lists ul{};
+        bool lists = lc_env_c08_lists() != 0;
+        if (lists) {
+            gr.c08l_tot.ensure(units + 1);
+            gr.c08l_j.ensure((size_t)units * kC08Stage + 1);
+            gr.c08l_f.ensure((size_t)units * kC08Stage + 1);
+            lists = gr.c08l_tot.p && gr.c08l_j.p && gr.c08l_f.p;
+            ul = C08Lists{gr.c08l_tot.p, gr.c08l_j.p, gr.c08l_f.p};
+        }
+        if (lists && gr.c08l_for != gr.build_id) {
+#define MDG_C08L(W) lc_c08_cellwarp_kernel<LAYOUT, MT, true, W, true, 1><<<units, 32 * W, 0, s>>>(gv, sp, sf, c.tab, c08tb, c08t2, cl, g.overlap[0], g.overlap[1], g.overlap[2], counter, ca, gr.cpart.p, ul), note_launch()
+            if (wpu >= 8) MDG_C08L(8); else if (wpu >= 4) MDG_C08L(4); else MDG_C08L(2);
+#undef MDG_C08L
+            gr.c08l_for = gr.build_id;
+        }
+#define MDG_C08A(N3, W, LM) lc_c08_cellwarp_kernel<LAYOUT, MT, N3, W, true, LM><<<units, 32 * W, 0, s>>>(gv, sp, sf, c.tab, c08tb, c08t2, cl, g.overlap[0], g.overlap[1], g.overlap[2], counter, ca, gr.cpart.p, ul), note_launch()
+        if (lists) {
+            if (newton3) {
+                if (wpu >= 8) MDG_C08A(true, 8, 2); else if (wpu >= 4) MDG_C08A(true, 4, 2); else MDG_C08A(true, 2, 2);
+            } else {
+                if (wpu >= 8) MDG_C08A(false, 8, 2); else if (wpu >= 4) MDG_C08A(false, 4, 2); else MDG_C08A(false, 2, 2);
+            }
         } else {
-            if (wpu >= 8) MDG_C08A(false, 8); else if (wpu >= 4) MDG_C08A(false, 4); else MDG_C08A(false, 2);
+            if (newton3) {
+                if (wpu >= 8) MDG_C08A(true, 8, 0); else if (wpu >= 4) MDG_C08A(true, 4, 0); else MDG_C08A(true, 2, 0);
+            } else {
+                if (wpu >= 8) MDG_C08A(false, 8, 0); else if (wpu >= 4) MDG_C08A(false, 4, 0); else MDG_C08A(false, 2, 0);
+            }
         }
 #undef MDG_C08A
         // the colour sums as their own element-parallel pass (the fold then
@@ -1112,8 +1236,10 @@ static void lc_launch(Context& c, Grid& gr, int traversal, int newton3) {
         // partials inside the fold, whose thread-per-particle chains of
         // dependent image loads then carry 8 loads per row (5.5 + 2.1 us
         // against 16.7 us at BASELINE config 1)
-        if (lc_env_c08_all() == 3)
+        if (lc_env_c08_all() == 3) {
             gr.cpart_ncol = ca.ncol;   // the fold adds the partials
+            gr.cpart_zero = 0;
+        }
         else
             c08_colour_sum_kernel<<<blocks_for((int64_t)len, 256), 256, 0, s>>>((int64_t)len, ca.ncol, gr.cpart.p, gr.sforce.p), note_launch();
     }

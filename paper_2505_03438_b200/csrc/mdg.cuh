@@ -103,6 +103,12 @@ struct Grid {
     DBuf<double> sforce;                            // 3*m ((m,3) AoS or (3,m) SoA)
     DBuf<double> cpart;                             // small-system C08: per-colour partial forces, colours x 3*m
     int cpart_ncol = 0;                             // > 0: the last compute left its forces in cpart (the fold adds them)
+    size_t cpart_zero = 0;                          // leading doubles of cpart known to be zero
+    int64_t build_id = 0;                           // bumped by every grid_rebuild
+    // small-system C08: per-unit staged partner lists of build c08l_for (lc.cu C08Lists)
+    DBuf<int> c08l_tot, c08l_j;
+    DBuf<uint8_t> c08l_f;
+    int64_t c08l_for = -1;
     void release();
 };
 

@@ -161,7 +161,8 @@ __device__ __forceinline__ unsigned long long f2fma(unsigned long long a, unsign
 constexpr int kBuildThreadsT = 256;
 constexpr int kMaxTZ = 48;
 
-__global__ void __launch_bounds__(kBuildThreadsT) vlt_build_kernel(
+template <int NT>
+__global__ void __launch_bounds__(NT) vlt_build_kernel(
     GridView gv, const TileDesc* __restrict__ desc, const int* __restrict__ tbase,
     const float4* __restrict__ b32, const double4* __restrict__ bpos,
     const unsigned* __restrict__ maxabs_bits, double ell2, int cap, int cap4,
@@ -991,6 +992,16 @@ static int vlt_env_build() {
 }
 static int vlt_prune_setup(Context& c, size_t list_entries, size_t slots);
 
+// threads per tile-build CTA (MDG_VLT_BT: 256, 384 (default), 512)
+static int vlt_env_bt() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_VLT_BT");
+        v = e ? atoi(e) : 384;
+    }
+    return v;
+}
+
 // One pass of the tiled build for the plan in v.plan: descriptors, list
 // bases, the build kernel; the host check's inputs are copied to the pinned
 // v.h_build.  0 = launched, 1 = tiling not applicable, -1 = error.
@@ -1025,11 +1036,21 @@ static int vlt_pass(Context& c) {
     }
     MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
     MDG_CUDA(cudaMemsetAsync(v.tcnt.p, 0, ((size_t)slots + 32) * sizeof(int), c.stream));
-    if (vlt_env_build() != 2)
-        vlt_build_kernel<<<ntiles, kBuildThreadsT, 0, c.stream>>>(
-            gv, desc, v.tbase.p, v.b32.p, gr.spos4.p, maxabs, ell2, v.cap, v.cap4, v.tl.p, v.tcnt.p,
-            maxcnt, gr.sort_by_z), note_launch();
-    else
+    if (vlt_env_build() != 2) {
+        // threads per tile CTA: a config-2 tile has ~283 rows, so 256 threads
+        // leave one warp for a second pass (measured 423 us at 256, 385 at 384,
+        // 467 at 512, config 2)
+#define MDG_VLTB(NT)                                                                                \
+    vlt_build_kernel<NT><<<ntiles, NT, 0, c.stream>>>(gv, desc, v.tbase.p, v.b32.p, gr.spos4.p,      \
+                                                      maxabs, ell2, v.cap, v.cap4, v.tl.p, v.tcnt.p, \
+                                                      maxcnt, gr.sort_by_z), note_launch()
+        switch (vlt_env_bt()) {
+            case 256: MDG_VLTB(256); break;
+            case 512: MDG_VLTB(512); break;
+            default: MDG_VLTB(384); break;
+        }
+#undef MDG_VLTB
+    } else
         vlt_build_warp_kernel<<<ntiles, kBuildThreadsT, 0, c.stream>>>(
             gv, desc, v.tbase.p, v.b32.p, gr.spos4.p, maxabs, ell2, v.cap, v.cap4, v.tl.p, v.tcnt.p,
             maxcnt, gr.sort_by_z), note_launch();

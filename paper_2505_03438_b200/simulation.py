@@ -158,6 +158,9 @@ class Simulation:
         self._skip_reorder = False
         self._perm_spare = None
         self._iota = self._inv = None
+        # untimed steady iterations of a fixed configuration run as one native
+        # call (mdg_run) inside run(); False: every iteration through step()
+        self.native = True
 
     @property
     def config(self):
@@ -402,9 +405,47 @@ class Simulation:
         self._restore_order()
 
     def run(self, steps, record=True):
-        for _ in range(steps):
-            self.step(record=record)
+        k = 0
+        while k < steps:
+            span = self._native_span(steps - k, record)
+            if span:
+                k += self._run_native(span)
+            else:
+                self.step(record=record)
+                k += 1
         self.flush()
+
+    # -- the fixed-configuration loop in one native call (mdg_run) ------------
+    def _native_span(self, left, record) -> int:
+        """How many of the next `left` iterations mdg_run may take: untimed
+        steady iterations of a fixed configuration whose container is built,
+        up to the next thermostat iteration (0: the eager step() runs)."""
+        if (not self.native or record or self.graphs or not self.fuse_kick_drift
+                or not isinstance(self.controller, _Fixed)
+                or not hasattr(self.calc, "run_fixed") or self._active_cfg is None):
+            return 0
+        cfg = self.controller.config
+        if self.active != cfg.id or self.p.layout != cfg.layout:
+            return 0
+        if self.reorder and cfg.container == VERLET_LISTS:
+            return 0
+        span = left
+        thermo = self.params.thermostat
+        if thermo is not None:
+            # iterations it with (it + 1) % interval == 0 run eagerly (kick, then thermostat)
+            span = min(span, (-(self.iteration + 1)) % thermo.interval_iterations)
+        return span
+
+    def _run_native(self, span) -> int:
+        cfg, params = self.controller.config, self.params
+        done, since, kick_due, flags = self.calc.run_fixed(
+            self.p, cfg, span, params.delta_t, params.gravity, params.rebuild_interval,
+            self.iteration, self.since, self._kick_due)
+        self.iteration += done
+        self.since, self._kick_due = since, kick_due
+        if flags:
+            self._check_flags(flags)   # raises (BlowUpError / ValueError), as step() does
+        return done
 
     def check(self):
         self.flush()

@@ -739,6 +739,56 @@ def test_fused_kick_drift_loop_is_bit_identical(pkg):
                 assert np.array_equal(a, b), (cid, boundary)
 
 
+def test_native_fixed_loop_matches_step_loop(pkg):
+    """Simulation.run's native spans (mdg_run: a fixed configuration's untimed
+    iterations in one C call) equal the Python step() loop bit for bit --
+    every container family, two types, gravity, a reflective axis, a
+    thermostat (its iterations run eagerly between native spans), runs split
+    at arbitrary points -- and a blow-up is reported at the same iteration."""
+    P, calc = pkg
+    from paper_2505_03438_b200.simulation import BlowUpError, Simulation
+    z = golden("traj_small.npz")
+    L = z["domain"]
+    n = len(z["pos0"])
+    tid = np.arange(n) % 2
+    types = [P.ParticleTypeInfo(0, 1.0, 1.0, 1.0), P.ParticleTypeInfo(1, 1.2, 0.9, 1.5)]
+    # the deterministic traversals (C18 / SLI / VCL-N3L add reactions with fp64 atomics)
+    for cid in ("LC-C08-N3L-SoA-CSF1", "LC-C08-N3L-AoS-CSF0.5", "LC-C01-NoN3L-SoA-CSF1",
+                "VL-List_Iter-NoN3L-AoS", "VCL-ClusterIter-NoN3L-SoA", "VL-List_Iter-NoN3L-SoA-FP32"):
+        out = []
+        for native in (False, True):
+            params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=4,
+                                        delta_t=1e-3, boundary=(P.PERIODIC, P.REFLECTIVE, P.PERIODIC),
+                                        gravity=-0.3, thermostat=P.ThermostatParams(0.9, 0.05, 7))
+            cfg = P.parse_configuration(cid)
+            parts = P.ParticleSet(z["pos0"], z["vel0"], type_ids=tid, types=types, layout=cfg.layout)
+            sim = Simulation(parts, params, cfg, fuse_kick_drift=True)
+            sim.native = native
+            snaps = []
+            for k in (3, 11, 1, 17):
+                sim.run(k, record=False)
+                snaps.append(parts.numpy("pos"))
+            sim.check()
+            out.append([parts.numpy("pos"), parts.numpy("vel"), parts.numpy("force"),
+                        parts.numpy("old_force"), np.array([sim.iteration, sim.since])] + snaps)
+        for a, b in zip(*out):
+            assert np.array_equal(a, b), cid
+    # a particle thrown out of the box: same failing iteration either way
+    pos = np.array(z["pos0"], copy=True)
+    pos[1] = pos[0] + np.array([0.3, 0.0, 0.0])
+    its = []
+    for native in (False, True):
+        params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=3,
+                                    delta_t=1e-3, boundary=(P.PERIODIC,) * 3)
+        parts = P.ParticleSet(np.mod(pos, L), z["vel0"])
+        sim = Simulation(parts, params, P.parse_configuration("LC-C08-N3L-AoS-CSF1"), fuse_kick_drift=True)
+        sim.native = native
+        with pytest.raises(BlowUpError):
+            sim.run(12, record=False)
+        its.append(sim.iteration)
+    assert its[0] == its[1], its
+
+
 def test_pipelined_host_run_blow_up_matches_step_path(pkg):
     """A particle thrown out of the box (two particles 0.3 sigma apart: the
     step-1 drift moves one by >> L) raises BlowUpError from HostSimulation.run

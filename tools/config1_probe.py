@@ -22,13 +22,19 @@ for _ in range(11):
 sim.check()
 torch.cuda.synchronize()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+import time
 a.record()
-for _ in range(steps):
-    sim.step()
+t0 = time.perf_counter()
+if os.environ.get("PROBE_EAGER"):
+    for _ in range(steps):
+        sim.step()
+else:
+    sim.run(steps, record=False)   # native fixed-configuration spans (mdg_run)
+t1 = time.perf_counter()
 sim.flush()
 b.record()
 b.synchronize()
-print(cid, "ms/step", round(a.elapsed_time(b) / steps, 4))
+print(cid, "ms/step", round(a.elapsed_time(b) / steps, 4), "host enqueue ms/step", round((t1 - t0) * 1e3 / steps, 4))
 if "--profile" in sys.argv:
     from torch.profiler import ProfilerActivity, profile
     with profile(activities=[ProfilerActivity.CUDA]) as prof:

@@ -400,10 +400,10 @@ __global__ void cell_sort_kernel(int64_t ncells, int64_t n, const int* __restric
         int v = lane < k ? tmp_ent[s + lane] : 0x7fffffff;
         double kv = lane < k ? key_of(v) : INFINITY;
         int rank = 0;
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < k; ++j) {   // k is the same for the whole warp
             int o = __shfl_sync(0xffffffffu, v, j);
             double ko = KEYZ ? __shfl_sync(0xffffffffu, kv, j) : 0.0;
-            rank += j < k && before(ko, o, kv, v);
+            rank += before(ko, o, kv, v);
         }
         MDG_DCHECK(lane >= k || rank < k);
         if (lane < k) emit(s + rank, v);

@@ -213,7 +213,8 @@ class ForceCalculator:
         if sw.value & 1:
             particles.force, particles.old_force = particles.old_force, particles.force
         if done.value:
-            self.generation += 1
+            if rebuild_now or s.value < int(since) + done.value:   # the loop rebuilt the container
+                self.generation += 1
             self._count_pending = True
         check(rc, "run")
         return int(done.value), int(s.value), bool(kd.value), int(fl.value)

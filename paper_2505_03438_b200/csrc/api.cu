@@ -169,6 +169,11 @@ int mdg_destroy(mdg_ctx* ctx) {
     for (cudaEvent_t e : ctx->c.ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->c.chunk_ev) cudaEventDestroy(e);
     if (ctx->c.step_exec) cudaGraphExecDestroy(ctx->c.step_exec);
+    for (auto& g : ctx->c.rg) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph_cur && g.graph_cur != g.graph_inst) cudaGraphDestroy(g.graph_cur);
+        if (g.graph_inst) cudaGraphDestroy(g.graph_inst);
+    }
     if (ctx->c.graph_in) cudaEventDestroy(ctx->c.graph_in);
     if (ctx->c.graph_out) cudaEventDestroy(ctx->c.graph_out);
     if (ctx->c.graph_stream) cudaStreamDestroy(ctx->c.graph_stream);
@@ -191,6 +196,7 @@ int mdg_set_system(mdg_ctx* ctx, const double domain[3], const int periodic[3], 
                    const double* mass) {
     CHECK_CTX(ctx);
     Context& c = ctx->c;
+    ++c.build_gen;
     if (!(cutoff > 0)) { set_error("cutoff must be > 0"); return MDG_EINVAL; }
     if (!(skin >= 0)) { set_error("skin must be >= 0"); return MDG_EINVAL; }
     if (ntypes < 1 || ntypes > kMaxTypes) {
@@ -267,6 +273,7 @@ int mdg_bind(mdg_ctx* ctx, int64_t n, int layout, double* pos, double* vel, doub
     if (n != c.n || layout != c.layout || pos != c.pos || vel != c.vel || force != c.force ||
         old_force != c.old_force || type_id != c.tid)
         ++c.gen;
+    if (n != c.n || layout != c.layout || type_id != c.tid) ++c.build_gen;
     c.n = n;
     c.layout = layout;
     c.pos = pos;
@@ -344,6 +351,7 @@ int mdg_rebuild(mdg_ctx* ctx, const mdg_config* cfg) {
     Context& c = ctx->c;
     tmark(c, 0);
     ++c.gen;
+    ++c.build_gen;
     if (cfg->container == MDG_VL) {
         if (vl_rebuild(c)) return MDG_ECUDA;
     } else if (cfg->container == MDG_VCL) {
@@ -624,6 +632,157 @@ int mdg_kick_drift(mdg_ctx* ctx, double dt, int has_gravity, double gravity, int
     return cuda_status("mdg_kick_drift");
 }
 
+// One steady step's device work after the drift (refresh + compute, as
+// mdg_refresh / mdg_compute do it for a built container), for capture.
+static void steady_step_kernels(Context& c, const mdg_config* cfg) {
+    if (cfg->container == MDG_LC) grid_refresh(c, *grid_for(c, cfg->csf), cfg->layout);
+    cudaMemsetAsync(c.scal.p, 0, sizeof(unsigned long long), c.stream);
+    if (cfg->container == MDG_VCL) {
+        vcl_compute(c, cfg->newton3);
+    } else if (cfg->container == MDG_VL) {
+        if (cfg->precision == MDG_FP32) vl_compute32(c);
+        else vl_compute(c, cfg->layout);
+    } else {
+        Grid& gr = *grid_for(c, cfg->csf);
+        lc_compute(c, gr, cfg->traversal, cfg->newton3, cfg->layout);
+        lc_fold_forces(c, gr, cfg->layout, cfg->traversal != MDG_C01);
+    }
+}
+
+// MDG_RUN_GRAPH: 1 (default) mdg_run replays steady steps from graphs, 0 eager
+static int run_graph_env() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_RUN_GRAPH");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
+// A steady step (kick + drift, refresh, compute) from a cached graph: 0 done,
+// 1 not possible here (the caller runs it eagerly), < 0 error.
+static int run_graph_step(Context& c, const mdg_config* cfg, double dt, int has_gravity, double gravity) {
+    if (c.n == 0) return 1;
+    bool built = cfg->container == MDG_VL ? c.vl.built
+               : cfg->container == MDG_VCL ? c.vcl.built
+               : grid_for(c, cfg->csf)->built && grid_for(c, cfg->csf)->scratch_layout == cfg->layout;
+    // mdg_timings / mdg_profile bracket kernels with events per call: eager
+    if (!built || c.layout != cfg->layout || c.timing || c.prof) return 1;
+    if (cfg->container == MDG_VL && c.vl.build_pending) return 1;   // the host check runs eagerly
+    if (!c.graph_stream) {
+        if (cudaStreamCreateWithFlags(&c.graph_stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c.graph_in, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c.graph_out, cudaEventDisableTiming) != cudaSuccess)
+            return -1;
+    }
+    struct Key {
+        mdg_config cfg;
+        double dt, gravity, prune_delta;
+        int has_gravity, layout;
+        uint64_t build_gen;
+        int64_t n, n_force;
+        const void *pos, *vel, *force, *old_force, *tid, *stream;
+    } key;
+    static_assert(sizeof(Key) <= sizeof(c.rg[0].key), "run graph key");
+    memset(&key, 0, sizeof key);
+    key.cfg = *cfg;
+    key.dt = dt;
+    key.gravity = gravity;
+    key.prune_delta = c.prune_delta;
+    key.has_gravity = has_gravity;
+    key.layout = c.layout;
+    key.build_gen = c.build_gen;
+    key.n = c.n;
+    key.n_force = c.n_force;
+    key.pos = c.pos; key.vel = c.vel; key.force = c.force; key.old_force = c.old_force;
+    key.tid = c.tid; key.stream = c.stream;
+    Context::RunGraph* g = nullptr;
+    for (auto& s : c.rg)
+        if (s.exec && memcmp(s.key, &key, sizeof key) == 0) g = &s;
+    if (!g) {
+        // capture this step; update the least recently used slot's executable
+        // graph with it (same topology after a rebuild: no re-instantiation),
+        // else instantiate anew
+        g = c.rg[0].used <= c.rg[1].used ? &c.rg[0] : &c.rg[1];
+        cudaStream_t home = c.stream;
+        bool prof = c.prof;
+        c.stream = c.graph_stream;
+        c.prof = false;
+        cudaGraph_t graph = nullptr;
+        bool ok = cudaStreamBeginCapture(c.graph_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            // as the eager step: kick + drift, then the force into the other buffer
+            integ_kick_drift(c, dt, has_gravity, gravity, false);
+            std::swap(c.force, c.old_force);
+            steady_step_kernels(c, cfg);
+            std::swap(c.force, c.old_force);   // the caller swaps after the replay
+            ok = cudaStreamEndCapture(c.graph_stream, &graph) == cudaSuccess && graph;
+        }
+        c.stream = home;
+        c.prof = prof;
+        cudaGraphNode_t root = nullptr;
+        cudaKernelNodeParams kp{};
+        size_t nroot = 1;
+        ok = ok && cudaGraphGetRootNodes(graph, &root, &nroot) == cudaSuccess && nroot == 1 &&
+             cudaGraphKernelNodeGetParams(root, &kp) == cudaSuccess;
+        bool updated = false;
+        if (ok && g->exec) {
+            cudaGraphExecUpdateResultInfo info;
+            updated = cudaGraphExecUpdate(g->exec, graph, &info) == cudaSuccess;
+            if (!updated) cudaGetLastError();
+        }
+        if (ok && !updated) {
+            if (g->exec) cudaGraphExecDestroy(g->exec);
+            if (g->graph_cur && g->graph_cur != g->graph_inst) cudaGraphDestroy(g->graph_cur);
+            if (g->graph_inst) cudaGraphDestroy(g->graph_inst);
+            g->exec = nullptr;
+            g->graph_inst = g->graph_cur = nullptr;
+            ok = cudaGraphInstantiate(&g->exec, graph, 0) == cudaSuccess;
+            if (ok) {
+                g->graph_inst = g->graph_cur = graph;
+                g->root = root;
+            }
+        } else if (ok) {
+            if (g->graph_cur && g->graph_cur != g->graph_inst) cudaGraphDestroy(g->graph_cur);
+            g->graph_cur = graph;
+        }
+        if (!ok) {
+            if (graph && graph != g->graph_inst) cudaGraphDestroy(graph);
+            if (g->exec && !g->graph_inst) {
+                cudaGraphExecDestroy(g->exec);
+                g->exec = nullptr;
+            }
+            memset(g->key, 0, sizeof g->key);
+            cudaGetLastError();
+            return 1;   // not capturable here: eager
+        }
+        g->kp = kp;
+        memcpy(g->key, &key, sizeof key);
+    }
+    g->used = ++c.rg_clock;
+    // this step's iteration tag into the captured kick_drift launch
+    alignas(16) unsigned char box[256];
+    const size_t bs = integ_box_size();
+    if (bs > sizeof box) return -1;
+    memcpy(box, g->kp.kernelParams[0], bs);
+    const unsigned long long tag = (unsigned long long)c.iter_tag;
+    memcpy(box + integ_box_tag_offset(), &tag, sizeof tag);
+    void* args[16];
+    const int na = integ_kick_drift_nparams();
+    for (int k = 0; k < na; ++k) args[k] = g->kp.kernelParams[k];
+    args[0] = box;
+    cudaKernelNodeParams kp = g->kp;
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    // (captured on the private stream; launched straight into the context
+    // stream, legacy default stream included)
+    if (cudaGraphExecKernelNodeSetParams(g->exec, g->root, &kp) != cudaSuccess ||
+        cudaGraphLaunch(g->exec, c.stream) != cudaSuccess)
+        return -1;
+    note_launch();
+    return 0;
+}
+
 int mdg_run(mdg_ctx* ctx, const mdg_config* cfg, int64_t steps, double dt, int has_gravity,
             double gravity, int rebuild_interval, int64_t iteration0, int rebuild_now, int* since,
             int* kick_due, int* swaps, int64_t* done, int* flags) {
@@ -639,6 +798,19 @@ int mdg_run(mdg_ctx* ctx, const mdg_config* cfg, int64_t steps, double dt, int h
     *flags = 0;
     for (int64_t k = 0; k < steps; ++k) {
         c.iter_tag = iteration0 + k;
+        const bool rebuild = rebuild_now || *since >= rebuild_interval;
+        if (!rebuild && *kick_due && run_graph_env()) {
+            const int r = run_graph_step(c, cfg, dt, has_gravity, gravity);
+            if (r < 0) return cuda_status("mdg_run: step graph");
+            if (r == 0) {
+                std::swap(c.force, c.old_force);
+                ++c.gen;
+                ++*swaps;
+                *since += 1;
+                *done = k + 1;
+                continue;
+            }
+        }
         if (*kick_due) {
             if (int e = mdg_kick_drift(ctx, dt, has_gravity, gravity, 0)) return e;
             std::swap(c.force, c.old_force);
@@ -648,7 +820,6 @@ int mdg_run(mdg_ctx* ctx, const mdg_config* cfg, int64_t steps, double dt, int h
         } else if (int e = mdg_drift_wrap(ctx, dt)) {
             return e;
         }
-        const bool rebuild = rebuild_now || *since >= rebuild_interval;
         if (rebuild) {
             int f = 0;
             if (int e = mdg_rebuild_checked(ctx, cfg, &f)) return e;

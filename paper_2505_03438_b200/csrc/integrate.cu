@@ -5,6 +5,8 @@
 // (loop order: drift, boundaries, F -> F_old, ..., gravity, finish_kick).
 // Arithmetic uses explicit round-to-nearest intrinsics so no multiply-add is
 // contracted: the update is bit-identical to the reference's numpy sequence.
+#include <cstddef>
+
 #include "device.cuh"
 
 namespace mdg {
@@ -218,6 +220,12 @@ void integ_kick_drift(Context& c, double dt, int has_gravity, double gravity, bo
     }
 #undef MDG_KD
 }
+
+// mdg_run's graph replays patch the iteration tag of the captured kick_drift
+// launch (its first parameter, a BoxParams)
+size_t integ_box_size() { return sizeof(BoxParams); }
+size_t integ_box_tag_offset() { return offsetof(BoxParams, tag); }
+int integ_kick_drift_nparams() { return 10; }
 
 void integ_sd_step(Context& c, double gamma, double dmax) {
     if (c.n == 0) return;

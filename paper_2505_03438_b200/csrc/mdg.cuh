@@ -243,6 +243,20 @@ struct Context {
     cudaEvent_t graph_in = nullptr, graph_out = nullptr;
     cudaGraphExec_t step_exec = nullptr;
     unsigned char step_key[96] = {0};       // what the cached graph was captured for
+    // mdg_run's steady steps replayed from graphs: one per force / old_force
+    // order (the loop swaps them every step), keyed by everything a captured
+    // step bakes in; the kick_drift node's iteration tag is patched per replay
+    uint64_t build_gen = 0;                 // bumped by rebuilds, set_system, new n / layout / types
+    struct RunGraph {
+        unsigned char key[192];
+        cudaGraph_t graph_inst = nullptr;   // instantiated from: its root is the node handle to patch
+        cudaGraph_t graph_cur = nullptr;    // the latest capture (cudaGraphExecUpdate'd in): its params
+        cudaGraphExec_t exec = nullptr;
+        cudaGraphNode_t root = nullptr;     // the kick_drift node (of graph_inst)
+        cudaKernelNodeParams kp{};          // of graph_cur's kick_drift node
+        uint64_t used = 0;
+    } rg[2];
+    uint64_t rg_clock = 0;
     DBuf<unsigned long long> scan_tmp;      // block partials for scans
     // optional CUDA-event bracketing of the force kernels (mdg_profile)
     bool prof = false;
@@ -319,6 +333,9 @@ void vl_force_rows_launch(Context& c, const uint8_t* only);
 void integ_drift_wrap(Context& c, double dt);
 void integ_finish_kick(Context& c, double dt, int has_gravity, double gravity);
 void integ_kick_drift(Context& c, double dt, int has_gravity, double gravity, bool copy);
+size_t integ_box_size();
+size_t integ_box_tag_offset();
+int integ_kick_drift_nparams();
 void integ_sd_step(Context& c, double gamma, double max_disp);
 int stats_temperature(Context& c, double* t);
 int stats_thermostat(Context& c, double target, double max_delta_t);

@@ -427,9 +427,10 @@ class Simulation:
         cfg = self.controller.config
         if self.active != cfg.id or self.p.layout != cfg.layout:
             return 0
-        if self.reorder and cfg.container == VERLET_LISTS:
-            return 0
         span = left
+        if self.reorder and cfg.container == VERLET_LISTS:
+            # the cell reorder runs at rebuilds, in step(): native spans stop short of them
+            span = min(span, max(0, self.params.rebuild_interval - self.since))
         thermo = self.params.thermostat
         if thermo is not None:
             # iterations it with (it + 1) % interval == 0 run eagerly (kick, then thermostat)
@@ -438,6 +439,7 @@ class Simulation:
 
     def _run_native(self, span) -> int:
         cfg, params = self.controller.config, self.params
+        self._reapply_order()   # as step() does: the container indexes the permuted arrays
         done, since, kick_due, flags = self.calc.run_fixed(
             self.p, cfg, span, params.delta_t, params.gravity, params.rebuild_interval,
             self.iteration, self.since, self._kick_due)

@@ -741,10 +741,12 @@ def test_fused_kick_drift_loop_is_bit_identical(pkg):
 
 def test_native_fixed_loop_matches_step_loop(pkg):
     """Simulation.run's native spans (mdg_run: a fixed configuration's untimed
-    iterations in one C call) equal the Python step() loop bit for bit --
-    every container family, two types, gravity, a reflective axis, a
-    thermostat (its iterations run eagerly between native spans), runs split
-    at arbitrary points -- and a blow-up is reported at the same iteration."""
+    iterations in one C call, steady steps replayed from captured graphs)
+    equal the Python step() loop bit for bit -- every deterministic container
+    family, two types, gravity, a reflective axis, a thermostat (its
+    iterations run eagerly between native spans), the cell reorder (spans stop
+    short of its rebuilds), runs split at arbitrary points -- and a blow-up is
+    reported at the same iteration."""
     P, calc = pkg
     from paper_2505_03438_b200.simulation import BlowUpError, Simulation
     z = golden("traj_small.npz")
@@ -753,8 +755,10 @@ def test_native_fixed_loop_matches_step_loop(pkg):
     tid = np.arange(n) % 2
     types = [P.ParticleTypeInfo(0, 1.0, 1.0, 1.0), P.ParticleTypeInfo(1, 1.2, 0.9, 1.5)]
     # the deterministic traversals (C18 / SLI / VCL-N3L add reactions with fp64 atomics)
-    for cid in ("LC-C08-N3L-SoA-CSF1", "LC-C08-N3L-AoS-CSF0.5", "LC-C01-NoN3L-SoA-CSF1",
-                "VL-List_Iter-NoN3L-AoS", "VCL-ClusterIter-NoN3L-SoA", "VL-List_Iter-NoN3L-SoA-FP32"):
+    for cid, reorder in (("LC-C08-N3L-SoA-CSF1", 0), ("LC-C08-N3L-AoS-CSF0.5", 0),
+                         ("LC-C01-NoN3L-SoA-CSF1", 0), ("VL-List_Iter-NoN3L-AoS", 0),
+                         ("VL-List_Iter-NoN3L-SoA", 1), ("VCL-ClusterIter-NoN3L-SoA", 0),
+                         ("VL-List_Iter-NoN3L-SoA-FP32", 0)):
         out = []
         for native in (False, True):
             params = P.SimulationParams(domain_size=L, cutoff=2.5, skin=0.3, rebuild_interval=4,
@@ -762,7 +766,7 @@ def test_native_fixed_loop_matches_step_loop(pkg):
                                         gravity=-0.3, thermostat=P.ThermostatParams(0.9, 0.05, 7))
             cfg = P.parse_configuration(cid)
             parts = P.ParticleSet(z["pos0"], z["vel0"], type_ids=tid, types=types, layout=cfg.layout)
-            sim = Simulation(parts, params, cfg, fuse_kick_drift=True)
+            sim = Simulation(parts, params, cfg, fuse_kick_drift=True, reorder=reorder)
             sim.native = native
             snaps = []
             for k in (3, 11, 1, 17):

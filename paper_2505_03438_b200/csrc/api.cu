@@ -420,7 +420,10 @@ int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg) {
         return MDG_EINVAL;
     }
     tmark(c, 2);
-    if (cudaMemsetAsync(c.scal.p, 0, sizeof(unsigned long long), c.stream) != cudaSuccess)
+    // the fp64 Verlet-list compute zeroes the eval count itself (in its
+    // refresh kernel, or before its row-space walk): one launch less per step
+    const bool vl64 = cfg->container == MDG_VL && cfg->precision != MDG_FP32 && c.n > 0 && c.vl.built;
+    if (!vl64 && cudaMemsetAsync(c.scal.p, 0, sizeof(unsigned long long), c.stream) != cudaSuccess)
         return cuda_status("counter reset");
     if (c.n == 0) {
         tmark(c, 3);
@@ -636,7 +639,8 @@ int mdg_kick_drift(mdg_ctx* ctx, double dt, int has_gravity, double gravity, int
 // mdg_refresh / mdg_compute do it for a built container), for capture.
 static void steady_step_kernels(Context& c, const mdg_config* cfg) {
     if (cfg->container == MDG_LC) grid_refresh(c, *grid_for(c, cfg->csf), cfg->layout);
-    cudaMemsetAsync(c.scal.p, 0, sizeof(unsigned long long), c.stream);
+    if (!(cfg->container == MDG_VL && cfg->precision != MDG_FP32))   // vl_compute zeroes it
+        cudaMemsetAsync(c.scal.p, 0, sizeof(unsigned long long), c.stream);
     if (cfg->container == MDG_VCL) {
         vcl_compute(c, cfg->newton3);
     } else if (cfg->container == MDG_VL) {

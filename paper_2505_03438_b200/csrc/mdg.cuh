@@ -327,7 +327,7 @@ struct KickArgs {
 };
 bool vlt_compute(Context& c, const KickArgs* kick = nullptr);
 template <int PLAYOUT, int SLAYOUT>
-void vl_refresh_launch(Context& c, int* zero_me);
+void vl_refresh_launch(Context& c, int* zero_me, unsigned long long* zero_cnt = nullptr);
 template <int PLAYOUT>
 void vl_force_rows_launch(Context& c, const uint8_t* only);
 void integ_drift_wrap(Context& c, double dt);

@@ -259,9 +259,10 @@ __global__ void vl_refresh_kernel(const double* __restrict__ pos, int64_t n, int
                                   const uint8_t* __restrict__ row_code, Wrap w,
                                   double4* __restrict__ s4, double* __restrict__ s3,
                                   bool from_s4, int* zero_me, float* __restrict__ disp, int* pst,
-                                  float thr) {
+                                  float thr, unsigned long long* zero_cnt = nullptr) {
     int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r == 0 && zero_me) *zero_me = 0;   // work counter of the tiled walk
+    if (r == 0 && zero_cnt) *zero_cnt = 0;   // the eval count the walk accumulates (no memset launch)
     bool over = false;
     if (r < m) {
         int src = row_src[r], code = row_code[r];
@@ -480,17 +481,17 @@ static Wrap make_wrap(const Context& c) {
 }
 
 template <int PLAYOUT, int SLAYOUT>
-void vl_refresh_launch(Context& c, int* zero_me) {
+void vl_refresh_launch(Context& c, int* zero_me, unsigned long long* zero_cnt) {
     Verlet& v = c.vl;
     Grid& gr = v.grid;
     int m = (int)gr.m;
     bool from_s4 = SLAYOUT == SOA && !v.s3_valid;
     vl_refresh_kernel<PLAYOUT, SLAYOUT><<<blocks_for(m, 256), 256, 0, c.stream>>>(
         c.pos, c.n, m, s3_stride(m), gr.row_src.p, gr.row_code.p, make_wrap(c), v.s4.p, v.s3.p, from_s4, zero_me,
-        v.prune ? v.disp.p : nullptr, v.pst.p, v.prune_thr), note_launch();
+        v.prune ? v.disp.p : nullptr, v.pst.p, v.prune_thr, zero_cnt), note_launch();
     if (SLAYOUT == SOA) v.s3_valid = true;
 }
-template void vl_refresh_launch<AOS, SOA>(Context&, int*);
+template void vl_refresh_launch<AOS, SOA>(Context&, int*, unsigned long long*);
 
 // the same unwrapped refresh for another container's rows (VCL, vcl.cu)
 void vl_refresh_into(Context& c, Grid& gr, double4* s4, double* s3, bool& s3_valid) {
@@ -506,7 +507,7 @@ void vl_refresh_into(Context& c, Grid& gr, double4* s4, double* s3, bool& s3_val
             nullptr, nullptr, nullptr, 0.f), note_launch();
     s3_valid = true;
 }
-template void vl_refresh_launch<SOA, SOA>(Context&, int*);
+template void vl_refresh_launch<SOA, SOA>(Context&, int*, unsigned long long*);
 
 // global-gather walk over the rows flagged in `only` (SoA source)
 template <int PLAYOUT>
@@ -542,8 +543,9 @@ void vl_compute(Context& c, int layout) {
     bool mt = c.tab.T > 1;
     if (v.tiled) {
         v.s3.ensure(3 * (size_t)s3_stride((int)v.grid.m) + 8);
-        if (vlt_compute(c)) return;
+        if (vlt_compute(c)) return;   // its refresh zeroes the eval count
     }
+    cudaMemsetAsync(c.scal.p, 0, sizeof(unsigned long long), c.stream);
     if (layout == SOA) v.s3.ensure(3 * (size_t)s3_stride((int)v.grid.m) + 8);
     if (c.layout == AOS) {
         if (layout == AOS) vl_launch<AOS, AOS>(c, mt);

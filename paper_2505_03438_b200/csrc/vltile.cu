@@ -1318,8 +1318,8 @@ bool vlt_compute(Context& c, const KickArgs* kick) {
     Verlet& v = c.vl;
     int* next = (int*)(c.scal.p + 6);
     bool mt = c.tab.T > 1;
-    if (c.layout == AOS) vl_refresh_launch<AOS, SOA>(c, next);
-    else vl_refresh_launch<SOA, SOA>(c, next);
+    if (c.layout == AOS) vl_refresh_launch<AOS, SOA>(c, next, c.scal.p);
+    else vl_refresh_launch<SOA, SOA>(c, next, c.scal.p);
     c.prof_mark();
     if (c.layout == AOS) {
         if (mt) vlt_launch<AOS, true>(c, kick); else vlt_launch<AOS, false>(c, kick);

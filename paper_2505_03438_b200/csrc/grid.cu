@@ -318,8 +318,10 @@ __device__ __forceinline__ int for_each_image(const BinParams& p, const int c[3]
 
 template <int LAYOUT>
 __global__ void bin_count_kernel(const double* __restrict__ pos, BinParams p,
-                                 int* __restrict__ cell_count, int* __restrict__ img_cnt) {
+                                 int* __restrict__ cell_count, int* __restrict__ img_cnt,
+                                 unsigned long long* occ2) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *occ2 = 0;   // occ2_kernel's accumulator (it runs after this launch)
     if (i >= p.n) return;
     double x, y, z;
     load_pos<LAYOUT>(pos, i, p.n, x, y, z);
@@ -329,6 +331,17 @@ __global__ void bin_count_kernel(const double* __restrict__ pos, BinParams p,
     atomicAdd(cell_count + own, 1);
     int k = for_each_image(p, c, [&](int, int cell) { atomicAdd(cell_count + cell, 1); });
     img_cnt[i] = k;
+}
+
+// sum of squared cell occupancies into *out (zeroed by bin_count_kernel)
+__global__ void occ2_kernel(const int* __restrict__ cell_count, int64_t nc, unsigned long long* out) {
+    unsigned long long s = 0;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long k = (unsigned)cell_count[c];
+        s += k * k;
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
 template <int LAYOUT>
@@ -439,16 +452,21 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
     gr.img_off.ensure(n + 1);
     MDG_CUDA(cudaMemsetAsync(gr.cell_count.p, 0, (nc + 1) * sizeof(int), st));
     MDG_CUDA(cudaMemsetAsync(gr.cell_fill.p, 0, (nc + 1) * sizeof(int), st));
+    unsigned long long* occ2 = c.scal.p + 9;
     if (n > 0) {
         if (layout == AOS)
-            bin_count_kernel<AOS><<<blocks_for(n, 256), 256, 0, st>>>(pos, p, gr.cell_count.p, gr.img_cnt.p), note_launch();
+            bin_count_kernel<AOS><<<blocks_for(n, 256), 256, 0, st>>>(pos, p, gr.cell_count.p, gr.img_cnt.p, occ2), note_launch();
         else
-            bin_count_kernel<SOA><<<blocks_for(n, 256), 256, 0, st>>>(pos, p, gr.cell_count.p, gr.img_cnt.p), note_launch();
+            bin_count_kernel<SOA><<<blocks_for(n, 256), 256, 0, st>>>(pos, p, gr.cell_count.p, gr.img_cnt.p, occ2), note_launch();
+        if (gr.sort_by_z)   // the Verlet grid: the tile plan's occupancy (Grid::occ2)
+            occ2_kernel<<<std::min<int64_t>(blocks_for(nc, 256), 4 * c.sm_count), 256, 0, st>>>(gr.cell_count.p, nc, occ2), note_launch();
     }
     // images total and cell offsets; the totals land in the pinned mirror
     exclusive_scan_i32(gr.img_cnt.p, gr.img_off.p, n, c.scal.p + 1, c.scan_tmp, st);
     MDG_CUDA(cudaMemcpyAsync(c.h_scal + 1, c.scal.p + 1, sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, st));
+    if (gr.sort_by_z)
+        MDG_CUDA(cudaMemcpyAsync(c.h_scal + 9, occ2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     exclusive_scan_i32(gr.cell_count.p, gr.cell_start.p, nc + 1, nullptr, c.scan_tmp, st);
     MDG_CUDA(cudaStreamSynchronize(st));
     if (c.flags_probe) {   // status word copied before this rebuild's first kernel
@@ -462,6 +480,7 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
     }
     gr.nimg = (int64_t)c.h_scal[1];
     gr.m = n + gr.nimg;
+    gr.occ2 = gr.sort_by_z && n > 0 ? (double)c.h_scal[9] : 0.0;
     int64_t m = gr.m;
     gr.img_src.ensure(gr.nimg + 1);
     gr.img_code.ensure(gr.nimg + 1);

@@ -88,6 +88,10 @@ struct Grid {
     int sli_major = 0;
     int sort_by_z = 0;                              // in-cell order: 0 = entry id (reference), 1 = z (VCL)
     int64_t n = 0, nimg = 0, m = 0;
+    // sum over cells of (rows in the cell)^2 at the last build: occ2 / m is the
+    // cell occupancy the average row sees (the tile plan's density; the plain
+    // mean undercounts slabs, droplets and vacuum)
+    double occ2 = 0.0;
     bool built = false;
     DBuf<int> cell_count, cell_start, cell_fill;   // ncells + 1
     DBuf<int> img_cnt, img_off;                     // n + 1

@@ -809,9 +809,21 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
         for (int it = 0;; ++it) {
             int b = it % STAGES;
             if (it >= STAGES) mbar_wait(&empty[b], (it / STAGES - 1) & 1);
+            // tiles with no walk work here -- no rows (vacuum: BASELINE
+            // config 3 is 80% empty space) or overflow tiles (the row-space
+            // kernel walks them) -- are skipped, not handed through the
+            // window ring; a dense system pays nothing extra (its descriptor
+            // load is the one the tile needs anyway)
             int t = 0;
-            if (lane == 0) t = atomicAdd(next, 1);
-            t = __shfl_sync(0xffffffffu, t, 0);
+            for (;;) {
+                if (lane == 0) t = atomicAdd(next, 1);
+                t = __shfl_sync(0xffffffffu, t, 0);
+                if (t >= ntiles) break;
+                if (lane < kDescInts / 4)
+                    reinterpret_cast<int4*>(&d[b])[lane] = reinterpret_cast<const int4*>(desc + t)[lane];
+                __syncwarp();
+                if (d[b].ni > 0 && !d[b].big) break;
+            }
             if (t >= ntiles) {
                 if (PRUNE && WRITE && lane == 0 && t == ntiles + (int)gridDim.x - 1) {
                     pst[0] = 0;   // the inner lists are fresh
@@ -823,9 +835,6 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force_kernel(
                 }
                 break;
             }
-            if (lane < kDescInts / 4)
-                reinterpret_cast<int4*>(&d[b])[lane] = reinterpret_cast<const int4*>(desc + t)[lane];
-            __syncwarp();
             const TileDesc& D = d[b];
             if (D.big) {
                 if (lane == 0) {
@@ -1082,8 +1091,12 @@ int vlt_build(Context& c) {
     v.ntiles = v.nbig = 0;
     if (!vlt_env_enabled() || c.n == 0 || gr.pruned.n != 26) return 1;
     const Geom& g = gr.g;
-    // TZ: the mean window (4 x 4 columns x TZ+2 cells) at 90% of the budget
+    // TZ: the window (4 x 4 columns x TZ+2 cells) at 90% of the budget, at
+    // the occupancy the average row sees: sum occ^2 / sum occ over the cells
+    // (BASELINE config 3's slab in 80% vacuum: 18 rows per cell against a
+    // mean of 4.3, whose tiles all overflowed the window before)
     double rho = (double)c.n / ((double)g.S[0] * g.S[1] * g.S[2]);
+    if (gr.occ2 > 0.0 && gr.m > 0) rho = std::max(rho, gr.occ2 / (double)gr.m);
     int tz = vlt_env_tz();
     int budget = vlt_env_budget();
     if (tz < 1) tz = (int)floor(0.9 * budget / ((kTX + 2) * (kTY + 2) * std::max(rho, 1e-9))) - 2;
@@ -1469,9 +1482,21 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
         for (int it = 0;; ++it) {
             int b = it % STAGES;
             if (it >= STAGES) mbar_wait(&empty[b], (it / STAGES - 1) & 1);
+            // tiles with no walk work here -- no rows (vacuum: BASELINE
+            // config 3 is 80% empty space) or overflow tiles (the row-space
+            // kernel walks them) -- are skipped, not handed through the
+            // window ring; a dense system pays nothing extra (its descriptor
+            // load is the one the tile needs anyway)
             int t = 0;
-            if (lane == 0) t = atomicAdd(next, 1);
-            t = __shfl_sync(0xffffffffu, t, 0);
+            for (;;) {
+                if (lane == 0) t = atomicAdd(next, 1);
+                t = __shfl_sync(0xffffffffu, t, 0);
+                if (t >= ntiles) break;
+                if (lane < kDescInts / 4)
+                    reinterpret_cast<int4*>(&d[b])[lane] = reinterpret_cast<const int4*>(desc + t)[lane];
+                __syncwarp();
+                if (d[b].ni > 0 && !d[b].big) break;
+            }
             if (t >= ntiles) {
                 if (PRUNE && WRITE && lane == 0 && t == ntiles + (int)gridDim.x - 1) {
                     pst[0] = 0;   // the inner lists are fresh
@@ -1483,9 +1508,6 @@ __global__ void __launch_bounds__(kTileThreads, 2) vlt_force32_kernel(
                 }
                 break;
             }
-            if (lane < kDescInts / 4)
-                reinterpret_cast<int4*>(&d[b])[lane] = reinterpret_cast<const int4*>(desc + t)[lane];
-            __syncwarp();
             const TileDesc& D = d[b];
             if (D.big) {
                 if (lane == 0) {

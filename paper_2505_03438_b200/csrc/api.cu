@@ -371,15 +371,17 @@ int mdg_rebuild_checked(mdg_ctx* ctx, const mdg_config* cfg, int* flags) {
     if (int e = validate(cfg)) return e;
     if (int e = need_system(ctx)) return e;
     Context& c = ctx->c;
-    if (cudaMemcpyAsync(c.h_scal + 2, c.scal.p + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                        c.stream) != cudaSuccess)
-        return cuda_status("mdg_rebuild_checked");
+    // the status word rides on grid_rebuild's copy of the scalars before its
+    // host synchronisation (flags_probe)
     c.flags_probe = true;
     c.flags_seen = 0;
     int e = mdg_rebuild(ctx, cfg);
-    if (c.flags_probe) {   // no synchronisation on the way (n == 0): read it now
+    if (c.flags_probe) {   // the rebuild stopped before that synchronisation: read it now
         c.flags_probe = false;
-        if (cudaStreamSynchronize(c.stream) != cudaSuccess) return cuda_status("mdg_rebuild_checked");
+        if (cudaMemcpyAsync(c.h_scal + 2, c.scal.p + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            c.stream) != cudaSuccess ||
+            cudaStreamSynchronize(c.stream) != cudaSuccess)
+            return cuda_status("mdg_rebuild_checked");
         c.flags_seen = (unsigned)(c.h_scal[2] & 3ull);
     }
     if (c.flags_seen) {

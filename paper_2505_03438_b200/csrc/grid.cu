@@ -153,111 +153,160 @@ void Verlet::release() {
 
 // ---------------------------------------------------------------- scans
 
-// Exclusive scan, three phases over tiles of 2048 elements: per-tile sums,
-// a single-CTA scan of the tile sums, then per-tile warp-shuffle scans.
-constexpr int kScanThreads = 512;
-constexpr int kScanPer = 4;
-constexpr int kTile = kScanThreads * kScanPer;
+// Exclusive scan in ONE launch (decoupled look-back): a CTA takes a tile of
+// kSpTile elements by ticket, publishes its aggregate, and warp 0 looks back
+// over the predecessors' published words, 32 at a time, until it meets an
+// inclusive prefix.  Status words carry the call's epoch (16 bits), a flag
+// (1 aggregate, 2 inclusive prefix) and the value (46 bits), so the array is
+// never cleared between calls.  Replaces three launches per scan (tile sums,
+// a one-CTA scan, tile scans): a rebuild runs three scans.  `sumsq`
+// (optional) receives the sum of squared inputs (the tile plan's occupancy).
+constexpr int kSpThreads = 256;
+constexpr int kSpPer = 16;
+constexpr int kSpTile = kSpThreads * kSpPer;
+constexpr unsigned long long kSpValMask = (1ull << 46) - 1ull;
 
-template <class TI>
-__global__ void scan_tile_sums(const TI* __restrict__ in, int64_t n, unsigned long long* sums) {
-    __shared__ unsigned long long ws[kScanThreads / 32];
-    int64_t base = (int64_t)blockIdx.x * kTile;
-    unsigned long long s = 0;
-    for (int k = 0; k < kScanPer; ++k) {
-        int64_t i = base + (int64_t)k * kScanThreads + threadIdx.x;
-        if (i < n) s += (unsigned long long)in[i];
+__device__ __forceinline__ unsigned long long sp_word(unsigned epoch, unsigned flag, unsigned long long v) {
+    return ((unsigned long long)epoch << 48) | ((unsigned long long)flag << 46) | (v & kSpValMask);
+}
+
+template <class TI, class TO>
+__global__ void __launch_bounds__(kSpThreads) scan_onepass_kernel(
+    const TI* __restrict__ in, TO* __restrict__ out, int64_t n, int64_t ntiles,
+    unsigned long long* __restrict__ st, unsigned epoch, unsigned long long* total,
+    unsigned long long* sumsq) {
+    __shared__ unsigned long long ws[kSpThreads / 32];
+    __shared__ unsigned long long s_excl;
+    __shared__ int64_t s_tile;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned* ticket = reinterpret_cast<unsigned*>(st);   // st[0]: the ticket counter
+    volatile unsigned long long* flags = st + 1;
+    if (threadIdx.x == 0) {
+        int64_t t = atomicAdd(ticket, 1u);
+        if (t == ntiles - 1) *ticket = 0u;   // every ticket of this launch is taken
+        s_tile = t;
     }
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
     __syncthreads();
-    if (threadIdx.x < 32) {
-        unsigned long long v = threadIdx.x < kScanThreads / 32 ? ws[threadIdx.x] : 0;
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (threadIdx.x == 0) sums[blockIdx.x] = v;
+    const int64_t tile = s_tile;
+    const int64_t i0 = tile * kSpTile + (int64_t)threadIdx.x * kSpPer;
+    unsigned long long v[kSpPer], loc = 0, sq = 0;
+    if (sizeof(TI) == 4 && i0 + kSpPer <= n && ((uintptr_t)in & 15) == 0) {   // a full run: four 16-byte loads
+        const int4* p4 = reinterpret_cast<const int4*>(in + i0);
+#pragma unroll
+        for (int k = 0; k < kSpPer / 4; ++k) {
+            const int4 q = p4[k];
+            v[4 * k] = (unsigned)q.x;
+            v[4 * k + 1] = (unsigned)q.y;
+            v[4 * k + 2] = (unsigned)q.z;
+            v[4 * k + 3] = (unsigned)q.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kSpPer; ++k) v[k] = i0 + k < n ? (unsigned long long)in[i0 + k] : 0ull;
     }
-}
-
-__device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long v) {
-    int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < kSpPer; ++k) {
+        loc += v[k];
+        sq += v[k] * v[k];
+    }
+    if (sumsq) {
+        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0 && sq) atomicAdd(sumsq, sq);
+    }
+    // block exclusive scan of the per-thread sums
+    unsigned long long inc = loc;
     for (int o = 1; o < 32; o <<= 1) {
-        unsigned long long t = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += t;
+        unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
     }
-    return v;
-}
-
-// Block-wide exclusive scan of one value per thread; returns the block total.
-__device__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long& total) {
-    __shared__ unsigned long long ws[32];
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    unsigned long long inc = warp_incl_scan(v);
     if (lane == 31) ws[w] = inc;
     __syncthreads();
     if (w == 0) {
-        unsigned long long x = lane < nw ? ws[lane] : 0;
-        unsigned long long xi = warp_incl_scan(x);
-        if (lane < nw) ws[lane] = xi - x;
-        if (lane == 31) ws[31] = xi;   // nw <= 31 here (512 threads -> 16 warps)
+        unsigned long long x = lane < kSpThreads / 32 ? ws[lane] : 0ull, xi = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long t = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += t;
+        }
+        const unsigned long long agg = __shfl_sync(0xffffffffu, xi, kSpThreads / 32 - 1);
+        if (lane < kSpThreads / 32) ws[lane] = xi - x;
+        // publish, then look back
+        unsigned long long excl = 0;
+        if (tile == 0) {
+            if (lane == 0) flags[0] = sp_word(epoch, 2, agg);
+        } else {
+            if (lane == 0) flags[tile] = sp_word(epoch, 1, agg);
+            int64_t p = tile - 1;
+            for (;;) {
+                const int64_t q = p - lane;
+                unsigned long long wv = 0;
+                unsigned fl = 2;   // before tile 0: nothing to add, stop
+                if (q >= 0) {
+                    do {
+                        wv = flags[q];
+                    } while ((unsigned)(wv >> 48) != epoch || ((wv >> 46) & 3ull) == 0ull);
+                    fl = (unsigned)((wv >> 46) & 3ull);
+                }
+                const unsigned pm = __ballot_sync(0xffffffffu, fl == 2);
+                const int stop = pm ? __ffs(pm) - 1 : 31;   // the nearest inclusive prefix
+                unsigned long long add = (lane <= stop && q >= 0) ? (wv & kSpValMask) : 0ull;
+                for (int o = 16; o; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+                excl += add;
+                if (pm) break;
+                p -= 32;
+            }
+            if (lane == 0) flags[tile] = sp_word(epoch, 2, excl + agg);
+        }
+        if (lane == 0) {
+            s_excl = excl;
+            if (tile == ntiles - 1 && total) *total = excl + agg;
+        }
     }
     __syncthreads();
-    unsigned long long r = inc - v + ws[w];
-    total = ws[31];
-    __syncthreads();
-    return r;
-}
-
-__global__ void scan_sums_single(unsigned long long* sums, int64_t nt, unsigned long long* total) {
-    unsigned long long carry = 0;
-    for (int64_t b = 0; b < nt; b += blockDim.x) {
-        int64_t i = b + threadIdx.x;
-        unsigned long long v = i < nt ? sums[i] : 0, tot;
-        unsigned long long e = block_excl_scan(v, tot);
-        if (i < nt) sums[i] = e + carry;
-        carry += tot;
+    unsigned long long e = s_excl + ws[w] + (inc - loc);
+    if (sizeof(TO) == 4 && i0 + kSpPer <= n && ((uintptr_t)out & 15) == 0) {   // four 16-byte stores
+        int4* o4 = reinterpret_cast<int4*>(out + i0);
+#pragma unroll
+        for (int k = 0; k < kSpPer / 4; ++k) {
+            int4 q;
+            q.x = (int)e; e += v[4 * k];
+            q.y = (int)e; e += v[4 * k + 1];
+            q.z = (int)e; e += v[4 * k + 2];
+            q.w = (int)e; e += v[4 * k + 3];
+            o4[k] = q;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kSpPer; ++k) {
+            if (i0 + k < n) out[i0 + k] = (TO)e;
+            e += v[k];
+        }
     }
-    if (threadIdx.x == 0 && total) *total = carry;
 }
 
 template <class TI, class TO>
-__global__ void scan_tiles(const TI* __restrict__ in, TO* __restrict__ out, int64_t n,
-                           const unsigned long long* __restrict__ sums) {
-    int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kScanPer;
-    unsigned long long v[kScanPer], loc = 0;
-    for (int k = 0; k < kScanPer; ++k) {
-        int64_t i = base + k;
-        v[k] = i < n ? (unsigned long long)in[i] : 0;
-        loc += v[k];
-    }
-    unsigned long long tot;
-    unsigned long long e = block_excl_scan(loc, tot) + sums[blockIdx.x];
-    for (int k = 0; k < kScanPer; ++k) {
-        int64_t i = base + k;
-        if (i < n) out[i] = (TO)e;
-        e += v[k];
-    }
-}
-
-template <class TI, class TO>
-static void scan_impl(const TI* in, TO* out, int64_t n, unsigned long long* total,
-                      DBuf<unsigned long long>& tmp, cudaStream_t s) {
-    int64_t nt = (n + kTile - 1) / kTile;
+static void scan_impl(Context& c, const TI* in, TO* out, int64_t n, unsigned long long* total,
+                      unsigned long long* sumsq) {
+    int64_t nt = (n + kSpTile - 1) / kSpTile;
     if (nt < 1) nt = 1;
-    tmp.ensure((size_t)nt);
-    scan_tile_sums<TI><<<(unsigned)nt, kScanThreads, 0, s>>>(in, n, tmp.p), note_launch();
-    scan_sums_single<<<1, kScanThreads, 0, s>>>(tmp.p, nt, total), note_launch();
-    scan_tiles<TI, TO><<<(unsigned)nt, kScanThreads, 0, s>>>(in, out, n, tmp.p), note_launch();
+    DBuf<unsigned long long>& st = c.scan_tmp;
+    const unsigned long long* before = st.p;
+    st.ensure((size_t)nt + 2);
+    if (st.p != before || ++c.scan_epoch >= 65536u) {   // fresh memory or the epoch wrapped
+        cudaMemsetAsync(st.p, 0, st.cap * sizeof(unsigned long long), c.stream);
+        c.scan_epoch = 1;
+    }
+    scan_onepass_kernel<TI, TO><<<(unsigned)nt, kSpThreads, 0, c.stream>>>(in, out, n, nt, st.p, c.scan_epoch,
+                                                                           total, sumsq), note_launch();
 }
 
-void exclusive_scan_i32(const int* in, int* out, int64_t n, unsigned long long* total,
-                        DBuf<unsigned long long>& tmp, cudaStream_t s) {
-    scan_impl<int, int>(in, out, n, total, tmp, s);
+void exclusive_scan_i32(Context& c, const int* in, int* out, int64_t n, unsigned long long* total,
+                        unsigned long long* sumsq) {
+    scan_impl<int, int>(c, in, out, n, total, sumsq);
 }
 
-void exclusive_scan_i32_to_i64(const int* in, long long* out, int64_t n,
-                               unsigned long long* total, DBuf<unsigned long long>& tmp,
-                               cudaStream_t s) {
-    scan_impl<int, long long>(in, out, n, total, tmp, s);
+void exclusive_scan_i32_to_i64(Context& c, const int* in, long long* out, int64_t n,
+                               unsigned long long* total) {
+    scan_impl<int, long long>(c, in, out, n, total, nullptr);
 }
 
 // ---------------------------------------------------------------- binning
@@ -319,9 +368,18 @@ __device__ __forceinline__ int for_each_image(const BinParams& p, const int c[3]
 template <int LAYOUT>
 __global__ void bin_count_kernel(const double* __restrict__ pos, BinParams p,
                                  int* __restrict__ cell_count, int* __restrict__ img_cnt,
-                                 unsigned long long* occ2) {
+                                 unsigned long long* scal) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) *occ2 = 0;   // occ2_kernel's accumulator (it runs after this launch)
+    if (i == 0) {
+        // this rebuild's accumulators in the context scalars, zeroed here
+        // instead of by memset launches: [9] sum of squared cell occupancies
+        // (the cell-count scan), and the Verlet build's [3] longest list, [5]
+        // max |coordinate|, [7] overflow tiles
+        scal[3] = 0;
+        scal[5] = 0;
+        scal[7] = 0;
+        scal[9] = 0;
+    }
     if (i >= p.n) return;
     double x, y, z;
     load_pos<LAYOUT>(pos, i, p.n, x, y, z);
@@ -331,17 +389,6 @@ __global__ void bin_count_kernel(const double* __restrict__ pos, BinParams p,
     atomicAdd(cell_count + own, 1);
     int k = for_each_image(p, c, [&](int, int cell) { atomicAdd(cell_count + cell, 1); });
     img_cnt[i] = k;
-}
-
-// sum of squared cell occupancies into *out (zeroed by bin_count_kernel)
-__global__ void occ2_kernel(const int* __restrict__ cell_count, int64_t nc, unsigned long long* out) {
-    unsigned long long s = 0;
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
-        unsigned long long k = (unsigned)cell_count[c];
-        s += k * k;
-    }
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
 template <int LAYOUT>
@@ -453,21 +500,20 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
     MDG_CUDA(cudaMemsetAsync(gr.cell_count.p, 0, (nc + 1) * sizeof(int), st));
     MDG_CUDA(cudaMemsetAsync(gr.cell_fill.p, 0, (nc + 1) * sizeof(int), st));
     unsigned long long* occ2 = c.scal.p + 9;
+    if (n == 0) MDG_CUDA(cudaMemsetAsync(occ2, 0, sizeof(unsigned long long), st));
     if (n > 0) {
         if (layout == AOS)
-            bin_count_kernel<AOS><<<blocks_for(n, 256), 256, 0, st>>>(pos, p, gr.cell_count.p, gr.img_cnt.p, occ2), note_launch();
+            bin_count_kernel<AOS><<<blocks_for(n, 256), 256, 0, st>>>(pos, p, gr.cell_count.p, gr.img_cnt.p, c.scal.p), note_launch();
         else
-            bin_count_kernel<SOA><<<blocks_for(n, 256), 256, 0, st>>>(pos, p, gr.cell_count.p, gr.img_cnt.p, occ2), note_launch();
-        if (gr.sort_by_z)   // the Verlet grid: the tile plan's occupancy (Grid::occ2)
-            occ2_kernel<<<std::min<int64_t>(blocks_for(nc, 256), 4 * c.sm_count), 256, 0, st>>>(gr.cell_count.p, nc, occ2), note_launch();
+            bin_count_kernel<SOA><<<blocks_for(n, 256), 256, 0, st>>>(pos, p, gr.cell_count.p, gr.img_cnt.p, c.scal.p), note_launch();
     }
-    // images total and cell offsets; the totals land in the pinned mirror
-    exclusive_scan_i32(gr.img_cnt.p, gr.img_off.p, n, c.scal.p + 1, c.scan_tmp, st);
-    MDG_CUDA(cudaMemcpyAsync(c.h_scal + 1, c.scal.p + 1, sizeof(unsigned long long),
+    // images total and cell offsets (+ the Verlet grid's squared occupancies);
+    // one copy brings [1] the image count, [2] the status word (mdg_rebuild_checked)
+    // and [9] the occupancy sum to the pinned mirror
+    exclusive_scan_i32(c, gr.img_cnt.p, gr.img_off.p, n, c.scal.p + 1);
+    exclusive_scan_i32(c, gr.cell_count.p, gr.cell_start.p, nc + 1, nullptr, gr.sort_by_z ? occ2 : nullptr);
+    MDG_CUDA(cudaMemcpyAsync(c.h_scal + 1, c.scal.p + 1, 9 * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, st));
-    if (gr.sort_by_z)
-        MDG_CUDA(cudaMemcpyAsync(c.h_scal + 9, occ2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    exclusive_scan_i32(gr.cell_count.p, gr.cell_start.p, nc + 1, nullptr, c.scan_tmp, st);
     MDG_CUDA(cudaStreamSynchronize(st));
     if (c.flags_probe) {   // status word copied before this rebuild's first kernel
         c.flags_probe = false;
@@ -543,7 +589,7 @@ int grid_owned_order(Context& c, Grid& gr, int* out) {
     int* flag = c.order_tmp.p;
     int* rank = c.order_tmp.p + m + 1;
     owned_flag_kernel<<<blocks_for(m, 256), 256, 0, c.stream>>>(m, gr.row_code.p, flag), note_launch();
-    exclusive_scan_i32(flag, rank, m, nullptr, c.scan_tmp, c.stream);
+    exclusive_scan_i32(c, flag, rank, m, nullptr);
     owned_order_kernel<<<blocks_for(m, 256), 256, 0, c.stream>>>(m, gr.row_code.p, gr.row_src.p, rank, out), note_launch();
     MDG_CUDA(cudaGetLastError());
     return 0;

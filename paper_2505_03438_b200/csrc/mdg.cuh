@@ -152,6 +152,7 @@ struct Verlet {
     DBuf<int> bmax;
     int64_t nblk = 0;
     DBuf<float> disp;          // per row: path length since the last prune (rounded up)
+    bool prune_ready = false;  // disp / pst allocated before this build (vlt_prune_prepare)
     DBuf<int> pst;             // [0] the next walk prunes, [1] prune walks since the build
     // the tile build's host check (list capacity, overflow tiles) deferred to
     // the first use of the lists (vlt_finish), so the host does not wait on
@@ -261,7 +262,8 @@ struct Context {
         uint64_t used = 0;
     } rg[2];
     uint64_t rg_clock = 0;
-    DBuf<unsigned long long> scan_tmp;      // block partials for scans
+    DBuf<unsigned long long> scan_tmp;      // single-pass scans: [0] ticket, [1..] tile status words
+    unsigned scan_epoch = 0;                // tags the status words of one scan call
     // optional CUDA-event bracketing of the force kernels (mdg_profile)
     bool prof = false;
     std::vector<cudaEvent_t> chunk_ev;   // mdg_host_step's per-chunk copy events
@@ -276,11 +278,10 @@ struct Context {
 };
 
 // ---- scans (warp-shuffle block scan, three phases) ----
-void exclusive_scan_i32(const int* in, int* out, int64_t n, unsigned long long* total,
-                        DBuf<unsigned long long>& tmp, cudaStream_t s);
-void exclusive_scan_i32_to_i64(const int* in, long long* out, int64_t n,
-                               unsigned long long* total, DBuf<unsigned long long>& tmp,
-                               cudaStream_t s);
+void exclusive_scan_i32(Context& c, const int* in, int* out, int64_t n, unsigned long long* total,
+                        unsigned long long* sumsq = nullptr);
+void exclusive_scan_i32_to_i64(Context& c, const int* in, long long* out, int64_t n,
+                               unsigned long long* total);
 
 // ---- pipeline pieces ----
 int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout);
@@ -330,6 +331,7 @@ struct KickArgs {
     int has_gravity;
 };
 bool vlt_compute(Context& c, const KickArgs* kick = nullptr);
+float* vlt_prune_prepare(Context& c);
 template <int PLAYOUT, int SLAYOUT>
 void vl_refresh_launch(Context& c, int* zero_me, unsigned long long* zero_cnt = nullptr);
 template <int PLAYOUT>

@@ -38,9 +38,11 @@ __global__ void vl_build_pos_kernel(const double* __restrict__ pos, int64_t n, i
                                     const int* __restrict__ row_src, const uint8_t* __restrict__ row_code,
                                     const int* __restrict__ row_tid, double L0, double L1, double L2,
                                     double4* __restrict__ spos4, double4* __restrict__ s4,
-                                    float4* __restrict__ b32, unsigned* __restrict__ maxabs_bits) {
+                                    float4* __restrict__ b32, unsigned* __restrict__ maxabs_bits,
+                                    float* __restrict__ disp) {
     int r = blockIdx.x * blockDim.x + threadIdx.x;
     float mx = 0.f;
+    if (disp && r <= m) disp[r] = 0.f;   // dynamic pruning: path lengths since the (first) prune
     if (r < m) {
         int src = row_src[r], code = row_code[r];
         double x = pos[pidx<PLAYOUT>(src, 0, n)] + (double)(code / 9 - 1) * L0;
@@ -215,21 +217,21 @@ int vl_rebuild(Context& c) {
         double expect = (double)c.n / vol * 4.18879020479 * ell * ell * ell;
         v.cap = ((int)(1.5 * expect) + 16 + 7) / 8 * 8;
     }
-    unsigned* maxabs = (unsigned*)(c.scal.p + 5);
+    unsigned* maxabs = (unsigned*)(c.scal.p + 5);   // zeroed by grid_rebuild's binning
     v.b32.ensure(mpad + 1);
     // the unwrapped force-time copy s4 starts from the build positions
     v.s4.ensure(mpad + 1);
-    MDG_CUDA(cudaMemsetAsync(maxabs, 0, sizeof(unsigned), c.stream));
+    float* disp = vlt_prune_prepare(c);
     if (m > 0) {
         // build-time positions pos[src] + shift (containers.py:356-358), s4, fp32 copy
         if (c.layout == AOS)
-            vl_build_pos_kernel<AOS><<<blocks_for(m, 256), 256, 0, c.stream>>>(
+            vl_build_pos_kernel<AOS><<<blocks_for(m + 1, 256), 256, 0, c.stream>>>(
                 c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_tid.p, c.L[0], c.L[1], c.L[2], gr.spos4.p,
-                v.s4.p, v.b32.p, maxabs), note_launch();
+                v.s4.p, v.b32.p, maxabs, disp), note_launch();
         else
-            vl_build_pos_kernel<SOA><<<blocks_for(m, 256), 256, 0, c.stream>>>(
+            vl_build_pos_kernel<SOA><<<blocks_for(m + 1, 256), 256, 0, c.stream>>>(
                 c.pos, c.n, m, gr.row_src.p, gr.row_code.p, gr.row_tid.p, c.L[0], c.L[1], c.L[2], gr.spos4.p,
-                v.s4.p, v.b32.p, maxabs), note_launch();
+                v.s4.p, v.b32.p, maxabs, disp), note_launch();
     }
     int e = vlt_build(c);               // tile lists (vltile.cu); 1 = not applicable
     if (e < 0) return -1;

@@ -981,7 +981,12 @@ static int vlt_env_budget();
 
 // per 32-row block of the list slots: the longest row (vlt_force_kernel's
 // producer prefetches ceil4(max) groups of every row of the block)
-__global__ void vlt_bmax_kernel(const int* __restrict__ tcnt, int64_t nblk, int* __restrict__ bmax) {
+__global__ void vlt_bmax_kernel(const int* __restrict__ tcnt, int64_t nblk, int* __restrict__ bmax,
+                                int* __restrict__ pst) {
+    if (pst && blockIdx.x == 0 && threadIdx.x == 0) {   // pruning state: the next walk prunes
+        pst[0] = 1;
+        pst[1] = pst[2] = pst[3] = 0;
+    }
     int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (w >= nblk) return;
     int c = tcnt[w * 32 + (threadIdx.x & 31)];
@@ -1014,7 +1019,7 @@ static int vlt_env_bt() {
 // One pass of the tiled build for the plan in v.plan: descriptors, list
 // bases, the build kernel; the host check's inputs are copied to the pinned
 // v.h_build.  0 = launched, 1 = tiling not applicable, -1 = error.
-static int vlt_pass(Context& c) {
+static int vlt_pass(Context& c, bool retry) {
     Verlet& v = c.vl;
     Grid& gr = v.grid;
     const TilePlan tp{v.plan[0], v.plan[1], v.plan[2], v.plan[3]};
@@ -1026,10 +1031,15 @@ static int vlt_pass(Context& c) {
     const unsigned* maxabs = (const unsigned*)(c.scal.p + 5);
     double ell2 = gr.g.ell * gr.g.ell;
     v.cap4 = std::max(8, (v.cap + 3) & ~3);   // >= 2 groups per row (walk prefetch)
-    MDG_CUDA(cudaMemsetAsync(nbig, 0, sizeof(int), c.stream));
+    // [3] longest list and [7] overflow tiles were zeroed by the rebuild's
+    // binning (bin_count_kernel); a capacity retry zeroes them here
+    if (retry) {
+        MDG_CUDA(cudaMemsetAsync(nbig, 0, sizeof(int), c.stream));
+        MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
+    }
     vlt_desc_kernel<<<blocks_for(ntiles, 128), 128, 0, c.stream>>>(gv, tp, ntiles, v.cap4, budget,
                                                                    desc, v.tsize.p, nbig), note_launch();
-    exclusive_scan_i32(v.tsize.p, v.tbase.p, ntiles, c.scal.p + 1, c.scan_tmp, c.stream);
+    exclusive_scan_i32(c, v.tsize.p, v.tbase.p, ntiles, c.scal.p + 1);
     // the lists get an upper-bound allocation (every tile's rows padded to
     // whole 32-row blocks), so their exact size is not needed on the host
     // before the build; slots (rows padded per tile) fit 32 bits, entries
@@ -1043,7 +1053,6 @@ static int vlt_pass(Context& c) {
         set_error("out of device memory (VL tile lists)");
         return -1;
     }
-    MDG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int), c.stream));
     MDG_CUDA(cudaMemsetAsync(v.tcnt.p, 0, ((size_t)slots + 32) * sizeof(int), c.stream));
     if (vlt_env_build() != 2) {
         // threads per tile CTA: a config-2 tile has ~283 rows, so 256 threads
@@ -1069,13 +1078,11 @@ static int vlt_pass(Context& c) {
         set_error("out of device memory (VL list blocks)");
         return -1;
     }
-    vlt_bmax_kernel<<<blocks_for(v.nblk * 32, 256), 256, 0, c.stream>>>(v.tcnt.p, v.nblk, v.bmax.p), note_launch();
-    MDG_CUDA(cudaMemcpyAsync(v.h_build, c.scal.p + 3, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+    vlt_bmax_kernel<<<blocks_for(v.nblk * 32, 256), 256, 0, c.stream>>>(v.tcnt.p, v.nblk, v.bmax.p,
+                                                                      v.prune_ready ? v.pst.p : nullptr), note_launch();
+    // one copy: h_build[0] = [1] list slots, [2] = [3] longest list, [6] = [7] overflow tiles
+    MDG_CUDA(cudaMemcpyAsync(v.h_build, c.scal.p + 1, 7 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                              c.stream));
-    MDG_CUDA(cudaMemcpyAsync(v.h_build + 1, c.scal.p + 1, sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, c.stream));
-    MDG_CUDA(cudaMemcpyAsync(v.h_build + 2, c.scal.p + 7, sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, c.stream));
     return 0;
 }
 
@@ -1112,7 +1119,7 @@ int vlt_build(Context& c) {
         set_error("out of device memory (VL tiles)");
         return -1;
     }
-    if (!v.h_build && cudaHostAlloc((void**)&v.h_build, 4 * sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess) {
+    if (!v.h_build && cudaHostAlloc((void**)&v.h_build, 8 * sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess) {
         v.h_build = nullptr;
         set_error("pinned allocation failed (VL tiles)");
         return -1;
@@ -1122,7 +1129,7 @@ int vlt_build(Context& c) {
         set_error("event creation failed (VL tiles)");
         return -1;
     }
-    if (int e = vlt_pass(c)) return e;
+    if (int e = vlt_pass(c, false)) return e;
     MDG_CUDA(cudaEventRecord(v.ev_build, c.stream));
     v.ntiles = ntiles;
     v.win_rows = budget;
@@ -1136,27 +1143,27 @@ int vlt_finish(Context& c) {
     if (!v.build_pending) return 0;
     v.build_pending = false;
     MDG_CUDA(cudaEventSynchronize(v.ev_build));
-    for (int attempt = 1; (int)(v.h_build[0] & 0xffffffffu) > v.cap; ++attempt) {
-        int hmax = (int)(v.h_build[0] & 0xffffffffu);
+    for (int attempt = 1; (int)(v.h_build[2] & 0xffffffffu) > v.cap; ++attempt) {
+        int hmax = (int)(v.h_build[2] & 0xffffffffu);
         if (attempt >= 3) {
             set_error("VL tile lists: capacity retries exhausted");
             v.tiled = false;
             return -1;
         }
         v.cap = (hmax + hmax / 8 + 7) / 8 * 8;
-        if (int e = vlt_pass(c)) {
+        if (int e = vlt_pass(c, true)) {
             v.tiled = false;
             return e < 0 ? -1 : (vl_build_rows(c, nullptr) ? -1 : 0);
         }
         MDG_CUDA(cudaStreamSynchronize(c.stream));
     }
     const int ntiles = v.ntiles;
-    const int big = (int)(v.h_build[2] & 0xffffffffu);
+    const int big = (int)(v.h_build[6] & 0xffffffffu);
     Grid& gr = v.grid;
     int m = (int)gr.m;
     TileDesc* desc = reinterpret_cast<TileDesc*>(v.tdesc.p);
     if (int order = vlt_env_order()) {
-        long long total = (long long)v.h_build[1];   // list slots
+        long long total = (long long)v.h_build[0];   // list slots
         int64_t nblocks = total / 32;
         int warps = (int)std::max<size_t>(1, std::min<size_t>(8, (200u << 10) / (32 * (size_t)v.cap4 * 2 + 16 * 32 * 8)));
         size_t smem = (size_t)warps * (2 * 16 * 32 * sizeof(int) + 32 * (size_t)v.cap4 * sizeof(uint16_t));
@@ -1290,9 +1297,7 @@ static int vlt_prune_setup(Context& c, size_t list_entries, size_t slots) {
     if (delta <= 0.0) return 0;
     v.tl_in.ensure(list_entries);
     v.tcnt_in.ensure(slots);
-    v.disp.ensure((size_t)v.grid.m + 1);
-    v.pst.ensure(4);
-    if (!v.tl_in.p || !v.tcnt_in.p || !v.disp.p || !v.pst.p) {
+    if (!v.tl_in.p || !v.tcnt_in.p || !v.disp.p || !v.pst.p || !v.prune_ready) {
         set_error("out of device memory (VL inner lists)");
         return -1;
     }
@@ -1300,11 +1305,24 @@ static int vlt_prune_setup(Context& c, size_t list_entries, size_t slots) {
     // rows may move (rp - rc) / 2 each; 1e-6 absorbs the rounding of r^2
     // and of the unwrapped copies (~1e-13 at these coordinates)
     v.prune_thr = (float)(0.5 * delta - 1e-6);
-    MDG_CUDA(cudaMemsetAsync(v.disp.p, 0, ((size_t)v.grid.m + 1) * sizeof(float), c.stream));
-    MDG_CUDA(cudaMemsetAsync(v.pst.p, 0, 4 * sizeof(int), c.stream));
-    MDG_CUDA(cudaMemsetAsync(v.pst.p, 1, sizeof(int), c.stream));
+    // the path lengths were zeroed by vl_build_pos_kernel and the state
+    // ("prune at the next walk") set by vlt_bmax_kernel: no memsets here,
+    // between the build's host check and the walk
     v.prune = true;
     return 0;
+}
+
+// Before the build positions pass: the pruning state's buffers, so the
+// build's own kernels initialise them (vl_rebuild).  The path lengths (nullptr:
+// no pruning configured).
+float* vlt_prune_prepare(Context& c) {
+    Verlet& v = c.vl;
+    v.prune_ready = false;
+    if (vlt_prune_delta(c) <= 0.0) return nullptr;
+    v.disp.ensure((size_t)v.grid.m + 1);
+    v.pst.ensure(4);
+    v.prune_ready = v.disp.p && v.pst.p;
+    return v.prune_ready ? v.disp.p : nullptr;
 }
 
 template <int PLAYOUT, bool MT>

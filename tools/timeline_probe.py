@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--steps", type=int, default=13)
     ap.add_argument("--config", type=int, default=2, help="BASELINE config (tools/configs_bench.py inputs)")
     ap.add_argument("--summary", action="store_true", help="per-kernel totals instead of the timeline")
+    ap.add_argument("--all", action="store_true", help="every event of the timeline (default: gaps > 3 us or > 20 us)")
     a = ap.parse_args()
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     import configs_bench
@@ -73,7 +74,7 @@ def main():
             print(f"  {us / a.steps:9.1f} us/step  x{cnt / a.steps:5.2f}  {n}")
         return
     for r in rows:
-        if r["gap_us"] > 3 or r["dur_us"] > 20:
+        if a.all or r["gap_us"] > 3 or r["dur_us"] > 20:
             print(f'{r["t_us"]:10.1f} {r["dur_us"]:8.1f} gap {r["gap_us"]:7.1f}  {r["name"]}')
 
 

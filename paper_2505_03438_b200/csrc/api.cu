@@ -674,7 +674,9 @@ static int run_graph_step(Context& c, const mdg_config* cfg, double dt, int has_
                : grid_for(c, cfg->csf)->built && grid_for(c, cfg->csf)->scratch_layout == cfg->layout;
     // mdg_timings / mdg_profile bracket kernels with events per call: eager
     if (!built || c.layout != cfg->layout || c.timing || c.prof) return 1;
-    if (cfg->container == MDG_VL && c.vl.build_pending) return 1;   // the host check runs eagerly
+    // first uses after a rebuild (host checks, lazy allocations and list
+    // builds) run eagerly: a capture must only record steady-state work
+    if (cfg->container == MDG_VL && (c.vl.build_pending || (!c.vl.tiled && !c.vl.rows_valid))) return 1;
     if (!c.graph_stream) {
         if (cudaStreamCreateWithFlags(&c.graph_stream, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&c.graph_in, cudaEventDisableTiming) != cudaSuccess ||

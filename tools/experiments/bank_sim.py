@@ -25,6 +25,9 @@ def main():
     ap.add_argument("--tz", type=int, default=4)
     ap.add_argument("--extra", type=int, default=0)
     ap.add_argument("--adaptive", action="store_true")
+    ap.add_argument("--two-choice", type=int, default=0,
+                    help="(a) with every window row stored twice, the copy offset by this many banks; "
+                         "each half-warp access picks a copy greedily (lane order)")
     ap.add_argument("--consecutive", action="store_true",
                     help="(c): no bank sort, step t = ascending entries [16t, 16t+16)")
     a = ap.parse_args()
@@ -77,9 +80,15 @@ def main():
                     for k in range(kmax):
                         wf = 0
                         for h in (chunk[:16], chunk[16:]):
-                            addr = {x[k] for x in h if k < len(x)}
-                            if addr:
-                                banks = np.bincount(np.array(sorted(addr)) % 16, minlength=16)
+                            addr = sorted({x[k] for x in h if k < len(x)})
+                            if addr and a.two_choice:
+                                load = np.zeros(16, dtype=int)
+                                for ad in addr:
+                                    b0, b1 = ad % 16, (ad + a.two_choice) % 16
+                                    load[b0 if load[b0] <= load[b1] else b1] += 1
+                                wf += load.max()
+                            elif addr:
+                                banks = np.bincount(np.array(addr) % 16, minlength=16)
                                 wf += banks.max()
                         res_a.append(wf)
                 # (b) half-warp per row, bank-sorted and dealt

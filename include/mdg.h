@@ -172,6 +172,11 @@ int mdg_ghost_unpack(mdg_ctx* ctx, const double* in, int64_t count, int64_t row0
  * Simulation(reorder=K) in one pass; no reference counterpart. */
 int mdg_gather_rows(mdg_ctx* ctx, const int64_t* order, int64_t n, int layout, const double* const* src,
                     double* const* dst, const int* tid_src, int* tid_dst);
+/* Index permutations of the cell reorder (no reference counterpart), on the
+ * context stream: op 0 out[i] = a[b[i]] (composition), 1 out[a[i]] = i
+ * (inverse), 2 out[i] = ((const int32_t*)a)[i] (mdg_owned_order's output
+ * widened to int64; b unused).  Device pointers, n entries. */
+int mdg_permutation(mdg_ctx* ctx, int op, int64_t n, const int64_t* a, const int64_t* b, int64_t* out);
 /* Rows whose particle index is >= n_force get no force work (zero force, no
  * eval count) in the tiled Verlet walk: the decomposition's ghost rows, whose
  * forces are never used (n_force < 0: every row).  Exact for the owned rows

@@ -32,7 +32,7 @@ EXPORTS = (
     "mdg_host_drift_wrap_range_ex", "mdg_d2h_async", "mdg_host_drift_wrap_range", "mdg_host_finish_kick_range",
     "mdg_set_prune", "mdg_prune_count", "mdg_rebuild_checked", "mdg_owned_order",
     "mdg_ghost_pack", "mdg_ghost_unpack", "mdg_gather_rows", "mdg_set_force_rows",
-    "mdg_set_iteration", "mdg_blowup_iteration", "mdg_run",
+    "mdg_set_iteration", "mdg_blowup_iteration", "mdg_run", "mdg_permutation",
 )
 FLAG_BLOWUP, FLAG_THERMO_ZERO = 1, 2
 
@@ -106,6 +106,7 @@ def _declare(L):
         "mdg_set_force_rows": (I, [P, I64]),
         "mdg_set_iteration": (I, [P, I64]),
         "mdg_blowup_iteration": (I, [P, ctypes.POINTER(I64)]),
+        "mdg_permutation": (I, [P, I, I64, P, P, P]),
         "mdg_run": (I, [P, CFG, I64, D, I, D, I, I64, I, ctypes.POINTER(I), ctypes.POINTER(I),
                         ctypes.POINTER(I), ctypes.POINTER(I64), ctypes.POINTER(I)]),
         "mdg_host_run": (I, [P, CFG, P, P, P, P, P, P, D, I, D, I, I, I, I, I, ctypes.POINTER(I),

@@ -125,10 +125,20 @@ class ForceCalculator:
     def owned_order(self, config):
         """Device int64 tensor: the particles in the row (cell) order of the
         container of `config` as of its last rebuild (mdg_owned_order)."""
-        out = torch.empty(self._bound_n, dtype=torch.int32, device=self.ctx.device)
-        check(lib().mdg_owned_order(self.ctx.h, ctypes.byref(config_struct(config)), out.data_ptr()),
+        n = self._bound_n
+        tmp = torch.empty(n, dtype=torch.int32, device=self.ctx.device)
+        check(lib().mdg_owned_order(self.ctx.h, ctypes.byref(config_struct(config)), tmp.data_ptr()),
               "owned_order")
-        return out.long()
+        out = torch.empty(n, dtype=torch.int64, device=self.ctx.device)
+        self.permutation(2, tmp, None, out)   # widened in libmdg, not by an eager torch cast
+        return out
+
+    def permutation(self, op, a, b, out):
+        """mdg_permutation on device tensors: op 0 out = a[b], 1 out[a] =
+        arange, 2 out = int64(a) (a int32)."""
+        check(lib().mdg_permutation(self.ctx.h, int(op), int(out.numel()), ctypes.c_void_p(a.data_ptr()),
+                                    ctypes.c_void_p(b.data_ptr() if b is not None else 0),
+                                    ctypes.c_void_p(out.data_ptr())), "permutation")
 
     def refresh(self, particles, config):
         self.bind(particles)

@@ -892,6 +892,16 @@ int mdg_gather_rows(mdg_ctx* ctx, const int64_t* order, int64_t n, int layout, c
     return cuda_status("mdg_gather_rows");
 }
 
+int mdg_permutation(mdg_ctx* ctx, int op, int64_t n, const int64_t* a, const int64_t* b, int64_t* out) {
+    CHECK_CTX(ctx);
+    if (n < 0 || op < 0 || op > 2 || (n && (!a || !out || (op == 0 && !b)))) {
+        set_error("mdg_permutation: bad arguments");
+        return MDG_EINVAL;
+    }
+    permutation(ctx->c, op, n, a, b, out);
+    return cuda_status("mdg_permutation");
+}
+
 int mdg_set_force_rows(mdg_ctx* ctx, int64_t n_force) {
     CHECK_CTX(ctx);
     ctx->c.n_force = n_force < 0 ? INT64_MAX : n_force;

@@ -84,4 +84,22 @@ void gather_rows(Context& c, const int64_t* order, int64_t n, int layout, Rows4 
     note_launch();
 }
 
+// Index permutations of the cell reorder (Simulation(reorder=K)), so the loop
+// runs no eager torch kernels: op 0 out[i] = a[b[i]] (composition), 1
+// out[a[i]] = i (inverse), 2 out[i] = ((const int32*)a)[i] (widening of
+// mdg_owned_order's output).
+__global__ void permutation_kernel(int op, int64_t n, const int64_t* __restrict__ a,
+                                   const int64_t* __restrict__ b, int64_t* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (op == 0) out[i] = a[b[i]];
+    else if (op == 1) out[a[i]] = i;
+    else out[i] = (int64_t)reinterpret_cast<const int*>(a)[i];
+}
+
+void permutation(Context& c, int op, int64_t n, const int64_t* a, const int64_t* b, int64_t* out) {
+    if (n > 0)
+        permutation_kernel<<<blocks_for(n, 256), 256, 0, c.stream>>>(op, n, a, b, out), note_launch();
+}
+
 }  // namespace mdg

@@ -312,6 +312,7 @@ void halo_unpack(Context& c, const double* in, int64_t count, int64_t row0);
 struct Rows4 {
     double* p[4];
 };
+void permutation(Context& c, int op, int64_t n, const int64_t* a, const int64_t* b, int64_t* out);
 void gather_rows(Context& c, const int64_t* order, int64_t n, int layout, Rows4 src, Rows4 dst,
                  const int* tsrc, int* tdst);
 // cell lengths for the fp32-compute Verlet walk (cell-relative positions)

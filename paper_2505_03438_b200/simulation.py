@@ -237,10 +237,9 @@ class Simulation:
         if self._perm is None or not self._permuted:
             return
         n = self._perm.numel()
-        if self._iota is None or self._iota.numel() != n or self._iota.device != self._perm.device:
-            self._iota = torch.arange(n, device=self._perm.device)
-            self._inv = torch.empty_like(self._iota)
-        self._inv[self._perm] = self._iota
+        if self._inv is None or self._inv.numel() != n or self._inv.device != self._perm.device:
+            self._inv = torch.empty_like(self._perm)
+        self.calc.permutation(1, self._perm, None, self._inv)   # inv[perm[i]] = i, in libmdg
         self._permute(self._inv)
         self._permuted = False
         self._perm_gen = self.calc.generation
@@ -262,7 +261,7 @@ class Simulation:
         self._inv = torch.empty_like(ident)
         self._reorder()                       # allocates the first spares
         self._perm_spare = torch.empty_like(self._perm)
-        torch.index_select(self._perm, 0, ident, out=self._perm_spare)   # (later compositions)
+        self.calc.permutation(0, self._perm, ident, self._perm_spare)   # (later compositions)
         self._restore_order()                 # the flush path ...
         self._reapply_order()                 # ... and the next step's re-apply
         self._permute(ident)                  # the second set of spares
@@ -279,7 +278,7 @@ class Simulation:
             out = self._perm_spare
             if out is None or out.shape != self._perm.shape or out.device != self._perm.device:
                 out = torch.empty_like(self._perm)
-            torch.index_select(self._perm, 0, order, out=out)
+            self.calc.permutation(0, self._perm, order, out)   # out = perm[order], in libmdg
             self._perm_spare, self._perm = self._perm, out
         self._permuted = True
 

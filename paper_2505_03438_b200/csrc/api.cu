@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <string>
 
+#include <vector>
 #include "../../include/mdg.h"
 #include "device.cuh"
 
@@ -22,6 +23,11 @@ void set_error(const std::string& msg) { g_err = msg; }
 
 void Context::prof_mark() {
     if (!prof) return;
+    if (capturing) {   // a step graph: an event-record node, re-pointed per replay
+        if (cap_marks < 2) cudaEventRecordWithFlags(cap_ev[cap_marks], stream, cudaEventRecordExternal);
+        ++cap_marks;
+        return;
+    }
     if (ev_used == ev_pool.size()) {
         cudaEvent_t e;
         cudaEventCreate(&e);
@@ -32,6 +38,7 @@ void Context::prof_mark() {
 
 static unsigned long long g_launches = 0;
 void note_launch() { ++g_launches; }
+void note_launches(int k) { g_launches += (unsigned long long)k; }
 unsigned long long launch_count() { return g_launches; }
 
 }  // namespace mdg
@@ -169,6 +176,8 @@ int mdg_destroy(mdg_ctx* ctx) {
     for (cudaEvent_t e : ctx->c.ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->c.chunk_ev) cudaEventDestroy(e);
     if (ctx->c.step_exec) cudaGraphExecDestroy(ctx->c.step_exec);
+    for (cudaEvent_t e : ctx->c.cap_ev)
+        if (e) cudaEventDestroy(e);
     for (auto& g : ctx->c.rg) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
         if (g.graph_cur && g.graph_cur != g.graph_inst) cudaGraphDestroy(g.graph_cur);
@@ -672,8 +681,9 @@ static int run_graph_step(Context& c, const mdg_config* cfg, double dt, int has_
     bool built = cfg->container == MDG_VL ? c.vl.built
                : cfg->container == MDG_VCL ? c.vcl.built
                : grid_for(c, cfg->csf)->built && grid_for(c, cfg->csf)->scratch_layout == cfg->layout;
-    // mdg_timings / mdg_profile bracket kernels with events per call: eager
-    if (!built || c.layout != cfg->layout || c.timing || c.prof) return 1;
+    // mdg_timings brackets kernels with events per call: eager (mdg_profile's
+    // marks become event-record nodes of the graph)
+    if (!built || c.layout != cfg->layout || c.timing) return 1;
     // first uses after a rebuild (host checks, lazy allocations and list
     // builds) run eagerly: a capture must only record steady-state work
     if (cfg->container == MDG_VL && (c.vl.build_pending || (!c.vl.tiled && !c.vl.rows_valid))) return 1;
@@ -690,6 +700,7 @@ static int run_graph_step(Context& c, const mdg_config* cfg, double dt, int has_
         uint64_t build_gen;
         int64_t n, n_force;
         const void *pos, *vel, *force, *old_force, *tid, *stream;
+        int prof;
     } key;
     static_assert(sizeof(Key) <= sizeof(c.rg[0].key), "run graph key");
     memset(&key, 0, sizeof key);
@@ -704,6 +715,10 @@ static int run_graph_step(Context& c, const mdg_config* cfg, double dt, int has_
     key.n_force = c.n_force;
     key.pos = c.pos; key.vel = c.vel; key.force = c.force; key.old_force = c.old_force;
     key.tid = c.tid; key.stream = c.stream;
+    key.prof = c.prof ? 1 : 0;
+    if (c.prof && !c.cap_ev[0]) {
+        if (cudaEventCreate(&c.cap_ev[0]) != cudaSuccess || cudaEventCreate(&c.cap_ev[1]) != cudaSuccess) return 1;
+    }
     Context::RunGraph* g = nullptr;
     for (auto& s : c.rg)
         if (s.exec && memcmp(s.key, &key, sizeof key) == 0) g = &s;
@@ -713,9 +728,9 @@ static int run_graph_step(Context& c, const mdg_config* cfg, double dt, int has_
         // else instantiate anew
         g = c.rg[0].used <= c.rg[1].used ? &c.rg[0] : &c.rg[1];
         cudaStream_t home = c.stream;
-        bool prof = c.prof;
         c.stream = c.graph_stream;
-        c.prof = false;
+        c.capturing = true;
+        c.cap_marks = 0;
         cudaGraph_t graph = nullptr;
         bool ok = cudaStreamBeginCapture(c.graph_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
         if (ok) {
@@ -727,12 +742,34 @@ static int run_graph_step(Context& c, const mdg_config* cfg, double dt, int has_
             ok = cudaStreamEndCapture(c.graph_stream, &graph) == cudaSuccess && graph;
         }
         c.stream = home;
-        c.prof = prof;
+        c.capturing = false;
+        ok = ok && (!c.prof || c.cap_marks == 2);   // the force path marks exactly twice
         cudaGraphNode_t root = nullptr;
         cudaKernelNodeParams kp{};
         size_t nroot = 1;
         ok = ok && cudaGraphGetRootNodes(graph, &root, &nroot) == cudaSuccess && nroot == 1 &&
              cudaGraphKernelNodeGetParams(root, &kp) == cudaSuccess;
+        // the graph's kernel nodes (launch accounting) and its two event-record
+        // nodes (profiling), found by their placeholder events
+        cudaGraphNode_t pn[2] = {nullptr, nullptr};
+        int nkern = 0;
+        if (ok) {
+            size_t nn = 0;
+            cudaGraphGetNodes(graph, nullptr, &nn);
+            std::vector<cudaGraphNode_t> nodes(nn);
+            if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+            for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType ty;
+                if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess) continue;
+                if (ty == cudaGraphNodeTypeKernel) ++nkern;
+                cudaEvent_t ev = nullptr;
+                if (c.prof && ty == cudaGraphNodeTypeEventRecord &&
+                    cudaGraphEventRecordNodeGetEvent(nd, &ev) == cudaSuccess)
+                    for (int k = 0; k < 2; ++k)
+                        if (ev == c.cap_ev[k]) pn[k] = nd;
+            }
+            if (c.prof) ok = pn[0] && pn[1];
+        }
         bool updated = false;
         if (ok && g->exec) {
             cudaGraphExecUpdateResultInfo info;
@@ -749,6 +786,8 @@ static int run_graph_step(Context& c, const mdg_config* cfg, double dt, int has_
             if (ok) {
                 g->graph_inst = g->graph_cur = graph;
                 g->root = root;
+                g->pnode[0] = pn[0];
+                g->pnode[1] = pn[1];
             }
         } else if (ok) {
             if (g->graph_cur && g->graph_cur != g->graph_inst) cudaGraphDestroy(g->graph_cur);
@@ -765,6 +804,7 @@ static int run_graph_step(Context& c, const mdg_config* cfg, double dt, int has_
             return 1;   // not capturable here: eager
         }
         g->kp = kp;
+        g->nkern = nkern;
         memcpy(g->key, &key, sizeof key);
     }
     g->used = ++c.rg_clock;
@@ -784,10 +824,20 @@ static int run_graph_step(Context& c, const mdg_config* cfg, double dt, int has_
     kp.extra = nullptr;
     // (captured on the private stream; launched straight into the context
     // stream, legacy default stream included)
-    if (cudaGraphExecKernelNodeSetParams(g->exec, g->root, &kp) != cudaSuccess ||
-        cudaGraphLaunch(g->exec, c.stream) != cudaSuccess)
-        return -1;
-    note_launch();
+    if (cudaGraphExecKernelNodeSetParams(g->exec, g->root, &kp) != cudaSuccess) return -1;
+    if (c.prof) {   // this replay's force-kernel marks: the next two pool events
+        for (int k = 0; k < 2; ++k) {
+            if (c.ev_used == c.ev_pool.size()) {
+                cudaEvent_t e;
+                if (cudaEventCreate(&e) != cudaSuccess) return -1;
+                c.ev_pool.push_back(e);
+            }
+            if (cudaGraphExecEventRecordNodeSetEvent(g->exec, g->pnode[k], c.ev_pool[c.ev_used++]) != cudaSuccess)
+                return -1;
+        }
+    }
+    if (cudaGraphLaunch(g->exec, c.stream) != cudaSuccess) return -1;
+    note_launches(g->nkern);
     return 0;
 }
 

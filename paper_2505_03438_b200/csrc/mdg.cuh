@@ -260,7 +260,16 @@ struct Context {
         cudaGraphNode_t root = nullptr;     // the kick_drift node (of graph_inst)
         cudaKernelNodeParams kp{};          // of graph_cur's kick_drift node
         uint64_t used = 0;
+        // mdg_profile inside the graph: the two event-record nodes around the
+        // force kernels (of graph_inst), re-pointed at pool events per replay
+        cudaGraphNode_t pnode[2] = {nullptr, nullptr};
+        int nkern = 0;                      // kernel nodes (mdg_launch_count counts them per replay)
     } rg[2];
+    // capture of a step graph in progress: prof_mark records into these
+    // placeholder events as event-record nodes (cudaEventRecordExternal)
+    bool capturing = false;
+    int cap_marks = 0;
+    cudaEvent_t cap_ev[2] = {nullptr, nullptr};
     uint64_t rg_clock = 0;
     DBuf<unsigned long long> scan_tmp;      // single-pass scans: [0] ticket, [1..] tile status words
     unsigned scan_epoch = 0;                // tags the status words of one scan call
@@ -351,6 +360,7 @@ void stats_release(Context& c);
 void set_error(const std::string& msg);
 // host-side count of kernel launches issued by the library (bench evidence)
 void note_launch();
+void note_launches(int k);
 unsigned long long launch_count();
 
 #define MDG_CUDA(x)                                                             \

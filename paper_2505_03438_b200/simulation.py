@@ -283,6 +283,12 @@ class Simulation:
         self._permuted = True
 
     def step(self, record=False):
+        # an untimed iteration of a fixed configuration: one native call
+        # (mdg_run; a steady step replays its captured graph)
+        if self._native_span(1, record):
+            since = self.since
+            self._run_native(1)
+            return self.since < since + 1   # rebuilt
         p, params, calc, ctl = self.p, self.params, self.calc, self.controller
         it = self.iteration
         self._reapply_order()

@@ -114,7 +114,8 @@ template struct DBuf<float>;
 template struct DBuf<PwLeaf>;
 
 void Grid::release() {
-    cell_count.release(); cell_start.release(); cell_fill.release();
+    cell_count.release(); cell_start.release();
+    counts_clear = 0;
     img_cnt.release(); img_off.release(); img_src.release(); img_code.release();
     tmp_ent.release(); row_ent.release(); row_src.release(); row_cell.release();
     row_tid.release(); inv.release(); row_code.release();
@@ -393,7 +394,7 @@ __global__ void bin_count_kernel(const double* __restrict__ pos, BinParams p,
 
 template <int LAYOUT>
 __global__ void bin_scatter_kernel(const double* __restrict__ pos, BinParams p,
-                                   const int* __restrict__ cell_start, int* __restrict__ cell_fill,
+                                   const int* __restrict__ cell_start, int* __restrict__ cell_count,
                                    const int* __restrict__ img_off, int* __restrict__ img_src,
                                    uint8_t* __restrict__ img_code, int* __restrict__ tmp_ent) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -404,8 +405,8 @@ __global__ void bin_scatter_kernel(const double* __restrict__ pos, BinParams p,
                 cell_coord(z, p.cl[2], p.S[2])};
     int own = ((c[0] + p.H[0]) * p.D[1] + c[1] + p.H[1]) * p.D[2] + c[2] + p.H[2];
     {
-        int slot = cell_start[own] + atomicAdd(cell_fill + own, 1);
-        MDG_DCHECK(slot < cell_start[own + 1]);
+        int slot = cell_start[own] + atomicSub(cell_count + own, 1) - 1;   // the in-cell order comes from cell_sort
+        MDG_DCHECK(slot >= cell_start[own] && slot < cell_start[own + 1]);
         tmp_ent[slot] = (int)i;
     }
     int base = img_off[i];
@@ -414,8 +415,8 @@ __global__ void bin_scatter_kernel(const double* __restrict__ pos, BinParams p,
         int e = base + q;
         img_src[e] = (int)i;
         img_code[e] = (uint8_t)code;
-        int slot = cell_start[cell] + atomicAdd(cell_fill + cell, 1);
-        MDG_DCHECK(slot < cell_start[cell + 1]);
+        int slot = cell_start[cell] + atomicSub(cell_count + cell, 1) - 1;
+        MDG_DCHECK(slot >= cell_start[cell] && slot < cell_start[cell + 1]);
         tmp_ent[slot] = (int)(p.n + e);
         ++q;
     });
@@ -492,13 +493,19 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
     }
     p.n = n;
     int64_t nc = gr.g.ncells;
+    // cell_count returns to zero by itself: bin_scatter claims slots by
+    // counting it back down, so a completed rebuild leaves it clear for the
+    // next one (no memset launches; cleared only after a fresh allocation,
+    // a change of grid or an abandoned rebuild)
+    const int* before = gr.cell_count.p;
     gr.cell_count.ensure(nc + 1);
     gr.cell_start.ensure(nc + 1);
-    gr.cell_fill.ensure(nc + 1);
     gr.img_cnt.ensure(n + 1);
     gr.img_off.ensure(n + 1);
-    MDG_CUDA(cudaMemsetAsync(gr.cell_count.p, 0, (nc + 1) * sizeof(int), st));
-    MDG_CUDA(cudaMemsetAsync(gr.cell_fill.p, 0, (nc + 1) * sizeof(int), st));
+    if (gr.cell_count.p != before || gr.counts_clear != nc + 1) {
+        MDG_CUDA(cudaMemsetAsync(gr.cell_count.p, 0, (nc + 1) * sizeof(int), st));
+    }
+    gr.counts_clear = 0;   // until this rebuild's scatter has counted them down
     unsigned long long* occ2 = c.scal.p + 9;
     if (n == 0) MDG_CUDA(cudaMemsetAsync(occ2, 0, sizeof(unsigned long long), st));
     if (n > 0) {
@@ -540,11 +547,11 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
     if (n > 0) {
         if (layout == AOS)
             bin_scatter_kernel<AOS><<<blocks_for(n, 256), 256, 0, st>>>(
-                pos, p, gr.cell_start.p, gr.cell_fill.p, gr.img_off.p, gr.img_src.p, gr.img_code.p,
+                pos, p, gr.cell_start.p, gr.cell_count.p, gr.img_off.p, gr.img_src.p, gr.img_code.p,
                 gr.tmp_ent.p), note_launch();
         else
             bin_scatter_kernel<SOA><<<blocks_for(n, 256), 256, 0, st>>>(
-                pos, p, gr.cell_start.p, gr.cell_fill.p, gr.img_off.p, gr.img_src.p, gr.img_code.p,
+                pos, p, gr.cell_start.p, gr.cell_count.p, gr.img_off.p, gr.img_src.p, gr.img_code.p,
                 gr.tmp_ent.p), note_launch();
 #define MDG_CSORT(KZ, PL)                                                                       \
     cell_sort_kernel<KZ, PL><<<blocks_for(nc * 32, 256), 256, 0, st>>>(                          \
@@ -557,6 +564,7 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
     }
     MDG_CUDA(cudaGetLastError());
     gr.built = true;
+    gr.counts_clear = nc + 1;   // the scatter counted every cell back to zero
     ++gr.build_id;
     gr.scratch_layout = -1;
     return 0;

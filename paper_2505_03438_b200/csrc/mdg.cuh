@@ -93,7 +93,8 @@ struct Grid {
     // mean undercounts slabs, droplets and vacuum)
     double occ2 = 0.0;
     bool built = false;
-    DBuf<int> cell_count, cell_start, cell_fill;   // ncells + 1
+    DBuf<int> cell_count, cell_start;              // ncells + 1
+    int64_t counts_clear = 0;                       // cell_count is all zero over this many entries
     DBuf<int> img_cnt, img_off;                     // n + 1
     DBuf<int> img_src;                              // nimg
     DBuf<uint8_t> img_code;                         // nimg

@@ -318,6 +318,9 @@ __global__ void __launch_bounds__(NT) vlt_build_kernel(
         tcnt[slot0 + q] = min(c, cap);
         if (c > cap) atomicMax(maxcnt, c);
     }
+    // the tile's padding slots (its last 32-row block): empty lists, written
+    // here instead of by a memset of every slot before the build
+    for (int q = d.ni + threadIdx.x; q < ((d.ni + 31) & ~31); q += blockDim.x) tcnt[slot0 + q] = 0;
 }
 
 // Warp-converged tiled build (MDG_VLT_BUILD=2; measured slower than the
@@ -1053,7 +1056,8 @@ static int vlt_pass(Context& c, bool retry) {
         set_error("out of device memory (VL tile lists)");
         return -1;
     }
-    MDG_CUDA(cudaMemsetAsync(v.tcnt.p, 0, ((size_t)slots + 32) * sizeof(int), c.stream));
+    // (every slot of every tile is written by the build: no memset)
+    if (vlt_env_build() == 2) MDG_CUDA(cudaMemsetAsync(v.tcnt.p, 0, ((size_t)slots + 32) * sizeof(int), c.stream));
     if (vlt_env_build() != 2) {
         // threads per tile CTA: a config-2 tile has ~283 rows, so 256 threads
         // leave one warp for a second pass (measured 423 us at 256, 385 at 384,

@@ -150,7 +150,8 @@ int mdg_create(int device, void* stream, mdg_ctx** out) {
     cudaDeviceGetAttribute(&ctx->c.sm_count, cudaDevAttrMultiProcessorCount, device);
     ctx->c.scal.ensure(16);
     if (!ctx->c.scal.p || cudaHostAlloc((void**)&ctx->c.h_scal, 16 * sizeof(unsigned long long),
-                                        cudaHostAllocDefault) != cudaSuccess) {
+                                        cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&ctx->c.d_h_scal, ctx->c.h_scal, 0) != cudaSuccess) {
         delete ctx;
         return cuda_status("allocating context scalars");
     }

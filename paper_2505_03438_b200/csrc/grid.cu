@@ -143,6 +143,7 @@ void Verlet::release() {
     if (h_build) cudaFreeHost(h_build);
     if (ev_build) cudaEventDestroy(ev_build);
     h_build = nullptr;
+    d_h_build = nullptr;
     ev_build = nullptr;
     build_pending = false;
     prune = false;
@@ -308,6 +309,17 @@ void exclusive_scan_i32(Context& c, const int* in, int* out, int64_t n, unsigned
 void exclusive_scan_i32_to_i64(Context& c, const int* in, long long* out, int64_t n,
                                unsigned long long* total) {
     scan_impl<int, long long>(c, in, out, n, total, nullptr);
+}
+
+// ---------------------------------------------------------------- scalars to host
+
+__global__ void scal_to_host_kernel(const unsigned long long* __restrict__ src, int count,
+                                    unsigned long long* __restrict__ dst) {
+    if (threadIdx.x < count) dst[threadIdx.x] = src[threadIdx.x];
+}
+
+void scal_to_host(Context& c, const unsigned long long* src, int count, unsigned long long* dst_mapped) {
+    scal_to_host_kernel<<<1, 32, 0, c.stream>>>(src, count, dst_mapped), note_launch();
 }
 
 // ---------------------------------------------------------------- binning
@@ -519,8 +531,7 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
     // and [9] the occupancy sum to the pinned mirror
     exclusive_scan_i32(c, gr.img_cnt.p, gr.img_off.p, n, c.scal.p + 1);
     exclusive_scan_i32(c, gr.cell_count.p, gr.cell_start.p, nc + 1, nullptr, gr.sort_by_z ? occ2 : nullptr);
-    MDG_CUDA(cudaMemcpyAsync(c.h_scal + 1, c.scal.p + 1, 9 * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, st));
+    scal_to_host(c, c.scal.p + 1, 9, c.d_h_scal + 1);   // (mapped pinned: no copy-engine bubble)
     MDG_CUDA(cudaStreamSynchronize(st));
     if (c.flags_probe) {   // status word copied before this rebuild's first kernel
         c.flags_probe = false;

@@ -160,7 +160,8 @@ struct Verlet {
     // the build kernel with the stream empty behind it
     bool build_pending = false;
     cudaEvent_t ev_build = nullptr;
-    unsigned long long* h_build = nullptr;   // pinned: [0] max count, [1] list slots, [2] overflow tiles
+    unsigned long long* h_build = nullptr;   // pinned (mapped): the build's scalars, written by vlt_bmax_kernel
+    unsigned long long* d_h_build = nullptr;
     int plan[5] = {0, 0, 0, 0, 0};           // ngx, ngy, nzt, tz, window budget
     void release();
 };
@@ -239,6 +240,7 @@ struct Context {
     // (bit 0 blow-up, bit 1 thermostat at T = 0)
     DBuf<unsigned long long> scal;
     unsigned long long* h_scal = nullptr;   // pinned mirror
+    unsigned long long* d_h_scal = nullptr; // its device address (mapped): kernels write it, no copy engine
     // cached steady-state step graph (mdg_step_graph)
     uint64_t gen = 0;                       // bumped by every rebuild / rebind
     // mdg_rebuild_checked: the status word rides on the rebuild's first host
@@ -343,6 +345,8 @@ struct KickArgs {
 };
 bool vlt_compute(Context& c, const KickArgs* kick = nullptr);
 float* vlt_prune_prepare(Context& c);
+bool vlt_speculate(Context& c);
+void vlt_big_rows(Context& c);
 template <int PLAYOUT, int SLAYOUT>
 void vl_refresh_launch(Context& c, int* zero_me, unsigned long long* zero_cnt = nullptr);
 template <int PLAYOUT>
@@ -362,6 +366,9 @@ void set_error(const std::string& msg);
 // host-side count of kernel launches issued by the library (bench evidence)
 void note_launch();
 void note_launches(int k);
+// scalars to a mapped pinned mirror by a one-thread kernel: a D2H copy in the
+// stream costs a ~17 us bubble between the copy and compute engines
+void scal_to_host(Context& c, const unsigned long long* src, int count, unsigned long long* dst_mapped);
 unsigned long long launch_count();
 
 #define MDG_CUDA(x)                                                             \

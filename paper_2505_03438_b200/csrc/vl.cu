@@ -212,10 +212,12 @@ int vl_rebuild(Context& c) {
     v.cnt.ensure(mpad + 1);
     if (v.cap == 0) {
         // first guess from the mean density: rho * 4/3 pi ell^3, plus headroom
+        // (MDG_VL_CAP0: a forced first guess, to exercise the capacity retry)
         double vol = c.L[0] * c.L[1] * c.L[2];
         double ell = gr.g.ell;
         double expect = (double)c.n / vol * 4.18879020479 * ell * ell * ell;
         v.cap = ((int)(1.5 * expect) + 16 + 7) / 8 * 8;
+        if (const char* e = getenv("MDG_VL_CAP0")) v.cap = std::max(8, atoi(e));
     }
     unsigned* maxabs = (unsigned*)(c.scal.p + 5);   // zeroed by grid_rebuild's binning
     v.b32.ensure(mpad + 1);
@@ -540,9 +542,30 @@ static void vl_finish_build(Context& c) {
 
 void vl_compute(Context& c, int layout) {
     if (c.n == 0) return;
-    vl_finish_build(c);
     Verlet& v = c.vl;
     bool mt = c.tab.T > 1;
+    if (vlt_speculate(c)) {
+        // the first walk after a build, queued before the build's host check
+        // (vlt_finish): the host then waits on the build while the GPU walks,
+        // instead of the GPU idling through the wake-up and the launches.  A
+        // failed check is repaired after the fact: lists rebuilt with a larger
+        // capacity are walked again (forces and count overwritten), overflow
+        // tiles' rows go through the row-space walk, a failed build falls back
+        // to the row-space lists below.
+        v.s3.ensure(3 * (size_t)s3_stride((int)v.grid.m) + 8);
+        const int cap0 = v.cap;
+        vlt_compute(c);
+        if (vlt_finish(c) == 0 && v.tiled) {
+            if (v.cap != cap0) vlt_compute(c);   // (walks the overflow tiles' rows too)
+            else vlt_big_rows(c);
+            return;
+        }
+        v.tiled = false;
+        v.prune = false;
+        vl_ensure_rows(c);
+    } else {
+        vl_finish_build(c);
+    }
     if (v.tiled) {
         v.s3.ensure(3 * (size_t)s3_stride((int)v.grid.m) + 8);
         if (vlt_compute(c)) return;   // its refresh zeroes the eval count

@@ -985,11 +985,16 @@ static int vlt_env_budget();
 // per 32-row block of the list slots: the longest row (vlt_force_kernel's
 // producer prefetches ceil4(max) groups of every row of the block)
 __global__ void vlt_bmax_kernel(const int* __restrict__ tcnt, int64_t nblk, int* __restrict__ bmax,
-                                int* __restrict__ pst) {
-    if (pst && blockIdx.x == 0 && threadIdx.x == 0) {   // pruning state: the next walk prunes
-        pst[0] = 1;
-        pst[1] = pst[2] = pst[3] = 0;
+                                int* __restrict__ pst, const unsigned long long* __restrict__ scal,
+                                unsigned long long* __restrict__ h_build) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (pst) {   // pruning state: the next walk prunes
+            pst[0] = 1;
+            pst[1] = pst[2] = pst[3] = 0;
+        }
     }
+    if (blockIdx.x == 0 && threadIdx.x < 7)   // the build's scalars [1..7] to the mapped pinned mirror
+        h_build[threadIdx.x] = scal[1 + threadIdx.x];
     int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (w >= nblk) return;
     int c = tcnt[w * 32 + (threadIdx.x & 31)];
@@ -1083,10 +1088,10 @@ static int vlt_pass(Context& c, bool retry) {
         return -1;
     }
     vlt_bmax_kernel<<<blocks_for(v.nblk * 32, 256), 256, 0, c.stream>>>(v.tcnt.p, v.nblk, v.bmax.p,
-                                                                      v.prune_ready ? v.pst.p : nullptr), note_launch();
-    // one copy: h_build[0] = [1] list slots, [2] = [3] longest list, [6] = [7] overflow tiles
-    MDG_CUDA(cudaMemcpyAsync(v.h_build, c.scal.p + 1, 7 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                             c.stream));
+                                                                      v.prune_ready ? v.pst.p : nullptr, c.scal.p,
+                                                                      v.d_h_build), note_launch();
+    // (vlt_bmax_kernel wrote h_build[0] = [1] list slots, [2] = [3] longest list,
+    // [6] = [7] overflow tiles into the mapped pinned mirror: no copy-engine bubble)
     return 0;
 }
 
@@ -1123,7 +1128,8 @@ int vlt_build(Context& c) {
         set_error("out of device memory (VL tiles)");
         return -1;
     }
-    if (!v.h_build && cudaHostAlloc((void**)&v.h_build, 8 * sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess) {
+    if (!v.h_build && (cudaHostAlloc((void**)&v.h_build, 8 * sizeof(unsigned long long), cudaHostAllocMapped) != cudaSuccess ||
+                       cudaHostGetDevicePointer((void**)&v.d_h_build, v.h_build, 0) != cudaSuccess)) {
         v.h_build = nullptr;
         set_error("pinned allocation failed (VL tiles)");
         return -1;
@@ -1199,6 +1205,37 @@ int vlt_finish(Context& c) {
     if (getenv("MDG_VLT_DEBUG"))
         fprintf(stderr, "vlt: tz=%d tiles=%d big=%d cap=%d cap4=%d\n", v.plan[3], ntiles, big, v.cap, v.cap4);
     return 0;
+}
+
+// MDG_VLT_SPECULATE: 1 (default) the first walk after a build is queued before
+// the build's host check (vlt_speculate / vl_compute), 0 after it
+static int vlt_env_speculate() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MDG_VLT_SPECULATE");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
+static int vlt_prune_setup(Context& c, size_t list_entries, size_t slots);
+
+// A build whose host check is still pending: prepare the walk to run before
+// that check (the inner-list buffers and the pruning state, assuming no
+// overflow tiles), so the host waits on the build while the GPU already
+// walks.  False: check first (speculation off, or the opt-in list reorder).
+bool vlt_speculate(Context& c) {
+    Verlet& v = c.vl;
+    if (!v.build_pending || !v.tiled || !vlt_env_speculate() || vlt_env_order()) return false;
+    long long slots = (long long)c.n + 32ll * v.ntiles;
+    return vlt_prune_setup(c, (size_t)(slots * v.cap4) + 8, (size_t)slots + 32) == 0;
+}
+
+// the overflow tiles' rows through the row-space walk (after vlt_finish)
+void vlt_big_rows(Context& c) {
+    if (!c.vl.nbig) return;
+    if (c.layout == AOS) vl_force_rows_launch<AOS>(c, c.vl.big_row.p);
+    else vl_force_rows_launch<SOA>(c, c.vl.big_row.p);
 }
 
 // window ring: STAGES buffers of `budget` rows (MDG_VLT_STAGES, MDG_VLT_WIN)

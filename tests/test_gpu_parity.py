@@ -584,13 +584,21 @@ def test_gpu_training_sweep_writes_reference_csv(pkg, tmp_path):
                                  {"MDG_VLT_STAGES": "3", "MDG_VLT_WIN": "1024"},
                                  {"MDG_LC_ROWS": "0", "_prefix": "LC-C18"},
                                  {"MDG_LC_C08": "0", "_prefix": "LC-C08"},
-                                 {"MDG_LC_C08": "2", "_prefix": "LC-C08"}])
+                                 {"MDG_LC_C08": "2", "_prefix": "LC-C08"},
+                                 {"MDG_VL_CAP0": "8"}, {"MDG_VL_CAP0": "8", "MDG_VLT_SPECULATE": "0"},
+                                 {"MDG_VLT_SPECULATE": "0", "MDG_VLT_WIN": "256"},
+                                 {"MDG_LC_C08_ALL": "0", "_prefix": "LC-C08"},
+                                 {"MDG_LC_C08_LISTS": "0", "_prefix": "LC-C08"},
+                                 {"MDG_LC_C08_ALL": "3", "_prefix": "LC-C08"}])
 def test_vl_walk_variants_match_reference(pkg, env):
     """The tunable paths of the Verlet walk against the reference forces and
     counts: a tiny window budget (most tiles overflow to the row-space walk),
-    bank-aware list order, the untiled walk, a 3-stage window ring; and the
-    alternative linked-cell realisations (C18 per-colour warp tiles, C08 warp
-    tiles, C08 in one launch)."""
+    bank-aware list order, the untiled walk, a 3-stage window ring, a list
+    capacity guessed far too small (the build's capacity retry, with the first
+    walk queued before the build's check and without); and the alternative
+    linked-cell realisations (C18 per-colour warp tiles, C08 warp tiles, C08
+    in one launch with atomics, colour by colour, without per-unit lists, with
+    the colour partials added in the fold)."""
     env = dict(env)
     prefix = env.pop("_prefix", "VL-")
     import os

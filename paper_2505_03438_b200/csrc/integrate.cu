@@ -6,6 +6,7 @@
 // Arithmetic uses explicit round-to-nearest intrinsics so no multiply-add is
 // contracted: the update is bit-identical to the reference's numpy sequence.
 #include <cstddef>
+#include <type_traits>
 
 #include "device.cuh"
 
@@ -223,9 +224,15 @@ void integ_kick_drift(Context& c, double dt, int has_gravity, double gravity, bo
 
 // mdg_run's graph replays patch the iteration tag of the captured kick_drift
 // launch (its first parameter, a BoxParams)
+template <class... A>
+constexpr int kernel_nparams(void (*)(A...)) { return (int)sizeof...(A); }
+static_assert(std::is_same<decltype(kick_drift_kernel<AOS, false>),
+                           void(BoxParams, const int*, const double*, double*, double*, double*,
+                                double*, int, double, unsigned long long*)>::value,
+              "mdg_run patches kick_drift_kernel's first parameter (a BoxParams) per graph replay");
 size_t integ_box_size() { return sizeof(BoxParams); }
 size_t integ_box_tag_offset() { return offsetof(BoxParams, tag); }
-int integ_kick_drift_nparams() { return 10; }
+int integ_kick_drift_nparams() { return kernel_nparams(&kick_drift_kernel<AOS, false>); }
 
 void integ_sd_step(Context& c, double gamma, double dmax) {
     if (c.n == 0) return;

@@ -747,6 +747,32 @@ def test_fused_kick_drift_loop_is_bit_identical(pkg):
                 assert np.array_equal(a, b), (cid, boundary)
 
 
+def test_permutation_ops_match_numpy(pkg):
+    """mdg_permutation (the cell reorder's index work in libmdg): composition,
+    inverse and the int32 -> int64 widening, against numpy."""
+    P, calc_mod = pkg
+    from paper_2505_03438_b200.calculator import ForceCalculator
+    z = golden("traj_small.npz")
+    params = P.SimulationParams(domain_size=z["domain"], cutoff=2.5, skin=0.3, rebuild_interval=10,
+                                delta_t=1e-3, boundary=(P.PERIODIC,) * 3)
+    calc = ForceCalculator(P.ParticleSet(z["pos0"]), params)
+    rng = np.random.default_rng(3)
+    for n in (1, 1000, 100_003):
+        a = rng.permutation(n)
+        b = rng.permutation(n)
+        ta, tb = torch.tensor(a, device="cuda"), torch.tensor(b, device="cuda")
+        out = torch.empty(n, dtype=torch.int64, device="cuda")
+        calc.permutation(0, ta, tb, out)
+        assert np.array_equal(out.cpu().numpy(), a[b])
+        calc.permutation(1, ta, None, out)
+        inv = np.empty(n, dtype=np.int64)
+        inv[a] = np.arange(n)
+        assert np.array_equal(out.cpu().numpy(), inv)
+        calc.permutation(2, torch.tensor(a.astype(np.int32), device="cuda"), None, out)
+        assert np.array_equal(out.cpu().numpy(), a)
+    calc.close()
+
+
 def test_native_fixed_loop_matches_step_loop(pkg):
     """Simulation.run's native spans (mdg_run: a fixed configuration's untimed
     iterations in one C call, steady steps replayed from captured graphs)

@@ -195,6 +195,15 @@ def test_empty_set_and_layout_mismatch(pkg):
         parts = P.ParticleSet(np.zeros((0, 3)))
         _, count = calc.compute_forces(parts, cfg, params)
         assert count == 0
+    # the loop on an empty set, native spans included (mdg_run)
+    from paper_2505_03438_b200.simulation import Simulation
+    for cid in ("VL-List_Iter-NoN3L-SoA", "LC-C08-N3L-AoS-CSF1", "VCL-ClusterIter-NoN3L-SoA"):
+        cfg = P.parse_configuration(cid)
+        parts = P.ParticleSet(np.zeros((0, 3)), layout=cfg.layout)
+        sim = Simulation(parts, params, cfg, fuse_kick_drift=True)
+        sim.run(13, record=False)
+        sim.check()
+        assert sim.iteration == 13 and sim.calc.last_eval_count == 0
     parts = P.ParticleSet(np.random.default_rng(0).uniform(0, 9, (20, 3)))
     fc = calc.ForceCalculator(parts, params)
     cfg = P.parse_configuration("LC-C08-N3L-SoA-CSF1")

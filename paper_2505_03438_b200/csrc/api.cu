@@ -8,6 +8,7 @@
 #include <string>
 
 #include <vector>
+#include <nvtx3/nvToolsExt.h>
 #include "../../include/mdg.h"
 #include "device.cuh"
 
@@ -128,6 +129,29 @@ static int need_system(mdg_ctx* ctx) {
     }
     return MDG_OK;
 }
+
+// NVTX ranges around the ABI's phases (SURVEY §5 tracing): visible to Nsight
+// tools in the "mdg" domain; without a tool attached a range is one pointer test.
+namespace {
+nvtxDomainHandle_t nvtx_domain() {
+    static nvtxDomainHandle_t d = nvtxDomainCreateA("mdg");
+    return d;
+}
+struct NvtxRange {
+    explicit NvtxRange(const char* name) {
+        nvtxEventAttributes_t a = {};
+        a.version = NVTX_VERSION;
+        a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+        a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+        a.message.ascii = name;
+        nvtxDomainRangePushEx(nvtx_domain(), &a);
+    }
+    ~NvtxRange() { nvtxDomainRangePop(nvtx_domain()); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
+#define MDG_RANGE(name) NvtxRange nvtx_range_(name)
 
 extern "C" {
 
@@ -355,6 +379,7 @@ int mdg_prune_count(mdg_ctx* ctx, int64_t* prunes) {
 }
 
 int mdg_rebuild(mdg_ctx* ctx, const mdg_config* cfg) {
+    MDG_RANGE("mdg_rebuild");
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;
     if (int e = need_system(ctx)) return e;
@@ -375,6 +400,7 @@ int mdg_rebuild(mdg_ctx* ctx, const mdg_config* cfg) {
 }
 
 int mdg_rebuild_checked(mdg_ctx* ctx, const mdg_config* cfg, int* flags) {
+    MDG_RANGE("mdg_rebuild_checked");
     CHECK_CTX(ctx);
     if (!flags) { set_error("null output"); return MDG_EINVAL; }
     *flags = 0;
@@ -406,6 +432,7 @@ int mdg_rebuild_checked(mdg_ctx* ctx, const mdg_config* cfg, int* flags) {
 }
 
 int mdg_refresh(mdg_ctx* ctx, const mdg_config* cfg) {
+    MDG_RANGE("mdg_refresh");
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;
     Context& c = ctx->c;
@@ -423,6 +450,7 @@ int mdg_refresh(mdg_ctx* ctx, const mdg_config* cfg) {
 }
 
 int mdg_compute(mdg_ctx* ctx, const mdg_config* cfg) {
+    MDG_RANGE("mdg_compute");
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;
     Context& c = ctx->c;
@@ -485,6 +513,7 @@ int mdg_lc_pairs(mdg_ctx* ctx, double csf, int64_t cap, int32_t* pairs, int64_t*
 
 int mdg_compute_kick(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gravity,
                      double gravity) {
+    MDG_RANGE("mdg_compute_kick");
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;
     if (int e = need_system(ctx)) return e;
@@ -521,6 +550,7 @@ int mdg_compute_kick(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gra
 }
 
 int mdg_step_graph(mdg_ctx* ctx, const mdg_config* cfg, double dt, int has_gravity, double gravity) {
+    MDG_RANGE("mdg_step_graph");
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;
     if (int e = need_system(ctx)) return e;
@@ -627,6 +657,7 @@ int mdg_eval_count(mdg_ctx* ctx, int64_t* count) {
 }
 
 int mdg_drift_wrap(mdg_ctx* ctx, double dt) {
+    MDG_RANGE("mdg_drift_wrap");
     CHECK_CTX(ctx);
     if (int e = need_system(ctx)) return e;
     integ_drift_wrap(ctx->c, dt);
@@ -634,6 +665,7 @@ int mdg_drift_wrap(mdg_ctx* ctx, double dt) {
 }
 
 int mdg_finish_kick(mdg_ctx* ctx, double dt, int has_gravity, double gravity) {
+    MDG_RANGE("mdg_finish_kick");
     CHECK_CTX(ctx);
     if (int e = need_system(ctx)) return e;
     integ_finish_kick(ctx->c, dt, has_gravity, gravity);
@@ -641,6 +673,7 @@ int mdg_finish_kick(mdg_ctx* ctx, double dt, int has_gravity, double gravity) {
 }
 
 int mdg_kick_drift(mdg_ctx* ctx, double dt, int has_gravity, double gravity, int copy_old_force) {
+    MDG_RANGE("mdg_kick_drift");
     CHECK_CTX(ctx);
     if (int e = need_system(ctx)) return e;
     integ_kick_drift(ctx->c, dt, has_gravity, gravity, copy_old_force != 0);
@@ -845,6 +878,7 @@ static int run_graph_step(Context& c, const mdg_config* cfg, double dt, int has_
 int mdg_run(mdg_ctx* ctx, const mdg_config* cfg, int64_t steps, double dt, int has_gravity,
             double gravity, int rebuild_interval, int64_t iteration0, int rebuild_now, int* since,
             int* kick_due, int* swaps, int64_t* done, int* flags) {
+    MDG_RANGE("mdg_run");
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;
     if (int e = need_system(ctx)) return e;
@@ -1008,6 +1042,7 @@ int mdg_temperature(mdg_ctx* ctx, double* temperature) {
 }
 
 int mdg_thermostat(mdg_ctx* ctx, double target, double max_delta_t) {
+    MDG_RANGE("mdg_thermostat");
     CHECK_CTX(ctx);
     if (int e = need_system(ctx)) return e;
     int r = stats_thermostat(ctx->c, target, max_delta_t);
@@ -1017,6 +1052,7 @@ int mdg_thermostat(mdg_ctx* ctx, double target, double max_delta_t) {
 }
 
 int mdg_live_stats(mdg_ctx* ctx, double out[6]) {
+    MDG_RANGE("mdg_live_stats");
     CHECK_CTX(ctx);
     if (int e = need_system(ctx)) return e;
     if (!out) { set_error("null output"); return MDG_EINVAL; }
@@ -1082,6 +1118,7 @@ int mdg_host_step(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel,
 int mdg_host_step_ex(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, double* force,
                      double* old_force, const int32_t* type_id, const double* mass, double dt,
                      int has_gravity, double gravity, int rebuild, int chunks, int flags, int* blowup) {
+    MDG_RANGE("mdg_host_step_ex");
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;
     if (int e = need_system(ctx)) return e;
@@ -1158,6 +1195,7 @@ int mdg_host_run(mdg_ctx* ctx, const mdg_config* cfg, double* pos, double* vel, 
                  double* old_force, const int32_t* type_id, const double* mass, double dt,
                  int has_gravity, double gravity, int steps, int rebuild_interval, int since,
                  int rebuild_first, int chunks, int* blowup, int* steps_done) {
+    MDG_RANGE("mdg_host_run");
     CHECK_CTX(ctx);
     if (int e = validate(cfg)) return e;
     if (int e = need_system(ctx)) return e;

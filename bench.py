@@ -306,28 +306,51 @@ def gpu_arm(args, rank, world, dist):
     for _ in range(args.warmup):
         sim.step()
     sim.check()
+    warm_extra = 0
     if hasattr(sim, "warm_reorder"):
         sim.warm_reorder()
+        # on through the loop's next cell reorder, untimed: the first reorder
+        # taken inside step() (the first to compose permutations and to hand
+        # the spare arrays back) stalled the host for 3-14 ms in ~10% of the
+        # runs during some periods on the GPU pool -- always that one, never a
+        # later reorder (profiles/round2_reorder_spike.txt)
+        if args.reorder and dist is None and cfg.container == P.VERLET_LISTS:
+            warm_extra = args.reorder * (params.rebuild_interval + 1)
+            for _ in range(warm_extra):
+                sim.step()
+            sim.check()
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, period_s=float(os.environ.get("MDG_BENCH_CLOCK_PERIOD", "0.001")))
     clocks.start()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.lib().mdg_launch_count()
-    calc.profile(True)
+    calc.profile(True, reserve=args.steps + 16)   # its events created here, not in the loop
+    # the per-step events too: created (first record) before the timed loop
+    step_ms = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+    for a, b in step_ms:
+        a.record()
+        b.record()
+    torch.cuda.synchronize()
     gc.disable()   # no collector pause stalls the host's launches inside the timed steps
-    step_ms = []
+    dev_allocs0 = torch.cuda.memory_stats(dev).get("num_device_alloc", 0)
+    if os.environ.get("MDG_BENCH_STEPS"):
+        print("timed loop starts", file=sys.stderr, flush=True)
+    host_ms = [] if os.environ.get("MDG_BENCH_STEPS") else None   # host time of each step() call
     for k in range(args.steps):
         flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a, b = step_ms[k]
         a.record()
+        t0 = time.perf_counter() if host_ms is not None else 0.0
         sim.step()
         if k == args.steps - 1:
             sim.flush()   # the last step's (deferred) kick inside the timed region
         b.record()
-        step_ms.append((a, b))
+        if host_ms is not None:
+            host_ms.append(round((time.perf_counter() - t0) * 1e3, 4))
     torch.cuda.synchronize()
     gc.enable()
     launches = _lib.lib().mdg_launch_count() - launches0
@@ -337,6 +360,8 @@ def gpu_arm(args, rank, world, dist):
     total_ms = sum(a.elapsed_time(b) for a, b in step_ms)
     if os.environ.get("MDG_BENCH_STEPS"):
         print(json.dumps([round(a.elapsed_time(b), 4) for a, b in step_ms]), file=sys.stderr)
+        print("host_ms " + json.dumps(host_ms), file=sys.stderr)
+        print("cudaMallocs by torch inside the timed loop: %d" % (torch.cuda.memory_stats(dev).get("num_device_alloc", 0) - dev_allocs0), file=sys.stderr)
     sim.check()
 
     if dist is not None:
@@ -371,6 +396,10 @@ def gpu_arm(args, rank, world, dist):
            "config": workload_config(args, world), "roofline": roofline,
            "pair_interactions_per_s": round(pairs / (avg_kernel_ms * 1e-3), 1),
            "gpu_launches": int(launches), "clocks": clk}
+    if warm_extra:
+        out["config"]["warmup_extra"] = (f"{warm_extra} further untimed steps after the {args.warmup} warm-up steps take the "
+                                         "loop through its next cell reorder (one-time first-use costs); the "
+                                         "timed steps keep the reorder cadence")
     if world == 1 and not args.no_e2e and args.workload == "config2":
         out["e2e"] = e2e_arm(args, host_pos, host_vel, params)
     if world == 1 and not args.no_cpu and args.workload == "config2":

@@ -218,8 +218,10 @@ int mdg_thermostat(mdg_ctx* ctx, double target, double max_delta_t);
  * bit-identical to the reference.  Synchronises. */
 int mdg_live_stats(mdg_ctx* ctx, double out[6]);
 /* Bracket every force-kernel launch with CUDA events on the context stream
- * (enable != 0; resets the record).  mdg_profile_read synchronises and
- * returns the summed kernel time and the number of bracketed launches. */
+ * (enable != 0; resets the record; enable > 1 also creates the events of that
+ * many launches up front, so that a timed loop creates none).
+ * mdg_profile_read synchronises and returns the summed kernel time and the
+ * number of bracketed launches. */
 int mdg_profile(mdg_ctx* ctx, int enable);
 int mdg_profile_read(mdg_ctx* ctx, double* total_ms, int64_t* launches);
 /* Wait for all work of the context's stream. */

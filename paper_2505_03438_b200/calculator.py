@@ -122,14 +122,20 @@ class ForceCalculator:
                                         ctypes.byref(f)), "rebuild")
         return int(f.value)
 
-    def owned_order(self, config):
+    def owned_order(self, config, out=None, tmp=None):
         """Device int64 tensor: the particles in the row (cell) order of the
-        container of `config` as of its last rebuild (mdg_owned_order)."""
+        container of `config` as of its last rebuild (mdg_owned_order).
+        ``out`` (int64) / ``tmp`` (int32), n elements each, are used when given:
+        a caller inside a timed loop passes its own buffers, because a fresh
+        block from the caching allocator can mean a cudaMalloc (milliseconds)."""
         n = self._bound_n
-        tmp = torch.empty(n, dtype=torch.int32, device=self.ctx.device)
+        dev = self.ctx.device
+        if tmp is None or tmp.numel() != n or tmp.dtype != torch.int32 or tmp.device != dev:
+            tmp = torch.empty(n, dtype=torch.int32, device=dev)
         check(lib().mdg_owned_order(self.ctx.h, ctypes.byref(config_struct(config)), tmp.data_ptr()),
               "owned_order")
-        out = torch.empty(n, dtype=torch.int64, device=self.ctx.device)
+        if out is None or out.numel() != n or out.dtype != torch.int64 or out.device != dev:
+            out = torch.empty(n, dtype=torch.int64, device=dev)
         self.permutation(2, tmp, None, out)   # widened in libmdg, not by an eager torch cast
         return out
 
@@ -295,9 +301,10 @@ class ForceCalculator:
               "potential_energy")
         return float(pe.value)
 
-    def profile(self, enable=True):
-        """Bracket each force-kernel launch with CUDA events on the context stream."""
-        check(lib().mdg_profile(self.ctx.h, int(enable)), "profile")
+    def profile(self, enable=True, reserve=0):
+        """Bracket each force-kernel launch with CUDA events on the context stream;
+        ``reserve``: launches whose events are created now instead of on demand."""
+        check(lib().mdg_profile(self.ctx.h, max(1, int(reserve)) if enable else 0), "profile")
 
     def profile_read(self):
         """(summed force-kernel milliseconds, bracketed launches) since profile()."""

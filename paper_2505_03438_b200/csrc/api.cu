@@ -151,7 +151,11 @@ struct NvtxRange {
     NvtxRange& operator=(const NvtxRange&) = delete;
 };
 }  // namespace
+#ifdef MDG_NO_NVTX
+#define MDG_RANGE(name) ((void)0)
+#else
 #define MDG_RANGE(name) NvtxRange nvtx_range_(name)
+#endif
 
 extern "C" {
 
@@ -1064,8 +1068,18 @@ int mdg_live_stats(mdg_ctx* ctx, double out[6]) {
 
 int mdg_profile(mdg_ctx* ctx, int enable) {
     CHECK_CTX(ctx);
-    ctx->c.prof = enable != 0;
-    ctx->c.ev_used = 0;
+    Context& c = ctx->c;
+    c.prof = enable != 0;
+    c.ev_used = 0;
+    // enable > 1: that many bracketed launches reserved now, so a timed loop
+    // creates no events (the pool otherwise grows on demand, two per launch)
+    if (enable > 1) {
+        while (c.ev_pool.size() < 2 * (size_t)enable) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) return cuda_status("mdg_profile: events");
+            c.ev_pool.push_back(e);
+        }
+    }
     return MDG_OK;
 }
 

@@ -86,6 +86,12 @@ template <class T>
 void DBuf<T>::ensure(size_t n) {
     if (n <= cap && p) return;
     size_t want = std::max<size_t>(n + n / 8, 64);
+    // MDG_ALLOC_TRACE=1: every (re)allocation on stderr (a cudaFree + cudaMalloc
+    // inside a timed loop is a host stall of milliseconds)
+    static const bool trace = getenv("MDG_ALLOC_TRACE") != nullptr;
+    if (trace)
+        fprintf(stderr, "mdg alloc: %zu -> %zu bytes (%s)\n", cap * sizeof(T), want * sizeof(T),
+                p ? "grow: cudaFree + cudaMalloc" : "new");
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;

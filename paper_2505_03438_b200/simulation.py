@@ -158,6 +158,7 @@ class Simulation:
         self._skip_reorder = False
         self._perm_spare = None
         self._iota = self._inv = None
+        self._order_tmp = self._order_buf = None   # owned_order's buffers (no allocation per reorder)
         # untimed steady iterations of a fixed configuration run as one native
         # call (mdg_run) inside run(); False: every iteration through step()
         self.native = True
@@ -270,10 +271,19 @@ class Simulation:
         torch.cuda.synchronize(self.p.pos.device)
 
     def _reorder(self):
-        order = self.calc.owned_order(self._active_cfg)
+        # the order lands in buffers this loop owns: nothing is allocated from
+        # the second reorder on
+        n = self.p.n
+        dev = self.p.pos.device
+        if self._order_tmp is None or self._order_tmp.numel() != n or self._order_tmp.device != dev:
+            self._order_tmp = torch.empty(n, dtype=torch.int32, device=dev)
+        if self._order_buf is None or self._order_buf.numel() != n or self._order_buf.device != dev:
+            self._order_buf = torch.empty(n, dtype=torch.int64, device=dev)
+        order = self.calc.owned_order(self._active_cfg, out=self._order_buf, tmp=self._order_tmp)
         self._permute(order)
         if self._perm is None:
             self._perm = order
+            self._order_buf = torch.empty_like(order)   # (the first reorder keeps its buffer)
         else:   # compose into the spare permutation buffer (no allocation)
             out = self._perm_spare
             if out is None or out.shape != self._perm.shape or out.device != self._perm.device:

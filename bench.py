@@ -314,7 +314,8 @@ def gpu_arm(args, rank, world, dist):
         # the spare arrays back) stalled the host for 3-14 ms in ~10% of the
         # runs during some periods on the GPU pool -- always that one, never a
         # later reorder (profiles/round2_reorder_spike.txt)
-        if args.reorder and dist is None and cfg.container == P.VERLET_LISTS:
+        if (args.reorder and dist is None and cfg.container == P.VERLET_LISTS
+                and not os.environ.get("MDG_BENCH_NO_WARM_EXTRA")):   # (the probe's way back to the stall)
             warm_extra = args.reorder * (params.rebuild_interval + 1)
             for _ in range(warm_extra):
                 sim.step()
@@ -361,6 +362,8 @@ def gpu_arm(args, rank, world, dist):
     if os.environ.get("MDG_BENCH_STEPS"):
         print(json.dumps([round(a.elapsed_time(b), 4) for a, b in step_ms]), file=sys.stderr)
         print("host_ms " + json.dumps(host_ms), file=sys.stderr)
+        from paper_2505_03438_b200 import simulation as _simmod
+        print("reorder steps (iteration, reorder, rebuild, refresh + compute host ms): " + json.dumps(_simmod.STEP_TRACE), file=sys.stderr)
         print("cudaMallocs by torch inside the timed loop: %d" % (torch.cuda.memory_stats(dev).get("num_device_alloc", 0) - dev_allocs0), file=sys.stderr)
     sim.check()
 

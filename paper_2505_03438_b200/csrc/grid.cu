@@ -6,6 +6,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 
 #include "device.cuh"
@@ -538,7 +539,13 @@ int grid_rebuild(Context& c, Grid& gr, const double* pos, int layout) {
     exclusive_scan_i32(c, gr.img_cnt.p, gr.img_off.p, n, c.scal.p + 1);
     exclusive_scan_i32(c, gr.cell_count.p, gr.cell_start.p, nc + 1, nullptr, gr.sort_by_z ? occ2 : nullptr);
     scal_to_host(c, c.scal.p + 1, 9, c.d_h_scal + 1);   // (mapped pinned: no copy-engine bubble)
+    static const bool trace = getenv("MDG_STEP_TRACE") != nullptr;   // host ms of this wait, when long
+    const auto t0 = std::chrono::steady_clock::now();
     MDG_CUDA(cudaStreamSynchronize(st));
+    if (trace) {
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms > 3.5) fprintf(stderr, "mdg grid_rebuild: waited %.3f ms for the stream\n", ms);
+    }
     if (c.flags_probe) {   // status word copied before this rebuild's first kernel
         c.flags_probe = false;
         c.flags_seen = (unsigned)(c.h_scal[2] & 3ull);

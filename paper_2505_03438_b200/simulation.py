@@ -29,6 +29,8 @@ and at the end of the run.
 
 from __future__ import annotations
 
+import os
+import time
 from dataclasses import dataclass, field
 
 import torch
@@ -61,6 +63,12 @@ class IterationRecord:
     build_ns: int
     rebuilt: bool
     phase_index: int = 0
+
+
+# MDG_STEP_TRACE=1: host wall time of each phase of a step() that reorders
+# (diagnostics for host stalls: tools/spike_probe.sh)
+_TRACE = bool(os.environ.get("MDG_STEP_TRACE"))
+STEP_TRACE = []
 
 
 @dataclass
@@ -314,6 +322,7 @@ class Simulation:
             calc.drift_wrap(p, params.delta_t)
         pending = getattr(self, "_pending", None)
         self._pending = None
+        tr = None
         while True:
             if pending is not None:
                 cfg, forced = pending
@@ -334,7 +343,11 @@ class Simulation:
                 if self._skip_reorder:
                     self._skip_reorder = False
                 else:
+                    if _TRACE:
+                        tr = [time.perf_counter()]
                     self._reorder()
+                    if _TRACE:
+                        tr.append(time.perf_counter())
             if timed:
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 ev[0].record()
@@ -348,6 +361,8 @@ class Simulation:
                             raise _StatusFlags(flags)
                     else:
                         calc.rebuild(p, cfg)
+                if tr is not None:
+                    tr.append(time.perf_counter())
                 calc.refresh(p, cfg)
                 if timed:
                     ev[1].record()
@@ -363,6 +378,9 @@ class Simulation:
                     calc.compute_kick_async(p, cfg, params.delta_t, params.gravity)
                 if timed:
                     ev[2].record()
+                if tr is not None:   # (iteration, reorder, rebuild, refresh + compute) host ms
+                    tr.append(time.perf_counter())
+                    STEP_TRACE.append((it,) + tuple(round((b - a) * 1e3, 3) for a, b in zip(tr, tr[1:])))
                 break
             except (BlowUpError, KeyboardInterrupt):
                 raise

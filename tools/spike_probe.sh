@@ -23,3 +23,4 @@ print(t, "MUPS", d["value"], "ms/step", d["ms_per_step"], "median", statistics.m
       [(i, x, hm[i] if hm else None, hm[i - 1] if hm and i else None) for i, x in enumerate(st) if x > 1.5], "clock samples", d["clocks"]["samples"])
 PY
 grep "cudaMallocs by torch" gpurun_out/sp/$tag.err
+grep "reorder steps\|grid_rebuild: waited" gpurun_out/sp/$tag.err | cut -c1-400

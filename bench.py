@@ -316,7 +316,10 @@ def gpu_arm(args, rank, world, dist):
         # later reorder (profiles/round2_reorder_spike.txt)
         if (args.reorder and dist is None and cfg.container == P.VERLET_LISTS
                 and not os.environ.get("MDG_BENCH_NO_WARM_EXTRA")):   # (the probe's way back to the stall)
-            warm_extra = args.reorder * (params.rebuild_interval + 1)
+            # (the reorder falls on the rebuild `reorder` rebuild intervals after this
+            # point; one more interval brings the loop back to a rebuild step, so the
+            # timed steps start on a rebuild as they always did)
+            warm_extra = (args.reorder + 1) * (params.rebuild_interval + 1)
             for _ in range(warm_extra):
                 sim.step()
             sim.check()
